@@ -1,0 +1,191 @@
+/* sgs.h -- C ABI of the B200 SG-splat rasterizer (libsgs.so, sm_100a).
+ *
+ * This is the drop-in boundary for the reference's render hot path.  The
+ * reference (`sgsplat`, pure Python/NumPy) has no FFI: its interface is the
+ * set of Python functions in pkg/src/sgsplat/render.py.  Each entry point
+ * below names the reference function (file:line) whose work it replaces; the
+ * Python host layer `paper_2509_07021_b200.render` binds these through ctypes
+ * and presents the reference signatures unchanged.
+ *
+ * Conventions
+ *   - every pointer argument that names an array is a DEVICE pointer, fp32
+ *     structure-of-arrays in the reference SceneParams layout
+ *     (render.py:90-108): position (N,3), quat (N,4) w-first, log_scale (N,3),
+ *     opacity (N) activated, diffuse (N,3), axis_raw (N,L,3), sharpness (N,L)
+ *     activated, amplitude (N,L,3); plus the soft-pruning masks lobe_mask
+ *     (N,L) and prim_mask (N) as floats in [0,1];
+ *   - `stream` is a cudaStream_t passed as void* (0 = legacy default stream);
+ *   - every call returns 0 on success or a negative SGS_E* code; no C++
+ *     exception crosses the ABI.  sgs_last_error() returns a message;
+ *   - all scratch lives in ONE caller-allocated device workspace whose size is
+ *     given by sgs_workspace_size(), so the caller's allocator (PyTorch's
+ *     caching allocator) accounts for every byte of render VRAM.
+ */
+#ifndef SGS_H_
+#define SGS_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SGS_OK 0
+#define SGS_E_ARG (-1)        /* invalid argument (the reference raises ValueError) */
+#define SGS_E_CUDA (-2)       /* CUDA runtime error */
+#define SGS_E_WORKSPACE (-3)  /* workspace too small for N / image size */
+#define SGS_E_CAPACITY (-4)   /* tile-entry capacity exceeded; grow and retry */
+
+#define SGS_SORT_DEPTH_FIRST 0  /* global depth sort of primitives + stable tile bucketing */
+#define SGS_SORT_KEY64 1        /* (tile<<32 | depth_bits) keys, 64-bit onesweep radix sort */
+
+/* Pinhole camera, render.py:30-57 (Camera).  rotation rows = (right, down,
+ * forward) world-to-camera; pixel = (fx x/z + cx, fy y/z + cy).  tile_y0/1 is
+ * a tile-row window [tile_y0, tile_y1) for tile-strip renders (0,0 = all). */
+typedef struct sgs_camera {
+  float rotation[9];
+  float translation[3];
+  float fx, fy, cx, cy;
+  float near_z;
+  int32_t width, height;
+  int32_t tile_y0, tile_y1;
+} sgs_camera;
+
+/* Packed parameter arrays, render.py:90-108 (SceneParams) + soft masks. */
+typedef struct sgs_params {
+  const float* position;
+  const float* quat;
+  const float* log_scale;
+  const float* opacity;
+  const float* diffuse;
+  const float* axis_raw;
+  const float* sharpness;
+  const float* amplitude;
+  const float* lobe_mask; /* (N,L); required */
+  const float* prim_mask; /* (N); NULL means all ones */
+  int64_t n;
+  int32_t n_lobes;
+} sgs_params;
+
+/* Parameter gradients, render.py:179-194 (GradientSet) + mask gradients.
+ * Outputs are OVERWRITTEN (not accumulated).  lobe_mask / prim_mask may be
+ * NULL when the caller does not train masks. */
+typedef struct sgs_grads {
+  float* position;
+  float* quat;
+  float* log_scale;
+  float* opacity;
+  float* diffuse;
+  float* axis_raw;
+  float* sharpness;
+  float* amplitude;
+  float* lobe_mask;
+  float* prim_mask;
+} sgs_grads;
+
+/* Device workspace descriptor.  `base` is ONE caller-allocated device buffer
+ * of at least sgs_workspace_size() bytes for the same (n, n_lobes, width,
+ * height, entry_capacity, sort_mode); the library carves it deterministically,
+ * so the descriptor is all the state there is. */
+typedef struct sgs_workspace {
+  void* base;
+  uint64_t bytes;
+  int64_t n;
+  int32_t n_lobes;
+  int32_t width, height;
+  int32_t sort_mode;
+  int64_t entry_capacity;
+} sgs_workspace;
+
+/* Frame counters, readable after any stage (device copy inside the workspace). */
+typedef struct sgs_stats {
+  uint64_t n_visible;      /* z > near, render.py:263 */
+  uint64_t n_emitting;     /* visible primitives with >= 1 tile entry */
+  uint64_t n_entries;      /* tile-depth key/value entries E */
+  uint64_t capacity;       /* entry capacity the workspace was carved for */
+  uint64_t overflow;       /* 1 if n_entries > capacity (frame must be redone) */
+  uint64_t vram3s_visible; /* reference VRAM model, postprocess.py:118-135 */
+  uint64_t vram3s_entries;
+} sgs_stats;
+
+/* Library / ABI version and last error message (thread-local). */
+int32_t sgs_version(void);
+const char* sgs_last_error(void);
+
+/* Bytes of device workspace for N primitives, an image of width x height
+ * and room for `entry_capacity` tile entries. */
+int sgs_workspace_size(const sgs_workspace* ws, uint64_t* bytes_out);
+
+/* K1 preprocess -- replaces _prepare (render.py:259-317) minus its depth
+ * argsort: projection, EWA conic, near/opacity/frustum culling, support
+ * rectangle, exact ellipse-tile counts and SG color (masked lobes skipped). */
+int sgs_preprocess(const sgs_params* params, const sgs_camera* cam, const sgs_workspace* ws,
+                   void* stream);
+
+/* K2-K4 binning -- replaces the depth argsort (render.py:307).  Emits one
+ * (tile, depth) entry per touched tile and sorts them stably by
+ * (tile, depth, primitive index); writes per-tile [start, end) ranges.
+ * `sort_mode` picks SGS_SORT_DEPTH_FIRST (default) or SGS_SORT_KEY64; both
+ * produce bit-identical results.  Sets SGS_E_CAPACITY when E > capacity. */
+int sgs_bin(const sgs_camera* cam, const sgs_workspace* ws, void* stream);
+
+/* K5 forward raster -- replaces _chunk_blend + _render_params
+ * (render.py:355-408).  out_img (H,W,3), out_T (H,W) final transmittance,
+ * out_ncontrib (H,W) number of per-tile entries consumed by each pixel.
+ * weight_sums (N) is ACCUMULATED (like the reference's in-place np.add.at,
+ * render.py:406-407) when non-NULL. */
+int sgs_raster_forward(const sgs_camera* cam, const float background[3],
+                       const sgs_workspace* ws, float* out_img, float* out_T,
+                       uint32_t* out_ncontrib, float* weight_sums, void* stream);
+
+/* Convenience: preprocess + bin + raster_forward in one call (graph-capturable). */
+int sgs_render_forward(const sgs_params* params, const sgs_camera* cam, const float background[3],
+                       const sgs_workspace* ws, float* out_img, float* out_T, uint32_t* out_ncontrib,
+                       float* weight_sums, void* stream);
+
+/* K6 backward raster -- replaces the pixel loop of _backward_from_blend
+ * (render.py:535-573).  dimg (H,W,3) = dL/dimage.  grad2d (N,9) is
+ * OVERWRITTEN with per-primitive [dL/dcolor(3), sum dq, sum dq dx, sum dq dy,
+ * sum dq dx^2, sum dq dx dy, sum dq dy^2] where q is the conic quadratic form. */
+int sgs_raster_backward(const sgs_camera* cam, const float background[3],
+                        const sgs_workspace* ws, const float* img, const float* final_T,
+                        const uint32_t* ncontrib, const float* dimg, float* grad2d, void* stream);
+
+/* K7 preprocess backward -- replaces render.py:575-636 (conic -> cov2d ->
+ * Sigma/J -> quat/log_scale/position, SG color path, scatter) and adds the
+ * soft-mask gradients dL/dm_p = o dL/do_eff, dL/dm_l = (dL/dc_pre . a_l) e_l. */
+int sgs_preprocess_backward(const sgs_params* params, const sgs_camera* cam, const float* grad2d,
+                            sgs_grads* grads, void* stream);
+
+/* Read the frame counters (synchronises `stream`). */
+int sgs_get_stats(const sgs_workspace* ws, sgs_stats* out, void* stream);
+
+/* Reference VRAM model (postprocess.py:101-137): 3-sigma AABB visible count
+ * and tile entries with `tile_px` tiles; results land in sgs_stats. */
+int sgs_vram_model(const sgs_params* params, const sgs_camera* cam, int32_t tile_px,
+                   const sgs_workspace* ws, void* stream);
+
+/* Export the sorted tile list as 64-bit (tile<<32 | depth_bits) keys and
+ * primitive-index values (device buffers of length >= n_entries), and the
+ * per-tile ranges (tiles_x*tiles_y uint32 pairs).  For parity checks. */
+int sgs_export_bins(const sgs_workspace* ws, const sgs_camera* cam, uint64_t* keys,
+                    uint32_t* values, uint32_t* ranges, void* stream);
+
+/* Export per-primitive preprocess outputs (device buffers, length N):
+ * depth bits, packed tile rect (tx0|tx1<<16, ty0|ty1<<16), tile counts and
+ * the 12-float raster record [geo(4), conic(4), color(4)]. */
+int sgs_export_projected(const sgs_workspace* ws, uint32_t* depth_bits,
+                         uint32_t* rect, uint32_t* tiles_touched, float* records, void* stream);
+
+/* Stable LSD radix sort of (key, value) pairs on the low `key_bits` bits of
+ * 64-bit keys (onesweep, decoupled look-back).  In-place on keys/values;
+ * `temp` of sgs_sort_temp_size() bytes. */
+int sgs_sort_temp_size(int64_t n, int32_t key_bits, uint64_t* bytes_out);
+int sgs_sort_pairs_u64(uint64_t* keys, uint32_t* values, int64_t n, int32_t key_bits, void* temp,
+                       uint64_t temp_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SGS_H_ */

@@ -1,0 +1,274 @@
+// api.cu -- extern "C" entry points of libsgs.so (declared in include/sgs.h).
+// Validation, workspace carving and kernel sequencing; no math here.
+#include <stdarg.h>
+
+#include <mutex>
+
+#include "common.cuh"
+
+namespace sgs {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  set_error("CUDA error in %s: %s", what, cudaGetErrorString(e));
+  return SGS_E_CUDA;
+}
+
+int device_sm_count() {
+  static int cached = 0;
+  if (!cached) {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = kNumSMs;
+    cached = v;
+  }
+  return cached;
+}
+
+int resident_ctas_per_sm(const void* kernel, int threads, size_t smem) {
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, smem) != cudaSuccess) return 0;
+  return n;
+}
+
+int launch_preprocess(const sgs_params& P, const SgsCam& cam, const sgs_workspace* ws, const Layout& lo,
+                      cudaStream_t st);
+int launch_vram3s(const sgs_params& P, const SgsCam& cam, int tile_px, Counters* ctr, cudaStream_t st);
+int launch_bin(const SgsCam& cam, const sgs_workspace* ws, const Layout& lo, cudaStream_t st);
+bool final_in_alt(const Layout& lo);
+int launch_raster_fwd(const SgsCam& cam, float3 bg, const sgs_workspace* ws, const Layout& lo, const uint32_t* vals,
+                      float* img, float* T, uint32_t* nc, float* weight_sums, cudaStream_t st);
+int launch_raster_bwd(const SgsCam& cam, float3 bg, const sgs_workspace* ws, const Layout& lo, const uint32_t* vals,
+                      const float* T, const uint32_t* nc, const float* dimg, float* grad2d, cudaStream_t st);
+int launch_preprocess_bwd(const sgs_params& P, const SgsCam& cam, const float* grad2d, const sgs_grads& g,
+                          cudaStream_t st);
+int launch_export_bins(const sgs_workspace* ws, const Layout& lo, unsigned long long* keys, uint32_t* vals,
+                       uint32_t* ranges, cudaStream_t st);
+int launch_sort_u64(unsigned long long* keys, uint32_t* vals, uint32_t n, int bits, void* temp, uint64_t temp_bytes,
+                    cudaStream_t st);
+uint64_t sort_u64_temp_bytes(uint64_t n, int bits);
+
+static int check_params(const sgs_params* p, const Layout* lo) {
+  if (!p || p->n < 0 || p->n_lobes < 0 || p->n_lobes > SGS_MAX_LOBES) {
+    set_error("invalid params");
+    return SGS_E_ARG;
+  }
+  if (p->n > 0 && (!p->position || !p->quat || !p->log_scale || !p->opacity || !p->diffuse ||
+                   (p->n_lobes > 0 && (!p->axis_raw || !p->sharpness || !p->amplitude || !p->lobe_mask)))) {
+    set_error("null parameter array");
+    return SGS_E_ARG;
+  }
+  if (lo && (p->n != lo->n || p->n_lobes != lo->L)) {
+    set_error("params (n=%lld, L=%d) do not match workspace (n=%lld, L=%d)", (long long)p->n, p->n_lobes,
+              (long long)lo->n, lo->L);
+    return SGS_E_ARG;
+  }
+  return SGS_OK;
+}
+
+static const uint32_t* final_vals(const sgs_workspace* ws, const Layout& lo) {
+  return at<uint32_t>(ws, final_in_alt(lo) ? lo.ent_val_alt : lo.ent_val);
+}
+
+}  // namespace sgs
+
+using namespace sgs;
+
+extern "C" {
+
+int32_t sgs_version(void) { return 100; }
+
+const char* sgs_last_error(void) { return g_err; }
+
+int sgs_workspace_size(const sgs_workspace* ws, uint64_t* bytes_out) {
+  Layout lo;
+  int rc = make_layout(ws, &lo);
+  if (rc) return rc;
+  if (!bytes_out) return SGS_E_ARG;
+  *bytes_out = lo.total;
+  return SGS_OK;
+}
+
+int sgs_preprocess(const sgs_params* params, const sgs_camera* cam, const sgs_workspace* ws, void* stream) {
+  Layout lo;
+  SgsCam c;
+  int rc = check_ws(ws, &lo);
+  if (!rc) rc = check_params(params, &lo);
+  if (!rc) rc = make_cam(cam, lo, &c);
+  if (rc) return rc;
+  cudaStream_t st = as_stream(stream);
+  SGS_CUDA(cudaMemsetAsync(at<Counters>(ws, lo.counters), 0, sizeof(Counters), st));
+  if (lo.n == 0) return SGS_OK;
+  return launch_preprocess(*params, c, ws, lo, st);
+}
+
+int sgs_bin(const sgs_camera* cam, const sgs_workspace* ws, void* stream) {
+  Layout lo;
+  SgsCam c;
+  int rc = check_ws(ws, &lo);
+  if (!rc) rc = make_cam(cam, lo, &c);
+  if (rc) return rc;
+  return launch_bin(c, ws, lo, as_stream(stream));
+}
+
+int sgs_raster_forward(const sgs_camera* cam, const float background[3], const sgs_workspace* ws, float* out_img,
+                       float* out_T, uint32_t* out_ncontrib, float* weight_sums, void* stream) {
+  Layout lo;
+  SgsCam c;
+  int rc = check_ws(ws, &lo);
+  if (!rc) rc = make_cam(cam, lo, &c);
+  if (rc) return rc;
+  if (!out_img || !out_T || !out_ncontrib || !background) {
+    set_error("null output buffer");
+    return SGS_E_ARG;
+  }
+  float3 bg = make_float3(background[0], background[1], background[2]);
+  return launch_raster_fwd(c, bg, ws, lo, final_vals(ws, lo), out_img, out_T, out_ncontrib, weight_sums,
+                           as_stream(stream));
+}
+
+int sgs_render_forward(const sgs_params* params, const sgs_camera* cam, const float background[3],
+                       const sgs_workspace* ws, float* out_img, float* out_T, uint32_t* out_ncontrib,
+                       float* weight_sums, void* stream) {
+  int rc = sgs_preprocess(params, cam, ws, stream);
+  if (!rc) rc = sgs_bin(cam, ws, stream);
+  if (!rc) rc = sgs_raster_forward(cam, background, ws, out_img, out_T, out_ncontrib, weight_sums, stream);
+  return rc;
+}
+
+int sgs_raster_backward(const sgs_camera* cam, const float background[3], const sgs_workspace* ws, const float* img,
+                        const float* final_T, const uint32_t* ncontrib, const float* dimg, float* grad2d,
+                        void* stream) {
+  Layout lo;
+  SgsCam c;
+  int rc = check_ws(ws, &lo);
+  if (!rc) rc = make_cam(cam, lo, &c);
+  if (rc) return rc;
+  if (!final_T || !ncontrib || !dimg || !grad2d || !background) {
+    set_error("null buffer");
+    return SGS_E_ARG;
+  }
+  (void)img;
+  float3 bg = make_float3(background[0], background[1], background[2]);
+  return launch_raster_bwd(c, bg, ws, lo, final_vals(ws, lo), final_T, ncontrib, dimg, grad2d, as_stream(stream));
+}
+
+int sgs_preprocess_backward(const sgs_params* params, const sgs_camera* cam, const float* grad2d, sgs_grads* grads,
+                            void* stream) {
+  int rc = check_params(params, nullptr);
+  if (rc) return rc;
+  if (!grads || !grad2d || (params->n > 0 && (!grads->position || !grads->quat || !grads->log_scale ||
+                                              !grads->opacity || !grads->diffuse ||
+                                              (params->n_lobes > 0 &&
+                                               (!grads->axis_raw || !grads->sharpness || !grads->amplitude))))) {
+    set_error("null gradient buffer");
+    return SGS_E_ARG;
+  }
+  Layout lo{};
+  lo.W = cam ? cam->width : 0;
+  lo.H = cam ? cam->height : 0;
+  lo.tiles_x = (lo.W + SGS_TILE - 1) / SGS_TILE;
+  lo.tiles_y = (lo.H + SGS_TILE - 1) / SGS_TILE;
+  SgsCam c;
+  rc = make_cam(cam, lo, &c);
+  if (rc) return rc;
+  if (params->n == 0) return SGS_OK;
+  return launch_preprocess_bwd(*params, c, grad2d, *grads, as_stream(stream));
+}
+
+int sgs_get_stats(const sgs_workspace* ws, sgs_stats* out, void* stream) {
+  Layout lo;
+  int rc = check_ws(ws, &lo);
+  if (rc) return rc;
+  if (!out) return SGS_E_ARG;
+  Counters h;
+  cudaStream_t st = as_stream(stream);
+  SGS_CUDA(cudaMemcpyAsync(&h, at<Counters>(ws, lo.counters), sizeof(Counters), cudaMemcpyDeviceToHost, st));
+  SGS_CUDA(cudaStreamSynchronize(st));
+  out->n_visible = h.n_visible;
+  out->n_emitting = h.n_emitting;
+  out->n_entries = h.n_entries;
+  out->capacity = (uint64_t)lo.cap;
+  out->overflow = h.n_entries > (unsigned long long)lo.cap ? 1 : 0;
+  out->vram3s_visible = h.vram3s_visible;
+  out->vram3s_entries = h.vram3s_entries;
+  return SGS_OK;
+}
+
+int sgs_vram_model(const sgs_params* params, const sgs_camera* cam, int32_t tile_px, const sgs_workspace* ws,
+                   void* stream) {
+  Layout lo;
+  SgsCam c;
+  int rc = check_ws(ws, &lo);
+  if (!rc) rc = check_params(params, &lo);
+  if (!rc) rc = make_cam(cam, lo, &c);
+  if (rc) return rc;
+  if (tile_px < 1) {
+    set_error("tile_px must be >= 1");
+    return SGS_E_ARG;
+  }
+  cudaStream_t st = as_stream(stream);
+  Counters* ctr = at<Counters>(ws, lo.counters);
+  SGS_CUDA(cudaMemsetAsync(&ctr->vram3s_visible, 0, 16, st));
+  if (lo.n == 0) return SGS_OK;
+  return launch_vram3s(*params, c, tile_px, ctr, st);
+}
+
+int sgs_export_bins(const sgs_workspace* ws, const sgs_camera* cam, uint64_t* keys, uint32_t* values,
+                    uint32_t* ranges, void* stream) {
+  Layout lo;
+  int rc = check_ws(ws, &lo);
+  if (rc) return rc;
+  (void)cam;
+  return launch_export_bins(ws, lo, reinterpret_cast<unsigned long long*>(keys), values, ranges, as_stream(stream));
+}
+
+int sgs_export_projected(const sgs_workspace* ws, uint32_t* depth_bits, uint32_t* rect, uint32_t* tiles_touched,
+                         float* records, void* stream) {
+  Layout lo;
+  int rc = check_ws(ws, &lo);
+  if (rc) return rc;
+  cudaStream_t st = as_stream(stream);
+  const size_t n = (size_t)lo.n;
+  if (depth_bits)
+    SGS_CUDA(cudaMemcpyAsync(depth_bits, at<uint32_t>(ws, lo.depth_key), n * 4, cudaMemcpyDeviceToDevice, st));
+  if (rect) SGS_CUDA(cudaMemcpyAsync(rect, at<uint2>(ws, lo.rect), n * 8, cudaMemcpyDeviceToDevice, st));
+  if (tiles_touched)
+    SGS_CUDA(cudaMemcpyAsync(tiles_touched, at<uint32_t>(ws, lo.tiles_touched), n * 4, cudaMemcpyDeviceToDevice, st));
+  if (records) {
+    SGS_CUDA(cudaMemcpy2DAsync(records, 48, at<float4>(ws, lo.rec_geo), 16, 16, n, cudaMemcpyDeviceToDevice, st));
+    SGS_CUDA(cudaMemcpy2DAsync(records + 4, 48, at<float4>(ws, lo.rec_con), 16, 16, n, cudaMemcpyDeviceToDevice, st));
+    SGS_CUDA(cudaMemcpy2DAsync(records + 8, 48, at<float4>(ws, lo.rec_col), 16, 16, n, cudaMemcpyDeviceToDevice, st));
+  }
+  return SGS_OK;
+}
+
+int sgs_sort_temp_size(int64_t n, int32_t key_bits, uint64_t* bytes_out) {
+  if (n < 0 || n > (int64_t)kMaxEntries || key_bits < 1 || key_bits > 64 || !bytes_out) {
+    set_error("invalid sort size");
+    return SGS_E_ARG;
+  }
+  *bytes_out = sort_u64_temp_bytes((uint64_t)n, key_bits);
+  return SGS_OK;
+}
+
+int sgs_sort_pairs_u64(uint64_t* keys, uint32_t* values, int64_t n, int32_t key_bits, void* temp,
+                       uint64_t temp_bytes, void* stream) {
+  if (n < 0 || n > (int64_t)kMaxEntries || key_bits < 1 || key_bits > 64 || (n > 0 && (!keys || !values || !temp))) {
+    set_error("invalid sort arguments");
+    return SGS_E_ARG;
+  }
+  if (n == 0) return SGS_OK;
+  return launch_sort_u64(reinterpret_cast<unsigned long long*>(keys), values, (uint32_t)n, key_bits, temp, temp_bytes,
+                         as_stream(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,195 @@
+// common.cuh -- error plumbing, workspace carving and camera setup shared by
+// every translation unit of libsgs.so.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include "../../include/sgs.h"
+#include "sgs_geom.h"
+
+namespace sgs {
+
+constexpr int kNumSMs = 148;
+constexpr int kRadixThreads = 256;
+constexpr int kTileSortIPT = 16;   // items per thread, tile-key onesweep passes
+constexpr int kDepthSortIPT = 16;
+constexpr int kKey64SortIPT = 12;
+constexpr uint32_t kMaxEntries = (1u << 30) - 1;  // look-back status packs 30-bit counts
+
+void set_error(const char* fmt, ...);
+int cuda_fail(cudaError_t e, const char* what);
+
+#define SGS_CUDA(call)                                     \
+  do {                                                     \
+    cudaError_t e__ = (call);                              \
+    if (e__ != cudaSuccess) return sgs::cuda_fail(e__, #call); \
+  } while (0)
+
+#define SGS_LAUNCH_CHECK(what)                             \
+  do {                                                     \
+    cudaError_t e__ = cudaGetLastError();                  \
+    if (e__ != cudaSuccess) return sgs::cuda_fail(e__, what); \
+  } while (0)
+
+// Device-side counters at the head of the workspace.
+struct Counters {
+  unsigned long long n_visible;
+  unsigned long long n_emitting;
+  unsigned long long n_entries;      // exact E (may exceed capacity)
+  unsigned long long capacity;
+  unsigned long long overflow;
+  unsigned long long vram3s_visible;
+  unsigned long long vram3s_entries;
+  unsigned long long pad0;
+  uint32_t n_sort;                   // min(E, capacity): items the tile sort processes
+  uint32_t n_depth;                  // primitives entering the depth sort
+  uint32_t part_counter[16];         // onesweep partition tickets, one per pass
+  uint32_t pad1[14];
+};
+
+// Carved workspace.  All sub-buffers 256-byte aligned.
+struct Layout {
+  int64_t n;
+  int32_t L, W, H, tiles_x, tiles_y, n_tiles;
+  int32_t sort_mode;
+  int64_t cap;
+  // offsets into the workspace
+  uint64_t counters, rec_geo, rec_con, rec_col, depth_key, rect, tiles_touched;
+  uint64_t dkey_alt, dkey_tmp, didx, didx_alt, offsets, scan_blocks;
+  uint64_t ent_key, ent_key_alt, ent_val, ent_val_alt, ranges;
+  uint64_t hist, status;
+  uint64_t status_bytes;
+  uint64_t total;
+};
+
+inline int ceil_log2_u64(uint64_t x) {
+  int b = 0;
+  while ((1ull << b) < x) ++b;
+  return b;
+}
+
+inline int tile_sort_bits(int n_tiles) { return n_tiles <= 1 ? 1 : ceil_log2_u64((uint64_t)n_tiles); }
+
+inline int tile_sort_passes(int n_tiles) { return (tile_sort_bits(n_tiles) + 7) / 8; }
+
+inline uint64_t align256(uint64_t x) { return (x + 255) & ~uint64_t(255); }
+
+inline int make_layout(const sgs_workspace* ws, Layout* lo) {
+  if (!ws || ws->n < 0 || ws->n > (int64_t)0x7fffffff || ws->width < 1 || ws->height < 1 ||
+      ws->n_lobes < 0 || ws->n_lobes > SGS_MAX_LOBES || ws->entry_capacity < 0 ||
+      ws->entry_capacity > (int64_t)kMaxEntries ||
+      (ws->sort_mode != SGS_SORT_DEPTH_FIRST && ws->sort_mode != SGS_SORT_KEY64)) {
+    set_error("invalid workspace descriptor");
+    return SGS_E_ARG;
+  }
+  lo->n = ws->n;
+  lo->L = ws->n_lobes;
+  lo->W = ws->width;
+  lo->H = ws->height;
+  lo->tiles_x = (ws->width + SGS_TILE - 1) / SGS_TILE;
+  lo->tiles_y = (ws->height + SGS_TILE - 1) / SGS_TILE;
+  lo->n_tiles = lo->tiles_x * lo->tiles_y;
+  lo->sort_mode = ws->sort_mode;
+  lo->cap = ws->entry_capacity;
+  const uint64_t n = (uint64_t)ws->n + 1, cap = (uint64_t)ws->entry_capacity + 1;
+  const bool k64 = ws->sort_mode == SGS_SORT_KEY64;
+  uint64_t off = 0;
+  auto take = [&](uint64_t bytes) {
+    uint64_t o = off;
+    off = align256(off + bytes);
+    return o;
+  };
+  lo->counters = take(sizeof(Counters));
+  lo->rec_geo = take(n * 16);
+  lo->rec_con = take(n * 16);
+  lo->rec_col = take(n * 16);
+  lo->depth_key = take(n * 4);
+  lo->rect = take(n * 8);
+  lo->tiles_touched = take(n * 4);
+  lo->dkey_alt = take(n * 4);
+  lo->dkey_tmp = take(n * 4);
+  lo->didx = take(n * 4);
+  lo->didx_alt = take(n * 4);
+  lo->offsets = take(n * 8);
+  lo->scan_blocks = take(((n + 2047) / 2048 + 1) * 8);
+  lo->ent_key = take(cap * (k64 ? 8 : 4));
+  lo->ent_key_alt = take(cap * (k64 ? 8 : 4));
+  lo->ent_val = take(cap * 4);
+  lo->ent_val_alt = take(cap * 4);
+  lo->ranges = take((uint64_t)lo->n_tiles * 8);
+  lo->hist = take(16 * 256 * 4);
+  // onesweep look-back status: per pass, per partition, 256 digits of u32
+  int tile_passes = k64 ? (32 + tile_sort_bits(lo->n_tiles) + 7) / 8 : tile_sort_passes(lo->n_tiles);
+  int ipt = k64 ? kKey64SortIPT : kTileSortIPT;
+  uint64_t parts_tile = (cap + (uint64_t)kRadixThreads * ipt - 1) / ((uint64_t)kRadixThreads * ipt);
+  uint64_t parts_depth = (n + (uint64_t)kRadixThreads * kDepthSortIPT - 1) / ((uint64_t)kRadixThreads * kDepthSortIPT);
+  uint64_t st_tile = parts_tile * 256 * 4 * (uint64_t)tile_passes;
+  uint64_t st_depth = k64 ? 0 : parts_depth * 256 * 4 * 4;
+  lo->status_bytes = st_tile > st_depth ? st_tile : st_depth;
+  lo->status = take(lo->status_bytes);
+  lo->total = off;
+  return SGS_OK;
+}
+
+template <typename T>
+inline T* at(const sgs_workspace* ws, uint64_t off) {
+  return reinterpret_cast<T*>(reinterpret_cast<char*>(ws->base) + off);
+}
+
+inline int check_ws(const sgs_workspace* ws, Layout* lo) {
+  int rc = make_layout(ws, lo);
+  if (rc) return rc;
+  if (!ws->base || ws->bytes < lo->total) {
+    set_error("workspace too small: have %llu bytes, need %llu",
+              (unsigned long long)ws->bytes, (unsigned long long)lo->total);
+    return SGS_E_WORKSPACE;
+  }
+  return SGS_OK;
+}
+
+inline int make_cam(const sgs_camera* c, const Layout& lo, SgsCam* out) {
+  if (!c || !(c->fx > 0.0f) || !(c->fy > 0.0f) || c->width != lo.W || c->height != lo.H) {
+    set_error("invalid camera (focal lengths must be positive and size must match workspace)");
+    return SGS_E_ARG;
+  }
+  for (int i = 0; i < 9; ++i) out->R[i] = c->rotation[i];
+  for (int i = 0; i < 3; ++i) out->t[i] = c->translation[i];
+  // C = -R^T t (render.py:54-57), computed in double and rounded once
+  for (int k = 0; k < 3; ++k) {
+    double s = 0.0;
+    for (int i = 0; i < 3; ++i) s += (double)c->rotation[3 * i + k] * (double)c->translation[i];
+    out->C[k] = (float)(-s);
+  }
+  out->fx = c->fx;
+  out->fy = c->fy;
+  out->cx = c->cx;
+  out->cy = c->cy;
+  out->near_z = c->near_z;
+  out->width = c->width;
+  out->height = c->height;
+  out->tiles_x = lo.tiles_x;
+  out->tiles_y = lo.tiles_y;
+  int y0 = c->tile_y0, y1 = c->tile_y1;
+  if (y0 == 0 && y1 == 0) y1 = lo.tiles_y;
+  if (y0 < 0 || y1 > lo.tiles_y || y0 >= y1) {
+    set_error("invalid tile-row window [%d, %d) for %d tile rows", y0, y1, lo.tiles_y);
+    return SGS_E_ARG;
+  }
+  out->tile_y0 = y0;
+  out->tile_y1 = y1;
+  return SGS_OK;
+}
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// persistent grid: a whole number of waves of `per_sm` resident CTAs
+inline int persistent_grid(uint64_t work_items, int items_per_cta, int per_sm) {
+  uint64_t need = (work_items + items_per_cta - 1) / items_per_cta;
+  uint64_t cap = (uint64_t)kNumSMs * per_sm;
+  if (need < 1) need = 1;
+  return (int)(need < cap ? need : cap);
+}
+
+}  // namespace sgs

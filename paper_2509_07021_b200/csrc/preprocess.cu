@@ -1,0 +1,129 @@
+// preprocess.cu -- K1: per-primitive projection, culling, support rectangle,
+// exact ellipse-tile counts and SG color.  Replaces _prepare
+// (/root/reference/pkg/src/sgsplat/render.py:259-317) minus the argsort, and
+// the reference VRAM model's 3-sigma counts (postprocess.py:118-135).
+//
+// One thread per primitive, grid-stride over N.  The arithmetic lives in
+// sgs_geom.h so the CPU restatement (oracle/) reproduces every bit that feeds
+// a tile key.  HBM-bound: ~156 B read + 60 B written per primitive.
+#include "common.cuh"
+
+namespace sgs {
+
+__device__ __forceinline__ void warp_count(unsigned long long* ctr, bool pred) {
+  unsigned m = __ballot_sync(0xffffffffu, pred);
+  if ((threadIdx.x & 31) == 0 && m) atomicAdd(ctr, (unsigned long long)__popc(m));
+}
+
+__global__ void __launch_bounds__(256) preprocess_kernel(sgs_params P, SgsCam cam, float4* __restrict__ rec_geo,
+                                                         float4* __restrict__ rec_con, float4* __restrict__ rec_col,
+                                                         uint32_t* __restrict__ depth_key, uint2* __restrict__ rect,
+                                                         uint32_t* __restrict__ tiles_touched, Counters* ctr) {
+  const int64_t n = P.n;
+  const int L = P.n_lobes;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  // iterate whole warps so the ballot counters see converged warps
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
+    const int64_t i = base + threadIdx.x;
+    bool live = i < n;
+    bool visible = false, emitting = false;
+    if (live) {
+      float pos[3] = {P.position[3 * i], P.position[3 * i + 1], P.position[3 * i + 2]};
+      float4 q4 = reinterpret_cast<const float4*>(P.quat)[i];
+      float quat[4] = {q4.x, q4.y, q4.z, q4.w};
+      float ls[3] = {P.log_scale[3 * i], P.log_scale[3 * i + 1], P.log_scale[3 * i + 2]};
+      float pm = P.prim_mask ? P.prim_mask[i] : 1.0f;
+      SgsProj pr;
+      sgs_project(pos, quat, ls, P.opacity[i], pm, &cam, &pr);
+      visible = pr.visible;
+      uint32_t cnt = 0;
+      float g[4], k[4];
+      if (pr.emits) {
+        sgs_pack_geo(&pr, g, k);
+        cnt = sgs_count_tiles(pr.tx0, pr.ty0, pr.tx1, pr.ty1, g, k, &cam);
+      }
+      emitting = cnt > 0;
+      tiles_touched[i] = cnt;
+      depth_key[i] = emitting ? sgs_float_to_bits(pr.depth) : 0x7fffffffu;
+      rect[i] = make_uint2((uint32_t)(pr.tx0 & 0xffff) | ((uint32_t)(pr.tx1 & 0xffff) << 16),
+                           (uint32_t)(pr.ty0 & 0xffff) | ((uint32_t)(pr.ty1 & 0xffff) << 16));
+      if (emitting) {
+        float diffuse[3] = {P.diffuse[3 * i], P.diffuse[3 * i + 1], P.diffuse[3 * i + 2]};
+        float axis[3 * SGS_MAX_LOBES], sharp[SGS_MAX_LOBES], amp[3 * SGS_MAX_LOBES], lm[SGS_MAX_LOBES];
+        for (int l = 0; l < L; ++l) {
+          sharp[l] = P.sharpness[i * L + l];
+          lm[l] = P.lobe_mask[i * L + l];
+          for (int kk = 0; kk < 3; ++kk) {
+            axis[3 * l + kk] = P.axis_raw[(i * L + l) * 3 + kk];
+            amp[3 * l + kk] = P.amplitude[(i * L + l) * 3 + kk];
+          }
+        }
+        float c_pre[3], c[3];
+        sgs_color(pos, diffuse, axis, sharp, amp, lm, L, &cam, c_pre, c);
+        rec_geo[i] = make_float4(g[0], g[1], g[2], g[3]);
+        rec_con[i] = make_float4(k[0], k[1], k[2], k[3]);
+        rec_col[i] = make_float4(c[0], c[1], c[2], 0.0f);
+      }
+    }
+    warp_count(&ctr->n_visible, visible);
+    warp_count(&ctr->n_emitting, emitting);
+  }
+}
+
+// Reference VRAM model: 3-sigma per-axis AABB, strict on-image test, floor /
+// clip tile rectangle (postprocess.py:118-135), in fp32 on the same
+// projection as the renderer.
+__global__ void __launch_bounds__(256) vram3s_kernel(sgs_params P, SgsCam cam, int tile_px, Counters* ctr) {
+  const int64_t n = P.n;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int tiles_x = (cam.width + tile_px - 1) / tile_px, tiles_y = (cam.height + tile_px - 1) / tile_px;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
+    const int64_t i = base + threadIdx.x;
+    bool on = false;
+    unsigned long long ent = 0;
+    if (i < n) {
+      float pos[3] = {P.position[3 * i], P.position[3 * i + 1], P.position[3 * i + 2]};
+      float4 q4 = reinterpret_cast<const float4*>(P.quat)[i];
+      float quat[4] = {q4.x, q4.y, q4.z, q4.w};
+      float ls[3] = {P.log_scale[3 * i], P.log_scale[3 * i + 1], P.log_scale[3 * i + 2]};
+      SgsProj pr;
+      sgs_project(pos, quat, ls, 1.0f, 1.0f, &cam, &pr);
+      if (pr.visible) {
+        float rx = F_MUL(3.0f, F_SQRT(pr.cov00)), ry = F_MUL(3.0f, F_SQRT(pr.cov11));
+        float x0 = F_SUB(pr.mx, rx), x1 = F_ADD(pr.mx, rx), y0 = F_SUB(pr.my, ry), y1 = F_ADD(pr.my, ry);
+        on = x1 > 0.0f && x0 < (float)cam.width && y1 > 0.0f && y0 < (float)cam.height;
+        if (on) {
+          float t = (float)tile_px;
+          int tx0 = (int)fminf(fmaxf(F_FLOOR(F_DIV(x0, t)), 0.0f), (float)(tiles_x - 1));
+          int tx1 = (int)fminf(fmaxf(F_FLOOR(F_DIV(x1, t)), 0.0f), (float)(tiles_x - 1));
+          int ty0 = (int)fminf(fmaxf(F_FLOOR(F_DIV(y0, t)), 0.0f), (float)(tiles_y - 1));
+          int ty1 = (int)fminf(fmaxf(F_FLOOR(F_DIV(y1, t)), 0.0f), (float)(tiles_y - 1));
+          ent = (unsigned long long)(tx1 - tx0 + 1) * (unsigned long long)(ty1 - ty0 + 1);
+        }
+      }
+    }
+    warp_count(&ctr->vram3s_visible, on);
+    for (int o = 16; o > 0; o >>= 1) ent += __shfl_xor_sync(0xffffffffu, ent, o);
+    if ((threadIdx.x & 31) == 0 && ent) atomicAdd(&ctr->vram3s_entries, ent);
+  }
+}
+
+int launch_preprocess(const sgs_params& P, const SgsCam& cam, const sgs_workspace* ws, const Layout& lo,
+                      cudaStream_t st) {
+  Counters* ctr = at<Counters>(ws, lo.counters);
+  int grid = persistent_grid((uint64_t)P.n, 256, 8);
+  preprocess_kernel<<<grid, 256, 0, st>>>(P, cam, at<float4>(ws, lo.rec_geo), at<float4>(ws, lo.rec_con),
+                                          at<float4>(ws, lo.rec_col), at<uint32_t>(ws, lo.depth_key),
+                                          at<uint2>(ws, lo.rect), at<uint32_t>(ws, lo.tiles_touched), ctr);
+  SGS_LAUNCH_CHECK("preprocess_kernel");
+  return SGS_OK;
+}
+
+int launch_vram3s(const sgs_params& P, const SgsCam& cam, int tile_px, Counters* ctr, cudaStream_t st) {
+  int grid = persistent_grid((uint64_t)P.n, 256, 8);
+  vram3s_kernel<<<grid, 256, 0, st>>>(P, cam, tile_px, ctr);
+  SGS_LAUNCH_CHECK("vram3s_kernel");
+  return SGS_OK;
+}
+
+}  // namespace sgs

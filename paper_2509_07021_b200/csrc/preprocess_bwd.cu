@@ -1,0 +1,198 @@
+// preprocess_bwd.cu -- K7: per-primitive chain rule from the raster partials
+// (dL/dcolor, conic moments) to every parameter class and the soft masks.
+// Replaces /root/reference/pkg/src/sgsplat/render.py:575-636 (conic ->
+// cov2d -> Sigma / J -> quaternion / log-scale / position, SG color path,
+// np.add.at scatter) and adds
+//   dL/dm_p = o   dL/do_eff          (o_eff = m_p o)
+//   dL/dm_l = (dL/dc_pre . a_l) e_l  (c_pre = diffuse + sum_l m_l a_l e_l)
+// One thread per primitive; every output row is written (zeros for
+// primitives no pixel kept), so outputs need no memset.
+#include "common.cuh"
+
+namespace sgs {
+
+constexpr int kG2 = 9;
+
+__global__ void __launch_bounds__(128) preprocess_bwd_kernel(sgs_params P, SgsCam cam,
+                                                             const float* __restrict__ grad2d, sgs_grads out) {
+  const int64_t n = P.n;
+  const int L = P.n_lobes;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float gv[kG2];
+    bool any = false;
+#pragma unroll
+    for (int c = 0; c < kG2; ++c) {
+      gv[c] = grad2d[i * kG2 + c];
+      any |= gv[c] != 0.0f;
+    }
+    float d_pos[3] = {0, 0, 0}, d_q[4] = {0, 0, 0, 0}, d_ls[3] = {0, 0, 0}, d_diff[3] = {0, 0, 0};
+    float d_op = 0.0f, d_pm = 0.0f;
+    const float* Wr = cam.R;
+    const float pos[3] = {P.position[3 * i], P.position[3 * i + 1], P.position[3 * i + 2]};
+    const float op = P.opacity[i];
+    const float pm = P.prim_mask ? P.prim_mask[i] : 1.0f;
+
+    if (any) {
+      // ---------------- forward recompute
+      const float x = Wr[0] * pos[0] + Wr[1] * pos[1] + Wr[2] * pos[2] + cam.t[0];
+      const float y = Wr[3] * pos[0] + Wr[4] * pos[1] + Wr[5] * pos[2] + cam.t[1];
+      const float z = Wr[6] * pos[0] + Wr[7] * pos[1] + Wr[8] * pos[2] + cam.t[2];
+      const float4 q4 = reinterpret_cast<const float4*>(P.quat)[i];
+      const float qn = sqrtf(q4.x * q4.x + q4.y * q4.y + q4.z * q4.z + q4.w * q4.w);
+      const float qw = q4.x / qn, qx = q4.y / qn, qy = q4.z / qn, qz = q4.w / qn;
+      float R[9];
+      sgs_quat_to_rot(qw, qx, qy, qz, R);
+      float D[3];
+      for (int k = 0; k < 3; ++k) D[k] = expf(2.0f * P.log_scale[3 * i + k]);
+      float S[9];
+      for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b)
+          S[3 * a + b] = R[3 * a] * D[0] * R[3 * b] + R[3 * a + 1] * D[1] * R[3 * b + 1] + R[3 * a + 2] * D[2] * R[3 * b + 2];
+      const float iz = 1.0f / z, iz2 = iz * iz;
+      const float J00 = cam.fx * iz, J02 = -cam.fx * x * iz2, J11 = cam.fy * iz, J12 = -cam.fy * y * iz2;
+      float M[6];
+      for (int k = 0; k < 3; ++k) {
+        M[k] = J00 * Wr[k] + J02 * Wr[6 + k];
+        M[3 + k] = J11 * Wr[3 + k] + J12 * Wr[6 + k];
+      }
+      float MS[6];  // M Sigma
+      for (int r = 0; r < 2; ++r)
+        for (int k = 0; k < 3; ++k)
+          MS[3 * r + k] = M[3 * r] * S[k] + M[3 * r + 1] * S[3 + k] + M[3 * r + 2] * S[6 + k];
+      const float ca = MS[0] * M[0] + MS[1] * M[1] + MS[2] * M[2] + SGS_LOWPASS;
+      const float cb = MS[0] * M[3] + MS[1] * M[4] + MS[2] * M[5];
+      const float cc = MS[3] * M[3] + MS[4] * M[4] + MS[5] * M[5] + SGS_LOWPASS;
+      const float det = ca * cc - cb * cb;
+      const float k00 = cc / det, k01 = -cb / det, k11 = ca / det;
+
+      // ---------------- 2D partials
+      const float m0 = gv[3], m1x = gv[4], m1y = gv[5], m2xx = gv[6], m2xy = gv[7], m2yy = gv[8];
+      const float dmx = -2.0f * (k00 * m1x + k01 * m1y);
+      const float dmy = -2.0f * (k01 * m1x + k11 * m1y);
+      const float oeff = op * pm;
+      const float d_oeff = oeff > 0.0f ? -2.0f * m0 / oeff : 0.0f;
+      d_op = pm * d_oeff;
+      d_pm = op * d_oeff;
+      // d_cov = -K dK K (K = conic, dK symmetric with off-diagonals m2xy)
+      const float t00 = k00 * m2xx + k01 * m2xy, t01 = k00 * m2xy + k01 * m2yy;
+      const float t10 = k01 * m2xx + k11 * m2xy, t11 = k01 * m2xy + k11 * m2yy;
+      const float dc00 = -(t00 * k00 + t01 * k01), dc01 = -(t00 * k01 + t01 * k11);
+      const float dc10 = -(t10 * k00 + t11 * k01), dc11 = -(t10 * k01 + t11 * k11);
+      // dSigma = M^T dcov M ; dM = 2 dcov M Sigma (dcov symmetric)
+      float dS[9];
+      for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b)
+          dS[3 * a + b] = M[a] * (dc00 * M[b] + dc01 * M[3 + b]) + M[3 + a] * (dc10 * M[b] + dc11 * M[3 + b]);
+      float dM[6];
+      for (int k = 0; k < 3; ++k) {
+        dM[k] = 2.0f * (dc00 * MS[k] + dc01 * MS[3 + k]);
+        dM[3 + k] = 2.0f * (dc10 * MS[k] + dc11 * MS[3 + k]);
+      }
+      // dJ = dM W^T (only J00, J02, J11, J12 are live)
+      const float dJ00 = dM[0] * Wr[0] + dM[1] * Wr[1] + dM[2] * Wr[2];
+      const float dJ02 = dM[0] * Wr[6] + dM[1] * Wr[7] + dM[2] * Wr[8];
+      const float dJ11 = dM[3] * Wr[3] + dM[4] * Wr[4] + dM[5] * Wr[5];
+      const float dJ12 = dM[3] * Wr[6] + dM[4] * Wr[7] + dM[5] * Wr[8];
+      const float iz3 = iz2 * iz;
+      float dpc0 = dJ02 * (-cam.fx * iz2) + dmx * cam.fx * iz;
+      float dpc1 = dJ12 * (-cam.fy * iz2) + dmy * cam.fy * iz;
+      float dpc2 = dJ00 * (-cam.fx * iz2) + dJ11 * (-cam.fy * iz2) + dJ02 * (2.0f * cam.fx * x * iz3) +
+                   dJ12 * (2.0f * cam.fy * y * iz3) - dmx * cam.fx * x * iz2 - dmy * cam.fy * y * iz2;
+      for (int k = 0; k < 3; ++k) d_pos[k] = Wr[k] * dpc0 + Wr[3 + k] * dpc1 + Wr[6 + k] * dpc2;
+
+      // Sigma = R D R^T
+      float dR[9];
+      for (int a = 0; a < 3; ++a)
+        for (int k = 0; k < 3; ++k)
+          dR[3 * a + k] = 2.0f * (dS[3 * a] * R[k] + dS[3 * a + 1] * R[3 + k] + dS[3 * a + 2] * R[6 + k]) * D[k];
+      for (int k = 0; k < 3; ++k) {
+        float s = 0.0f;
+        for (int a = 0; a < 3; ++a)
+          s += R[3 * a + k] * (dS[3 * a] * R[k] + dS[3 * a + 1] * R[3 + k] + dS[3 * a + 2] * R[6 + k]);
+        d_ls[k] = 2.0f * D[k] * s;
+      }
+      // d qhat = sum_ij dR_ij dR_ij/dqhat (render.py:217-229)
+      const float gw = 2.0f * (-qz * dR[1] + qy * dR[2] + qz * dR[3] - qx * dR[5] - qy * dR[6] + qx * dR[7]);
+      const float gx = 2.0f * (qy * dR[1] + qz * dR[2] + qy * dR[3] - 2.0f * qx * dR[4] - qw * dR[5] + qz * dR[6] +
+                               qw * dR[7] - 2.0f * qx * dR[8]);
+      const float gy = 2.0f * (-2.0f * qy * dR[0] + qx * dR[1] + qw * dR[2] + qx * dR[3] + qz * dR[5] - qw * dR[6] +
+                               qz * dR[7] - 2.0f * qy * dR[8]);
+      const float gz = 2.0f * (-2.0f * qz * dR[0] - qw * dR[1] + qx * dR[2] + qw * dR[3] - 2.0f * qz * dR[4] +
+                               qy * dR[5] + qx * dR[6] + qy * dR[7]);
+      const float qd = qw * gw + qx * gx + qy * gy + qz * gz;
+      d_q[0] = (gw - qw * qd) / qn;
+      d_q[1] = (gx - qx * qd) / qn;
+      d_q[2] = (gy - qy * qd) / qn;
+      d_q[3] = (gz - qz * qd) / qn;
+    }
+
+    // ---------------- color path (all lobes, masked ones too: dL/dm_l)
+    const float v0r = pos[0] - cam.C[0], v1r = pos[1] - cam.C[1], v2r = pos[2] - cam.C[2];
+    const float rd = sqrtf(v0r * v0r + v1r * v1r + v2r * v2r);
+    const float v0 = v0r / rd, v1 = v1r / rd, v2 = v2r / rd;
+    float cpre[3] = {P.diffuse[3 * i], P.diffuse[3 * i + 1], P.diffuse[3 * i + 2]};
+    float e[SGS_MAX_LOBES], dotv[SGS_MAX_LOBES];
+    for (int l = 0; l < L; ++l) {
+      const float* u = P.axis_raw + (i * L + l) * 3;
+      const float un = sqrtf(u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
+      dotv[l] = (u[0] * v0 + u[1] * v1 + u[2] * v2) / un;
+      e[l] = expf(P.sharpness[i * L + l] * (dotv[l] - 1.0f));
+      const float m = P.lobe_mask[i * L + l];
+      if (m != 0.0f)
+        for (int c = 0; c < 3; ++c) cpre[c] += e[l] * m * P.amplitude[(i * L + l) * 3 + c];
+    }
+    float dcp[3];
+    for (int c = 0; c < 3; ++c) {
+      dcp[c] = cpre[c] > 0.0f ? gv[c] : 0.0f;
+      d_diff[c] = dcp[c];
+    }
+    float dv[3] = {0, 0, 0};
+    for (int l = 0; l < L; ++l) {
+      const float* u = P.axis_raw + (i * L + l) * 3;
+      const float* a = P.amplitude + (i * L + l) * 3;
+      const float m = P.lobe_mask[i * L + l];
+      const float s = P.sharpness[i * L + l];
+      const float da = dcp[0] * a[0] + dcp[1] * a[1] + dcp[2] * a[2];
+      const float em = e[l] * m;
+      for (int c = 0; c < 3; ++c) out.amplitude[(i * L + l) * 3 + c] = dcp[c] * em;
+      const float ga = da * em;
+      out.sharpness[i * L + l] = ga * (dotv[l] - 1.0f);
+      if (out.lobe_mask) out.lobe_mask[i * L + l] = da * e[l];
+      const float un = sqrtf(u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
+      const float mu0 = u[0] / un, mu1 = u[1] / un, mu2 = u[2] / un;
+      // d mu = ga s v ; d u = (I - mu mu^T) d mu / |u|
+      const float gs = ga * s;
+      const float dm0 = gs * v0, dm1 = gs * v1, dm2 = gs * v2;
+      const float pr = mu0 * dm0 + mu1 * dm1 + mu2 * dm2;
+      out.axis_raw[(i * L + l) * 3 + 0] = (dm0 - mu0 * pr) / un;
+      out.axis_raw[(i * L + l) * 3 + 1] = (dm1 - mu1 * pr) / un;
+      out.axis_raw[(i * L + l) * 3 + 2] = (dm2 - mu2 * pr) / un;
+      dv[0] += gs * mu0;
+      dv[1] += gs * mu1;
+      dv[2] += gs * mu2;
+    }
+    const float pv = v0 * dv[0] + v1 * dv[1] + v2 * dv[2];
+    d_pos[0] += (dv[0] - v0 * pv) / rd;
+    d_pos[1] += (dv[1] - v1 * pv) / rd;
+    d_pos[2] += (dv[2] - v2 * pv) / rd;
+
+    for (int k = 0; k < 3; ++k) {
+      out.position[3 * i + k] = d_pos[k];
+      out.log_scale[3 * i + k] = d_ls[k];
+      out.diffuse[3 * i + k] = d_diff[k];
+    }
+    reinterpret_cast<float4*>(out.quat)[i] = make_float4(d_q[0], d_q[1], d_q[2], d_q[3]);
+    out.opacity[i] = d_op;
+    if (out.prim_mask) out.prim_mask[i] = d_pm;
+  }
+}
+
+int launch_preprocess_bwd(const sgs_params& P, const SgsCam& cam, const float* grad2d, const sgs_grads& g,
+                          cudaStream_t st) {
+  int grid = persistent_grid((uint64_t)P.n, 128, 16);
+  preprocess_bwd_kernel<<<grid, 128, 0, st>>>(P, cam, grad2d, g);
+  SGS_LAUNCH_CHECK("preprocess_bwd_kernel");
+  return SGS_OK;
+}
+
+}  // namespace sgs

@@ -1,0 +1,388 @@
+// sgs_geom.h -- per-primitive preprocess math shared by the sm_100a kernels and
+// the CPU tiled restatement under oracle/.
+//
+// Everything that decides a tile key, a sorted order, a per-tile range or a
+// visibility count flows through this header: camera transform, EWA
+// covariance projection, conic, the opacity-aware support radius, the tile
+// rectangle and the exact ellipse-vs-tile test.  Bit-exactness between the
+// GPU and the CPU restatement is guaranteed by construction:
+//   * every operation is an explicitly IEEE-rounded primitive (F_MUL/F_ADD/
+//     F_FMA ...): on the device these are the __f*_rn intrinsics, which ptxas
+//     never contracts; on the host the oracle is compiled with
+//     -ffp-contract=off and no fast-math, and fmaf is the correctly rounded
+//     fused multiply-add;
+//   * exp and log are evaluated by the polynomial restatements below (Cody-
+//     Waite reduction + minimax polynomial), not by libdevice / glibc, whose
+//     last-bit behaviour differs.
+//
+// Semantics follow the reference renderer:
+//   _prepare            /root/reference/pkg/src/sgsplat/render.py:259-317
+//   quat_to_rot         /root/reference/pkg/src/sgsplat/render.py:208-214
+//   Camera/pixel model  /root/reference/pkg/src/sgsplat/render.py:30-76, 333-337
+//   SG lobe color       /root/reference/pkg/src/sgsplat/render.py:298-305
+//                       (independent form: sg.py:55-79 eval_sg_lobe/eval_color)
+// The reference blends every visible primitive against every pixel (no
+// spatial cutoff).  This build bins with the opacity-aware support
+//   o_eff * exp(-q/2) >= SGS_EPS   <=>   q <= qmax = 2 (ln o_eff - ln SGS_EPS)
+// with SGS_EPS = 1e-7, which SURVEY.md §0.4 measured at 2.1e-7 max-abs image
+// error against the no-cutoff reference (the 3-sigma rule is 2.2e-3).
+#pragma once
+
+#include <stdint.h>
+#include <math.h>
+#include <string.h>
+
+#if defined(__CUDACC__)
+#define SGS_HD __host__ __device__ __forceinline__
+#else
+#define SGS_HD static inline
+#endif
+
+#if defined(__CUDA_ARCH__)
+#define F_MUL(a, b) __fmul_rn((a), (b))
+#define F_ADD(a, b) __fadd_rn((a), (b))
+#define F_SUB(a, b) __fsub_rn((a), (b))
+#define F_DIV(a, b) __fdiv_rn((a), (b))
+#define F_SQRT(a) __fsqrt_rn((a))
+#define F_FMA(a, b, c) __fmaf_rn((a), (b), (c))
+#define F_RINT(a) rintf((a))
+#define F_FLOOR(a) floorf((a))
+#else
+#define F_MUL(a, b) ((float)(a) * (float)(b))
+#define F_ADD(a, b) ((float)(a) + (float)(b))
+#define F_SUB(a, b) ((float)(a) - (float)(b))
+#define F_DIV(a, b) ((float)(a) / (float)(b))
+#define F_SQRT(a) sqrtf((a))
+#define F_FMA(a, b, c) fmaf((a), (b), (c))
+#define F_RINT(a) rintf((a))
+#define F_FLOOR(a) floorf((a))
+#endif
+
+#define SGS_TILE 16
+#define SGS_ALPHA_MAX 0.99f      // render.py:24
+#define SGS_T_CUTOFF 1e-4f       // render.py:25
+#define SGS_LOWPASS 0.3f         // render.py:26
+#define SGS_EPS 1e-7f            // opacity-aware support threshold
+#define SGS_LN_EPS (-16.11809565095832f)  // ln(1e-7)
+#define SGS_LOG2E 1.4426950408889634f
+#define SGS_MAX_LOBES 8
+
+SGS_HD int min_i32_(int a, int b) { return a < b ? a : b; }
+
+SGS_HD float sgs_bits_to_float(uint32_t u) {
+#if defined(__CUDA_ARCH__)
+  return __uint_as_float(u);
+#else
+  float f;
+  memcpy(&f, &u, 4);
+  return f;
+#endif
+}
+
+SGS_HD uint32_t sgs_float_to_bits(float f) {
+#if defined(__CUDA_ARCH__)
+  return __float_as_uint(f);
+#else
+  uint32_t u;
+  memcpy(&u, &f, 4);
+  return u;
+#endif
+}
+
+// exp(x): Cody-Waite reduction by ln2 (hi part has 9 significant bits so
+// k*ln2_hi is exact), degree-6 polynomial on |r| <= ln2/2 (Cephes expf
+// coefficients), then an exact power-of-two scale.
+SGS_HD float sgs_expf(float x) {
+  if (!(x == x)) return x;
+  if (x > 88.72283f) return INFINITY;
+  if (x < -103.97208f) return 0.0f;
+  float kf = F_RINT(F_MUL(x, 1.44269504088896341f));
+  float r = F_FMA(kf, -0.693359375f, x);
+  r = F_FMA(kf, 2.12194440e-4f, r);
+  float p = 1.9875691500e-4f;
+  p = F_FMA(p, r, 1.3981999507e-3f);
+  p = F_FMA(p, r, 8.3334519073e-3f);
+  p = F_FMA(p, r, 4.1665795894e-2f);
+  p = F_FMA(p, r, 1.6666665459e-1f);
+  p = F_FMA(p, r, 5.0000001201e-1f);
+  p = F_FMA(F_MUL(p, r), r, r);
+  p = F_ADD(p, 1.0f);
+  int k = (int)kf;
+  if (k > 127) {
+    p = F_MUL(p, 2.0f);
+    k -= 1;
+  }
+  if (k < -125) {
+    p = F_MUL(p, 5.421010862427522e-20f);  // 2^-64
+    k += 64;
+  }
+  return F_MUL(p, sgs_bits_to_float((uint32_t)(k + 127) << 23));
+}
+
+// ln(x) for finite x > 0: split x = m * 2^e with m in [sqrt(1/2), sqrt(2)),
+// f = m - 1 (exact), Cephes logf polynomial, ln2 in two parts.
+SGS_HD float sgs_logf(float x) {
+  if (!(x > 0.0f)) return (x == 0.0f) ? -INFINITY : NAN;
+  if (x == INFINITY) return x;
+  int e = 0;
+  if (x < 1.17549435e-38f) {  // subnormal: scale into the normal range
+    x = F_MUL(x, 8388608.0f);
+    e = -23;
+  }
+  uint32_t bits = sgs_float_to_bits(x);
+  e += (int)((bits >> 23) & 0xffu) - 127;
+  float m = sgs_bits_to_float((bits & 0x007fffffu) | 0x3f800000u);
+  if (m > 1.41421356f) {
+    m = F_MUL(m, 0.5f);
+    e += 1;
+  }
+  float f = F_SUB(m, 1.0f);
+  float z = F_MUL(f, f);
+  float y = 7.0376836292e-2f;
+  y = F_FMA(y, f, -1.1514610310e-1f);
+  y = F_FMA(y, f, 1.1676998740e-1f);
+  y = F_FMA(y, f, -1.2420140846e-1f);
+  y = F_FMA(y, f, 1.4249322787e-1f);
+  y = F_FMA(y, f, -1.6668057665e-1f);
+  y = F_FMA(y, f, 2.0000714765e-1f);
+  y = F_FMA(y, f, -2.4999993993e-1f);
+  y = F_FMA(y, f, 3.3333331174e-1f);
+  y = F_MUL(F_MUL(y, f), z);
+  float ef = (float)e;
+  y = F_FMA(ef, -2.12194440e-4f, y);
+  y = F_FMA(-0.5f, z, y);
+  float r = F_ADD(f, y);
+  return F_FMA(ef, 0.693359375f, r);
+}
+
+// Camera in the reference convention: rows of R are (right, down, forward),
+// p_cam = R x + t, pixel = (fx x/z + cx, fy y/z + cy), pixel (row, col) has
+// center (col + 0.5, row + 0.5).  C = -R^T t is the camera center.
+typedef struct SgsCam {
+  float R[9];
+  float t[3];
+  float C[3];
+  float fx, fy, cx, cy;
+  float near_z;
+  int32_t width, height;
+  int32_t tiles_x, tiles_y;
+  int32_t tile_y0, tile_y1;  // tile-row window [y0, y1) for strip renders
+} SgsCam;
+
+// Projected primitive: everything the binning stage and the forward raster
+// read.  conic/cov are the symmetric 2x2 (00, 01, 11) entries.
+typedef struct SgsProj {
+  float depth;
+  float mx, my;
+  float cov00, cov01, cov11;
+  float con00, con01, con11;
+  float o_eff;
+  float qmax;
+  int32_t tx0, ty0, tx1, ty1;
+  int32_t visible;   // z > near (render.py:263)
+  int32_t emits;     // visible, o_eff > eps, support rectangle on the image
+} SgsProj;
+
+// render.py:208-214, w-first unit quaternion -> rotation matrix rows.
+SGS_HD void sgs_quat_to_rot(float w, float x, float y, float z, float R[9]) {
+  float xx = F_MUL(x, x), yy = F_MUL(y, y), zz = F_MUL(z, z);
+  float xy = F_MUL(x, y), xz = F_MUL(x, z), yz = F_MUL(y, z);
+  float wx = F_MUL(w, x), wy = F_MUL(w, y), wz = F_MUL(w, z);
+  R[0] = F_SUB(1.0f, F_MUL(2.0f, F_ADD(yy, zz)));
+  R[1] = F_MUL(2.0f, F_SUB(xy, wz));
+  R[2] = F_MUL(2.0f, F_ADD(xz, wy));
+  R[3] = F_MUL(2.0f, F_ADD(xy, wz));
+  R[4] = F_SUB(1.0f, F_MUL(2.0f, F_ADD(xx, zz)));
+  R[5] = F_MUL(2.0f, F_SUB(yz, wx));
+  R[6] = F_MUL(2.0f, F_SUB(xz, wy));
+  R[7] = F_MUL(2.0f, F_ADD(yz, wx));
+  R[8] = F_SUB(1.0f, F_MUL(2.0f, F_ADD(xx, yy)));
+}
+
+SGS_HD float sgs_dot3(float a0, float a1, float a2, float b0, float b1, float b2) {
+  return F_ADD(F_ADD(F_MUL(a0, b0), F_MUL(a1, b1)), F_MUL(a2, b2));
+}
+
+// Geometry of one primitive (render.py:262-292 plus the support rectangle).
+SGS_HD void sgs_project(const float pos[3], const float quat[4], const float ls[3],
+                        float opacity, float pmask, const SgsCam* cam, SgsProj* o) {
+  const float* W = cam->R;
+  float x = F_ADD(sgs_dot3(W[0], W[1], W[2], pos[0], pos[1], pos[2]), cam->t[0]);
+  float y = F_ADD(sgs_dot3(W[3], W[4], W[5], pos[0], pos[1], pos[2]), cam->t[1]);
+  float z = F_ADD(sgs_dot3(W[6], W[7], W[8], pos[0], pos[1], pos[2]), cam->t[2]);
+  o->depth = z;
+  o->visible = z > cam->near_z;
+  o->emits = 0;
+  o->tx0 = o->ty0 = 0;
+  o->tx1 = o->ty1 = -1;
+  if (!o->visible) return;
+
+  o->mx = F_ADD(F_DIV(F_MUL(cam->fx, x), z), cam->cx);
+  o->my = F_ADD(F_DIV(F_MUL(cam->fy, y), z), cam->cy);
+
+  // Sigma = R diag(exp(2 ls)) R^T
+  float qn = F_SQRT(F_ADD(F_ADD(F_ADD(F_MUL(quat[0], quat[0]), F_MUL(quat[1], quat[1])),
+                                F_MUL(quat[2], quat[2])), F_MUL(quat[3], quat[3])));
+  float R[9];
+  sgs_quat_to_rot(F_DIV(quat[0], qn), F_DIV(quat[1], qn), F_DIV(quat[2], qn),
+                  F_DIV(quat[3], qn), R);
+  float D0 = sgs_expf(F_MUL(2.0f, ls[0]));
+  float D1 = sgs_expf(F_MUL(2.0f, ls[1]));
+  float D2 = sgs_expf(F_MUL(2.0f, ls[2]));
+  float S[9];
+  for (int i = 0; i < 3; ++i)
+    for (int k = i; k < 3; ++k) {
+      float s = F_ADD(F_ADD(F_MUL(F_MUL(R[3 * i + 0], D0), R[3 * k + 0]),
+                            F_MUL(F_MUL(R[3 * i + 1], D1), R[3 * k + 1])),
+                      F_MUL(F_MUL(R[3 * i + 2], D2), R[3 * k + 2]));
+      S[3 * i + k] = s;
+      S[3 * k + i] = s;
+    }
+
+  // J (render.py:278-282), M = J W (2x3)
+  float iz = F_DIV(1.0f, z);
+  float J00 = F_MUL(cam->fx, iz);
+  float J02 = -F_DIV(F_MUL(cam->fx, x), F_MUL(z, z));
+  float J11 = F_MUL(cam->fy, iz);
+  float J12 = -F_DIV(F_MUL(cam->fy, y), F_MUL(z, z));
+  float M0[3], M1[3];
+  for (int k = 0; k < 3; ++k) {
+    M0[k] = F_ADD(F_MUL(J00, W[k]), F_MUL(J02, W[6 + k]));
+    M1[k] = F_ADD(F_MUL(J11, W[3 + k]), F_MUL(J12, W[6 + k]));
+  }
+  // T = M Sigma, cov = T M^T
+  float T0[3], T1[3];
+  for (int k = 0; k < 3; ++k) {
+    T0[k] = sgs_dot3(M0[0], M0[1], M0[2], S[k], S[3 + k], S[6 + k]);
+    T1[k] = sgs_dot3(M1[0], M1[1], M1[2], S[k], S[3 + k], S[6 + k]);
+  }
+  float a = F_ADD(sgs_dot3(T0[0], T0[1], T0[2], M0[0], M0[1], M0[2]), SGS_LOWPASS);
+  float b = sgs_dot3(T0[0], T0[1], T0[2], M1[0], M1[1], M1[2]);
+  float c = F_ADD(sgs_dot3(T1[0], T1[1], T1[2], M1[0], M1[1], M1[2]), SGS_LOWPASS);
+  o->cov00 = a;
+  o->cov01 = b;
+  o->cov11 = c;
+  float det = F_SUB(F_MUL(a, c), F_MUL(b, b));
+  o->con00 = F_DIV(c, det);
+  o->con01 = -F_DIV(b, det);
+  o->con11 = F_DIV(a, det);
+
+  float oe = F_MUL(opacity, pmask);
+  o->o_eff = oe;
+  if (!(oe > SGS_EPS) || !(det > 0.0f)) {
+    o->qmax = 0.0f;
+    return;
+  }
+  float qmax = F_MUL(2.0f, F_SUB(sgs_logf(oe), SGS_LN_EPS));
+  o->qmax = qmax;
+  // exact bounding box of {d : d^T cov^-1 d <= qmax} is sqrt(qmax * cov_ii)
+  float rx = F_SQRT(F_MUL(qmax, a));
+  float ry = F_SQRT(F_MUL(qmax, c));
+  float x0 = F_SUB(o->mx, rx), x1 = F_ADD(o->mx, rx);
+  float y0 = F_SUB(o->my, ry), y1 = F_ADD(o->my, ry);
+  if (!(x1 > 0.0f && x0 < (float)cam->width && y1 > 0.0f && y0 < (float)cam->height)) return;
+  const float inv_tile = 1.0f / SGS_TILE;
+  float ftx0 = F_FLOOR(F_MUL(x0, inv_tile)), ftx1 = F_FLOOR(F_MUL(x1, inv_tile));
+  float fty0 = F_FLOOR(F_MUL(y0, inv_tile)), fty1 = F_FLOOR(F_MUL(y1, inv_tile));
+  float mxx = (float)(cam->tiles_x - 1);
+  ftx0 = fminf(fmaxf(ftx0, 0.0f), mxx);
+  ftx1 = fminf(fmaxf(ftx1, 0.0f), mxx);
+  fty0 = fminf(fmaxf(fty0, (float)cam->tile_y0), (float)(cam->tile_y1 - 1));
+  fty1 = fminf(fmaxf(fty1, (float)cam->tile_y0), (float)(cam->tile_y1 - 1));
+  if (!(y1 > (float)(cam->tile_y0 * SGS_TILE) && y0 < (float)(cam->tile_y1 * SGS_TILE))) return;
+  o->tx0 = (int32_t)ftx0;
+  o->tx1 = (int32_t)ftx1;
+  o->ty0 = (int32_t)fty0;
+  o->ty1 = (int32_t)fty1;
+  o->emits = 1;
+}
+
+// max over v in [v0, v1] of p(u, v) = a u^2 + b u v + c v^2 (c < 0).
+SGS_HD float sgs_seg_max_p(float a, float b, float c, float u, float v0, float v1) {
+  float v = -F_DIV(F_MUL(b, u), F_MUL(2.0f, c));
+  v = fminf(fmaxf(v, v0), v1);
+  return F_ADD(F_MUL(u, F_ADD(F_MUL(a, u), F_MUL(b, v))), F_MUL(F_MUL(c, v), v));
+}
+
+// Exact ellipse-vs-tile test on the packed raster record (see
+// sgs_pack_records): does any point of the tile's pixel-center box satisfy
+// p2 = A dx^2 + B dx dy + C dy^2 >= pmin?  The maximum of the negative-
+// definite form over the box is 0 when the mean lies inside the box, else it
+// lies on an edge facing the mean.  The raster evaluates a pair iff
+// p2(pixel) >= pmin, so this is the same support, tested per tile.
+SGS_HD int sgs_tile_hit(const float geo[4], const float con[4], const SgsCam* cam, int tx, int ty) {
+  const float mx = geo[0], my = geo[1], pmin = geo[3];
+  float bx0 = (float)(tx * SGS_TILE) + 0.5f;
+  float bx1 = (float)min_i32_(tx * SGS_TILE + SGS_TILE - 1, cam->width - 1) + 0.5f;
+  float by0 = (float)(ty * SGS_TILE) + 0.5f;
+  float by1 = (float)min_i32_(ty * SGS_TILE + SGS_TILE - 1, cam->height - 1) + 0.5f;
+  int in_x = mx >= bx0 && mx <= bx1;
+  int in_y = my >= by0 && my <= by1;
+  if (in_x && in_y) return 1;
+  float dx0 = F_SUB(bx0, mx), dx1 = F_SUB(bx1, mx);
+  float dy0 = F_SUB(by0, my), dy1 = F_SUB(by1, my);
+  float pmax = -INFINITY;
+  if (!in_x) {
+    float u = (mx < bx0) ? dx0 : dx1;
+    pmax = fmaxf(pmax, sgs_seg_max_p(con[0], con[1], con[2], u, dy0, dy1));
+  }
+  if (!in_y) {
+    float u = (my < by0) ? dy0 : dy1;
+    pmax = fmaxf(pmax, sgs_seg_max_p(con[2], con[1], con[0], u, dx0, dx1));
+  }
+  return pmax >= pmin;
+}
+
+// Packed tile rectangle: (tx0 | tx1 << 16, ty0 | ty1 << 16); empty when tx1 < tx0.
+SGS_HD uint32_t sgs_count_tiles(int tx0, int ty0, int tx1, int ty1, const float geo[4], const float con[4],
+                                const SgsCam* cam) {
+  uint32_t n = 0;
+  for (int ty = ty0; ty <= ty1; ++ty)
+    for (int tx = tx0; tx <= tx1; ++tx) n += (uint32_t)sgs_tile_hit(geo, con, cam, tx, ty);
+  return n;
+}
+
+// SG color for the camera-to-center view direction (render.py:294-305):
+//   c_pre = diffuse + sum_l m_l a_l exp(s_l (mu_l . v - 1)),  c = max(c_pre, 0)
+// Lobes with mask exactly 0 are skipped (bit-identical to multiplying by 0).
+SGS_HD void sgs_color(const float pos[3], const float diffuse[3], const float* axis,
+                      const float* sharp, const float* amp, const float* lmask, int L,
+                      const SgsCam* cam, float c_pre[3], float c[3]) {
+  float d0 = F_SUB(pos[0], cam->C[0]), d1 = F_SUB(pos[1], cam->C[1]), d2 = F_SUB(pos[2], cam->C[2]);
+  float r = F_SQRT(sgs_dot3(d0, d1, d2, d0, d1, d2));
+  float v0 = F_DIV(d0, r), v1 = F_DIV(d1, r), v2 = F_DIV(d2, r);
+  float acc0 = 0.0f, acc1 = 0.0f, acc2 = 0.0f;
+  for (int l = 0; l < L; ++l) {
+    float m = lmask[l];
+    if (m == 0.0f) continue;
+    const float* u = axis + 3 * l;
+    float un = F_SQRT(sgs_dot3(u[0], u[1], u[2], u[0], u[1], u[2]));
+    float dot = sgs_dot3(F_DIV(u[0], un), F_DIV(u[1], un), F_DIV(u[2], un), v0, v1, v2);
+    float e = F_MUL(sgs_expf(F_MUL(sharp[l], F_SUB(dot, 1.0f))), m);
+    acc0 = F_ADD(acc0, F_MUL(e, amp[3 * l + 0]));
+    acc1 = F_ADD(acc1, F_MUL(e, amp[3 * l + 1]));
+    acc2 = F_ADD(acc2, F_MUL(e, amp[3 * l + 2]));
+  }
+  c_pre[0] = F_ADD(diffuse[0], acc0);
+  c_pre[1] = F_ADD(diffuse[1], acc1);
+  c_pre[2] = F_ADD(diffuse[2], acc2);
+  c[0] = fmaxf(c_pre[0], 0.0f);
+  c[1] = fmaxf(c_pre[1], 0.0f);
+  c[2] = fmaxf(c_pre[2], 0.0f);
+}
+
+// Raster record packing: the forward kernel evaluates
+//   p2 = A dx^2 + B dx dy + C dy^2  (= -q/2 * log2 e),  G = 2^p2,
+// and skips the pair when p2 < pmin (= -qmax/2 * log2 e), i.e. q > qmax.
+//   geo = (mx, my, o_eff, pmin), con = (A, B, C, 0)
+SGS_HD void sgs_pack_geo(const SgsProj* p, float geo[4], float con[4]) {
+  const float k = -0.5f * SGS_LOG2E;
+  geo[0] = p->mx;
+  geo[1] = p->my;
+  geo[2] = p->o_eff;
+  geo[3] = F_MUL(k, p->qmax);
+  con[0] = F_MUL(k, p->con00);
+  con[1] = F_MUL(2.0f * k, p->con01);
+  con[2] = F_MUL(k, p->con11);
+  con[3] = 0.0f;
+}

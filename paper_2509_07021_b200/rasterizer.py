@@ -1,0 +1,333 @@
+"""Device-side render pipeline: PyTorch owns memory and streams, libsgs.so
+does every computation.
+
+``Rasterizer.forward`` = preprocess (K1) -> bin (K2-K4) -> raster (K5) and
+``Rasterizer.backward`` = raster backward (K6) -> preprocess backward (K7),
+all enqueued on the current torch stream through the C ABI.  There is no
+CPU fallback: a missing or unloadable libsgs.so raises.
+
+Workspaces are single torch byte tensors carved by the library, so
+``torch.cuda.max_memory_allocated`` sees all render VRAM (the paper's VRAM
+protocol).  The tile-entry capacity grows geometrically on
+overflow; overflow is detected from the device counters (one 56-byte D2H
+read) when ``check=True`` or by ``Frame.ensure_ok()``.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _ffi
+from .camera import to_sgs
+
+GRAD_FIELDS = ("position", "quat", "log_scale", "opacity", "diffuse", "axis_raw", "sharpness",
+               "amplitude")
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _stream_ptr() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _dev_f32(a, device) -> torch.Tensor:
+    if isinstance(a, torch.Tensor):
+        return a.detach().to(device=device, dtype=torch.float32).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.float32))).to(device)
+
+
+class GaussianTensors:
+    """Device float32 SoA of one scene (SceneParams layout + soft masks)."""
+
+    def __init__(self, position, quat, log_scale, opacity, diffuse, axis_raw, sharpness, amplitude,
+                 lobe_mask=None, prim_mask=None):
+        self.position = position
+        self.quat = quat
+        self.log_scale = log_scale
+        self.opacity = opacity
+        self.diffuse = diffuse
+        self.axis_raw = axis_raw
+        self.sharpness = sharpness
+        self.amplitude = amplitude
+        n, L = position.shape[0], axis_raw.shape[1] if axis_raw.dim() == 3 else 0
+        if lobe_mask is None:
+            lobe_mask = torch.ones((n, L), dtype=torch.float32, device=position.device)
+        self.lobe_mask = lobe_mask
+        self.prim_mask = prim_mask
+        self._check()
+
+    def _check(self):
+        n = self.position.shape[0]
+        L = self.n_lobes
+        shapes = {"position": (n, 3), "quat": (n, 4), "log_scale": (n, 3), "opacity": (n,),
+                  "diffuse": (n, 3), "axis_raw": (n, L, 3), "sharpness": (n, L),
+                  "amplitude": (n, L, 3), "lobe_mask": (n, L)}
+        for k, shp in shapes.items():
+            t = getattr(self, k)
+            if tuple(t.shape) != shp:
+                raise ValueError(f"{k} has shape {tuple(t.shape)}, expected {shp}")
+            if t.dtype != torch.float32 or not t.is_contiguous() or not t.is_cuda:
+                raise ValueError(f"{k} must be a contiguous float32 CUDA tensor")
+        if self.prim_mask is not None and tuple(self.prim_mask.shape) != (n,):
+            raise ValueError("prim_mask must have shape (N,)")
+
+    @property
+    def n(self) -> int:
+        return int(self.position.shape[0])
+
+    @property
+    def n_lobes(self) -> int:
+        return int(self.axis_raw.shape[1])
+
+    @property
+    def device(self):
+        return self.position.device
+
+    @classmethod
+    def from_arrays(cls, p, device="cuda", prim_mask=None) -> "GaussianTensors":
+        """From any object with SceneParams attributes (numpy or torch; the
+        reference's f64 SceneParams, this package's SceneArrays, ...).  A bool
+        lobe_mask becomes 0/1 floats; ``prim_mask`` falls back to
+        ``p.prim_mask`` when present."""
+        kw = {f: _dev_f32(getattr(p, f), device) for f in GRAD_FIELDS}
+        lm = getattr(p, "lobe_mask", None)
+        kw["lobe_mask"] = None if lm is None else _dev_f32(lm, device)
+        pm = prim_mask if prim_mask is not None else getattr(p, "prim_mask", None)
+        kw["prim_mask"] = None if pm is None else _dev_f32(pm, device)
+        return cls(**kw)
+
+    def c_params(self) -> _ffi.SgsParams:
+        s = _ffi.SgsParams()
+        for f in GRAD_FIELDS + ("lobe_mask",):
+            setattr(s, f, _ptr(getattr(self, f)))
+        s.prim_mask = _ptr(self.prim_mask)
+        s.n = self.n
+        s.n_lobes = self.n_lobes
+        return s
+
+
+class Workspace:
+    """One device byte buffer carved by libsgs.so for (N, L, W, H, capacity)."""
+
+    def __init__(self, n, n_lobes, width, height, capacity, sort_mode, device):
+        self.desc = _ffi.SgsWorkspace()
+        self.desc.n, self.desc.n_lobes = int(n), int(n_lobes)
+        self.desc.width, self.desc.height = int(width), int(height)
+        self.desc.sort_mode = int(sort_mode)
+        self.desc.entry_capacity = int(capacity)
+        nbytes = C.c_uint64()
+        _ffi.call("sgs_workspace_size", C.byref(self.desc), C.byref(nbytes))
+        self.buf = torch.empty(int(nbytes.value), dtype=torch.uint8, device=device)
+        self.desc.base = self.buf.data_ptr()
+        self.desc.bytes = int(nbytes.value)
+
+    @property
+    def capacity(self) -> int:
+        return int(self.desc.entry_capacity)
+
+    @property
+    def nbytes(self) -> int:
+        return int(self.desc.bytes)
+
+    def stats(self) -> dict:
+        s = _ffi.SgsStats()
+        _ffi.call("sgs_get_stats", C.byref(self.desc), C.byref(s), C.c_void_p(_stream_ptr()))
+        return {k: int(getattr(s, k)) for k, _ in _ffi.SgsStats._fields_}
+
+
+@dataclass
+class Frame:
+    """Outputs of one forward render plus what the backward needs."""
+
+    img: torch.Tensor          # (H, W, 3) float32
+    final_T: torch.Tensor      # (H, W) float32
+    ncontrib: torch.Tensor     # (H, W) int32 (uint32 on the device)
+    ws: Workspace
+    cam: _ffi.SgsCamera
+    bg: tuple
+
+    def stats(self) -> dict:
+        return self.ws.stats()
+
+
+MAX_CAPACITY = (1 << 30) - 1
+
+
+class Rasterizer:
+    """Reusable render context (workspace cache + capacity policy)."""
+
+    def __init__(self, sort_mode: int = _ffi.SORT_DEPTH_FIRST, device="cuda", headroom=1.25,
+                 initial_capacity: int | None = None):
+        _ffi.load()
+        self.sort_mode = sort_mode
+        self.device = torch.device(device)
+        self.headroom = headroom
+        self.initial_capacity = initial_capacity
+        self._cap_hint: dict = {}
+        self._shared: dict = {}
+
+    # --------------------------------------------------------------- workspace
+    def _key(self, g, cam):
+        return (g.n, g.n_lobes, int(cam.width), int(cam.height))
+
+    def _capacity(self, key, g) -> int:
+        if key in self._cap_hint:
+            return self._cap_hint[key]
+        if self.initial_capacity is not None:
+            return self.initial_capacity
+        return int(min(MAX_CAPACITY, max(1 << 16, 16 * g.n)))
+
+    def workspace(self, g, cam, private=False, capacity=None) -> Workspace:
+        key = self._key(g, cam)
+        cap = capacity if capacity is not None else self._capacity(key, g)
+        if private:
+            return Workspace(*key[:4], cap, self.sort_mode, self.device)
+        ws = self._shared.get(key)
+        if ws is None or ws.capacity < cap:
+            self._shared.pop(key, None)
+            ws = Workspace(*key[:4], cap, self.sort_mode, self.device)
+            self._shared[key] = ws
+        return ws
+
+    def release(self):
+        self._shared.clear()
+
+    # ------------------------------------------------------------------ forward
+    def forward(self, g: GaussianTensors, cam, background=(0.0, 0.0, 0.0), weight_sums=None,
+                check=True, private=False, tile_rows=None, out=None) -> Frame:
+        """Render one view.  ``weight_sums`` (N float32 device tensor) is
+        accumulated in place (render.py:406-407).  ``out`` may supply
+        preallocated (img, T, nc) tensors."""
+        c_cam = to_sgs(cam, tile_rows)
+        bg = tuple(float(v) for v in np.asarray(background, dtype=np.float64).reshape(3))
+        c_bg = (C.c_float * 3)(*bg)
+        H, W = int(cam.height), int(cam.width)
+        if out is None:
+            img = torch.empty((H, W, 3), dtype=torch.float32, device=self.device)
+            T = torch.empty((H, W), dtype=torch.float32, device=self.device)
+            nc = torch.empty((H, W), dtype=torch.int32, device=self.device)
+        else:
+            img, T, nc = out
+        if weight_sums is not None:
+            if weight_sums.dtype != torch.float32 or tuple(weight_sums.shape) != (g.n,):
+                raise ValueError("weight_sums must be a float32 (N,) tensor")
+        params = g.c_params()
+        stream = C.c_void_p(_stream_ptr())
+        key = self._key(g, cam)
+        while True:
+            ws = self.workspace(g, cam, private=private)
+            _ffi.call("sgs_preprocess", C.byref(params), C.byref(c_cam), C.byref(ws.desc), stream)
+            _ffi.call("sgs_bin", C.byref(c_cam), C.byref(ws.desc), stream)
+            if check:
+                st = ws.stats()
+                if st["overflow"]:
+                    need = int(st["n_entries"] * self.headroom) + 1024
+                    if st["n_entries"] > MAX_CAPACITY:
+                        raise _ffi.CapacityError(
+                            "sgs_bin", _ffi.SGS_E_CAPACITY,
+                            f"{st['n_entries']} tile entries exceed one bin call's limit "
+                            f"{MAX_CAPACITY}; render in tile-row strips")
+                    self._cap_hint[key] = min(MAX_CAPACITY, need)
+                    continue
+            break
+        _ffi.call("sgs_raster_forward", C.byref(c_cam), c_bg, C.byref(ws.desc), _ptr(img), _ptr(T),
+                  _ptr(nc), _ptr(weight_sums), stream)
+        return Frame(img=img, final_T=T, ncontrib=nc, ws=ws, cam=c_cam, bg=bg)
+
+    # ----------------------------------------------------------------- backward
+    def backward(self, g: GaussianTensors, frame: Frame, dimg: torch.Tensor,
+                 mask_grads: bool = True) -> dict:
+        """dL/dparams for dL/dimg (H,W,3).  Returns a dict of float32 tensors
+        shaped like the parameters (+ 'lobe_mask' / 'prim_mask' when
+        ``mask_grads``) and 'grad2d' (N,9)."""
+        dimg = dimg.to(device=self.device, dtype=torch.float32).contiguous()
+        if tuple(dimg.shape) != tuple(frame.img.shape):
+            raise ValueError(f"dimg shape {tuple(dimg.shape)} != image {tuple(frame.img.shape)}")
+        stream = C.c_void_p(_stream_ptr())
+        c_bg = (C.c_float * 3)(*frame.bg)
+        grad2d = torch.empty((g.n, 9), dtype=torch.float32, device=self.device)
+        _ffi.call("sgs_raster_backward", C.byref(frame.cam), c_bg, C.byref(frame.ws.desc),
+                  _ptr(frame.img), _ptr(frame.final_T), _ptr(frame.ncontrib), _ptr(dimg),
+                  _ptr(grad2d), stream)
+        out = {f: torch.empty_like(getattr(g, f)) for f in GRAD_FIELDS}
+        if mask_grads:
+            out["lobe_mask"] = torch.empty_like(g.lobe_mask)
+            out["prim_mask"] = torch.empty((g.n,), dtype=torch.float32, device=self.device)
+        cg = _ffi.SgsGrads()
+        for f in GRAD_FIELDS:
+            setattr(cg, f, _ptr(out[f]))
+        cg.lobe_mask = _ptr(out.get("lobe_mask"))
+        cg.prim_mask = _ptr(out.get("prim_mask"))
+        params = g.c_params()
+        _ffi.call("sgs_preprocess_backward", C.byref(params), C.byref(frame.cam), _ptr(grad2d),
+                  C.byref(cg), stream)
+        out["grad2d"] = grad2d
+        return out
+
+    # ----------------------------------------------------------------- exports
+    def export_bins(self, frame: Frame):
+        """(keys u64 as int64, values int32, ranges (T,2) int32) of the sorted tile list."""
+        st = frame.ws.stats()
+        n = int(min(st["n_entries"], st["capacity"]))
+        keys = torch.empty(max(n, 1), dtype=torch.int64, device=self.device)
+        vals = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
+        tiles = ((frame.cam.width + 15) // 16) * ((frame.cam.height + 15) // 16)
+        ranges = torch.empty((tiles, 2), dtype=torch.int32, device=self.device)
+        _ffi.call("sgs_export_bins", C.byref(frame.ws.desc), C.byref(frame.cam), _ptr(keys),
+                  _ptr(vals), _ptr(ranges), C.c_void_p(_stream_ptr()))
+        return keys[:n], vals[:n], ranges
+
+    def export_projected(self, frame: Frame):
+        n = int(frame.ws.desc.n)
+        depth = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
+        rect = torch.empty((max(n, 1), 2), dtype=torch.int32, device=self.device)
+        tt = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
+        rec = torch.empty((max(n, 1), 12), dtype=torch.float32, device=self.device)
+        _ffi.call("sgs_export_projected", C.byref(frame.ws.desc), _ptr(depth), _ptr(rect),
+                  _ptr(tt), _ptr(rec), C.c_void_p(_stream_ptr()))
+        return depth[:n], rect[:n], tt[:n], rec[:n]
+
+
+def sort_pairs_u64(keys: torch.Tensor, vals: torch.Tensor, key_bits: int) -> None:
+    """In-place stable radix sort of int64-stored u64 keys with int32 values."""
+    n = keys.numel()
+    tb = C.c_uint64()
+    _ffi.call("sgs_sort_temp_size", n, key_bits, C.byref(tb))
+    tmp = torch.empty(int(tb.value), dtype=torch.uint8, device=keys.device)
+    _ffi.call("sgs_sort_pairs_u64", _ptr(keys), _ptr(vals), n, key_bits, _ptr(tmp),
+              int(tb.value), C.c_void_p(_stream_ptr()))
+
+
+class RenderFunction(torch.autograd.Function):
+    """Autograd wrapper: image = render(params) with the CUDA backward."""
+
+    @staticmethod
+    def forward(ctx, rast, cam, background, position, quat, log_scale, opacity, diffuse, axis_raw,
+                sharpness, amplitude, lobe_mask, prim_mask):
+        g = GaussianTensors(position.detach(), quat.detach(), log_scale.detach(),
+                            opacity.detach(), diffuse.detach(), axis_raw.detach(),
+                            sharpness.detach(), amplitude.detach(), lobe_mask.detach(),
+                            None if prim_mask is None else prim_mask.detach())
+        frame = rast.forward(g, cam, background, private=True)
+        ctx.rast, ctx.g, ctx.frame = rast, g, frame
+        ctx.has_pm = prim_mask is not None
+        return frame.img
+
+    @staticmethod
+    def backward(ctx, dimg):
+        gr = ctx.rast.backward(ctx.g, ctx.frame, dimg, mask_grads=True)
+        ctx.frame = None
+        return (None, None, None, *[gr[f] for f in GRAD_FIELDS], gr["lobe_mask"],
+                gr["prim_mask"] if ctx.has_pm else None)
+
+
+def render_torch(rast: Rasterizer, cam, background, position, quat, log_scale, opacity, diffuse,
+                 axis_raw, sharpness, amplitude, lobe_mask, prim_mask=None) -> torch.Tensor:
+    return RenderFunction.apply(rast, cam, background, position, quat, log_scale, opacity,
+                                diffuse, axis_raw, sharpness, amplitude, lobe_mask, prim_mask)
