@@ -1,0 +1,176 @@
+"""GPU parity: libsgs.so (through the C ABI) against the CPU tiled oracle.
+
+Bit-exact: preprocess integer outputs and records, tile key lists, sorted
+orders, per-tile ranges, visibility counts.  Tolerance: images (<= 1e-5 vs
+the oracle's fp32 raster; the 1e-4 reference bar is checked in
+test_gpu_reference.py) and gradients (composite criterion).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import tiled
+from paper_2509_07021_b200 import _ffi, scenes
+from paper_2509_07021_b200.rasterizer import GaussianTensors, Rasterizer, sort_pairs_u64
+
+pytestmark = pytest.mark.gpu
+
+MODES = [_ffi.SORT_DEPTH_FIRST, _ffi.SORT_KEY64]
+
+
+def _gpu_frame(scene, cam, mode=_ffi.SORT_DEPTH_FIRST, bg=(0.0, 0.0, 0.0), tile_rows=None):
+    rast = Rasterizer(sort_mode=mode)
+    g = GaussianTensors.from_arrays(scene)
+    frame = rast.forward(g, cam, bg, tile_rows=tile_rows)
+    torch.cuda.synchronize()
+    return rast, g, frame
+
+
+def _check_bins(rast, frame, ref):
+    st = frame.stats()
+    assert st["n_visible"] == ref.n_visible
+    assert st["n_emitting"] == ref.n_emitting
+    assert st["n_entries"] == ref.n_entries
+    keys, vals, ranges = rast.export_bins(frame)
+    assert np.array_equal(keys.cpu().numpy().view(np.uint64), ref.keys)
+    assert np.array_equal(vals.cpu().numpy().view(np.uint32), ref.vals)
+    assert np.array_equal(ranges.cpu().numpy().view(np.uint32), ref.ranges)
+
+
+def _check_projected(rast, frame, ref):
+    depth, rect, tt, rec = (t.cpu().numpy() for t in rast.export_projected(frame))
+    assert np.array_equal(depth.view(np.uint32), ref.depth_bits)
+    assert np.array_equal(tt.view(np.uint32), ref.tiles_touched)
+    emit = ref.tiles_touched > 0
+    assert np.array_equal(rect.view(np.uint32)[emit], ref.rect[emit])
+    assert np.array_equal(rec[emit].view(np.uint32), ref.records[emit].view(np.uint32))
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_config0_bit_exact_bins(mode):
+    scene, cams = scenes.config0()
+    ref = tiled.render(scene, cams[0])
+    rast, g, frame = _gpu_frame(scene, cams[0], mode)
+    _check_projected(rast, frame, ref)
+    _check_bins(rast, frame, ref)
+    img = frame.img.cpu().numpy()
+    assert np.abs(img - ref.img).max() <= 1e-5
+    assert np.array_equal(frame.ncontrib.cpu().numpy().view(np.uint32) > 0, ref.nc > 0)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_config1_masks_bit_exact(mode):
+    scene, cams = scenes.config1()
+    ref = tiled.render(scene, cams[0])
+    rast, g, frame = _gpu_frame(scene, cams[0], mode)
+    _check_projected(rast, frame, ref)
+    _check_bins(rast, frame, ref)
+    assert np.abs(frame.img.cpu().numpy() - ref.img).max() <= 1e-5
+
+
+def test_config2_camera0_bit_exact():
+    scene, cams = scenes.config2(n_cams=1)
+    ref = tiled.preprocess(scene, cams[0])
+    tiled.bin(ref)
+    rast, g, frame = _gpu_frame(scene, cams[0])
+    _check_projected(rast, frame, ref)
+    _check_bins(rast, frame, ref)
+
+
+def test_background_and_importance():
+    scene, cams = scenes.config0(n=3000)
+    cam = cams[0].crop(32, 40, 96, 80)
+    bg = (0.2, 0.5, 0.9)
+    ref = tiled.render(scene, cam, bg, importance=True)
+    rast = Rasterizer()
+    g = GaussianTensors.from_arrays(scene)
+    ws = torch.zeros(g.n, dtype=torch.float32, device="cuda")
+    frame = rast.forward(g, cam, bg, weight_sums=ws)
+    assert np.abs(frame.img.cpu().numpy() - ref.img).max() <= 1e-5
+    assert np.abs(frame.final_T.cpu().numpy() - ref.T).max() <= 1e-5
+    np.testing.assert_allclose(ws.cpu().numpy(), ref.weight_sums, rtol=1e-4, atol=1e-4)
+
+
+def test_strips_equal_full_frame():
+    scene, cams = scenes.config0()
+    cam = cams[0]
+    rast = Rasterizer()
+    g = GaussianTensors.from_arrays(scene)
+    full = rast.forward(g, cam).img.clone()
+    parts = torch.zeros_like(full)
+    for y0, y1 in [(0, 5), (5, 11), (11, 16)]:
+        f = rast.forward(g, cam, tile_rows=(y0, y1))
+        parts[y0 * 16:y1 * 16] = f.img[y0 * 16:y1 * 16]
+        ref = tiled.render(scene, cam, tile_rows=(y0, y1))
+        _check_bins(rast, f, ref)
+    assert torch.equal(full, parts)
+
+
+def test_empty_and_culled():
+    scene, cams = scenes.config0(n=50)
+    cam = cams[0]
+    behind = scene.subset(np.arange(50))
+    behind.position = (np.asarray(cam.center) * 2.0 + np.zeros((50, 3))).astype(np.float32)
+    rast, g, frame = _gpu_frame(behind, cam, bg=(0.3, 0.3, 0.3))
+    st = frame.stats()
+    assert st["n_emitting"] == 0 and st["n_entries"] == 0
+    assert torch.allclose(frame.img, torch.full_like(frame.img, 0.3))
+    zero_op = scene.subset(np.arange(50))
+    zero_op.opacity = np.zeros(50, np.float32)
+    rast, g, frame = _gpu_frame(zero_op, cam)
+    assert frame.stats()["n_entries"] == 0
+    assert float(frame.img.abs().max()) == 0.0
+
+
+def test_capacity_growth():
+    scene, cams = scenes.config0()
+    rast = Rasterizer(initial_capacity=1000)
+    g = GaussianTensors.from_arrays(scene)
+    frame = rast.forward(g, cams[0])
+    ref = tiled.render(scene, cams[0])
+    assert frame.ws.capacity >= ref.n_entries
+    _check_bins(rast, frame, ref)
+
+
+@pytest.mark.parametrize("n,bits", [(1, 8), (1000, 13), (70_001, 45), (1_000_003, 40), (5000, 64)])
+def test_sort_pairs_u64(n, bits):
+    rng = np.random.default_rng(n)
+    hi = np.uint64((1 << bits) - 1) if bits < 64 else np.uint64(0xFFFFFFFFFFFFFFFF)
+    keys = rng.integers(0, 1 << 62, size=n, dtype=np.uint64) * np.uint64(3) & hi
+    keys[: n // 3] = keys[0]  # many ties -> stability matters
+    vals = np.arange(n, dtype=np.uint32)
+    kt = torch.from_numpy(keys.view(np.int64).copy()).cuda()
+    vt = torch.from_numpy(vals.view(np.int32).copy()).cuda()
+    sort_pairs_u64(kt, vt, bits)
+    order = np.argsort(keys, kind="stable")
+    assert np.array_equal(kt.cpu().numpy().view(np.uint64), keys[order])
+    assert np.array_equal(vt.cpu().numpy().view(np.uint32), vals[order])
+
+
+def _composite_ok(a, b, rel=1e-3, floor=1e-5):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    tol = rel * np.abs(b) + floor * max(np.abs(b).max(), 1e-30)
+    return np.abs(a - b) <= tol
+
+
+@pytest.mark.parametrize("bg", [(0.0, 0.0, 0.0), (0.3, 0.6, 0.1)])
+def test_backward_matches_oracle(bg):
+    scene, cams = scenes.config0()
+    cam = cams[0].crop(64, 64, 128, 96)
+    target = scenes.target_image(0, cam.height, cam.width)
+    ref = tiled.render(scene, cam, bg)
+    rast = Rasterizer()
+    g = GaussianTensors.from_arrays(scene)
+    frame = rast.forward(g, cam, bg)
+    dimg = np.sign(frame.img.cpu().numpy() - target) / target.size
+    grads = rast.backward(g, frame, torch.from_numpy(dimg.astype(np.float32)).cuda())
+    tiled.raster_backward(ref, dimg)
+    og = tiled.preprocess_backward(ref)
+    g2 = grads["grad2d"].cpu().numpy()
+    assert _composite_ok(g2, ref.grad2d, floor=1e-4).all()
+    for k in ("position", "quat", "log_scale", "opacity", "diffuse", "axis_raw", "sharpness",
+              "amplitude", "lobe_mask", "prim_mask"):
+        ok = _composite_ok(grads[k].cpu().numpy(), og[k])
+        assert ok.mean() == 1.0, f"{k}: {np.count_nonzero(~ok)} of {ok.size} outside tolerance"
