@@ -125,23 +125,28 @@ int sgs_preprocess(const sgs_params* params, const sgs_camera* cam, const sgs_wo
 /* K2-K4 binning -- replaces the depth argsort (render.py:307).  Emits one
  * (tile, depth) entry per touched tile and sorts them stably by
  * (tile, depth, primitive index); writes per-tile [start, end) ranges.
- * `sort_mode` picks SGS_SORT_DEPTH_FIRST (default) or SGS_SORT_KEY64; both
- * produce bit-identical results.  Sets SGS_E_CAPACITY when E > capacity. */
+ * ws->sort_mode picks SGS_SORT_DEPTH_FIRST or SGS_SORT_KEY64; both produce
+ * bit-identical results.  Never synchronises: when E exceeds the workspace's
+ * entry capacity only the first `capacity` entries are kept and
+ * sgs_stats.overflow is set -- grow the workspace and redo the frame. */
 int sgs_bin(const sgs_camera* cam, const sgs_workspace* ws, void* stream);
 
 /* K5 forward raster -- replaces _chunk_blend + _render_params
  * (render.py:355-408).  out_img (H,W,3), out_T (H,W) final transmittance,
  * out_ncontrib (H,W) number of per-tile entries consumed by each pixel.
  * weight_sums (N) is ACCUMULATED (like the reference's in-place np.add.at,
- * render.py:406-407) when non-NULL. */
+ * render.py:406-407) when non-NULL.  pair_count (one device uint64), when
+ * non-NULL, is incremented by the number of (pixel, entry) pairs evaluated
+ * before each pixel terminated -- the raster's algorithmic work unit. */
 int sgs_raster_forward(const sgs_camera* cam, const float background[3],
                        const sgs_workspace* ws, float* out_img, float* out_T,
-                       uint32_t* out_ncontrib, float* weight_sums, void* stream);
+                       uint32_t* out_ncontrib, float* weight_sums, uint64_t* pair_count,
+                       void* stream);
 
 /* Convenience: preprocess + bin + raster_forward in one call (graph-capturable). */
 int sgs_render_forward(const sgs_params* params, const sgs_camera* cam, const float background[3],
                        const sgs_workspace* ws, float* out_img, float* out_T, uint32_t* out_ncontrib,
-                       float* weight_sums, void* stream);
+                       float* weight_sums, uint64_t* pair_count, void* stream);
 
 /* K6 backward raster -- replaces the pixel loop of _backward_from_blend
  * (render.py:535-573).  dimg (H,W,3) = dL/dimage.  grad2d (N,9) is

@@ -62,9 +62,10 @@ SIGNATURES = {
     "sgs_preprocess": (C.c_int, [_P(SgsParams), _P(SgsCamera), _P(SgsWorkspace), C.c_void_p]),
     "sgs_bin": (C.c_int, [_P(SgsCamera), _P(SgsWorkspace), C.c_void_p]),
     "sgs_raster_forward": (C.c_int, [_P(SgsCamera), _P(C.c_float), _P(SgsWorkspace), C.c_void_p,
-                                     C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
-    "sgs_render_forward": (C.c_int, [_P(SgsParams), _P(SgsCamera), _P(C.c_float), _P(SgsWorkspace),
                                      C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "sgs_render_forward": (C.c_int, [_P(SgsParams), _P(SgsCamera), _P(C.c_float), _P(SgsWorkspace),
+                                     C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                     C.c_void_p]),
     "sgs_raster_backward": (C.c_int, [_P(SgsCamera), _P(C.c_float), _P(SgsWorkspace), C.c_void_p,
                                       C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "sgs_preprocess_backward": (C.c_int, [_P(SgsParams), _P(SgsCamera), C.c_void_p, _P(SgsGrads),

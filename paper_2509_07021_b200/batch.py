@@ -1,0 +1,85 @@
+"""Host-buffer batch rendering: the end-to-end path a user of the reference's
+``render(scene, cam)`` API takes for many views of one scene.
+
+Per call: the scene's float32 SoA is copied host -> device once (from pinned
+memory), every view is rendered on the compute stream, and each finished
+image is copied device -> host on a side stream while the next view renders.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from .rasterizer import GRAD_FIELDS, GaussianTensors, Rasterizer
+
+HOST_FIELDS = GRAD_FIELDS + ("lobe_mask",)
+
+
+class PinnedScene:
+    """Page-locked float32 copy of a scene's parameter arrays."""
+
+    def __init__(self, p):
+        self.arrays = {}
+        for f in HOST_FIELDS:
+            a = np.ascontiguousarray(np.asarray(getattr(p, f)), dtype=np.float32)
+            t = torch.empty(a.shape, dtype=torch.float32, pin_memory=True)
+            t.numpy()[...] = a
+            self.arrays[f] = t
+        pm = getattr(p, "prim_mask", None)
+        self.prim_mask = None
+        if pm is not None:
+            a = np.ascontiguousarray(np.asarray(pm), dtype=np.float32)
+            self.prim_mask = torch.empty(a.shape, dtype=torch.float32, pin_memory=True)
+            self.prim_mask.numpy()[...] = a
+
+    @property
+    def nbytes(self) -> int:
+        n = sum(t.numel() * 4 for t in self.arrays.values())
+        return n + (0 if self.prim_mask is None else self.prim_mask.numel() * 4)
+
+    def upload(self, device) -> GaussianTensors:
+        dev = {f: t.to(device, non_blocking=True) for f, t in self.arrays.items()}
+        pm = None if self.prim_mask is None else self.prim_mask.to(device, non_blocking=True)
+        return GaussianTensors(**dev, prim_mask=pm)
+
+
+class BatchRenderer:
+    """render_views(pinned_scene, cams) -> list of (H, W, 3) float32 host arrays."""
+
+    def __init__(self, rast: Rasterizer | None = None, device="cuda"):
+        self.rast = rast or Rasterizer(device=device)
+        self.device = torch.device(device)
+        self.copy_stream = torch.cuda.Stream(device=self.device)
+        self._host = {}
+
+    def _host_buf(self, k, shape):
+        buf = self._host.get(k)
+        if buf is None or tuple(buf.shape) != shape:
+            buf = torch.empty(shape, dtype=torch.float32, pin_memory=True)
+            self._host[k] = buf
+        return buf
+
+    def render_views(self, scene: PinnedScene, cams, background=(0.0, 0.0, 0.0), check=False):
+        g = scene.upload(self.device)
+        main = torch.cuda.current_stream(self.device)
+        outs = []
+        imgs = []
+        for k, cam in enumerate(cams):
+            frame = self.rast.forward(g, cam, background, check=check)
+            img = frame.img
+            done = torch.cuda.Event()
+            done.record(main)
+            host = self._host_buf(k, tuple(img.shape))
+            with torch.cuda.stream(self.copy_stream):
+                self.copy_stream.wait_event(done)
+                host.copy_(img, non_blocking=True)
+                img.record_stream(self.copy_stream)
+            imgs.append(img)
+            outs.append(host)
+        main.wait_stream(self.copy_stream)
+        return outs
+
+    @staticmethod
+    def d2h_bytes(cams) -> int:
+        return sum(int(c.width) * int(c.height) * 3 * 4 for c in cams)

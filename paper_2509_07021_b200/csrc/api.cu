@@ -45,7 +45,8 @@ int launch_vram3s(const sgs_params& P, const SgsCam& cam, int tile_px, Counters*
 int launch_bin(const SgsCam& cam, const sgs_workspace* ws, const Layout& lo, cudaStream_t st);
 bool final_in_alt(const Layout& lo);
 int launch_raster_fwd(const SgsCam& cam, float3 bg, const sgs_workspace* ws, const Layout& lo, const uint32_t* vals,
-                      float* img, float* T, uint32_t* nc, float* weight_sums, cudaStream_t st);
+                      float* img, float* T, uint32_t* nc, float* weight_sums, unsigned long long* pairs,
+                      cudaStream_t st);
 int launch_raster_bwd(const SgsCam& cam, float3 bg, const sgs_workspace* ws, const Layout& lo, const uint32_t* vals,
                       const float* T, const uint32_t* nc, const float* dimg, float* grad2d, cudaStream_t st);
 int launch_preprocess_bwd(const sgs_params& P, const SgsCam& cam, const float* grad2d, const sgs_grads& g,
@@ -120,7 +121,8 @@ int sgs_bin(const sgs_camera* cam, const sgs_workspace* ws, void* stream) {
 }
 
 int sgs_raster_forward(const sgs_camera* cam, const float background[3], const sgs_workspace* ws, float* out_img,
-                       float* out_T, uint32_t* out_ncontrib, float* weight_sums, void* stream) {
+                       float* out_T, uint32_t* out_ncontrib, float* weight_sums, uint64_t* pair_count,
+                       void* stream) {
   Layout lo;
   SgsCam c;
   int rc = check_ws(ws, &lo);
@@ -132,15 +134,16 @@ int sgs_raster_forward(const sgs_camera* cam, const float background[3], const s
   }
   float3 bg = make_float3(background[0], background[1], background[2]);
   return launch_raster_fwd(c, bg, ws, lo, final_vals(ws, lo), out_img, out_T, out_ncontrib, weight_sums,
-                           as_stream(stream));
+                           reinterpret_cast<unsigned long long*>(pair_count), as_stream(stream));
 }
 
 int sgs_render_forward(const sgs_params* params, const sgs_camera* cam, const float background[3],
                        const sgs_workspace* ws, float* out_img, float* out_T, uint32_t* out_ncontrib,
-                       float* weight_sums, void* stream) {
+                       float* weight_sums, uint64_t* pair_count, void* stream) {
   int rc = sgs_preprocess(params, cam, ws, stream);
   if (!rc) rc = sgs_bin(cam, ws, stream);
-  if (!rc) rc = sgs_raster_forward(cam, background, ws, out_img, out_T, out_ncontrib, weight_sums, stream);
+  if (!rc)
+    rc = sgs_raster_forward(cam, background, ws, out_img, out_T, out_ncontrib, weight_sums, pair_count, stream);
   return rc;
 }
 

@@ -38,7 +38,7 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
-template <bool kImportance>
+template <bool kImportance, bool kCount>
 __global__ void __launch_bounds__(256) raster_fwd_kernel(const uint2* __restrict__ ranges,
                                                          const uint32_t* __restrict__ vals,
                                                          const float4* __restrict__ rec_geo,
@@ -46,7 +46,8 @@ __global__ void __launch_bounds__(256) raster_fwd_kernel(const uint2* __restrict
                                                          const float4* __restrict__ rec_col, SgsCam cam, float3 bg,
                                                          float* __restrict__ out_img, float* __restrict__ out_T,
                                                          uint32_t* __restrict__ out_nc,
-                                                         float* __restrict__ weight_sums) {
+                                                         float* __restrict__ weight_sums,
+                                                         unsigned long long* __restrict__ pair_count) {
   __shared__ float4 s_geo[256];
   __shared__ float4 s_con[256];
   __shared__ float4 s_col[256];
@@ -62,7 +63,7 @@ __global__ void __launch_bounds__(256) raster_fwd_kernel(const uint2* __restrict
   const uint32_t start = rg.x, end = rg.y > rg.x ? rg.y : rg.x;
 
   float T = 1.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
-  uint32_t nc = 0;
+  uint32_t nc = 0, reached = 0;
   bool done = !inside;
 
   for (uint32_t b = start; b < end; b += 256) {
@@ -84,6 +85,7 @@ __global__ void __launch_bounds__(256) raster_fwd_kernel(const uint2* __restrict
       const float dx = fx - G.x, dy = fy - G.y;
       const float p = dx * (K.x * dx + K.y * dy) + K.z * dy * dy;
       float w = 0.0f;
+      if (kCount && !done) ++reached;
       if (!done && p >= G.w) {
         const float a = G.z * ex2_approx(p);
         const float alpha = fminf(a, SGS_ALPHA_MAX);
@@ -105,6 +107,11 @@ __global__ void __launch_bounds__(256) raster_fwd_kernel(const uint2* __restrict
         if (lane == 0 && ws != 0.0f) atomicAdd(&weight_sums[s_id[k]], ws);
       }
     }
+  }
+  if (kCount) {
+    unsigned long long r = reached;
+    for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+    if (lane == 0 && r) atomicAdd(pair_count, r);
   }
   if (inside) {
     const size_t pix = (size_t)py * cam.width + px;
@@ -234,17 +241,23 @@ __global__ void __launch_bounds__(256) raster_bwd_kernel(const uint2* __restrict
 }
 
 int launch_raster_fwd(const SgsCam& cam, float3 bg, const sgs_workspace* ws, const Layout& lo, const uint32_t* vals,
-                      float* img, float* T, uint32_t* nc, float* weight_sums, cudaStream_t st) {
+                      float* img, float* T, uint32_t* nc, float* weight_sums, unsigned long long* pairs,
+                      cudaStream_t st) {
   const int grid = (cam.tile_y1 - cam.tile_y0) * cam.tiles_x;
   const uint2* ranges = at<uint2>(ws, lo.ranges);
-  if (weight_sums) {
-    raster_fwd_kernel<true><<<grid, 256, 0, st>>>(ranges, vals, at<float4>(ws, lo.rec_geo), at<float4>(ws, lo.rec_con),
-                                                  at<float4>(ws, lo.rec_col), cam, bg, img, T, nc, weight_sums);
-  } else {
-    raster_fwd_kernel<false><<<grid, 256, 0, st>>>(ranges, vals, at<float4>(ws, lo.rec_geo),
-                                                   at<float4>(ws, lo.rec_con), at<float4>(ws, lo.rec_col), cam, bg,
-                                                   img, T, nc, nullptr);
-  }
+  const float4* g = at<float4>(ws, lo.rec_geo);
+  const float4* k = at<float4>(ws, lo.rec_con);
+  const float4* c = at<float4>(ws, lo.rec_col);
+  if (weight_sums && pairs)
+    raster_fwd_kernel<true, true><<<grid, 256, 0, st>>>(ranges, vals, g, k, c, cam, bg, img, T, nc, weight_sums, pairs);
+  else if (weight_sums)
+    raster_fwd_kernel<true, false><<<grid, 256, 0, st>>>(ranges, vals, g, k, c, cam, bg, img, T, nc, weight_sums,
+                                                         nullptr);
+  else if (pairs)
+    raster_fwd_kernel<false, true><<<grid, 256, 0, st>>>(ranges, vals, g, k, c, cam, bg, img, T, nc, nullptr, pairs);
+  else
+    raster_fwd_kernel<false, false><<<grid, 256, 0, st>>>(ranges, vals, g, k, c, cam, bg, img, T, nc, nullptr,
+                                                          nullptr);
   SGS_LAUNCH_CHECK("raster_fwd_kernel");
   return SGS_OK;
 }

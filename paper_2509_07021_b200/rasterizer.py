@@ -200,7 +200,8 @@ class Rasterizer:
 
     # ------------------------------------------------------------------ forward
     def forward(self, g: GaussianTensors, cam, background=(0.0, 0.0, 0.0), weight_sums=None,
-                check=True, private=False, tile_rows=None, out=None) -> Frame:
+                check=True, private=False, tile_rows=None, out=None, pair_count=None,
+                _events=None) -> Frame:
         """Render one view.  ``weight_sums`` (N float32 device tensor) is
         accumulated in place (render.py:406-407).  ``out`` may supply
         preallocated (img, T, nc) tensors."""
@@ -236,8 +237,12 @@ class Rasterizer:
                     self._cap_hint[key] = min(MAX_CAPACITY, need)
                     continue
             break
+        if _events is not None:
+            _events[0].record()
         _ffi.call("sgs_raster_forward", C.byref(c_cam), c_bg, C.byref(ws.desc), _ptr(img), _ptr(T),
-                  _ptr(nc), _ptr(weight_sums), stream)
+                  _ptr(nc), _ptr(weight_sums), _ptr(pair_count), stream)
+        if _events is not None:
+            _events[1].record()
         return Frame(img=img, final_T=T, ncontrib=nc, ws=ws, cam=c_cam, bg=bg)
 
     # ----------------------------------------------------------------- backward
