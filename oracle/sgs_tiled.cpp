@@ -127,10 +127,13 @@ void oracle_bin(int64_t n, const uint32_t* depth_bits, const uint32_t* rect, con
     int ty0 = (int)(rect[2 * i + 1] & 0xffff), ty1 = (int)(int16_t)(rect[2 * i + 1] >> 16);
     const float* g = records + 12 * i;
     const float* k = g + 4;
-    for (int ty = ty0; ty <= ty1; ++ty)
-      for (int tx = tx0; tx <= tx1; ++tx)
-        if (sgs_tile_hit(g, k, &cam, tx, ty))
-          ent.emplace_back(((uint64_t)(ty * cam.tiles_x + tx) << 32) | depth_bits[i], (uint32_t)i);
+    const SgsSpan sp = sgs_span(g, k);
+    for (int ty = ty0; ty <= ty1; ++ty) {
+      int first;
+      const int cnt = sgs_row_span(&sp, &cam, ty, tx0, tx1, &first);
+      for (int tx = first; tx < first + cnt; ++tx)
+        ent.emplace_back(((uint64_t)(ty * cam.tiles_x + tx) << 32) | depth_bits[i], (uint32_t)i);
+    }
   }
   std::stable_sort(ent.begin(), ent.end(),
                    [](const std::pair<uint64_t, uint32_t>& a, const std::pair<uint64_t, uint32_t>& b) {

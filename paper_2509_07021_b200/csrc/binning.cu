@@ -159,19 +159,20 @@ __global__ void __launch_bounds__(256) emit_entries(const uint32_t* __restrict__
     const float4 g4 = rec_geo[g], c4 = rec_con[g];
     const float geo[4] = {g4.x, g4.y, g4.z, g4.w}, con[4] = {c4.x, c4.y, c4.z, c4.w};
     const unsigned long long dbits = kKey64 ? (unsigned long long)depth_key[g] : 0ull;
-    for (int ty = ty0; ty <= ty1; ++ty)
-      for (int tx = tx0; tx <= tx1; ++tx) {
-        if (!sgs_tile_hit(geo, con, &cam, tx, ty)) continue;
-        if (off < cap) {
-          uint32_t tile = (uint32_t)(ty * cam.tiles_x + tx);
-          if (kKey64)
-            reinterpret_cast<unsigned long long*>(keys_out)[off] = ((unsigned long long)tile << 32) | dbits;
-          else
-            reinterpret_cast<uint32_t*>(keys_out)[off] = tile;
-          vals_out[off] = g;
-        }
-        ++off;
+    const SgsSpan sp = sgs_span(geo, con);
+    for (int ty = ty0; ty <= ty1; ++ty) {
+      int first;
+      const int cnt_row = sgs_row_span(&sp, &cam, ty, tx0, tx1, &first);
+      const uint32_t tile0 = (uint32_t)(ty * cam.tiles_x + first);
+      for (int j = 0; j < cnt_row; ++j, ++off) {
+        if (off >= cap) break;
+        if (kKey64)
+          reinterpret_cast<unsigned long long*>(keys_out)[off] = ((unsigned long long)(tile0 + j) << 32) | dbits;
+        else
+          reinterpret_cast<uint32_t*>(keys_out)[off] = tile0 + j;
+        vals_out[off] = g;
       }
+    }
   }
 }
 

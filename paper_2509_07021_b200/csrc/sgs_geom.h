@@ -297,48 +297,93 @@ SGS_HD void sgs_project(const float pos[3], const float quat[4], const float ls[
   o->emits = 1;
 }
 
-// max over v in [v0, v1] of p(u, v) = a u^2 + b u v + c v^2 (c < 0).
-SGS_HD float sgs_seg_max_p(float a, float b, float c, float u, float v0, float v1) {
-  float v = -F_DIV(F_MUL(b, u), F_MUL(2.0f, c));
-  v = fminf(fmaxf(v, v0), v1);
-  return F_ADD(F_MUL(u, F_ADD(F_MUL(a, u), F_MUL(b, v))), F_MUL(F_MUL(c, v), v));
+// Support shape of one packed record (see sgs_pack_geo): the ellipse
+//   E = {(dx, dy) : A dx^2 + B dx dy + C dy^2 >= pmin},  A, C < 0, 4AC > B^2,
+// with (dx, dy) = pixel center - mean.  Its x-extreme points lie on the line
+// dy = kx dx, its y-extremes on dx = ky dy; xm / ym are the half extents.
+typedef struct SgsSpan {
+  float mx, my, A, B, C, pmin;
+  float kx, xm, ym;
+  int valid;
+} SgsSpan;
+
+SGS_HD SgsSpan sgs_span(const float geo[4], const float con[4]) {
+  SgsSpan s;
+  s.mx = geo[0];
+  s.my = geo[1];
+  s.pmin = geo[3];
+  s.A = con[0];
+  s.B = con[1];
+  s.C = con[2];
+  // D = 4AC - B^2 > 0 for a negative-definite form
+  float D = F_SUB(F_MUL(F_MUL(4.0f, s.A), s.C), F_MUL(s.B, s.B));
+  s.valid = D > 0.0f && s.A < 0.0f && s.C < 0.0f && s.pmin < 0.0f;
+  s.kx = -F_DIV(s.B, F_MUL(2.0f, s.C));
+  s.xm = s.valid ? F_SQRT(F_DIV(F_MUL(F_MUL(4.0f, s.C), s.pmin), D)) : 0.0f;
+  s.ym = s.valid ? F_SQRT(F_DIV(F_MUL(F_MUL(4.0f, s.A), s.pmin), D)) : 0.0f;
+  return s;
 }
 
-// Exact ellipse-vs-tile test on the packed raster record (see
-// sgs_pack_records): does any point of the tile's pixel-center box satisfy
-// p2 = A dx^2 + B dx dy + C dy^2 >= pmin?  The maximum of the negative-
-// definite form over the box is 0 when the mean lies inside the box, else it
-// lies on an edge facing the mean.  The raster evaluates a pair iff
-// p2(pixel) >= pmin, so this is the same support, tested per tile.
-SGS_HD int sgs_tile_hit(const float geo[4], const float con[4], const SgsCam* cam, int tx, int ty) {
-  const float mx = geo[0], my = geo[1], pmin = geo[3];
-  float bx0 = (float)(tx * SGS_TILE) + 0.5f;
-  float bx1 = (float)min_i32_(tx * SGS_TILE + SGS_TILE - 1, cam->width - 1) + 0.5f;
-  float by0 = (float)(ty * SGS_TILE) + 0.5f;
-  float by1 = (float)min_i32_(ty * SGS_TILE + SGS_TILE - 1, cam->height - 1) + 0.5f;
-  int in_x = mx >= bx0 && mx <= bx1;
-  int in_y = my >= by0 && my <= by1;
-  if (in_x && in_y) return 1;
-  float dx0 = F_SUB(bx0, mx), dx1 = F_SUB(bx1, mx);
-  float dy0 = F_SUB(by0, my), dy1 = F_SUB(by1, my);
-  float pmax = -INFINITY;
-  if (!in_x) {
-    float u = (mx < bx0) ? dx0 : dx1;
-    pmax = fmaxf(pmax, sgs_seg_max_p(con[0], con[1], con[2], u, dy0, dy1));
-  }
-  if (!in_y) {
-    float u = (my < by0) ? dy0 : dy1;
-    pmax = fmaxf(pmax, sgs_seg_max_p(con[2], con[1], con[0], u, dx0, dx1));
-  }
-  return pmax >= pmin;
+// x where the ellipse boundary crosses the horizontal line dy (the larger root
+// when `right`, else the smaller); the caller guarantees |dy| <= ym up to
+// rounding, and a slightly negative discriminant is clamped to 0.
+SGS_HD float sgs_span_root(const SgsSpan* s, float dy, int right) {
+  float b = F_MUL(s->B, dy);
+  float c = F_SUB(F_MUL(F_MUL(s->C, dy), dy), s->pmin);
+  float disc = F_SUB(F_MUL(b, b), F_MUL(F_MUL(4.0f, s->A), c));
+  float r = F_SQRT(fmaxf(disc, 0.0f));
+  float den = F_MUL(2.0f, s->A);  // < 0: (-b - r)/den is the larger root
+  return right ? F_DIV(F_SUB(-b, r), den) : F_DIV(F_ADD(-b, r), den);
 }
 
-// Packed tile rectangle: (tx0 | tx1 << 16, ty0 | ty1 << 16); empty when tx1 < tx0.
+// Tiles of tile-row `ty` (clipped to [tx0, tx1]) whose pixel-center box meets
+// the support: the ellipse's x-interval over the row's pixel-center band
+// [yc0, yc1] is exact -- its right end is the ellipse's rightmost point when
+// that lies inside the band, else the crossing at the band edge nearest to
+// it (likewise on the left) -- and tile tx is hit iff its pixel-center
+// columns [16 tx + 0.5, 16 tx + 15.5] meet that interval.  One definition
+// serves the tile counts (preprocess), the emission (binning) and the CPU
+// oracle, so counts, keys and ranges agree bit for bit.  Returns the count
+// and the first hit column.
+SGS_HD int sgs_row_span(const SgsSpan* s, const SgsCam* cam, int ty, int tx0, int tx1, int* first) {
+  *first = 0;
+  if (!s->valid) return 0;
+  float yc0 = (float)(ty * SGS_TILE) + 0.5f;
+  float yc1 = (float)min_i32_(ty * SGS_TILE + SGS_TILE - 1, cam->height - 1) + 0.5f;
+  float dy0 = F_SUB(yc0, s->my), dy1 = F_SUB(yc1, s->my);
+  if (dy1 < -s->ym || dy0 > s->ym) return 0;
+  float dyr = F_MUL(s->kx, s->xm);  // dy of the rightmost point; leftmost is at -dyr
+  float xr, xl;
+  if (dyr >= dy0 && dyr <= dy1) {
+    xr = s->xm;
+  } else {
+    xr = sgs_span_root(s, dyr < dy0 ? dy0 : dy1, 1);
+  }
+  float dyl = -dyr;
+  if (dyl >= dy0 && dyl <= dy1) {
+    xl = -s->xm;
+  } else {
+    xl = sgs_span_root(s, dyl < dy0 ? dy0 : dy1, 0);
+  }
+  float XL = F_ADD(s->mx, xl), XR = F_ADD(s->mx, xr);
+  if (!(XR >= 0.5f && XL <= (float)cam->width - 0.5f && XL <= XR)) return 0;
+  const float inv_tile = 1.0f / SGS_TILE;
+  float flo = ceilf(F_MUL(F_SUB(XL, 15.5f), inv_tile));
+  float fhi = F_FLOOR(F_MUL(F_SUB(XR, 0.5f), inv_tile));
+  int lo = flo < (float)tx0 ? tx0 : (int)flo;
+  int hi = fhi > (float)tx1 ? tx1 : (int)fhi;
+  if (hi < lo) return 0;
+  *first = lo;
+  return hi - lo + 1;
+}
+
+// Number of tiles whose box meets the support, over the rectangle rows.
 SGS_HD uint32_t sgs_count_tiles(int tx0, int ty0, int tx1, int ty1, const float geo[4], const float con[4],
                                 const SgsCam* cam) {
+  SgsSpan s = sgs_span(geo, con);
   uint32_t n = 0;
-  for (int ty = ty0; ty <= ty1; ++ty)
-    for (int tx = tx0; tx <= tx1; ++tx) n += (uint32_t)sgs_tile_hit(geo, con, cam, tx, ty);
+  int first;
+  for (int ty = ty0; ty <= ty1; ++ty) n += (uint32_t)sgs_row_span(&s, cam, ty, tx0, tx1, &first);
   return n;
 }
 
