@@ -182,6 +182,12 @@ int sgs_export_bins(const sgs_workspace* ws, const sgs_camera* cam, uint64_t* ke
 int sgs_export_projected(const sgs_workspace* ws, uint32_t* depth_bits,
                          uint32_t* rect, uint32_t* tiles_touched, float* records, void* stream);
 
+/* Device address of an internal workspace sub-buffer (debugging / tests):
+ * 0 counters, 1-3 records, 4 depth keys, 5 rects, 6 tile counts, 7-8 depth
+ * sort keys, 9-10 depth order, 11 offsets, 12 scan blocks, 13-14 entry keys,
+ * 15-16 entry values, 17 ranges, 18 histograms, 19 look-back status. */
+int sgs_debug_buffer(const sgs_workspace* ws, int32_t which, void** ptr, uint64_t* offset_bytes);
+
 /* Stable LSD radix sort of (key, value) pairs on the low `key_bits` bits of
  * 64-bit keys (onesweep, decoupled look-back).  In-place on keys/values;
  * `temp` of sgs_sort_temp_size() bytes. */

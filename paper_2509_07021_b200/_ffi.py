@@ -77,6 +77,7 @@ SIGNATURES = {
                                   C.c_void_p, C.c_void_p]),
     "sgs_export_projected": (C.c_int, [_P(SgsWorkspace), C.c_void_p, C.c_void_p, C.c_void_p,
                                        C.c_void_p, C.c_void_p]),
+    "sgs_debug_buffer": (C.c_int, [_P(SgsWorkspace), C.c_int32, _P(C.c_void_p), _P(C.c_uint64)]),
     "sgs_sort_temp_size": (C.c_int, [C.c_int64, C.c_int32, _P(C.c_uint64)]),
     "sgs_sort_pairs_u64": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p,
                                      C.c_uint64, C.c_void_p]),

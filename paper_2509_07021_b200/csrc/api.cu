@@ -254,6 +254,23 @@ int sgs_export_projected(const sgs_workspace* ws, uint32_t* depth_bits, uint32_t
   return SGS_OK;
 }
 
+int sgs_debug_buffer(const sgs_workspace* ws, int32_t which, void** ptr, uint64_t* offset_bytes) {
+  Layout lo;
+  int rc = check_ws(ws, &lo);
+  if (rc) return rc;
+  const uint64_t offs[] = {lo.counters, lo.rec_geo, lo.rec_con, lo.rec_col, lo.depth_key, lo.rect,
+                           lo.tiles_touched, lo.dkey_alt, lo.dkey_tmp, lo.didx, lo.didx_alt, lo.offsets,
+                           lo.scan_blocks, lo.ent_key, lo.ent_key_alt, lo.ent_val, lo.ent_val_alt, lo.ranges,
+                           lo.hist, lo.status};
+  if (which < 0 || which >= (int)(sizeof(offs) / sizeof(offs[0])) || !ptr) {
+    set_error("unknown debug buffer %d", which);
+    return SGS_E_ARG;
+  }
+  *ptr = at<char>(ws, offs[which]);
+  if (offset_bytes) *offset_bytes = offs[which];
+  return SGS_OK;
+}
+
 int sgs_sort_temp_size(int64_t n, int32_t key_bits, uint64_t* bytes_out) {
   if (n < 0 || n > (int64_t)kMaxEntries || key_bits < 1 || key_bits > 64 || !bytes_out) {
     set_error("invalid sort size");

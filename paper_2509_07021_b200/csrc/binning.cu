@@ -117,6 +117,8 @@ __global__ void __launch_bounds__(256) scan_down(const uint32_t* __restrict__ tt
   }
 }
 
+__global__ void set_count(uint32_t* p, uint32_t v) { *p = v; }
+
 static int launch_scan(const uint32_t* tt, const uint32_t* perm, uint32_t n, uint32_t cap,
                        unsigned long long* block_sums,
                        unsigned long long* offsets, Counters* ctr, cudaStream_t st) {
@@ -139,63 +141,120 @@ __device__ __forceinline__ void unpack_rect(uint2 r, int& tx0, int& ty0, int& tx
   ty1 = (int)(int16_t)(r.y >> 16);
 }
 
-template <bool kKey64>
+template <typename KT>
+__device__ __forceinline__ KT make_key(uint32_t tile, uint32_t dbits) {
+  if (sizeof(KT) == 8) return (KT)(((unsigned long long)tile << 32) | dbits);
+  return (KT)tile;
+}
+
+// Largest lane L with x_L <= k, for x non-decreasing across lanes and x_0 <= k.
+__device__ __forceinline__ int lane_search(uint32_t x, uint32_t k) {
+  int L = 0;
+#pragma unroll
+  for (int step = 16; step >= 1; step >>= 1) {
+    const int c = L + step;
+    if (__shfl_sync(0xffffffffu, x, c & 31) <= k && c < 32) L = c;
+  }
+  return L;
+}
+
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += y;
+  }
+  return v;
+}
+
+// Emission (K2), warp-cooperative and load-balanced.  A warp takes 32
+// consecutive primitives in rank order; their entries form one contiguous
+// output range, ordered by (primitive, tile row, tile column).  The warp
+// flattens the primitives' tile rows into a list of row items and processes
+// 32 row items at a time: lane = row item computes the row's exact span (one
+// span evaluation per row, no redundancy, no divergence), a warp scan gives
+// each row's output offset, then lane = entry writes 32 consecutive entries
+// per store instruction.
+template <typename KT>
 __global__ void __launch_bounds__(256) emit_entries(const uint32_t* __restrict__ perm, uint32_t n,
                                                     const uint32_t* __restrict__ tt, const uint2* __restrict__ rect,
                                                     const float4* __restrict__ rec_geo,
                                                     const float4* __restrict__ rec_con,
                                                     const uint32_t* __restrict__ depth_key,
                                                     const unsigned long long* __restrict__ offsets, SgsCam cam,
-                                                    uint32_t cap, void* __restrict__ keys_out,
-                                                    uint32_t* __restrict__ vals_out) {
-  for (uint32_t r = blockIdx.x * 256 + threadIdx.x; r < n; r += gridDim.x * 256) {
-    const uint32_t g = perm ? perm[r] : r;
-    const uint32_t cnt = tt[g];
-    if (cnt == 0) continue;
-    unsigned long long off = offsets[r];
-    if (off >= cap) continue;
-    int tx0, ty0, tx1, ty1;
-    unpack_rect(rect[g], tx0, ty0, tx1, ty1);
-    const float4 g4 = rec_geo[g], c4 = rec_con[g];
-    const float geo[4] = {g4.x, g4.y, g4.z, g4.w}, con[4] = {c4.x, c4.y, c4.z, c4.w};
-    const unsigned long long dbits = kKey64 ? (unsigned long long)depth_key[g] : 0ull;
-    const SgsSpan sp = sgs_span(geo, con);
-    for (int ty = ty0; ty <= ty1; ++ty) {
-      int first;
-      const int cnt_row = sgs_row_span(&sp, &cam, ty, tx0, tx1, &first);
-      const uint32_t tile0 = (uint32_t)(ty * cam.tiles_x + first);
-      for (int j = 0; j < cnt_row; ++j, ++off) {
-        if (off >= cap) break;
-        if (kKey64)
-          reinterpret_cast<unsigned long long*>(keys_out)[off] = ((unsigned long long)(tile0 + j) << 32) | dbits;
-        else
-          reinterpret_cast<uint32_t*>(keys_out)[off] = tile0 + j;
-        vals_out[off] = g;
+                                                    uint32_t cap, const unsigned long long* __restrict__ total_ptr,
+                                                    KT* __restrict__ keys_out, uint32_t* __restrict__ vals_out) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  const unsigned long long total = *total_ptr;
+  const unsigned long long lim = total < cap ? total : cap;
+  for (uint32_t base = warp * 32; base < n; base += nwarps * 32) {
+    unsigned long long out = offsets[base];  // uniform: every lane reads the same word
+    if (out >= lim) continue;
+    const uint32_t r = base + lane;
+    uint32_t g = 0, nrows = 0;
+    int tx0 = 0, ty0 = 0, tx1 = -1, ty1 = -1;
+    if (r < n) {
+      g = perm ? perm[r] : r;
+      if (tt[g]) {
+        unpack_rect(rect[g], tx0, ty0, tx1, ty1);
+        nrows = (uint32_t)(ty1 - ty0 + 1);
       }
+    }
+    const uint32_t rincl = warp_incl_scan(nrows, lane);
+    const uint32_t rstart = rincl - nrows;
+    const uint32_t R = __shfl_sync(0xffffffffu, rincl, 31);
+    for (uint32_t k0 = 0; k0 < R; k0 += 32) {
+      const uint32_t k = k0 + lane;
+      const int owner = lane_search(rstart, k);
+      const uint32_t og = __shfl_sync(0xffffffffu, g, owner);
+      const int oty0 = __shfl_sync(0xffffffffu, ty0, owner);
+      const int otx0 = __shfl_sync(0xffffffffu, tx0, owner);
+      const int otx1 = __shfl_sync(0xffffffffu, tx1, owner);
+      const uint32_t ors = __shfl_sync(0xffffffffu, rstart, owner);
+      const int ty = oty0 + (int)(k - ors);
+      uint32_t c = 0;
+      int first = 0;
+      if (k < R) {
+        const float4 g4 = rec_geo[og], c4 = rec_con[og];
+        const float geo[4] = {g4.x, g4.y, g4.z, g4.w}, con[4] = {c4.x, c4.y, c4.z, c4.w};
+        const SgsSpan sp = sgs_span(geo, con);
+        c = (uint32_t)sgs_row_span(&sp, &cam, ty, otx0, otx1, &first);
+      }
+      const uint32_t cincl = warp_incl_scan(c, lane);
+      const uint32_t cexcl = cincl - c;
+      const uint32_t Ctot = __shfl_sync(0xffffffffu, cincl, 31);
+      for (uint32_t j0 = 0; j0 < Ctot; j0 += 32) {
+        const uint32_t j = j0 + lane;
+        const int ro = lane_search(cexcl, j);
+        const int rfirst = __shfl_sync(0xffffffffu, first, ro);
+        const int rty = __shfl_sync(0xffffffffu, ty, ro);
+        const uint32_t rex = __shfl_sync(0xffffffffu, cexcl, ro);
+        const uint32_t rg = __shfl_sync(0xffffffffu, og, ro);
+        if (j < Ctot) {
+          const unsigned long long o = out + j;
+          if (o < lim) {
+            const uint32_t tile = (uint32_t)(rty * cam.tiles_x + rfirst) + (j - rex);
+            keys_out[o] = make_key<KT>(tile, sizeof(KT) == 8 ? depth_key[rg] : 0u);
+            vals_out[o] = rg;
+          }
+        }
+      }
+      out += Ctot;
     }
   }
 }
 
-// ---------------------------------------------------------------- tile ranges
-template <typename K>
-__device__ __forceinline__ uint32_t tile_of(K k) {
-  return (uint32_t)(sizeof(K) == 8 ? (k >> 32) : k);
+__global__ void ranges_init(uint2* __restrict__ ranges, int n_tiles) {
+  for (int i = blockIdx.x * 256 + threadIdx.x; i < n_tiles; i += gridDim.x * 256) ranges[i] = make_uint2(0xffffffffu, 0u);
 }
 
-template <typename K>
-__global__ void __launch_bounds__(256) tile_ranges(const K* __restrict__ keys, const uint32_t* n_ptr,
-                                                   uint2* __restrict__ ranges) {
-  const uint32_t n = *n_ptr;
-  for (uint32_t i = blockIdx.x * 256 + threadIdx.x; i < n; i += gridDim.x * 256) {
-    uint32_t t = tile_of(keys[i]);
-    if (i == 0 || tile_of(keys[i - 1]) != t) ranges[t].x = i;
-    if (i + 1 == n || tile_of(keys[i + 1]) != t) ranges[t].y = i + 1;
+__global__ void ranges_fix(uint2* __restrict__ ranges, int n_tiles) {
+  for (int i = blockIdx.x * 256 + threadIdx.x; i < n_tiles; i += gridDim.x * 256) {
+    uint2 r = ranges[i];
+    if (r.x == 0xffffffffu) ranges[i] = make_uint2(0u, 0u);
   }
-}
-
-__global__ void iota_kernel(uint32_t* __restrict__ v, uint32_t n, Counters* ctr) {
-  for (uint32_t i = blockIdx.x * 256 + threadIdx.x; i < n; i += gridDim.x * 256) v[i] = i;
-  if (blockIdx.x == 0 && threadIdx.x == 0) ctr->n_depth = n;
 }
 
 // Final location of the sorted values (which ping-pong buffer).
@@ -205,110 +264,93 @@ bool final_in_alt(const Layout& lo) {
   return (passes & 1) != 0;
 }
 
+template <typename KT, int IPT>
+static int bin_tiles(const SgsCam& cam, const sgs_workspace* ws, const Layout& lo, const uint32_t* perm, int key_bits,
+                     int tile_shift, cudaStream_t st) {
+  Counters* ctr = at<Counters>(ws, lo.counters);
+  const uint32_t n = (uint32_t)lo.n;
+  const uint32_t cap = (uint32_t)lo.cap;
+  KT* k0 = at<KT>(ws, lo.ent_key);
+  KT* k1 = at<KT>(ws, lo.ent_key_alt);
+  uint32_t* v0 = at<uint32_t>(ws, lo.ent_val);
+  uint32_t* v1 = at<uint32_t>(ws, lo.ent_val_alt);
+  uint2* ranges = at<uint2>(ws, lo.ranges);
+  const int rgrid = persistent_grid((uint64_t)lo.n_tiles, 256, 4);
+  ranges_init<<<rgrid, 256, 0, st>>>(ranges, lo.n_tiles);
+  SGS_LAUNCH_CHECK("ranges_init");
+  emit_entries<KT><<<persistent_grid(n, 256, 8), 256, 0, st>>>(
+      perm, n, at<uint32_t>(ws, lo.tiles_touched), at<uint2>(ws, lo.rect), at<float4>(ws, lo.rec_geo),
+      at<float4>(ws, lo.rec_con), at<uint32_t>(ws, lo.depth_key), at<unsigned long long>(ws, lo.offsets), cam, cap,
+      &ctr->n_entries, k0, v0);
+  SGS_LAUNCH_CHECK("emit_entries");
+  bool alt = false;
+  int rc = radix_sort_pairs<KT, IPT>(k0, v0, k1, v1, &ctr->n_sort, cap, key_bits, at<uint32_t>(ws, lo.hist),
+                                     at<uint32_t>(ws, lo.status), &ctr->part_counter[8], &alt, st, false,
+                                     RsRangeOut{ranges, tile_shift});
+  if (rc) return rc;
+  ranges_fix<<<rgrid, 256, 0, st>>>(ranges, lo.n_tiles);
+  SGS_LAUNCH_CHECK("ranges_fix");
+  return SGS_OK;
+}
+
 int launch_bin(const SgsCam& cam, const sgs_workspace* ws, const Layout& lo, cudaStream_t st) {
   Counters* ctr = at<Counters>(ws, lo.counters);
   const uint32_t n = (uint32_t)lo.n;
   const uint32_t cap = (uint32_t)lo.cap;
-  const int sms = device_sm_count();
   uint32_t* tt = at<uint32_t>(ws, lo.tiles_touched);
-  uint32_t* hist = at<uint32_t>(ws, lo.hist);
-  uint32_t* status = at<uint32_t>(ws, lo.status);
   unsigned long long* offsets = at<unsigned long long>(ws, lo.offsets);
   unsigned long long* block_sums = at<unsigned long long>(ws, lo.scan_blocks);
-  uint2* ranges = at<uint2>(ws, lo.ranges);
-  SGS_CUDA(cudaMemsetAsync(ranges, 0, (size_t)lo.n_tiles * 8, st));
-  const int egrid = persistent_grid(n, 256, 8);
-
   if (lo.sort_mode == SGS_SORT_DEPTH_FIRST) {
     uint32_t* dkey = at<uint32_t>(ws, lo.depth_key);
-    uint32_t* dkey_alt = at<uint32_t>(ws, lo.dkey_alt);
-    uint32_t* didx = at<uint32_t>(ws, lo.didx);
-    uint32_t* didx_alt = at<uint32_t>(ws, lo.didx_alt);
-    iota_kernel<<<persistent_grid(n, 256, 8), 256, 0, st>>>(didx, n, ctr);
-    SGS_LAUNCH_CHECK("iota_kernel");
-    // depth keys are 31-bit (0x7fffffff = not emitting): 4 passes over N.
-    // The depth sort must not clobber the preprocess depth keys (exported
-    // and used for the 64-bit key view), so sort a copy.
-    SGS_CUDA(cudaMemcpyAsync(dkey_alt, dkey, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
-    uint32_t* kbuf0 = dkey_alt;
-    uint32_t* kbuf1 = at<uint32_t>(ws, lo.dkey_tmp);
+    uint32_t* ka = at<uint32_t>(ws, lo.dkey_alt);
+    uint32_t* kb = at<uint32_t>(ws, lo.dkey_tmp);
+    uint32_t* ia = at<uint32_t>(ws, lo.didx);
+    uint32_t* ib = at<uint32_t>(ws, lo.didx_alt);
+    // N as a device count for the depth sort (graph-friendly: no host value baked in)
+    SGS_CUDA(cudaMemcpyAsync(ka, dkey, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
+    SGS_CUDA(cudaMemsetAsync(&ctr->n_depth, 0, 4, st));
+    set_count<<<1, 1, 0, st>>>(&ctr->n_depth, n);
+    SGS_LAUNCH_CHECK("set_count");
     bool alt = false;
-    int rc = radix_sort_pairs<uint32_t, kDepthSortIPT>(kbuf0, didx, kbuf1, didx_alt, &ctr->n_depth, n, 31, hist,
-                                                        status, &ctr->part_counter[0], &alt, st);
+    // depth keys are 31-bit (0x7fffffff = not emitting): 4 passes over N
+    int rc = radix_sort_pairs<uint32_t, kDepthSortIPT>(ka, ia, kb, ib, &ctr->n_depth, n, 31, at<uint32_t>(ws, lo.hist),
+                                                        at<uint32_t>(ws, lo.status), &ctr->part_counter[0], &alt, st,
+                                                        true);
     if (rc) return rc;
-    const uint32_t* perm = alt ? didx_alt : didx;
+    const uint32_t* perm = alt ? ib : ia;
     rc = launch_scan(tt, perm, n, cap, block_sums, offsets, ctr, st);
     if (rc) return rc;
-    uint32_t* k0 = at<uint32_t>(ws, lo.ent_key);
-    uint32_t* k1 = at<uint32_t>(ws, lo.ent_key_alt);
-    uint32_t* v0 = at<uint32_t>(ws, lo.ent_val);
-    uint32_t* v1 = at<uint32_t>(ws, lo.ent_val_alt);
-    emit_entries<false><<<egrid, 256, 0, st>>>(perm, n, tt, at<uint2>(ws, lo.rect), at<float4>(ws, lo.rec_geo),
-                                               at<float4>(ws, lo.rec_con), dkey, offsets, cam, cap, k0, v0);
-    SGS_LAUNCH_CHECK("emit_entries");
-    rc = radix_sort_pairs<uint32_t, kTileSortIPT>(k0, v0, k1, v1, &ctr->n_sort, cap, tile_sort_bits(lo.n_tiles), hist,
-                                                   status, &ctr->part_counter[4], &alt, st);
-    if (rc) return rc;
-    const uint32_t* kfinal = alt ? k1 : k0;
-    tile_ranges<uint32_t><<<persistent_grid(cap, 256, 8), 256, 0, st>>>(kfinal, &ctr->n_sort, ranges);
-    SGS_LAUNCH_CHECK("tile_ranges");
-  } else {
-    uint32_t* dkey = at<uint32_t>(ws, lo.depth_key);
-    int rc = launch_scan(tt, nullptr, n, cap, block_sums, offsets, ctr, st);
-    if (rc) return rc;
-    auto* k0 = at<unsigned long long>(ws, lo.ent_key);
-    auto* k1 = at<unsigned long long>(ws, lo.ent_key_alt);
-    uint32_t* v0 = at<uint32_t>(ws, lo.ent_val);
-    uint32_t* v1 = at<uint32_t>(ws, lo.ent_val_alt);
-    emit_entries<true><<<egrid, 256, 0, st>>>(nullptr, n, tt, at<uint2>(ws, lo.rect), at<float4>(ws, lo.rec_geo),
-                                              at<float4>(ws, lo.rec_con), dkey, offsets, cam, cap, k0, v0);
-    SGS_LAUNCH_CHECK("emit_entries");
-    bool alt = false;
-    rc = radix_sort_pairs<unsigned long long, kKey64SortIPT>(k0, v0, k1, v1, &ctr->n_sort, cap,
-                                                             32 + tile_sort_bits(lo.n_tiles), hist, status,
-                                                             &ctr->part_counter[0], &alt, st);
-    if (rc) return rc;
-    const unsigned long long* kfinal = alt ? k1 : k0;
-    tile_ranges<unsigned long long><<<persistent_grid(cap, 256, 8), 256, 0, st>>>(kfinal, &ctr->n_sort, ranges);
-    SGS_LAUNCH_CHECK("tile_ranges");
+    if (lo.n_tiles <= 65536)
+      return bin_tiles<uint16_t, kTileSortIPT>(cam, ws, lo, perm, tile_sort_bits(lo.n_tiles), 0, st);
+    return bin_tiles<uint32_t, kTileSortIPT>(cam, ws, lo, perm, tile_sort_bits(lo.n_tiles), 0, st);
   }
-  (void)sms;
-  return SGS_OK;
+  int rc = launch_scan(tt, nullptr, n, cap, block_sums, offsets, ctr, st);
+  if (rc) return rc;
+  return bin_tiles<unsigned long long, kKey64SortIPT>(cam, ws, lo, nullptr, 32 + tile_sort_bits(lo.n_tiles), 32, st);
 }
 
-// Export the sorted list as 64-bit keys (either mode).
-template <typename K>
-__global__ void export_keys(const K* __restrict__ keys, const uint32_t* __restrict__ vals,
-                            const uint32_t* __restrict__ depth_key, const uint32_t* n_ptr,
-                            unsigned long long* __restrict__ out_keys, uint32_t* __restrict__ out_vals) {
-  const uint32_t n = *n_ptr;
-  for (uint32_t i = blockIdx.x * 256 + threadIdx.x; i < n; i += gridDim.x * 256) {
-    uint32_t v = vals[i];
-    unsigned long long k;
-    if (sizeof(K) == 8)
-      k = (unsigned long long)keys[i];
-    else
-      k = ((unsigned long long)(uint32_t)keys[i] << 32) | depth_key[v];
-    out_keys[i] = k;
-    out_vals[i] = v;
+// Export the sorted list as 64-bit keys (either mode): tile from the ranges,
+// depth bits from the preprocess keys.
+__global__ void export_keys(const uint2* __restrict__ ranges, int n_tiles, const uint32_t* __restrict__ vals,
+                            const uint32_t* __restrict__ depth_key, unsigned long long* __restrict__ out_keys,
+                            uint32_t* __restrict__ out_vals) {
+  for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    const uint2 r = ranges[t];
+    for (uint32_t i = r.x + threadIdx.x; i < r.y; i += blockDim.x) {
+      const uint32_t v = vals[i];
+      out_keys[i] = ((unsigned long long)t << 32) | depth_key[v];
+      out_vals[i] = v;
+    }
   }
 }
 
 int launch_export_bins(const sgs_workspace* ws, const Layout& lo, unsigned long long* keys, uint32_t* vals,
                        uint32_t* ranges, cudaStream_t st) {
-  Counters* ctr = at<Counters>(ws, lo.counters);
   bool alt = final_in_alt(lo);
-  const int grid = persistent_grid((uint64_t)lo.cap, 256, 8);
   const uint32_t* v = at<uint32_t>(ws, alt ? lo.ent_val_alt : lo.ent_val);
   if (keys && vals) {
-    if (lo.sort_mode == SGS_SORT_KEY64) {
-      export_keys<unsigned long long><<<grid, 256, 0, st>>>(
-          at<unsigned long long>(ws, alt ? lo.ent_key_alt : lo.ent_key), v, at<uint32_t>(ws, lo.depth_key),
-          &ctr->n_sort, keys, vals);
-    } else {
-      export_keys<uint32_t><<<grid, 256, 0, st>>>(at<uint32_t>(ws, alt ? lo.ent_key_alt : lo.ent_key), v,
-                                                  at<uint32_t>(ws, lo.depth_key), &ctr->n_sort, keys, vals);
-    }
+    export_keys<<<persistent_grid((uint64_t)lo.n_tiles, 1, 8), 256, 0, st>>>(
+        at<uint2>(ws, lo.ranges), lo.n_tiles, v, at<uint32_t>(ws, lo.depth_key), keys, vals);
     SGS_LAUNCH_CHECK("export_keys");
   }
   if (ranges) SGS_CUDA(cudaMemcpyAsync(ranges, at<uint2>(ws, lo.ranges), (size_t)lo.n_tiles * 8,
@@ -317,26 +359,31 @@ int launch_export_bins(const sgs_workspace* ws, const Layout& lo, unsigned long 
 }
 
 // Generic 64-bit pair sort exported through the ABI (for tests / tools).
+uint64_t sort_u64_temp_bytes(uint64_t n, int bits) {
+  const uint64_t parts = rs_parts<unsigned long long, kKey64SortIPT>(n);
+  const int passes = (bits + 7) / 8;
+  return align256(n * 8) + align256(n * 4) + 16 * 256 * 4 + 256 + parts * 256 * 4 * passes + 64;
+}
+
 int launch_sort_u64(unsigned long long* keys, uint32_t* vals, uint32_t n, int bits, void* temp, uint64_t temp_bytes,
                     cudaStream_t st) {
-  constexpr int kTile = 256 * kKey64SortIPT;
-  const uint64_t parts = ((uint64_t)n + kTile - 1) / kTile;
-  const int passes = (bits + 7) / 8;
-  uint64_t need = align256((uint64_t)n * 12) + 16 * 256 * 4 + 256 + parts * 256 * 4 * passes + 64;
+  const uint64_t need = sort_u64_temp_bytes(n, bits);
   if (temp_bytes < need) {
     set_error("sort temp too small: need %llu", (unsigned long long)need);
     return SGS_E_WORKSPACE;
   }
   char* p = reinterpret_cast<char*>(temp);
   auto* k1 = reinterpret_cast<unsigned long long*>(p);
-  auto* v1 = reinterpret_cast<uint32_t*>(p + (uint64_t)n * 8);
-  p += align256((uint64_t)n * 12);
+  p += align256((uint64_t)n * 8);
+  auto* v1 = reinterpret_cast<uint32_t*>(p);
+  p += align256((uint64_t)n * 4);
   uint32_t* hist = reinterpret_cast<uint32_t*>(p);
   p += 16 * 256 * 4;
   uint32_t* meta = reinterpret_cast<uint32_t*>(p);  // [0] = n, [1..16] tickets
   p += 256;
   uint32_t* status = reinterpret_cast<uint32_t*>(p);
-  SGS_CUDA(cudaMemcpyAsync(meta, &n, 4, cudaMemcpyHostToDevice, st));
+  set_count<<<1, 1, 0, st>>>(meta, n);
+  SGS_LAUNCH_CHECK("set_count");
   bool alt = false;
   int rc = radix_sort_pairs<unsigned long long, kKey64SortIPT>(keys, vals, k1, v1, meta, n, bits, hist, status,
                                                                meta + 1, &alt, st);
@@ -346,13 +393,6 @@ int launch_sort_u64(unsigned long long* keys, uint32_t* vals, uint32_t n, int bi
     SGS_CUDA(cudaMemcpyAsync(vals, v1, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
   }
   return SGS_OK;
-}
-
-uint64_t sort_u64_temp_bytes(uint64_t n, int bits) {
-  constexpr int kTile = 256 * kKey64SortIPT;
-  const uint64_t parts = (n + kTile - 1) / kTile;
-  const int passes = (bits + 7) / 8;
-  return align256(n * 12) + 16 * 256 * 4 + 256 + parts * 256 * 4 * passes + 64;
 }
 
 }  // namespace sgs

@@ -12,10 +12,10 @@
 namespace sgs {
 
 constexpr int kNumSMs = 148;
-constexpr int kRadixThreads = 256;
-constexpr int kTileSortIPT = 16;   // items per thread, tile-key onesweep passes
-constexpr int kDepthSortIPT = 16;
-constexpr int kKey64SortIPT = 12;
+constexpr int kRadixThreads = 512;  // = kRsThreads in sort.cuh
+constexpr int kTileSortIPT = 8;   // items per thread, tile-key onesweep passes (4096 per CTA)
+constexpr int kDepthSortIPT = 8;
+constexpr int kKey64SortIPT = 6;
 constexpr uint32_t kMaxEntries = (1u << 30) - 1;  // look-back status packs 30-bit counts
 
 void set_error(const char* fmt, ...);
@@ -114,8 +114,9 @@ inline int make_layout(const sgs_workspace* ws, Layout* lo) {
   lo->didx_alt = take(n * 4);
   lo->offsets = take(n * 8);
   lo->scan_blocks = take(((n + 2047) / 2048 + 1) * 8);
-  lo->ent_key = take(cap * (k64 ? 8 : 4));
-  lo->ent_key_alt = take(cap * (k64 ? 8 : 4));
+  const uint64_t key_bytes = k64 ? 8 : (lo->n_tiles <= 65536 ? 2 : 4);
+  lo->ent_key = take(cap * key_bytes);
+  lo->ent_key_alt = take(cap * key_bytes);
   lo->ent_val = take(cap * 4);
   lo->ent_val_alt = take(cap * 4);
   lo->ranges = take((uint64_t)lo->n_tiles * 8);

@@ -1,33 +1,40 @@
 // sort.cuh -- stable LSD radix sort of (key, u32 value) pairs, onesweep style:
 // one up-front histogram kernel computes every pass's 256-bin digit counts
-// in a single read of the keys, then each 8-bit pass is ONE kernel that
-// ranks a tile of keys in shared memory (warp match_any + per-warp digit
-// histograms, order-preserving), publishes its per-digit counts, resolves
-// its global digit offsets by decoupled look-back over earlier tiles, and
-// scatters keys/values through shared memory.
+// in a single (vectorised) read of the keys, then each 8-bit pass is ONE
+// kernel that ranks a tile of keys in shared memory (warp ballot-match +
+// per-warp digit counters, order-preserving), publishes its per-digit
+// counts, resolves its global digit offsets by decoupled look-back over
+// earlier tiles, and scatters keys / values through shared memory so the
+// global writes are runs of consecutive addresses.
 //
 // Persistent: the grid is at most the number of co-resident CTAs and tiles
-// are claimed in order from an atomic ticket, so look-back always waits on a
-// CTA that is running.  Item counts are read from device memory, so a whole
+// are claimed in order from an atomic ticket, so look-back only ever waits on
+// a CTA that is running.  Item counts are read from device memory, so a whole
 // frame can be enqueued (or graph-captured) without a host round trip.
+//
+// The final pass of a tile-key sort can skip writing keys and instead emits
+// the per-tile [start, end) ranges: a tile's entries form one contiguous run
+// inside each CTA's shared-memory order, so each run contributes one
+// atomicMin / atomicMax (K4 fused into K3).
 #pragma once
+
+#include <algorithm>
+#include <utility>
 
 #include "common.cuh"
 
 namespace sgs {
 
 // status word: [31:30] flag (0 empty, 1 aggregate, 2 inclusive prefix), [29:0] count
-constexpr uint32_t kFlagAgg = 1u << 30;
-constexpr uint32_t kFlagInc = 2u << 30;
-constexpr uint32_t kCountMask = (1u << 30) - 1;
+enum : uint32_t { kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kCountMask = (1u << 30) - 1 };
 
 template <typename K>
 __device__ __forceinline__ uint32_t rs_digit(K k, int shift) {
   return (uint32_t)(k >> shift) & 0xffu;
 }
 
-// Lanes of the warp holding the same 8-bit digit, from 8 ballots (cheaper
-// than match.any on sm_100).  Lanes outside `valid` never match.
+// Lanes of the warp holding the same 8-bit digit, from 8 ballots.  Lanes
+// outside `valid` never match.
 __device__ __forceinline__ uint32_t match_digit8(uint32_t d, uint32_t valid) {
   uint32_t peers = valid;
 #pragma unroll
@@ -45,21 +52,29 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   return m;
 }
 
-// Histogram of `num_passes` digits starting at bit `begin_bit`; hist is
-// num_passes x 256 u32 and must be zeroed.  n = min(*n_ptr, n_cap).
+// Histogram of `num_passes` 8-bit digits; hist is num_passes x 256 u32 and
+// must be zeroed.  n = min(*n_ptr, n_cap).  16-byte vector loads.
 template <typename K>
 __global__ void __launch_bounds__(256) rs_histogram(const K* __restrict__ keys, const uint32_t* n_ptr, uint32_t n_cap,
-                                                    int begin_bit, int num_passes, uint32_t* __restrict__ hist) {
-  // one private 256-bin histogram per warp and pass (contention stays inside a warp)
-  extern __shared__ uint32_t sh[];  // [num_passes][8][256]
+                                                    int num_passes, uint32_t* __restrict__ hist) {
+  extern __shared__ uint32_t sh[];  // [num_passes][8 warps][256]
+  constexpr int V = 16 / sizeof(K);
   const uint32_t n = min(*n_ptr, n_cap);
   const int w = threadIdx.x >> 5;
   for (int j = threadIdx.x; j < num_passes * 8 * 256; j += 256) sh[j] = 0;
   __syncthreads();
-  for (uint32_t i = blockIdx.x * 256u + threadIdx.x; i < n; i += gridDim.x * 256u) {
+  const uint32_t nvec = n / V;
+  const uint4* kv = reinterpret_cast<const uint4*>(keys);
+  for (uint32_t i = blockIdx.x * 256u + threadIdx.x; i < nvec; i += gridDim.x * 256u) {
+    uint4 raw = kv[i];
+    const K* ks = reinterpret_cast<const K*>(&raw);
+#pragma unroll
+    for (int v = 0; v < V; ++v)
+      for (int p = 0; p < num_passes; ++p) atomicAdd(&sh[(p * 8 + w) * 256 + rs_digit(ks[v], 8 * p)], 1u);
+  }
+  for (uint32_t i = nvec * V + blockIdx.x * 256u + threadIdx.x; i < n; i += gridDim.x * 256u) {
     K k = keys[i];
-#pragma unroll 1
-    for (int p = 0; p < num_passes; ++p) atomicAdd(&sh[(p * 8 + w) * 256 + rs_digit(k, begin_bit + 8 * p)], 1u);
+    for (int p = 0; p < num_passes; ++p) atomicAdd(&sh[(p * 8 + w) * 256 + rs_digit(k, 8 * p)], 1u);
   }
   __syncthreads();
   for (int j = threadIdx.x; j < num_passes * 256; j += 256) {
@@ -89,25 +104,35 @@ __global__ void __launch_bounds__(256) rs_scan_hist(uint32_t* hist) {
   h[t] = pre + x - v;
 }
 
+constexpr int kRsThreads = 512;  // 16 warps per CTA
+constexpr int kRsWarps = kRsThreads / 32;
+
 template <typename K, int IPT>
 struct RsSmem {
-  static constexpr int kTile = 256 * IPT;
-  uint32_t warp_hist[8][256];
+  static constexpr int kTile = kRsThreads * IPT;
+  uint32_t warp_hist[kRsWarps][256];
   uint32_t digit_start[256];
   uint32_t global_base[256];
   uint32_t warp_tot[8];
   uint32_t part;
-  K keys[kTile];
   uint32_t vals[kTile];
+  K keys[kTile];
+};
+
+struct RsRangeOut {
+  uint2* ranges;   // per-tile [start, end), pre-set to (0xffffffff, 0); null = none
+  int tile_shift;  // tile id = key >> tile_shift
 };
 
 // One 8-bit pass.  status: nparts x 256 u32, zeroed; ticket zeroed.
+// vin == nullptr means values are the item indices (first pass of an argsort).
+// kout == nullptr skips the key writes (last pass).
 template <typename K, int IPT>
-__global__ void __launch_bounds__(256) rs_onesweep(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
-                                                   K* __restrict__ kout, uint32_t* __restrict__ vout,
-                                                   const uint32_t* n_ptr, uint32_t n_cap, int shift,
-                                                   const uint32_t* __restrict__ pass_base, uint32_t* status,
-                                                   uint32_t* ticket) {
+__global__ void __launch_bounds__(kRsThreads) rs_onesweep(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
+                                                          K* __restrict__ kout, uint32_t* __restrict__ vout,
+                                                          const uint32_t* n_ptr, uint32_t n_cap, int shift,
+                                                          const uint32_t* __restrict__ pass_base, uint32_t* status,
+                                                          uint32_t* ticket, RsRangeOut rout) {
   using S = RsSmem<K, IPT>;
   constexpr int kTile = S::kTile;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -119,99 +144,124 @@ __global__ void __launch_bounds__(256) rs_onesweep(const K* __restrict__ kin, co
 
   for (;;) {
     if (t == 0) s.part = atomicAdd(ticket, 1u);
-    for (int j = t; j < 8 * 256; j += 256) (&s.warp_hist[0][0])[j] = 0;
+    for (int j = t; j < kRsWarps * 256; j += kRsThreads) (&s.warp_hist[0][0])[j] = 0;
     __syncthreads();
     const uint32_t part = s.part;
     if (part >= nparts) return;
 
-    // ---- load (warp-striped) and rank within the warp, order-preserving
+    // ---- load keys + values (warp-striped), rank within the warp, order-preserving
     const uint32_t base = part * kTile + w * 32 * IPT;
     K keys[IPT];
-    uint32_t vals[IPT], rank[IPT];
+    uint32_t vals[IPT];
+    uint16_t rank[IPT];
 #pragma unroll
     for (int i = 0; i < IPT; ++i) {
-      uint32_t idx = base + i * 32 + lane;
-      bool valid = idx < n;
+      const uint32_t idx = base + i * 32 + lane;
+      const bool valid = idx < n;
       keys[i] = valid ? kin[idx] : K(0);
-      vals[i] = valid ? vin[idx] : 0u;
+      vals[i] = valid ? (vin ? vin[idx] : idx) : 0u;
     }
 #pragma unroll
     for (int i = 0; i < IPT; ++i) {
-      uint32_t idx = base + i * 32 + lane;
-      bool valid = idx < n;
-      uint32_t d = rs_digit(keys[i], shift);
-      uint32_t peers = match_digit8(d, __ballot_sync(0xffffffffu, valid));
-      uint32_t before = valid ? s.warp_hist[w][d] : 0u;
+      const uint32_t idx = base + i * 32 + lane;
+      const bool valid = idx < n;
+      const uint32_t d = rs_digit(keys[i], shift);
+      const uint32_t peers = match_digit8(d, __ballot_sync(0xffffffffu, valid));
+      const int leader = __ffs(peers) - 1;
+      uint32_t old = 0;
+      if (valid && lane == leader) old = atomicAdd(&s.warp_hist[w][d], (uint32_t)__popc(peers));
+      old = __shfl_sync(0xffffffffu, old, valid ? leader : lane);
+      rank[i] = (uint16_t)(old + __popc(peers & lt));
+      // the leaders of successive items are different threads: order their
+      // counter updates explicitly (stability depends on it)
       __syncwarp();
-      if (valid && (peers & lt) == 0) s.warp_hist[w][d] = before + __popc(peers);
-      __syncwarp();
-      rank[i] = before + __popc(peers & lt);
     }
     __syncthreads();
 
-    // ---- per digit: scan over warps, publish, look back
-    uint32_t run = 0;
+    // ---- per digit (threads 0..255): scan over warps, publish, look back
+    uint32_t run = 0, wexcl = 0;
+    if (t < 256) {
 #pragma unroll
-    for (int ww = 0; ww < 8; ++ww) {
-      uint32_t c = s.warp_hist[ww][t];
-      s.warp_hist[ww][t] = run;
-      run += c;
-    }
-    uint32_t* my_status = status + (size_t)part * 256 + t;
-    if (part == 0) {
-      atomicExch(my_status, kFlagInc | run);
-    } else {
-      atomicExch(my_status, kFlagAgg | run);
-    }
-    // block exclusive scan of run over digits -> digit_start
-    {
-      uint32_t x = run;
+      for (int ww = 0; ww < kRsWarps; ++ww) {
+        const uint32_t c = s.warp_hist[ww][t];
+        s.warp_hist[ww][t] = run;
+        run += c;
+      }
+      atomicExch(status + (size_t)part * 256 + t, (part == 0 ? kFlagInc : kFlagAgg) | run);
+      uint32_t x = run;  // block exclusive scan of the digit counts -> digit_start
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
         if (lane >= o) x += y;
       }
       if (lane == 31) s.warp_tot[w] = x;
-      __syncthreads();
+      wexcl = x - run;
+    }
+    __syncthreads();
+    if (t < 256) {
       uint32_t pre = 0;
       for (int i = 0; i < w; ++i) pre += s.warp_tot[i];
-      s.digit_start[t] = pre + x - run;
-    }
-    uint32_t excl = 0;
-    if (part > 0) {
-      int64_t p = (int64_t)part - 1;
-      for (;;) {
-        uint32_t v = *reinterpret_cast<volatile uint32_t*>(status + (size_t)p * 256 + t);
-        uint32_t flag = v & ~kCountMask;
-        if (flag == 0) continue;
-        excl += v & kCountMask;
-        if (flag == kFlagInc) break;
-        --p;
+      s.digit_start[t] = pre + wexcl;
+      uint32_t excl = 0;
+      if (part > 0) {
+        // windowed decoupled look-back: kLookback predecessors are loaded at
+        // once, summed from the nearest until the first inclusive prefix; a
+        // not-yet-published predecessor restarts the window there.
+        constexpr int kLookback = 16;
+        int64_t p = (int64_t)part - 1;
+        for (;;) {
+          uint32_t v[kLookback];
+#pragma unroll
+          for (int j = 0; j < kLookback; ++j)
+            v[j] = (p - j >= 0) ? *reinterpret_cast<volatile uint32_t*>(status + (size_t)(p - j) * 256 + t)
+                                : (uint32_t)kFlagInc;
+          int used = 0;
+          bool done = false;
+#pragma unroll
+          for (int j = 0; j < kLookback; ++j) {
+            const uint32_t flag = v[j] & ~kCountMask;
+            if (flag == 0) break;
+            excl += v[j] & kCountMask;
+            used = j + 1;
+            if (flag == kFlagInc) {
+              done = true;
+              break;
+            }
+          }
+          if (done) break;
+          p -= used;
+        }
+        atomicExch(status + (size_t)part * 256 + t, kFlagInc | (excl + run));
       }
-      atomicExch(my_status, kFlagInc | (excl + run));
+      s.global_base[t] = pass_base[t] + excl;
     }
-    s.global_base[t] = pass_base[t] + excl;
     __syncthreads();
 
     // ---- scatter into shared memory in local sorted order
 #pragma unroll
     for (int i = 0; i < IPT; ++i) {
-      uint32_t idx = base + i * 32 + lane;
+      const uint32_t idx = base + i * 32 + lane;
       if (idx < n) {
-        uint32_t d = rs_digit(keys[i], shift);
-        uint32_t pos = s.digit_start[d] + s.warp_hist[w][d] + rank[i];
+        const uint32_t d = rs_digit(keys[i], shift);
+        const uint32_t pos = s.digit_start[d] + s.warp_hist[w][d] + rank[i];
         s.keys[pos] = keys[i];
         s.vals[pos] = vals[i];
       }
     }
     __syncthreads();
     const uint32_t cnt = min((uint32_t)kTile, n - part * kTile);
-    for (uint32_t j = t; j < cnt; j += 256) {
-      K k = s.keys[j];
-      uint32_t d = rs_digit(k, shift);
-      uint32_t g = s.global_base[d] + j - s.digit_start[d];
-      kout[g] = k;
+    for (uint32_t j = t; j < cnt; j += kRsThreads) {
+      const K k = s.keys[j];
+      const uint32_t d = rs_digit(k, shift);
+      const uint32_t g = s.global_base[d] + j - s.digit_start[d];
+      if (kout) kout[g] = k;
       vout[g] = s.vals[j];
+      if (rout.ranges) {
+        const uint32_t tile = (uint32_t)(k >> rout.tile_shift);
+        if (j == 0 || (uint32_t)(s.keys[j - 1] >> rout.tile_shift) != tile) atomicMin(&rout.ranges[tile].x, g);
+        if (j + 1 == cnt || (uint32_t)(s.keys[j + 1] >> rout.tile_shift) != tile)
+          atomicMax(&rout.ranges[tile].y, g + 1);
+      }
     }
     __syncthreads();
   }
@@ -220,29 +270,35 @@ __global__ void __launch_bounds__(256) rs_onesweep(const K* __restrict__ kin, co
 int resident_ctas_per_sm(const void* kernel, int threads, size_t smem);
 int device_sm_count();
 
+template <typename K, int IPT>
+inline uint64_t rs_parts(uint64_t n) {
+  return (n + kRsThreads * IPT - 1) / (kRsThreads * IPT);
+}
+
 // Sort `n_cap`-bounded pairs (count in *n_ptr on the device) over bits
-// [0, bits).  Ping-pongs between (k0, v0) and (k1, v1); returns in *result_in_alt
-// whether the sorted data ends in (k1, v1).  hist: 16*256 u32; status: parts*256*passes u32;
-// tickets: >= passes u32; all three zeroed by this function.
+// [0, bits).  Ping-pongs between (k0, v0) and (k1, v1); *result_in_alt says
+// whether the result is in (k1, v1).  iota_values: the input values are the
+// item indices (v0 is not read).  With `rout.ranges`, the last pass writes
+// only values plus the tile ranges.  hist: 16*256 u32; status:
+// parts*256*passes u32; tickets: >= passes u32; all zeroed here.
 template <typename K, int IPT>
 int radix_sort_pairs(K* k0, uint32_t* v0, K* k1, uint32_t* v1, const uint32_t* n_ptr, uint32_t n_cap, int bits,
-                     uint32_t* hist, uint32_t* status, uint32_t* tickets, bool* result_in_alt, cudaStream_t st) {
+                     uint32_t* hist, uint32_t* status, uint32_t* tickets, bool* result_in_alt, cudaStream_t st,
+                     bool iota_values = false, RsRangeOut rout = RsRangeOut{nullptr, 0}) {
   const int passes = (bits + 7) / 8;
-  constexpr int kTile = 256 * IPT;
-  const uint64_t parts = ((uint64_t)n_cap + kTile - 1) / kTile;
+  const uint64_t parts = rs_parts<K, IPT>(n_cap);
   *result_in_alt = false;
   if (n_cap == 0 || passes == 0) return SGS_OK;
   SGS_CUDA(cudaMemsetAsync(hist, 0, (size_t)passes * 256 * 4, st));
   SGS_CUDA(cudaMemsetAsync(status, 0, (size_t)parts * 256 * 4 * passes, st));
   SGS_CUDA(cudaMemsetAsync(tickets, 0, (size_t)passes * 4, st));
   const int sms = device_sm_count();
-  int hgrid = (int)std::min<uint64_t>((n_cap + 256 * 32 - 1) / (256 * 32), (uint64_t)sms * 4);
+  constexpr int V = 16 / sizeof(K);
+  int hgrid = (int)std::min<uint64_t>((n_cap / V + 256 * 8 - 1) / (256 * 8), (uint64_t)sms * 4);
   if (hgrid < 1) hgrid = 1;
   const size_t hsmem = (size_t)passes * 8 * 256 * 4;
-  if (hsmem > 48 * 1024) {
-    SGS_CUDA(cudaFuncSetAttribute(rs_histogram<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsmem));
-  }
-  rs_histogram<K><<<hgrid, 256, hsmem, st>>>(k0, n_ptr, n_cap, 0, passes, hist);
+  SGS_CUDA(cudaFuncSetAttribute(rs_histogram<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+  rs_histogram<K><<<hgrid, 256, hsmem, st>>>(k0, n_ptr, n_cap, passes, hist);
   SGS_LAUNCH_CHECK("rs_histogram");
   rs_scan_hist<<<passes, 256, 0, st>>>(hist);
   SGS_LAUNCH_CHECK("rs_scan_hist");
@@ -252,7 +308,8 @@ int radix_sort_pairs(K* k0, uint32_t* v0, K* k1, uint32_t* v1, const uint32_t* n
     SGS_CUDA(cudaFuncSetAttribute(rs_onesweep<K, IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr_set = true;
   }
-  const int per_sm = resident_ctas_per_sm((const void*)rs_onesweep<K, IPT>, 256, smem);
+  static int per_sm = 0;
+  if (!per_sm) per_sm = resident_ctas_per_sm((const void*)rs_onesweep<K, IPT>, kRsThreads, smem);
   if (per_sm < 1) {
     set_error("onesweep kernel cannot be resident");
     return SGS_E_CUDA;
@@ -263,8 +320,11 @@ int radix_sort_pairs(K* k0, uint32_t* v0, K* k1, uint32_t* v1, const uint32_t* n
   uint32_t* va = v0;
   uint32_t* vb = v1;
   for (int p = 0; p < passes; ++p) {
-    rs_onesweep<K, IPT><<<grid, 256, smem, st>>>(ka, va, kb, vb, n_ptr, n_cap, 8 * p, hist + 256 * p,
-                                                  status + (size_t)parts * 256 * p, tickets + p);
+    const bool last = p + 1 == passes;
+    rs_onesweep<K, IPT><<<grid, kRsThreads, smem, st>>>(ka, (p == 0 && iota_values) ? nullptr : va,
+                                                  (last && rout.ranges) ? nullptr : kb, vb, n_ptr, n_cap, 8 * p,
+                                                  hist + 256 * p, status + (size_t)parts * 256 * p, tickets + p,
+                                                  last ? rout : RsRangeOut{nullptr, 0});
     SGS_LAUNCH_CHECK("rs_onesweep");
     std::swap(ka, kb);
     std::swap(va, vb);

@@ -276,6 +276,21 @@ class Rasterizer:
         return out
 
     # ----------------------------------------------------------------- exports
+    DEBUG_BUFFERS = ("counters", "rec_geo", "rec_con", "rec_col", "depth_key", "rect",
+                     "tiles_touched", "dkey_alt", "dkey_tmp", "didx", "didx_alt", "offsets",
+                     "scan_blocks", "ent_key", "ent_key_alt", "ent_val", "ent_val_alt", "ranges",
+                     "hist", "status")
+
+    @staticmethod
+    def debug_view(frame: Frame, name: str, count: int, dtype=torch.int32) -> torch.Tensor:
+        """Copy of `count` elements of an internal workspace buffer (debugging)."""
+        ptr = C.c_void_p()
+        off = C.c_uint64()
+        _ffi.call("sgs_debug_buffer", C.byref(frame.ws.desc),
+                  Rasterizer.DEBUG_BUFFERS.index(name), C.byref(ptr), C.byref(off))
+        nbytes = count * torch.tensor([], dtype=dtype).element_size()
+        return frame.ws.buf[off.value:off.value + nbytes].view(dtype).clone()
+
     def export_bins(self, frame: Frame):
         """(keys u64 as int64, values int32, ranges (T,2) int32) of the sorted tile list."""
         st = frame.ws.stats()
