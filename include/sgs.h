@@ -41,7 +41,8 @@ extern "C" {
 
 /* Pinhole camera, render.py:30-57 (Camera).  rotation rows = (right, down,
  * forward) world-to-camera; pixel = (fx x/z + cx, fy y/z + cy).  tile_y0/1 is
- * a tile-row window [tile_y0, tile_y1) for tile-strip renders (0,0 = all). */
+ * a tile-row window [tile_y0, tile_y1) for tile-strip renders (0,0 = all);
+ * lowpass is the `lowpass` argument of _prepare / project (render.py:259, 320). */
 typedef struct sgs_camera {
   float rotation[9];
   float translation[3];
@@ -49,6 +50,7 @@ typedef struct sgs_camera {
   float near_z;
   int32_t width, height;
   int32_t tile_y0, tile_y1;
+  float lowpass; /* cov2d diagonal floor in px^2, render.py:26 (0.3) */
 } sgs_camera;
 
 /* Packed parameter arrays, render.py:90-108 (SceneParams) + soft masks. */
@@ -161,6 +163,12 @@ int sgs_raster_backward(const sgs_camera* cam, const float background[3],
  * soft-mask gradients dL/dm_p = o dL/do_eff, dL/dm_l = (dL/dc_pre . a_l) e_l. */
 int sgs_preprocess_backward(const sgs_params* params, const sgs_camera* cam, const float* grad2d,
                             sgs_grads* grads, void* stream);
+
+/* Per-primitive projection (all N primitives, 16 floats each):
+ * [visible, depth, mean2d x/y, cov2d 00/01/11, conic 00/01/11, color_pre rgb,
+ * color rgb] -- the per-primitive outputs of _prepare (render.py:259-317) and
+ * project (render.py:320-330), for the host API and inspection. */
+int sgs_project_records(const sgs_params* params, const sgs_camera* cam, float* out, void* stream);
 
 /* Read the frame counters (synchronises `stream`). */
 int sgs_get_stats(const sgs_workspace* ws, sgs_stats* out, void* stream);

@@ -306,3 +306,20 @@ def loss_and_grads(p, cam, target, lambda_ssim=0.2, background=(0.0, 0.0, 0.0)):
     img = render(p, cam, background)
     val, dimg = loss_and_dimg(img, target, lambda_ssim)
     return val, backward(p, cam, project(p, cam), dimg, background), img
+
+
+def vram_model_counts(p, cam, tile_px=16):
+    """Reference 3-sigma VRAM model (postprocess.py:118-135): (visible, entries)."""
+    pr = project(p, cam)
+    if pr is None:
+        return 0, 0
+    rx = 3.0 * np.sqrt(pr.cov[:, 0, 0])
+    ry = 3.0 * np.sqrt(pr.cov[:, 1, 1])
+    x0, x1 = pr.mean[:, 0] - rx, pr.mean[:, 0] + rx
+    y0, y1 = pr.mean[:, 1] - ry, pr.mean[:, 1] + ry
+    on = (x1 > 0) & (x0 < cam.width) & (y1 > 0) & (y0 < cam.height)
+    tx = (cam.width + tile_px - 1) // tile_px
+    ty = (cam.height + tile_px - 1) // tile_px
+    c = lambda v, m: np.clip(np.floor(v / tile_px), 0, m - 1).astype(np.int64)  # noqa: E731
+    ent = (c(x1, tx) - c(x0, tx) + 1) * (c(y1, ty) - c(y0, ty) + 1)
+    return int(on.sum()), int(ent[on].sum())

@@ -35,8 +35,9 @@
 namespace {
 
 SgsCam make_cam(const float* R, const float* t, float fx, float fy, float cx, float cy, float near_z, int W, int H,
-                int tile_y0, int tile_y1) {
+                int tile_y0, int tile_y1, float lowpass) {
   SgsCam c;
+  c.lowpass = lowpass;
   for (int i = 0; i < 9; ++i) c.R[i] = R[i];
   for (int i = 0; i < 3; ++i) c.t[i] = t[i];
   for (int k = 0; k < 3; ++k) {
@@ -63,7 +64,7 @@ SgsCam make_cam(const float* R, const float* t, float fx, float fy, float cx, fl
 
 extern "C" {
 
-// cam_f: R[9], t[3], fx, fy, cx, cy, near (17 floats); cam_i: W, H, tile_y0, tile_y1
+// cam_f: R[9], t[3], fx, fy, cx, cy, near, lowpass (18 floats); cam_i: W, H, tile_y0, tile_y1
 // outputs (length N): depth_bits, rect (2 u32 packed like the GPU), tiles_touched,
 // records (12 floats: geo, con, col); counts[0] = visible, counts[1] = emitting.
 void oracle_preprocess(int64_t n, int L, const float* pos, const float* quat, const float* ls, const float* opac,
@@ -72,7 +73,7 @@ void oracle_preprocess(int64_t n, int L, const float* pos, const float* quat, co
                        uint32_t* depth_bits, uint32_t* rect, uint32_t* tiles_touched, float* records,
                        int64_t* counts) {
   SgsCam cam = make_cam(cam_f, cam_f + 9, cam_f[12], cam_f[13], cam_f[14], cam_f[15], cam_f[16], cam_i[0], cam_i[1],
-                        cam_i[2], cam_i[3]);
+                        cam_i[2], cam_i[3], cam_f[17]);
   int64_t vis = 0, emit = 0;
   for (int64_t i = 0; i < n; ++i) {
     SgsProj pr;
@@ -119,7 +120,7 @@ void oracle_bin(int64_t n, const uint32_t* depth_bits, const uint32_t* rect, con
                 const float* records, const float* cam_f, const int32_t* cam_i, uint64_t* keys, uint32_t* vals,
                 uint32_t* ranges) {
   SgsCam cam = make_cam(cam_f, cam_f + 9, cam_f[12], cam_f[13], cam_f[14], cam_f[15], cam_f[16], cam_i[0], cam_i[1],
-                        cam_i[2], cam_i[3]);
+                        cam_i[2], cam_i[3], cam_f[17]);
   std::vector<std::pair<uint64_t, uint32_t>> ent;
   for (int64_t i = 0; i < n; ++i) {
     if (!tiles_touched[i]) continue;
@@ -155,7 +156,7 @@ void oracle_raster_forward(const uint32_t* ranges, const uint32_t* vals, const f
                            const int32_t* cam_i, const float* bg, float* img, float* Tout, uint32_t* nc_out,
                            double* weight_sums) {
   SgsCam cam = make_cam(cam_f, cam_f + 9, cam_f[12], cam_f[13], cam_f[14], cam_f[15], cam_f[16], cam_i[0], cam_i[1],
-                        cam_i[2], cam_i[3]);
+                        cam_i[2], cam_i[3], cam_f[17]);
   for (int py = cam.tile_y0 * SGS_TILE; py < std::min(cam.height, cam.tile_y1 * SGS_TILE); ++py)
     for (int px = 0; px < cam.width; ++px) {
       const int tile = (py / SGS_TILE) * cam.tiles_x + px / SGS_TILE;
@@ -191,7 +192,7 @@ void oracle_raster_forward(const uint32_t* ranges, const uint32_t* vals, const f
 void oracle_raster_backward(const uint32_t* ranges, const uint32_t* vals, const float* records, const float* cam_f,
                             const int32_t* cam_i, const float* bg, const float* dimg, double* grad2d) {
   SgsCam cam = make_cam(cam_f, cam_f + 9, cam_f[12], cam_f[13], cam_f[14], cam_f[15], cam_f[16], cam_i[0], cam_i[1],
-                        cam_i[2], cam_i[3]);
+                        cam_i[2], cam_i[3], cam_f[17]);
   struct Item {
     uint32_t g;
     double G, a, alpha, T, dx, dy;
@@ -308,8 +309,8 @@ void oracle_preprocess_backward(int64_t n, int L, const float* pos, const float*
           for (int j = 0; j < 3; ++j) s += MS[3 * r + j] * M[3 * c + j];
           cov[2 * r + c] = s;
         }
-      cov[0] += 0.3;
-      cov[3] += 0.3;
+      cov[0] += (double)cam_f[17];
+      cov[3] += (double)cam_f[17];
       const double det = cov[0] * cov[3] - cov[1] * cov[2];
       const double K[4] = {cov[3] / det, -cov[1] / det, -cov[2] / det, cov[0] / det};
       const double dK[4] = {gv[6], gv[7], gv[7], gv[8]};

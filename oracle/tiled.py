@@ -43,11 +43,11 @@ def _p(a):
     return None if a is None else a.ctypes.data_as(C.c_void_p)
 
 
-def cam_arrays(cam, tile_rows=(0, 0)):
-    f = np.zeros(17, np.float32)
+def cam_arrays(cam, tile_rows=(0, 0), lowpass=0.3):
+    f = np.zeros(18, np.float32)
     f[:9] = np.asarray(cam.rotation, dtype=np.float64).reshape(9)
     f[9:12] = np.asarray(cam.translation, dtype=np.float64).reshape(3)
-    f[12:17] = [cam.fx, cam.fy, cam.cx, cam.cy, getattr(cam, "near", 0.1)]
+    f[12:18] = [cam.fx, cam.fy, cam.cx, cam.cy, getattr(cam, "near", 0.1), lowpass]
     i = np.array([cam.width, cam.height, tile_rows[0], tile_rows[1]], np.int32)
     return f, i
 
@@ -65,10 +65,10 @@ class TiledResult:
     pass
 
 
-def preprocess(scene, cam, tile_rows=(0, 0)):
+def preprocess(scene, cam, tile_rows=(0, 0), lowpass=0.3):
     a = _arrays(scene)
     n, L = a["position"].shape[0], a["axis_raw"].shape[1]
-    cf, ci = cam_arrays(cam, tile_rows)
+    cf, ci = cam_arrays(cam, tile_rows, lowpass)
     r = TiledResult()
     r.depth_bits = np.zeros(n, np.uint32)
     r.rect = np.zeros((n, 2), np.uint32)

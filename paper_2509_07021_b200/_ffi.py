@@ -24,7 +24,7 @@ class SgsCamera(C.Structure):
     _fields_ = [("rotation", C.c_float * 9), ("translation", C.c_float * 3),
                 ("fx", C.c_float), ("fy", C.c_float), ("cx", C.c_float), ("cy", C.c_float),
                 ("near_z", C.c_float), ("width", C.c_int32), ("height", C.c_int32),
-                ("tile_y0", C.c_int32), ("tile_y1", C.c_int32)]
+                ("tile_y0", C.c_int32), ("tile_y1", C.c_int32), ("lowpass", C.c_float)]
 
 
 class SgsParams(C.Structure):
@@ -70,6 +70,7 @@ SIGNATURES = {
                                       C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "sgs_preprocess_backward": (C.c_int, [_P(SgsParams), _P(SgsCamera), C.c_void_p, _P(SgsGrads),
                                           C.c_void_p]),
+    "sgs_project_records": (C.c_int, [_P(SgsParams), _P(SgsCamera), C.c_void_p, C.c_void_p]),
     "sgs_get_stats": (C.c_int, [_P(SgsWorkspace), _P(SgsStats), C.c_void_p]),
     "sgs_vram_model": (C.c_int, [_P(SgsParams), _P(SgsCamera), C.c_int32, _P(SgsWorkspace),
                                  C.c_void_p]),

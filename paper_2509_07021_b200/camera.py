@@ -67,7 +67,7 @@ class Camera:
                       near=self.near)
 
 
-def to_sgs(cam, tile_rows: tuple[int, int] | None = None) -> _ffi.SgsCamera:
+def to_sgs(cam, tile_rows: tuple[int, int] | None = None, lowpass: float = 0.3) -> _ffi.SgsCamera:
     """Duck-typed camera -> C struct (float32, as the GPU computes)."""
     c = _ffi.SgsCamera()
     rot = np.asarray(cam.rotation, dtype=np.float64).reshape(9).astype(np.float32)
@@ -83,4 +83,5 @@ def to_sgs(cam, tile_rows: tuple[int, int] | None = None) -> _ffi.SgsCamera:
         c.tile_y0, c.tile_y1 = 0, 0
     else:
         c.tile_y0, c.tile_y1 = int(tile_rows[0]), int(tile_rows[1])
+    c.lowpass = float(np.float32(lowpass))
     return c

@@ -41,6 +41,7 @@ int resident_ctas_per_sm(const void* kernel, int threads, size_t smem) {
 
 int launch_preprocess(const sgs_params& P, const SgsCam& cam, const sgs_workspace* ws, const Layout& lo,
                       cudaStream_t st);
+int launch_project_records(const sgs_params& P, const SgsCam& cam, float* out, cudaStream_t st);
 int launch_vram3s(const sgs_params& P, const SgsCam& cam, int tile_px, Counters* ctr, cudaStream_t st);
 int launch_bin(const SgsCam& cam, const sgs_workspace* ws, const Layout& lo, cudaStream_t st);
 bool final_in_alt(const Layout& lo);
@@ -185,6 +186,25 @@ int sgs_preprocess_backward(const sgs_params* params, const sgs_camera* cam, con
   if (rc) return rc;
   if (params->n == 0) return SGS_OK;
   return launch_preprocess_bwd(*params, c, grad2d, *grads, as_stream(stream));
+}
+
+int sgs_project_records(const sgs_params* params, const sgs_camera* cam, float* out, void* stream) {
+  int rc = check_params(params, nullptr);
+  if (rc) return rc;
+  if (!out && params->n > 0) {
+    set_error("null output");
+    return SGS_E_ARG;
+  }
+  Layout lo{};
+  lo.W = cam ? cam->width : 0;
+  lo.H = cam ? cam->height : 0;
+  lo.tiles_x = (lo.W + SGS_TILE - 1) / SGS_TILE;
+  lo.tiles_y = (lo.H + SGS_TILE - 1) / SGS_TILE;
+  SgsCam c;
+  rc = make_cam(cam, lo, &c);
+  if (rc) return rc;
+  if (params->n == 0) return SGS_OK;
+  return launch_project_records(*params, c, out, as_stream(stream));
 }
 
 int sgs_get_stats(const sgs_workspace* ws, sgs_stats* out, void* stream) {

@@ -180,6 +180,11 @@ inline int make_cam(const sgs_camera* c, const Layout& lo, SgsCam* out) {
   }
   out->tile_y0 = y0;
   out->tile_y1 = y1;
+  if (!(c->lowpass >= 0.0f)) {
+    set_error("lowpass must be >= 0");
+    return SGS_E_ARG;
+  }
+  out->lowpass = c->lowpass;
   return SGS_OK;
 }
 

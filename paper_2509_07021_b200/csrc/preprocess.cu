@@ -108,6 +108,50 @@ __global__ void __launch_bounds__(256) vram3s_kernel(sgs_params P, SgsCam cam, i
   }
 }
 
+// Per-primitive projection record for the host API's _prepare / project
+// (render.py:259-330): [visible, depth, mean2d(2), cov2d 00/01/11, conic
+// 00/01/11, color_pre(3), color(3)], 16 floats, every primitive.
+__global__ void __launch_bounds__(256) project_records_kernel(sgs_params P, SgsCam cam, float* __restrict__ out) {
+  const int64_t n = P.n;
+  const int L = P.n_lobes;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float pos[3] = {P.position[3 * i], P.position[3 * i + 1], P.position[3 * i + 2]};
+    float4 q4 = reinterpret_cast<const float4*>(P.quat)[i];
+    float quat[4] = {q4.x, q4.y, q4.z, q4.w};
+    float ls[3] = {P.log_scale[3 * i], P.log_scale[3 * i + 1], P.log_scale[3 * i + 2]};
+    SgsProj pr;
+    sgs_project(pos, quat, ls, P.opacity[i], P.prim_mask ? P.prim_mask[i] : 1.0f, &cam, &pr);
+    float* o = out + 16 * i;
+    for (int k = 0; k < 16; ++k) o[k] = 0.0f;
+    o[0] = pr.visible ? 1.0f : 0.0f;
+    o[1] = pr.depth;
+    if (!pr.visible) continue;
+    o[2] = pr.mx;
+    o[3] = pr.my;
+    o[4] = pr.cov00;
+    o[5] = pr.cov01;
+    o[6] = pr.cov11;
+    o[7] = pr.con00;
+    o[8] = pr.con01;
+    o[9] = pr.con11;
+    float diffuse[3] = {P.diffuse[3 * i], P.diffuse[3 * i + 1], P.diffuse[3 * i + 2]};
+    float c_pre[3], c[3];
+    sgs_color(pos, diffuse, P.axis_raw + (size_t)i * L * 3, P.sharpness + (size_t)i * L,
+              P.amplitude + (size_t)i * L * 3, P.lobe_mask + (size_t)i * L, L, &cam, c_pre, c);
+    for (int k = 0; k < 3; ++k) {
+      o[10 + k] = c_pre[k];
+      o[13 + k] = c[k];
+    }
+  }
+}
+
+int launch_project_records(const sgs_params& P, const SgsCam& cam, float* out, cudaStream_t st) {
+  int grid = persistent_grid((uint64_t)P.n, 256, 8);
+  project_records_kernel<<<grid, 256, 0, st>>>(P, cam, out);
+  SGS_LAUNCH_CHECK("project_records_kernel");
+  return SGS_OK;
+}
+
 int launch_preprocess(const sgs_params& P, const SgsCam& cam, const sgs_workspace* ws, const Layout& lo,
                       cudaStream_t st) {
   Counters* ctr = at<Counters>(ws, lo.counters);

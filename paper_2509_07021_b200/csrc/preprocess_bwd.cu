@@ -59,9 +59,9 @@ __global__ void __launch_bounds__(128) preprocess_bwd_kernel(sgs_params P, SgsCa
       for (int r = 0; r < 2; ++r)
         for (int k = 0; k < 3; ++k)
           MS[3 * r + k] = M[3 * r] * S[k] + M[3 * r + 1] * S[3 + k] + M[3 * r + 2] * S[6 + k];
-      const float ca = MS[0] * M[0] + MS[1] * M[1] + MS[2] * M[2] + SGS_LOWPASS;
+      const float ca = MS[0] * M[0] + MS[1] * M[1] + MS[2] * M[2] + cam.lowpass;
       const float cb = MS[0] * M[3] + MS[1] * M[4] + MS[2] * M[5];
-      const float cc = MS[3] * M[3] + MS[4] * M[4] + MS[5] * M[5] + SGS_LOWPASS;
+      const float cc = MS[3] * M[3] + MS[4] * M[4] + MS[5] * M[5] + cam.lowpass;
       const float det = ca * cc - cb * cb;
       const float k00 = cc / det, k01 = -cb / det, k11 = ca / det;
 

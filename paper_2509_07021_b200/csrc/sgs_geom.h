@@ -167,6 +167,7 @@ typedef struct SgsCam {
   int32_t width, height;
   int32_t tiles_x, tiles_y;
   int32_t tile_y0, tile_y1;  // tile-row window [y0, y1) for strip renders
+  float lowpass;             // px^2 added to the cov2d diagonal (render.py:26, 285-286)
 } SgsCam;
 
 // Projected primitive: everything the binning stage and the forward raster
@@ -256,9 +257,9 @@ SGS_HD void sgs_project(const float pos[3], const float quat[4], const float ls[
     T0[k] = sgs_dot3(M0[0], M0[1], M0[2], S[k], S[3 + k], S[6 + k]);
     T1[k] = sgs_dot3(M1[0], M1[1], M1[2], S[k], S[3 + k], S[6 + k]);
   }
-  float a = F_ADD(sgs_dot3(T0[0], T0[1], T0[2], M0[0], M0[1], M0[2]), SGS_LOWPASS);
+  float a = F_ADD(sgs_dot3(T0[0], T0[1], T0[2], M0[0], M0[1], M0[2]), cam->lowpass);
   float b = sgs_dot3(T0[0], T0[1], T0[2], M1[0], M1[1], M1[2]);
-  float c = F_ADD(sgs_dot3(T1[0], T1[1], T1[2], M1[0], M1[1], M1[2]), SGS_LOWPASS);
+  float c = F_ADD(sgs_dot3(T1[0], T1[1], T1[2], M1[0], M1[1], M1[2]), cam->lowpass);
   o->cov00 = a;
   o->cov01 = b;
   o->cov11 = c;

@@ -1,0 +1,63 @@
+"""Shared test helpers: golden fixtures (made by the reference itself, see
+tests/golden/make_golden.py) and the composite gradient criterion."""
+
+from __future__ import annotations
+
+import hashlib
+from pathlib import Path
+
+import numpy as np
+
+from paper_2509_07021_b200 import scenes
+from paper_2509_07021_b200.camera import Camera
+
+GOLDEN = Path(__file__).resolve().parent / "golden"
+FIELDS = scenes.FIELDS
+
+
+def golden(name: str) -> dict:
+    with np.load(GOLDEN / f"{name}.npz", allow_pickle=False) as z:
+        return {k: z[k] for k in z.files}
+
+
+def golden_camera(d: dict, prefix: str = "") -> Camera:
+    fx, fy, cx, cy, near = d[prefix + "cam_intr"]
+    w, h = d[prefix + "cam_size"]
+    return Camera(rotation=d[prefix + "cam_R"], translation=d[prefix + "cam_t"], fx=fx, fy=fy,
+                  cx=cx, cy=cy, width=int(w), height=int(h), near=near)
+
+
+def golden_scene(d: dict) -> scenes.SceneArrays:
+    kw = {f: np.ascontiguousarray(d[f], dtype=np.float32) for f in FIELDS}
+    return scenes.SceneArrays(**kw, lobe_mask=np.ascontiguousarray(d["lobe_mask"], np.float32),
+                              prim_mask=(np.ascontiguousarray(d["prim_mask"], np.float32)
+                                         if "prim_mask" in d else None))
+
+
+def digest(s: scenes.SceneArrays) -> str:
+    h = hashlib.sha256()
+    for f in FIELDS + ("lobe_mask",):
+        h.update(np.ascontiguousarray(getattr(s, f)).tobytes())
+    if s.prim_mask is not None:
+        h.update(np.ascontiguousarray(s.prim_mask).tobytes())
+    return h.hexdigest()
+
+
+def crop_fixture(name: str):
+    """(scene, crop camera, reference image) for a cfgN_crop fixture; the
+    scene is regenerated from the seeded generator and checked by digest."""
+    d = golden(name)
+    cfg = int(d["cfg"])
+    scene, cams = scenes.CONFIGS[cfg]()
+    assert digest(scene) == str(d["digest"]), f"generator drift for configs[{cfg}]"
+    x0, y0, w, h = (int(v) for v in d["crop"])
+    cam = cams[int(d["cam_index"])].crop(x0, y0, w, h)
+    return scene, cam, d["img"]
+
+
+def composite_ok(a, b, rel=1e-3, floor=1e-5):
+    """|a - b| <= rel |b| + floor max|b| (the scaled form of
+    the reference's err <= 1e-6 or rel <= 1e-3, test_acceptance.py:168)."""
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return np.abs(a - b) <= rel * np.abs(b) + floor * max(float(np.abs(b).max()), 1e-30)
