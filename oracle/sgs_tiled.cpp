@@ -171,8 +171,8 @@ void oracle_raster_forward(const uint32_t* ranges, const uint32_t* vals, const f
         if (p < r[3]) continue;
         const float a = r[2] * exp2f(p);
         const float alpha = std::min(a, SGS_ALPHA_MAX);
-        const float Tn = T * (1.0f - alpha);
-        if (Tn < SGS_T_CUTOFF) break;
+        const float Tn = T * (a < SGS_ALPHA_MAX ? 1.0f - a : SGS_ONE_MINUS_ALPHA_MAX);
+        if (Tn < SGS_T_KEEP) break;
         const float w = alpha * T;
         for (int c = 0; c < 3; ++c) C[c] += w * r[8 + c];
         if (weight_sums) weight_sums[vals[j]] += w;
@@ -214,7 +214,7 @@ void oracle_raster_backward(const uint32_t* ranges, const uint32_t* vals, const 
         const double a = (double)r[2] * G;
         const double alpha = std::min(a, 0.99);
         const double Tn = T * (1.0 - alpha);
-        if (Tn < 1e-4) break;
+        if (Tn < (double)SGS_T_KEEP) break;
         kept.push_back({vals[j], G, a, alpha, T, dx, dy});
         T = Tn;
       }

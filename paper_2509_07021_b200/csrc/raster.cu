@@ -89,8 +89,8 @@ __global__ void __launch_bounds__(256) raster_fwd_kernel(const uint2* __restrict
       if (!done && p >= G.w) {
         const float a = G.z * ex2_approx(p);
         const float alpha = fminf(a, SGS_ALPHA_MAX);
-        const float Tn = T * (1.0f - alpha);
-        if (Tn < SGS_T_CUTOFF) {
+        const float Tn = T * (a < SGS_ALPHA_MAX ? 1.0f - a : SGS_ONE_MINUS_ALPHA_MAX);
+        if (Tn < SGS_T_KEEP) {
           done = true;
         } else {
           const float4 c = s_col[k];
@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(256) raster_bwd_kernel(const uint2* __restrict
         const float Gv = ex2_approx(p);
         const float a = G.z * Gv;
         const float alpha = fminf(a, SGS_ALPHA_MAX);
-        const float om = 1.0f - alpha;
+        const float om = a < SGS_ALPHA_MAX ? 1.0f - a : SGS_ONE_MINUS_ALPHA_MAX;
         const float Ti = T / om;
         const float w = alpha * Ti;
         const float cg = col.x * g0 + col.y * g1 + col.z * g2;

@@ -296,7 +296,7 @@ def _loss_and_dimg_t(img: torch.Tensor, target: torch.Tensor, cfg: LossConfig):
     y = target.detach().to(torch.float64)
     val = _loss_t(x, y, cfg)
     (dimg,) = torch.autograd.grad(val, x)
-    return float(val), dimg
+    return float(val.detach()), dimg
 
 
 def _loss_and_dimg(img, target, cfg: LossConfig):
