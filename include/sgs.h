@@ -103,11 +103,14 @@ typedef struct sgs_workspace {
 typedef struct sgs_stats {
   uint64_t n_visible;      /* z > near, render.py:263 */
   uint64_t n_emitting;     /* visible primitives with >= 1 tile entry */
-  uint64_t n_entries;      /* tile-depth key/value entries E */
+  uint64_t n_entries;      /* per-tile (tile, depth) entries E of the tile lists */
   uint64_t capacity;       /* entry capacity the workspace was carved for */
   uint64_t overflow;       /* 1 if n_entries > capacity (frame must be redone) */
   uint64_t vram3s_visible; /* reference VRAM model, postprocess.py:118-135 */
   uint64_t vram3s_entries;
+  uint64_t n_bin_entries;  /* entries the binning sorted: (super-tile, primitive)
+                              in depth-first mode, (tile, primitive) in key64 mode;
+                              the entry capacity bounds this number */
 } sgs_stats;
 
 /* Library / ABI version and last error message (thread-local). */
@@ -178,9 +181,11 @@ int sgs_get_stats(const sgs_workspace* ws, sgs_stats* out, void* stream);
 int sgs_vram_model(const sgs_params* params, const sgs_camera* cam, int32_t tile_px,
                    const sgs_workspace* ws, void* stream);
 
-/* Export the sorted tile list as 64-bit (tile<<32 | depth_bits) keys and
+/* Export the per-tile lists as 64-bit (tile<<32 | depth_bits) keys and
  * primitive-index values (device buffers of length >= n_entries), and the
- * per-tile ranges (tiles_x*tiles_y uint32 pairs).  For parity checks. */
+ * per-tile [start, end) ranges (tiles_x*tiles_y uint32 pairs), materialised
+ * from the binned lists with the raster's own membership test.  For parity
+ * checks; all three buffers are required. */
 int sgs_export_bins(const sgs_workspace* ws, const sgs_camera* cam, uint64_t* keys,
                     uint32_t* values, uint32_t* ranges, void* stream);
 

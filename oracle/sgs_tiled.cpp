@@ -93,6 +93,9 @@ void oracle_preprocess(int64_t n, int L, const float* pos, const float* quat, co
     memset(rec, 0, 12 * sizeof(float));
     if (cnt) {
       ++emit;
+      const SgsSpan sp = sgs_span(g, k);
+      float span2[2];
+      sgs_span_cache(&sp, &k[3], span2);
       float c_pre[3], c[3];
       sgs_color(pos + 3 * i, diffuse + 3 * i, axis + (size_t)i * L * 3, sharp + (size_t)i * L, amp + (size_t)i * L * 3,
                 lmask + (size_t)i * L, L, &cam, c_pre, c);

@@ -50,7 +50,8 @@ class SgsWorkspace(C.Structure):
 class SgsStats(C.Structure):
     _fields_ = [("n_visible", C.c_uint64), ("n_emitting", C.c_uint64), ("n_entries", C.c_uint64),
                 ("capacity", C.c_uint64), ("overflow", C.c_uint64),
-                ("vram3s_visible", C.c_uint64), ("vram3s_entries", C.c_uint64)]
+                ("vram3s_visible", C.c_uint64), ("vram3s_entries", C.c_uint64),
+                ("n_bin_entries", C.c_uint64)]
 
 
 # every exported symbol and its signature (tests check the .so exports all of them)

@@ -52,8 +52,8 @@ int launch_raster_bwd(const SgsCam& cam, float3 bg, const sgs_workspace* ws, con
                       const float* T, const uint32_t* nc, const float* dimg, float* grad2d, cudaStream_t st);
 int launch_preprocess_bwd(const sgs_params& P, const SgsCam& cam, const float* grad2d, const sgs_grads& g,
                           cudaStream_t st);
-int launch_export_bins(const sgs_workspace* ws, const Layout& lo, unsigned long long* keys, uint32_t* vals,
-                       uint32_t* ranges, cudaStream_t st);
+int launch_export_lists(const SgsCam& cam, const sgs_workspace* ws, const Layout& lo, const uint32_t* vals,
+                        unsigned long long* keys, uint32_t* out_vals, uint32_t* ranges, cudaStream_t st);
 int launch_sort_u64(unsigned long long* keys, uint32_t* vals, uint32_t n, int bits, void* temp, uint64_t temp_bytes,
                     cudaStream_t st);
 uint64_t sort_u64_temp_bytes(uint64_t n, int bits);
@@ -220,7 +220,8 @@ int sgs_get_stats(const sgs_workspace* ws, sgs_stats* out, void* stream) {
   out->n_emitting = h.n_emitting;
   out->n_entries = h.n_entries;
   out->capacity = (uint64_t)lo.cap;
-  out->overflow = h.n_entries > (unsigned long long)lo.cap ? 1 : 0;
+  out->overflow = h.n_bin > (unsigned long long)lo.cap ? 1 : 0;
+  out->n_bin_entries = h.n_bin;
   out->vram3s_visible = h.vram3s_visible;
   out->vram3s_entries = h.vram3s_entries;
   return SGS_OK;
@@ -248,10 +249,16 @@ int sgs_vram_model(const sgs_params* params, const sgs_camera* cam, int32_t tile
 int sgs_export_bins(const sgs_workspace* ws, const sgs_camera* cam, uint64_t* keys, uint32_t* values,
                     uint32_t* ranges, void* stream) {
   Layout lo;
+  SgsCam c;
   int rc = check_ws(ws, &lo);
+  if (!rc) rc = make_cam(cam, lo, &c);
   if (rc) return rc;
-  (void)cam;
-  return launch_export_bins(ws, lo, reinterpret_cast<unsigned long long*>(keys), values, ranges, as_stream(stream));
+  if (!keys || !values || !ranges) {
+    set_error("export needs keys, values and ranges buffers");
+    return SGS_E_ARG;
+  }
+  return launch_export_lists(c, ws, lo, final_vals(ws, lo), reinterpret_cast<unsigned long long*>(keys), values,
+                             ranges, as_stream(stream));
 }
 
 int sgs_export_projected(const sgs_workspace* ws, uint32_t* depth_bits, uint32_t* rect, uint32_t* tiles_touched,

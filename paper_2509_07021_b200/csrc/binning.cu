@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(1024) scan_blocks(unsigned long long* block_su
   }
   if (threadIdx.x == 0) {
     unsigned long long total = carry;
-    ctr->n_entries = total;
+    ctr->n_bin = total;
     ctr->capacity = cap;
     ctr->overflow = total > cap ? 1ull : 0ull;
     ctr->n_sort = (uint32_t)(total < cap ? total : cap);
@@ -169,26 +169,31 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
 
 // Emission (K2), warp-cooperative and load-balanced.  A warp takes 32
 // consecutive primitives in rank order; their entries form one contiguous
-// output range, ordered by (primitive, tile row, tile column).  The warp
-// flattens the primitives' tile rows into a list of row items and processes
-// 32 row items at a time: lane = row item computes the row's exact span (one
-// span evaluation per row, no redundancy, no divergence), a warp scan gives
-// each row's output offset, then lane = entry writes 32 consecutive entries
-// per store instruction.
-template <typename KT>
+// output range, ordered by (primitive, row, column).  The warp flattens the
+// primitives' rows into a list of row items and processes 32 row items at a
+// time: lane = row item computes the row's span (one span evaluation per row,
+// no redundancy), a warp scan gives each row's output offset, then lane =
+// entry writes 32 consecutive entries per store instruction.
+// kSuper: rows are super-tile rows and entries are (super-tile, primitive);
+// otherwise rows are tile rows and entries (tile, primitive).
+template <typename KT, bool kSuper>
 __global__ void __launch_bounds__(256) emit_entries(const uint32_t* __restrict__ perm, uint32_t n,
-                                                    const uint32_t* __restrict__ tt, const uint2* __restrict__ rect,
+                                                    const uint32_t* __restrict__ counts,
+                                                    const uint2* __restrict__ rect,
                                                     const float4* __restrict__ rec_geo,
                                                     const float4* __restrict__ rec_con,
+                                                    const float2* __restrict__ rec_span,
                                                     const uint32_t* __restrict__ depth_key,
                                                     const unsigned long long* __restrict__ offsets, SgsCam cam,
-                                                    uint32_t cap, const unsigned long long* __restrict__ total_ptr,
+                                                    int super_x, uint32_t cap,
+                                                    const unsigned long long* __restrict__ total_ptr,
                                                     KT* __restrict__ keys_out, uint32_t* __restrict__ vals_out) {
   const int lane = threadIdx.x & 31;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
   const unsigned long long total = *total_ptr;
   const unsigned long long lim = total < cap ? total : cap;
+  const int row_w = kSuper ? super_x : cam.tiles_x;
   for (uint32_t base = warp * 32; base < n; base += nwarps * 32) {
     unsigned long long out = offsets[base];  // uniform: every lane reads the same word
     if (out >= lim) continue;
@@ -197,9 +202,9 @@ __global__ void __launch_bounds__(256) emit_entries(const uint32_t* __restrict__
     int tx0 = 0, ty0 = 0, tx1 = -1, ty1 = -1;
     if (r < n) {
       g = perm ? perm[r] : r;
-      if (tt[g]) {
+      if (counts[g]) {
         unpack_rect(rect[g], tx0, ty0, tx1, ty1);
-        nrows = (uint32_t)(ty1 - ty0 + 1);
+        nrows = kSuper ? (uint32_t)(ty1 / SGS_SUPER - ty0 / SGS_SUPER + 1) : (uint32_t)(ty1 - ty0 + 1);
       }
     }
     const uint32_t rincl = warp_incl_scan(nrows, lane);
@@ -210,17 +215,22 @@ __global__ void __launch_bounds__(256) emit_entries(const uint32_t* __restrict__
       const int owner = lane_search(rstart, k);
       const uint32_t og = __shfl_sync(0xffffffffu, g, owner);
       const int oty0 = __shfl_sync(0xffffffffu, ty0, owner);
+      const int oty1 = __shfl_sync(0xffffffffu, ty1, owner);
       const int otx0 = __shfl_sync(0xffffffffu, tx0, owner);
       const int otx1 = __shfl_sync(0xffffffffu, tx1, owner);
       const uint32_t ors = __shfl_sync(0xffffffffu, rstart, owner);
-      const int ty = oty0 + (int)(k - ors);
+      const int row = (kSuper ? oty0 / SGS_SUPER : oty0) + (int)(k - ors);
       uint32_t c = 0;
       int first = 0;
+      int rf[SGS_SUPER] = {0, 0, 0, 0}, rc[SGS_SUPER] = {0, 0, 0, 0};
       if (k < R) {
         const float4 g4 = rec_geo[og], c4 = rec_con[og];
+        const float2 s2 = rec_span[og];
         const float geo[4] = {g4.x, g4.y, g4.z, g4.w}, con[4] = {c4.x, c4.y, c4.z, c4.w};
-        const SgsSpan sp = sgs_span(geo, con);
-        c = (uint32_t)sgs_row_span(&sp, &cam, ty, otx0, otx1, &first);
+        const float span2[2] = {s2.x, s2.y};
+        const SgsSpan sp = sgs_span_cached(geo, con, span2);
+        c = kSuper ? (uint32_t)sgs_super_row_spans(&sp, &cam, otx0, oty0, otx1, oty1, row, rf, rc, &first)
+                   : (uint32_t)sgs_row_span(&sp, &cam, row, otx0, otx1, &first);
       }
       const uint32_t cincl = warp_incl_scan(c, lane);
       const uint32_t cexcl = cincl - c;
@@ -229,14 +239,26 @@ __global__ void __launch_bounds__(256) emit_entries(const uint32_t* __restrict__
         const uint32_t j = j0 + lane;
         const int ro = lane_search(cexcl, j);
         const int rfirst = __shfl_sync(0xffffffffu, first, ro);
-        const int rty = __shfl_sync(0xffffffffu, ty, ro);
+        const int rrow = __shfl_sync(0xffffffffu, row, ro);
         const uint32_t rex = __shfl_sync(0xffffffffu, cexcl, ro);
         const uint32_t rg = __shfl_sync(0xffffffffu, og, ro);
+        int mf[SGS_SUPER], mc[SGS_SUPER];
+        if (kSuper) {
+#pragma unroll
+          for (int q = 0; q < SGS_SUPER; ++q) {
+            mf[q] = __shfl_sync(0xffffffffu, rf[q], ro);
+            mc[q] = __shfl_sync(0xffffffffu, rc[q], ro);
+          }
+        }
         if (j < Ctot) {
           const unsigned long long o = out + j;
           if (o < lim) {
-            const uint32_t tile = (uint32_t)(rty * cam.tiles_x + rfirst) + (j - rex);
-            keys_out[o] = make_key<KT>(tile, sizeof(KT) == 8 ? depth_key[rg] : 0u);
+            const uint32_t col = (uint32_t)rfirst + (j - rex);
+            const uint32_t cell = (uint32_t)(rrow * row_w) + col;
+            if (kSuper)
+              keys_out[o] = (KT)((cell << 16) | sgs_super_mask(mf, mc, (int)col));
+            else
+              keys_out[o] = make_key<KT>(cell, sizeof(KT) == 8 ? depth_key[rg] : 0u);
             vals_out[o] = rg;
           }
         }
@@ -260,13 +282,13 @@ __global__ void ranges_fix(uint2* __restrict__ ranges, int n_tiles) {
 // Final location of the sorted values (which ping-pong buffer).
 bool final_in_alt(const Layout& lo) {
   int passes = lo.sort_mode == SGS_SORT_KEY64 ? (32 + tile_sort_bits(lo.n_tiles) + 7) / 8
-                                              : tile_sort_passes(lo.n_tiles);
+                                              : tile_sort_passes(lo.n_super);
   return (passes & 1) != 0;
 }
 
-template <typename KT, int IPT>
-static int bin_tiles(const SgsCam& cam, const sgs_workspace* ws, const Layout& lo, const uint32_t* perm, int key_bits,
-                     int tile_shift, cudaStream_t st) {
+template <typename KT, int IPT, bool kSuper>
+static int bin_entries(const SgsCam& cam, const sgs_workspace* ws, const Layout& lo, const uint32_t* perm,
+                       int key_bits, int tile_shift, cudaStream_t st) {
   Counters* ctr = at<Counters>(ws, lo.counters);
   const uint32_t n = (uint32_t)lo.n;
   const uint32_t cap = (uint32_t)lo.cap;
@@ -275,20 +297,22 @@ static int bin_tiles(const SgsCam& cam, const sgs_workspace* ws, const Layout& l
   uint32_t* v0 = at<uint32_t>(ws, lo.ent_val);
   uint32_t* v1 = at<uint32_t>(ws, lo.ent_val_alt);
   uint2* ranges = at<uint2>(ws, lo.ranges);
-  const int rgrid = persistent_grid((uint64_t)lo.n_tiles, 256, 4);
-  ranges_init<<<rgrid, 256, 0, st>>>(ranges, lo.n_tiles);
+  const int n_cells = kSuper ? lo.n_super : lo.n_tiles;
+  const int rgrid = persistent_grid((uint64_t)n_cells, 256, 4);
+  ranges_init<<<rgrid, 256, 0, st>>>(ranges, n_cells);
   SGS_LAUNCH_CHECK("ranges_init");
-  emit_entries<KT><<<persistent_grid(n, 256, 8), 256, 0, st>>>(
-      perm, n, at<uint32_t>(ws, lo.tiles_touched), at<uint2>(ws, lo.rect), at<float4>(ws, lo.rec_geo),
-      at<float4>(ws, lo.rec_con), at<uint32_t>(ws, lo.depth_key), at<unsigned long long>(ws, lo.offsets), cam, cap,
-      &ctr->n_entries, k0, v0);
+  emit_entries<KT, kSuper><<<persistent_grid(n, 256, 8), 256, 0, st>>>(
+      perm, n, at<uint32_t>(ws, kSuper ? lo.super_touched : lo.tiles_touched), at<uint2>(ws, lo.rect),
+      at<float4>(ws, lo.rec_geo), at<float4>(ws, lo.rec_con), at<float2>(ws, lo.rec_span),
+      at<uint32_t>(ws, lo.depth_key),
+      at<unsigned long long>(ws, lo.offsets), cam, lo.super_x, cap, &ctr->n_bin, k0, v0);
   SGS_LAUNCH_CHECK("emit_entries");
   bool alt = false;
   int rc = radix_sort_pairs<KT, IPT>(k0, v0, k1, v1, &ctr->n_sort, cap, key_bits, at<uint32_t>(ws, lo.hist),
                                      at<uint32_t>(ws, lo.status), &ctr->part_counter[8], &alt, st, false,
-                                     RsRangeOut{ranges, tile_shift});
+                                     RsRangeOut{ranges, tile_shift}, kSuper ? 16 : 0, kSuper);
   if (rc) return rc;
-  ranges_fix<<<rgrid, 256, 0, st>>>(ranges, lo.n_tiles);
+  ranges_fix<<<rgrid, 256, 0, st>>>(ranges, n_cells);
   SGS_LAUNCH_CHECK("ranges_fix");
   return SGS_OK;
 }
@@ -297,7 +321,6 @@ int launch_bin(const SgsCam& cam, const sgs_workspace* ws, const Layout& lo, cud
   Counters* ctr = at<Counters>(ws, lo.counters);
   const uint32_t n = (uint32_t)lo.n;
   const uint32_t cap = (uint32_t)lo.cap;
-  uint32_t* tt = at<uint32_t>(ws, lo.tiles_touched);
   unsigned long long* offsets = at<unsigned long long>(ws, lo.offsets);
   unsigned long long* block_sums = at<unsigned long long>(ws, lo.scan_blocks);
   if (lo.sort_mode == SGS_SORT_DEPTH_FIRST) {
@@ -306,9 +329,7 @@ int launch_bin(const SgsCam& cam, const sgs_workspace* ws, const Layout& lo, cud
     uint32_t* kb = at<uint32_t>(ws, lo.dkey_tmp);
     uint32_t* ia = at<uint32_t>(ws, lo.didx);
     uint32_t* ib = at<uint32_t>(ws, lo.didx_alt);
-    // N as a device count for the depth sort (graph-friendly: no host value baked in)
     SGS_CUDA(cudaMemcpyAsync(ka, dkey, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
-    SGS_CUDA(cudaMemsetAsync(&ctr->n_depth, 0, 4, st));
     set_count<<<1, 1, 0, st>>>(&ctr->n_depth, n);
     SGS_LAUNCH_CHECK("set_count");
     bool alt = false;
@@ -318,44 +339,15 @@ int launch_bin(const SgsCam& cam, const sgs_workspace* ws, const Layout& lo, cud
                                                         true);
     if (rc) return rc;
     const uint32_t* perm = alt ? ib : ia;
-    rc = launch_scan(tt, perm, n, cap, block_sums, offsets, ctr, st);
+    rc = launch_scan(at<uint32_t>(ws, lo.super_touched), perm, n, cap, block_sums, offsets, ctr, st);
     if (rc) return rc;
-    if (lo.n_tiles <= 65536)
-      return bin_tiles<uint16_t, kTileSortIPT>(cam, ws, lo, perm, tile_sort_bits(lo.n_tiles), 0, st);
-    return bin_tiles<uint32_t, kTileSortIPT>(cam, ws, lo, perm, tile_sort_bits(lo.n_tiles), 0, st);
+    // keys (super_id << 16 | 16-bit tile mask), sorted on the super id bits only
+    return bin_entries<uint32_t, kTileSortIPT, true>(cam, ws, lo, perm, tile_sort_bits(lo.n_super), 16, st);
   }
-  int rc = launch_scan(tt, nullptr, n, cap, block_sums, offsets, ctr, st);
+  int rc = launch_scan(at<uint32_t>(ws, lo.tiles_touched), nullptr, n, cap, block_sums, offsets, ctr, st);
   if (rc) return rc;
-  return bin_tiles<unsigned long long, kKey64SortIPT>(cam, ws, lo, nullptr, 32 + tile_sort_bits(lo.n_tiles), 32, st);
-}
-
-// Export the sorted list as 64-bit keys (either mode): tile from the ranges,
-// depth bits from the preprocess keys.
-__global__ void export_keys(const uint2* __restrict__ ranges, int n_tiles, const uint32_t* __restrict__ vals,
-                            const uint32_t* __restrict__ depth_key, unsigned long long* __restrict__ out_keys,
-                            uint32_t* __restrict__ out_vals) {
-  for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-    const uint2 r = ranges[t];
-    for (uint32_t i = r.x + threadIdx.x; i < r.y; i += blockDim.x) {
-      const uint32_t v = vals[i];
-      out_keys[i] = ((unsigned long long)t << 32) | depth_key[v];
-      out_vals[i] = v;
-    }
-  }
-}
-
-int launch_export_bins(const sgs_workspace* ws, const Layout& lo, unsigned long long* keys, uint32_t* vals,
-                       uint32_t* ranges, cudaStream_t st) {
-  bool alt = final_in_alt(lo);
-  const uint32_t* v = at<uint32_t>(ws, alt ? lo.ent_val_alt : lo.ent_val);
-  if (keys && vals) {
-    export_keys<<<persistent_grid((uint64_t)lo.n_tiles, 1, 8), 256, 0, st>>>(
-        at<uint2>(ws, lo.ranges), lo.n_tiles, v, at<uint32_t>(ws, lo.depth_key), keys, vals);
-    SGS_LAUNCH_CHECK("export_keys");
-  }
-  if (ranges) SGS_CUDA(cudaMemcpyAsync(ranges, at<uint2>(ws, lo.ranges), (size_t)lo.n_tiles * 8,
-                                       cudaMemcpyDeviceToDevice, st));
-  return SGS_OK;
+  return bin_entries<unsigned long long, kKey64SortIPT, false>(cam, ws, lo, nullptr, 32 + tile_sort_bits(lo.n_tiles),
+                                                               32, st);
 }
 
 // Generic 64-bit pair sort exported through the ABI (for tests / tools).

@@ -42,7 +42,7 @@ struct Counters {
   unsigned long long overflow;
   unsigned long long vram3s_visible;
   unsigned long long vram3s_entries;
-  unsigned long long pad0;
+  unsigned long long n_bin;          // entries the binning sorts (super-tile entries in depth-first mode)
   uint32_t n_sort;                   // min(E, capacity): items the tile sort processes
   uint32_t n_depth;                  // primitives entering the depth sort
   uint32_t part_counter[16];         // onesweep partition tickets, one per pass
@@ -53,10 +53,11 @@ struct Counters {
 struct Layout {
   int64_t n;
   int32_t L, W, H, tiles_x, tiles_y, n_tiles;
+  int32_t super_x, super_y, n_super;
   int32_t sort_mode;
   int64_t cap;
   // offsets into the workspace
-  uint64_t counters, rec_geo, rec_con, rec_col, depth_key, rect, tiles_touched;
+  uint64_t counters, rec_geo, rec_con, rec_col, rec_span, depth_key, rect, tiles_touched, super_touched, cand_end;
   uint64_t dkey_alt, dkey_tmp, didx, didx_alt, offsets, scan_blocks;
   uint64_t ent_key, ent_key_alt, ent_val, ent_val_alt, ranges;
   uint64_t hist, status;
@@ -79,7 +80,7 @@ inline uint64_t align256(uint64_t x) { return (x + 255) & ~uint64_t(255); }
 inline int make_layout(const sgs_workspace* ws, Layout* lo) {
   if (!ws || ws->n < 0 || ws->n > (int64_t)0x7fffffff || ws->width < 1 || ws->height < 1 ||
       ws->n_lobes < 0 || ws->n_lobes > SGS_MAX_LOBES || ws->entry_capacity < 0 ||
-      ws->entry_capacity > (int64_t)kMaxEntries ||
+      ws->entry_capacity > (int64_t)kMaxEntries || (ws->width + 63) / 64 * ((ws->height + 63) / 64) > 65536 ||
       (ws->sort_mode != SGS_SORT_DEPTH_FIRST && ws->sort_mode != SGS_SORT_KEY64)) {
     set_error("invalid workspace descriptor");
     return SGS_E_ARG;
@@ -91,6 +92,9 @@ inline int make_layout(const sgs_workspace* ws, Layout* lo) {
   lo->tiles_x = (ws->width + SGS_TILE - 1) / SGS_TILE;
   lo->tiles_y = (ws->height + SGS_TILE - 1) / SGS_TILE;
   lo->n_tiles = lo->tiles_x * lo->tiles_y;
+  lo->super_x = (lo->tiles_x + SGS_SUPER - 1) / SGS_SUPER;
+  lo->super_y = (lo->tiles_y + SGS_SUPER - 1) / SGS_SUPER;
+  lo->n_super = lo->super_x * lo->super_y;
   lo->sort_mode = ws->sort_mode;
   lo->cap = ws->entry_capacity;
   const uint64_t n = (uint64_t)ws->n + 1, cap = (uint64_t)ws->entry_capacity + 1;
@@ -105,16 +109,19 @@ inline int make_layout(const sgs_workspace* ws, Layout* lo) {
   lo->rec_geo = take(n * 16);
   lo->rec_con = take(n * 16);
   lo->rec_col = take(n * 16);
+  lo->rec_span = take(n * 8);
   lo->depth_key = take(n * 4);
   lo->rect = take(n * 8);
   lo->tiles_touched = take(n * 4);
+  lo->super_touched = take(n * 4);
+  lo->cand_end = take((uint64_t)lo->n_tiles * 4);
   lo->dkey_alt = take(n * 4);
   lo->dkey_tmp = take(n * 4);
   lo->didx = take(n * 4);
   lo->didx_alt = take(n * 4);
   lo->offsets = take(n * 8);
   lo->scan_blocks = take(((n + 2047) / 2048 + 1) * 8);
-  const uint64_t key_bytes = k64 ? 8 : (lo->n_tiles <= 65536 ? 2 : 4);
+  const uint64_t key_bytes = k64 ? 8 : 4;  // depth-first: (super_id << 16 | tile mask)
   lo->ent_key = take(cap * key_bytes);
   lo->ent_key_alt = take(cap * key_bytes);
   lo->ent_val = take(cap * 4);
@@ -122,7 +129,7 @@ inline int make_layout(const sgs_workspace* ws, Layout* lo) {
   lo->ranges = take((uint64_t)lo->n_tiles * 8);
   lo->hist = take(16 * 256 * 4);
   // onesweep look-back status: per pass, per partition, 256 digits of u32
-  int tile_passes = k64 ? (32 + tile_sort_bits(lo->n_tiles) + 7) / 8 : tile_sort_passes(lo->n_tiles);
+  int tile_passes = k64 ? (32 + tile_sort_bits(lo->n_tiles) + 7) / 8 : tile_sort_passes(lo->n_super);
   int ipt = k64 ? kKey64SortIPT : kTileSortIPT;
   uint64_t parts_tile = (cap + (uint64_t)kRadixThreads * ipt - 1) / ((uint64_t)kRadixThreads * ipt);
   uint64_t parts_depth = (n + (uint64_t)kRadixThreads * kDepthSortIPT - 1) / ((uint64_t)kRadixThreads * kDepthSortIPT);

@@ -17,8 +17,10 @@ __device__ __forceinline__ void warp_count(unsigned long long* ctr, bool pred) {
 
 __global__ void __launch_bounds__(256) preprocess_kernel(sgs_params P, SgsCam cam, float4* __restrict__ rec_geo,
                                                          float4* __restrict__ rec_con, float4* __restrict__ rec_col,
+                                                         float2* __restrict__ rec_span,
                                                          uint32_t* __restrict__ depth_key, uint2* __restrict__ rect,
-                                                         uint32_t* __restrict__ tiles_touched, Counters* ctr) {
+                                                         uint32_t* __restrict__ tiles_touched,
+                                                         uint32_t* __restrict__ super_touched, Counters* ctr) {
   const int64_t n = P.n;
   const int L = P.n_lobes;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -27,6 +29,7 @@ __global__ void __launch_bounds__(256) preprocess_kernel(sgs_params P, SgsCam ca
     const int64_t i = base + threadIdx.x;
     bool live = i < n;
     bool visible = false, emitting = false;
+    uint32_t cnt = 0;
     if (live) {
       float pos[3] = {P.position[3 * i], P.position[3 * i + 1], P.position[3 * i + 2]};
       float4 q4 = reinterpret_cast<const float4*>(P.quat)[i];
@@ -36,14 +39,15 @@ __global__ void __launch_bounds__(256) preprocess_kernel(sgs_params P, SgsCam ca
       SgsProj pr;
       sgs_project(pos, quat, ls, P.opacity[i], pm, &cam, &pr);
       visible = pr.visible;
-      uint32_t cnt = 0;
+      uint32_t nsup = 0;
       float g[4], k[4];
       if (pr.emits) {
         sgs_pack_geo(&pr, g, k);
-        cnt = sgs_count_tiles(pr.tx0, pr.ty0, pr.tx1, pr.ty1, g, k, &cam);
+        sgs_count_hits(pr.tx0, pr.ty0, pr.tx1, pr.ty1, g, k, &cam, &cnt, &nsup);
       }
       emitting = cnt > 0;
       tiles_touched[i] = cnt;
+      super_touched[i] = nsup;
       depth_key[i] = emitting ? sgs_float_to_bits(pr.depth) : 0x7fffffffu;
       rect[i] = make_uint2((uint32_t)(pr.tx0 & 0xffff) | ((uint32_t)(pr.tx1 & 0xffff) << 16),
                            (uint32_t)(pr.ty0 & 0xffff) | ((uint32_t)(pr.ty1 & 0xffff) << 16));
@@ -60,13 +64,20 @@ __global__ void __launch_bounds__(256) preprocess_kernel(sgs_params P, SgsCam ca
         }
         float c_pre[3], c[3];
         sgs_color(pos, diffuse, axis, sharp, amp, lm, L, &cam, c_pre, c);
+        const SgsSpan sp = sgs_span(g, k);
+        float span2[2];
+        sgs_span_cache(&sp, &k[3], span2);
         rec_geo[i] = make_float4(g[0], g[1], g[2], g[3]);
         rec_con[i] = make_float4(k[0], k[1], k[2], k[3]);
+        rec_span[i] = make_float2(span2[0], span2[1]);
         rec_col[i] = make_float4(c[0], c[1], c[2], 0.0f);
       }
     }
     warp_count(&ctr->n_visible, visible);
     warp_count(&ctr->n_emitting, emitting);
+    unsigned long long e = cnt;
+    for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+    if ((threadIdx.x & 31) == 0 && e) atomicAdd(&ctr->n_entries, e);
   }
 }
 
@@ -157,8 +168,10 @@ int launch_preprocess(const sgs_params& P, const SgsCam& cam, const sgs_workspac
   Counters* ctr = at<Counters>(ws, lo.counters);
   int grid = persistent_grid((uint64_t)P.n, 256, 8);
   preprocess_kernel<<<grid, 256, 0, st>>>(P, cam, at<float4>(ws, lo.rec_geo), at<float4>(ws, lo.rec_con),
-                                          at<float4>(ws, lo.rec_col), at<uint32_t>(ws, lo.depth_key),
-                                          at<uint2>(ws, lo.rect), at<uint32_t>(ws, lo.tiles_touched), ctr);
+                                          at<float4>(ws, lo.rec_col), at<float2>(ws, lo.rec_span),
+                                          at<uint32_t>(ws, lo.depth_key),
+                                          at<uint2>(ws, lo.rect), at<uint32_t>(ws, lo.tiles_touched),
+                                          at<uint32_t>(ws, lo.super_touched), ctr);
   SGS_LAUNCH_CHECK("preprocess_kernel");
   return SGS_OK;
 }

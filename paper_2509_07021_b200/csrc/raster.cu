@@ -8,16 +8,18 @@
 // No alpha < 1/255 skip.  Pairs outside the opacity-aware support (q > qmax,
 // i.e. o G < 1e-7) are skipped; see sgs_geom.h.
 //
-// One CTA per 16x16 tile, one pixel per thread.  Batches of 256 records of
-// the tile's list are staged in shared memory (coalesced gather by sorted
-// value), then every warp walks the batch in lock step; a warp leaves the
-// batch once all of its pixels have terminated, the CTA leaves the tile once
-// all 256 have (__syncthreads_count).
+// One CTA per 16x16 tile.  The tile's primitive list is read from its cell's
+// sorted list -- the super-tile list in depth-first mode, filtered to this
+// tile with the exact per-tile membership test (sgs_tile_member), or the
+// tile's own list in 64-bit-key mode -- in batches that are compacted
+// (stable) into shared memory.  The per-tile list index of a staged entry is
+// its rank among the tile's hits, identical in both modes.
 //
 // Backward (render.py:535-573) walks each tile's list back to front from the
-// last primitive any pixel kept, recovering T_i = T_{i+1} / (1 - alpha_i) and
-// the suffix sum S_i = sum_{j>i} w_j (c_j . g) + T_bg (bg . g) exactly as the
-// reference's reverse cumsum does, so
+// last entry any pixel kept (the forward records that candidate position per
+// tile), recovering T_i = T_{i+1} / (1 - alpha_i) and the suffix sum
+// S_i = sum_{j>i} w_j (c_j . g) + T_bg (bg . g) exactly as the reference's
+// reverse cumsum does, so
 //   dL/dalpha_i = (T_i (c_i . g) - S_i / (1 - alpha_i)) [a_i < 0.99]
 // Per-primitive partials are reduced across the warp with shuffles, across
 // warps in shared memory, and flushed to HBM with one atomic per value per
@@ -38,20 +40,229 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
-template <bool kImportance, bool kCount>
-__global__ void __launch_bounds__(256) raster_fwd_kernel(const uint2* __restrict__ ranges,
-                                                         const uint32_t* __restrict__ vals,
-                                                         const float4* __restrict__ rec_geo,
-                                                         const float4* __restrict__ rec_con,
-                                                         const float4* __restrict__ rec_col, SgsCam cam, float3 bg,
-                                                         float* __restrict__ out_img, float* __restrict__ out_T,
-                                                         uint32_t* __restrict__ out_nc,
-                                                         float* __restrict__ weight_sums,
-                                                         unsigned long long* __restrict__ pair_count) {
-  __shared__ float4 s_geo[256];
-  __shared__ float4 s_con[256];
-  __shared__ float4 s_col[256];
-  __shared__ uint32_t s_id[kImportance ? 256 : 1];
+struct ListArgs {
+  const uint2* ranges;      // per cell [start, end) into vals
+  const uint32_t* keys;     // depth-first: sorted (super_id << 16 | tile mask) keys
+  const uint32_t* vals;     // sorted primitive indices
+  const uint2* rect;        // per primitive packed tile rectangle
+  const float4* geo;
+  const float4* con;
+  const float4* col;
+  const float2* span;
+  uint32_t* cand_end;       // per tile: one past the last candidate any pixel kept
+  int super_x;
+};
+
+__device__ __forceinline__ int list_cell(bool filter, int tx, int ty, int tile, int super_x) {
+  return filter ? (ty / SGS_SUPER) * super_x + tx / SGS_SUPER : tile;
+}
+
+// Append the members of tile (tx, ty) among candidates [c_lo, c_hi) (at
+// most THREADS * CPT) of the cell list to the shared-memory batch at `base`,
+// in list order.  Depth-first mode reads membership from the 16-bit tile mask
+// carried in each sorted key (bit `local_bit`); 64-bit-key lists are per
+// tile already.  Returns the number appended.  Ends with __syncthreads().
+template <int THREADS, int CPT, bool kFilter, bool kColor>
+__device__ __forceinline__ int stage_append(uint32_t c_lo, uint32_t c_hi, uint32_t local_bit, const ListArgs& a,
+                                            int base, float4* s_geo, float4* s_con, float4* s_col, uint32_t* s_id,
+                                            uint32_t* s_cand, uint32_t* s_wcnt) {
+  constexpr int W = THREADS / 32;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const uint32_t lt = (1u << lane) - 1u;
+  uint32_t bal[CPT];
+#pragma unroll
+  for (int h = 0; h < CPT; ++h) {
+    const uint32_t c = c_lo + t + h * THREADS;
+    bool hit = c < c_hi;
+    if (kFilter && hit) hit = (a.keys[c] >> local_bit) & 1u;
+    bal[h] = __ballot_sync(0xffffffffu, hit);
+    if (lane == 0) s_wcnt[h * W + warp] = __popc(bal[h]);
+  }
+  __syncthreads();
+  int total = 0;
+#pragma unroll
+  for (int h = 0; h < CPT; ++h) {
+    int pre = 0;
+    for (int j = 0; j < CPT * W; ++j) {
+      const int v = (int)s_wcnt[j];
+      pre += (j < h * W + warp) ? v : 0;
+      if (h == 0) total += v;
+    }
+    if ((bal[h] >> lane) & 1u) {
+      const uint32_t c = c_lo + t + h * THREADS;
+      const int pos = base + pre + __popc(bal[h] & lt);
+      const uint32_t g = a.vals[c];
+      s_geo[pos] = a.geo[g];
+      s_con[pos] = a.con[g];
+      if (kColor) s_col[pos] = a.col[g];
+      s_id[pos] = g;
+      s_cand[pos] = c;
+    }
+  }
+  __syncthreads();
+  return total;
+}
+
+__device__ __forceinline__ uint32_t tile_local_bit(int tx, int ty) {
+  return (uint32_t)((ty % SGS_SUPER) * SGS_SUPER + (tx % SGS_SUPER));
+}
+
+// Forward raster: 128 threads per 16x16 tile, each thread owns two
+// vertically adjacent pixels (a warp covers a 16x4 block, which keeps its
+// lanes' supports and termination coherent).  Per staged record the two
+// pixels share the record loads, dx and A dx; the per-pixel blend is
+// predicated, and a warp skips a record outright when none of its 64 pixels
+// is inside the record's support.
+constexpr int kFwdThreads = 128;
+constexpr int kFwdCPT = 2;
+constexpr int kFwdChunk = kFwdThreads * kFwdCPT;  // candidates examined per staging step
+constexpr int kFwdBatch = 256;                    // staged entries processed per block sync
+constexpr int kFwdBuf = kFwdBatch + kFwdChunk;
+
+template <bool kImportance, bool kCount, bool kFilter>
+__global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(ListArgs la, SgsCam cam, float3 bg,
+                                                                 float* __restrict__ out_img,
+                                                                 float* __restrict__ out_T,
+                                                                 uint32_t* __restrict__ out_nc,
+                                                                 float* __restrict__ weight_sums,
+                                                                 unsigned long long* __restrict__ pair_count) {
+  __shared__ float4 s_geo[kFwdBuf];
+  __shared__ float4 s_con[kFwdBuf];
+  __shared__ float4 s_col[kFwdBuf];
+  __shared__ uint32_t s_id[kFwdBuf];
+  __shared__ uint32_t s_cand[kFwdBuf];
+  __shared__ uint32_t s_wcnt[kFwdCPT * kFwdThreads / 32];
+  __shared__ uint32_t s_kend;
+
+  const int tile = blockIdx.x + cam.tile_y0 * cam.tiles_x;
+  const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
+  const int t = threadIdx.x, lane = t & 31;
+  const int px = tx * SGS_TILE + (t & 15);
+  const int py0 = ty * SGS_TILE + 2 * (t >> 4);  // rows py0 and py0 + 1
+  const bool in0 = px < cam.width && py0 < cam.height;
+  const bool in1 = px < cam.width && py0 + 1 < cam.height;
+  const float fx = (float)px + 0.5f, fy0 = (float)py0 + 0.5f;
+  const uint2 rg = la.ranges[list_cell(kFilter, tx, ty, tile, la.super_x)];
+  const uint32_t cs = rg.x, ce = rg.y > rg.x ? rg.y : rg.x;
+
+  float T0 = 1.0f, T1 = 1.0f;
+  float C00 = 0.0f, C01 = 0.0f, C02 = 0.0f, C10 = 0.0f, C11 = 0.0f, C12 = 0.0f;
+  uint32_t nc0 = 0, nc1 = 0, reached = 0, kend = 0, hits_before = 0;
+  bool live0 = in0, live1 = in1;
+  if (t == 0) s_kend = 0;
+
+  const uint32_t lbit = tile_local_bit(tx, ty);
+  uint32_t cb = cs;
+  for (;;) {
+    // stage until a full batch of this tile's entries (or the list ends)
+    int nb = 0;
+    while (nb < kFwdBatch && cb < ce) {
+      const uint32_t chi = cb + kFwdChunk < ce ? cb + kFwdChunk : ce;
+      nb += stage_append<kFwdThreads, kFwdCPT, kFilter, true>(cb, chi, lbit, la, nb, s_geo, s_con, s_col, s_id,
+                                                              s_cand, s_wcnt);
+      cb = chi;
+    }
+    if (nb == 0) break;
+    for (int k = 0; k < nb; ++k) {
+      if (!__any_sync(0xffffffffu, live0 || live1)) break;
+      const float4 G = s_geo[k];
+      const float4 K = s_con[k];
+      const float dx = fx - G.x;
+      const float dy0 = fy0 - G.y, dy1 = dy0 + 1.0f;
+      const float adx = K.x * dx;
+      const float p0 = fmaf(dx, fmaf(K.y, dy0, adx), (K.z * dy0) * dy0);
+      const float p1 = fmaf(dx, fmaf(K.y, dy1, adx), (K.z * dy1) * dy1);
+      const bool e0 = live0 && p0 >= G.w;
+      const bool e1 = live1 && p1 >= G.w;
+      if (kCount) reached += (uint32_t)live0 + (uint32_t)live1;
+      float w0 = 0.0f, w1 = 0.0f;
+      if (__any_sync(0xffffffffu, e0 || e1)) {
+        const float4 c = s_col[k];
+        const uint32_t idx = hits_before + (uint32_t)k + 1u;
+        const uint32_t cnext = s_cand[k] + 1u;
+        {
+          const float a = G.z * ex2_approx(p0);
+          const float Tn = T0 * (a < SGS_ALPHA_MAX ? 1.0f - a : SGS_ONE_MINUS_ALPHA_MAX);
+          const bool keep = e0 && Tn >= SGS_T_KEEP;
+          live0 = live0 && !(e0 && !keep);
+          if (keep) {
+            w0 = fminf(a, SGS_ALPHA_MAX) * T0;
+            C00 = fmaf(w0, c.x, C00);
+            C01 = fmaf(w0, c.y, C01);
+            C02 = fmaf(w0, c.z, C02);
+            T0 = Tn;
+            nc0 = idx;
+            kend = cnext;
+          }
+        }
+        {
+          const float a = G.z * ex2_approx(p1);
+          const float Tn = T1 * (a < SGS_ALPHA_MAX ? 1.0f - a : SGS_ONE_MINUS_ALPHA_MAX);
+          const bool keep = e1 && Tn >= SGS_T_KEEP;
+          live1 = live1 && !(e1 && !keep);
+          if (keep) {
+            w1 = fminf(a, SGS_ALPHA_MAX) * T1;
+            C10 = fmaf(w1, c.x, C10);
+            C11 = fmaf(w1, c.y, C11);
+            C12 = fmaf(w1, c.z, C12);
+            T1 = Tn;
+            nc1 = idx;
+            kend = cnext;
+          }
+        }
+      }
+      if (kImportance) {
+        const float ws = warp_sum(w0 + w1);
+        if (lane == 0 && ws != 0.0f) atomicAdd(&weight_sums[s_id[k]], ws);
+      }
+    }
+    hits_before += (uint32_t)nb;
+    if (cb >= ce) break;
+    if (__syncthreads_count(live0 || live1) == 0) break;
+  }
+  if (kCount) {
+    unsigned long long r = reached;
+    for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+    if (lane == 0 && r) atomicAdd(pair_count, r);
+  }
+  if (kend) atomicMax(&s_kend, kend);
+  if (in0) {
+    const size_t pix = (size_t)py0 * cam.width + px;
+    out_img[3 * pix + 0] = C00 + T0 * bg.x;
+    out_img[3 * pix + 1] = C01 + T0 * bg.y;
+    out_img[3 * pix + 2] = C02 + T0 * bg.z;
+    out_T[pix] = T0;
+    out_nc[pix] = nc0;
+  }
+  if (in1) {
+    const size_t pix = (size_t)(py0 + 1) * cam.width + px;
+    out_img[3 * pix + 0] = C10 + T1 * bg.x;
+    out_img[3 * pix + 1] = C11 + T1 * bg.y;
+    out_img[3 * pix + 2] = C12 + T1 * bg.z;
+    out_T[pix] = T1;
+    out_nc[pix] = nc1;
+  }
+  __syncthreads();
+  if (t == 0) la.cand_end[tile] = s_kend ? s_kend : cs;
+}
+
+constexpr int kGrad = 9;
+constexpr int kBwdThreads = 256;
+
+template <bool kFilter>
+__global__ void __launch_bounds__(kBwdThreads) raster_bwd_kernel(ListArgs la, SgsCam cam, float3 bg,
+                                                                 const float* __restrict__ final_T,
+                                                                 const uint32_t* __restrict__ ncontrib,
+                                                                 const float* __restrict__ dimg,
+                                                                 float* __restrict__ grad2d) {
+  __shared__ float4 s_geo[kBwdThreads];
+  __shared__ float4 s_con[kBwdThreads];
+  __shared__ float4 s_col[kBwdThreads];
+  __shared__ uint32_t s_id[kBwdThreads];
+  __shared__ uint32_t s_cand[kBwdThreads];
+  __shared__ uint32_t s_wcnt[kBwdThreads / 32];
+  __shared__ float s_acc[kBwdThreads][kGrad];
+  __shared__ uint32_t s_max_nc;
 
   const int tile = blockIdx.x + cam.tile_y0 * cam.tiles_x;
   const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
@@ -59,95 +270,9 @@ __global__ void __launch_bounds__(256) raster_fwd_kernel(const uint2* __restrict
   const int px = tx * SGS_TILE + (t & 15), py = ty * SGS_TILE + (t >> 4);
   const bool inside = px < cam.width && py < cam.height;
   const float fx = (float)px + 0.5f, fy = (float)py + 0.5f;
-  const uint2 rg = ranges[tile];
-  const uint32_t start = rg.x, end = rg.y > rg.x ? rg.y : rg.x;
-
-  float T = 1.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
-  uint32_t nc = 0, reached = 0;
-  bool done = !inside;
-
-  for (uint32_t b = start; b < end; b += 256) {
-    if (__syncthreads_count(done) == 256) break;
-    const uint32_t j = b + t;
-    if (j < end) {
-      const uint32_t g = vals[j];
-      s_geo[t] = rec_geo[g];
-      s_con[t] = rec_con[g];
-      s_col[t] = rec_col[g];
-      if (kImportance) s_id[t] = g;
-    }
-    __syncthreads();
-    const int nb = (int)min(256u, end - b);
-    for (int k = 0; k < nb; ++k) {
-      if (__all_sync(0xffffffffu, done)) break;
-      const float4 G = s_geo[k];
-      const float4 K = s_con[k];
-      const float dx = fx - G.x, dy = fy - G.y;
-      const float p = dx * (K.x * dx + K.y * dy) + K.z * dy * dy;
-      float w = 0.0f;
-      if (kCount && !done) ++reached;
-      if (!done && p >= G.w) {
-        const float a = G.z * ex2_approx(p);
-        const float alpha = fminf(a, SGS_ALPHA_MAX);
-        const float Tn = T * (a < SGS_ALPHA_MAX ? 1.0f - a : SGS_ONE_MINUS_ALPHA_MAX);
-        if (Tn < SGS_T_KEEP) {
-          done = true;
-        } else {
-          const float4 c = s_col[k];
-          w = alpha * T;
-          C0 += w * c.x;
-          C1 += w * c.y;
-          C2 += w * c.z;
-          T = Tn;
-          nc = b - start + k + 1;
-        }
-      }
-      if (kImportance) {
-        float ws = warp_sum(w);
-        if (lane == 0 && ws != 0.0f) atomicAdd(&weight_sums[s_id[k]], ws);
-      }
-    }
-  }
-  if (kCount) {
-    unsigned long long r = reached;
-    for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
-    if (lane == 0 && r) atomicAdd(pair_count, r);
-  }
-  if (inside) {
-    const size_t pix = (size_t)py * cam.width + px;
-    out_img[3 * pix + 0] = C0 + T * bg.x;
-    out_img[3 * pix + 1] = C1 + T * bg.y;
-    out_img[3 * pix + 2] = C2 + T * bg.z;
-    out_T[pix] = T;
-    out_nc[pix] = nc;
-  }
-}
-
-constexpr int kGrad = 9;
-
-__global__ void __launch_bounds__(256) raster_bwd_kernel(const uint2* __restrict__ ranges,
-                                                         const uint32_t* __restrict__ vals,
-                                                         const float4* __restrict__ rec_geo,
-                                                         const float4* __restrict__ rec_con,
-                                                         const float4* __restrict__ rec_col, SgsCam cam, float3 bg,
-                                                         const float* __restrict__ final_T,
-                                                         const uint32_t* __restrict__ ncontrib,
-                                                         const float* __restrict__ dimg, float* __restrict__ grad2d) {
-  __shared__ float4 s_geo[256];
-  __shared__ float4 s_con[256];
-  __shared__ float4 s_col[256];
-  __shared__ uint32_t s_id[256];
-  __shared__ float s_acc[256][kGrad];
-  __shared__ uint32_t s_max_nc;
-
-  const int tile = blockIdx.x + cam.tile_y0 * cam.tiles_x;
-  const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int px = tx * SGS_TILE + (t & 15), py = ty * SGS_TILE + (t >> 4);
-  const bool inside = px < cam.width && py < cam.height;
-  const float fx = (float)px + 0.5f, fy = (float)py + 0.5f;
-  const uint2 rg = ranges[tile];
-  const uint32_t start = rg.x;
+  const uint2 rg = la.ranges[list_cell(kFilter, tx, ty, tile, la.super_x)];
+  const uint32_t cs = rg.x;
+  const uint32_t cend = la.cand_end[tile];
 
   float T = 1.0f, g0 = 0.0f, g1 = 0.0f, g2 = 0.0f, S = 0.0f;
   uint32_t nc = 0;
@@ -164,30 +289,26 @@ __global__ void __launch_bounds__(256) raster_bwd_kernel(const uint2* __restrict
     atomicMax(&s_max_nc, nc);
   }
   __syncthreads();
-  const uint32_t stop = start + s_max_nc;  // one past the last entry any pixel kept
-  const uint32_t my_end = start + nc;
+  const uint32_t max_nc = s_max_nc;
+  const uint32_t lbit = tile_local_bit(tx, ty);
+  uint32_t hits_after = 0;
 
-  for (uint32_t hi = stop; hi > start;) {
-    const uint32_t lo = hi - start > 256 ? hi - 256 : start;
-    const int nb = (int)(hi - lo);
+  for (uint32_t hi = cend; hi > cs;) {
+    const uint32_t lo = hi - cs > (uint32_t)kBwdThreads ? hi - kBwdThreads : cs;
     __syncthreads();  // previous batch fully flushed
-    if (t < nb) {
-      const uint32_t g = vals[lo + t];
-      s_geo[t] = rec_geo[g];
-      s_con[t] = rec_con[g];
-      s_col[t] = rec_col[g];
-      s_id[t] = g;
-    }
+#pragma unroll
     for (int c = 0; c < kGrad; ++c) s_acc[t][c] = 0.0f;
-    __syncthreads();
+    const int nb = stage_append<kBwdThreads, 1, kFilter, true>(lo, hi, lbit, la, 0, s_geo, s_con, s_col, s_id,
+                                                               s_cand, s_wcnt);
+    const uint32_t base = max_nc - hits_after - (uint32_t)nb;  // per-tile list index of staged entry 0
     for (int k = nb - 1; k >= 0; --k) {
-      const uint32_t idx = lo + k;
-      if (__all_sync(0xffffffffu, idx >= my_end)) continue;
+      const uint32_t idx = base + (uint32_t)k;
+      if (__all_sync(0xffffffffu, idx >= nc)) continue;
       const float4 G = s_geo[k];
       const float4 K = s_con[k];
       const float dx = fx - G.x, dy = fy - G.y;
-      const float p = dx * (K.x * dx + K.y * dy) + K.z * dy * dy;
-      bool active = idx < my_end && p >= G.w;
+      const float p = fmaf(dx, fmaf(K.y, dy, K.x * dx), (K.z * dy) * dy);
+      const bool active = idx < nc && p >= G.w;
       float v[kGrad];
 #pragma unroll
       for (int c = 0; c < kGrad; ++c) v[c] = 0.0f;
@@ -235,29 +356,110 @@ __global__ void __launch_bounds__(256) raster_bwd_kernel(const uint2* __restrict
         if (x != 0.0f) atomicAdd(dst + c, x);
       }
     }
+    hits_after += (uint32_t)nb;
     hi = lo;
   }
-  (void)warp;
+}
+
+// ------------------------------------------------------------- list export
+// Per-tile lists materialised from the cell lists (parity checks): pass 0
+// counts each tile's hits into ranges[t].y, a scan turns them into
+// [start, end), pass 1 writes (tile << 32 | depth_bits, primitive) in order.
+template <bool kFilter>
+__global__ void __launch_bounds__(kFwdThreads) export_lists_kernel(ListArgs la, SgsCam cam, int pass,
+                                                                   const uint32_t* __restrict__ depth_key,
+                                                                   uint2* __restrict__ tile_ranges,
+                                                                   unsigned long long* __restrict__ keys,
+                                                                   uint32_t* __restrict__ vals) {
+  __shared__ float4 s_geo[kFwdChunk];
+  __shared__ float4 s_con[kFwdChunk];
+  __shared__ uint32_t s_id[kFwdChunk];
+  __shared__ uint32_t s_cand[kFwdChunk];
+  __shared__ uint32_t s_wcnt[kFwdCPT * kFwdThreads / 32];
+  const int tile = blockIdx.x;
+  const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
+  const uint2 rg = la.ranges[list_cell(kFilter, tx, ty, tile, la.super_x)];
+  const uint32_t cs = rg.x, ce = rg.y > rg.x ? rg.y : rg.x;
+  uint32_t out = pass == 0 ? 0u : tile_ranges[tile].x;
+  const uint32_t lbit = tile_local_bit(tx, ty);
+  for (uint32_t cb = cs; cb < ce; cb += kFwdChunk) {
+    const uint32_t chi = cb + kFwdChunk < ce ? cb + kFwdChunk : ce;
+    const int nb = stage_append<kFwdThreads, kFwdCPT, kFilter, false>(cb, chi, lbit, la, 0, s_geo, s_con, nullptr,
+                                                                       s_id, s_cand, s_wcnt);
+    if (pass == 1)
+      for (int k = threadIdx.x; k < nb; k += kFwdThreads) {
+        const uint32_t g = s_id[k];
+        keys[out + k] = ((unsigned long long)tile << 32) | depth_key[g];
+        vals[out + k] = g;
+      }
+    out += (uint32_t)nb;
+    __syncthreads();
+  }
+  if (pass == 0 && threadIdx.x == 0) tile_ranges[tile] = make_uint2(0u, out);
+}
+
+__global__ void __launch_bounds__(1024) export_scan_kernel(uint2* __restrict__ r, int n) {
+  __shared__ uint32_t warp_tot[32];
+  __shared__ uint32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int base = 0; base < n; base += 1024) {
+    const int i = base + threadIdx.x;
+    const uint32_t v = i < n ? r[i].y : 0u;
+    uint32_t x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[w] = x;
+    __syncthreads();
+    uint32_t pre = carry;
+    for (int k = 0; k < w; ++k) pre += warp_tot[k];
+    if (i < n) r[i] = v ? make_uint2(pre + x - v, pre + x) : make_uint2(0u, 0u);
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = pre + x;
+    __syncthreads();
+  }
+}
+
+bool final_in_alt(const Layout& lo);
+
+static ListArgs list_args(const sgs_workspace* ws, const Layout& lo, const uint32_t* vals) {
+  ListArgs a;
+  a.ranges = at<uint2>(ws, lo.ranges);
+  a.keys = at<uint32_t>(ws, final_in_alt(lo) ? lo.ent_key_alt : lo.ent_key);
+  a.vals = vals;
+  a.rect = at<uint2>(ws, lo.rect);
+  a.geo = at<float4>(ws, lo.rec_geo);
+  a.con = at<float4>(ws, lo.rec_con);
+  a.col = at<float4>(ws, lo.rec_col);
+  a.span = at<float2>(ws, lo.rec_span);
+  a.cand_end = at<uint32_t>(ws, lo.cand_end);
+  a.super_x = lo.super_x;
+  return a;
 }
 
 int launch_raster_fwd(const SgsCam& cam, float3 bg, const sgs_workspace* ws, const Layout& lo, const uint32_t* vals,
                       float* img, float* T, uint32_t* nc, float* weight_sums, unsigned long long* pairs,
                       cudaStream_t st) {
   const int grid = (cam.tile_y1 - cam.tile_y0) * cam.tiles_x;
-  const uint2* ranges = at<uint2>(ws, lo.ranges);
-  const float4* g = at<float4>(ws, lo.rec_geo);
-  const float4* k = at<float4>(ws, lo.rec_con);
-  const float4* c = at<float4>(ws, lo.rec_col);
-  if (weight_sums && pairs)
-    raster_fwd_kernel<true, true><<<grid, 256, 0, st>>>(ranges, vals, g, k, c, cam, bg, img, T, nc, weight_sums, pairs);
-  else if (weight_sums)
-    raster_fwd_kernel<true, false><<<grid, 256, 0, st>>>(ranges, vals, g, k, c, cam, bg, img, T, nc, weight_sums,
-                                                         nullptr);
-  else if (pairs)
-    raster_fwd_kernel<false, true><<<grid, 256, 0, st>>>(ranges, vals, g, k, c, cam, bg, img, T, nc, nullptr, pairs);
-  else
-    raster_fwd_kernel<false, false><<<grid, 256, 0, st>>>(ranges, vals, g, k, c, cam, bg, img, T, nc, nullptr,
-                                                          nullptr);
+  const ListArgs a = list_args(ws, lo, vals);
+  const bool filt = lo.sort_mode == SGS_SORT_DEPTH_FIRST;
+#define SGS_FWD(I, C, F) \
+  raster_fwd_kernel<I, C, F><<<grid, kFwdThreads, 0, st>>>(a, cam, bg, img, T, nc, weight_sums, pairs)
+  if (filt) {
+    if (weight_sums && pairs) SGS_FWD(true, true, true);
+    else if (weight_sums) SGS_FWD(true, false, true);
+    else if (pairs) SGS_FWD(false, true, true);
+    else SGS_FWD(false, false, true);
+  } else {
+    if (weight_sums && pairs) SGS_FWD(true, true, false);
+    else if (weight_sums) SGS_FWD(true, false, false);
+    else if (pairs) SGS_FWD(false, true, false);
+    else SGS_FWD(false, false, false);
+  }
+#undef SGS_FWD
   SGS_LAUNCH_CHECK("raster_fwd_kernel");
   return SGS_OK;
 }
@@ -266,10 +468,32 @@ int launch_raster_bwd(const SgsCam& cam, float3 bg, const sgs_workspace* ws, con
                       const float* T, const uint32_t* nc, const float* dimg, float* grad2d, cudaStream_t st) {
   const int grid = (cam.tile_y1 - cam.tile_y0) * cam.tiles_x;
   SGS_CUDA(cudaMemsetAsync(grad2d, 0, (size_t)lo.n * kGrad * sizeof(float), st));
-  raster_bwd_kernel<<<grid, 256, 0, st>>>(at<uint2>(ws, lo.ranges), vals, at<float4>(ws, lo.rec_geo),
-                                          at<float4>(ws, lo.rec_con), at<float4>(ws, lo.rec_col), cam, bg, T, nc,
-                                          dimg, grad2d);
+  const ListArgs a = list_args(ws, lo, vals);
+  if (lo.sort_mode == SGS_SORT_DEPTH_FIRST)
+    raster_bwd_kernel<true><<<grid, kBwdThreads, 0, st>>>(a, cam, bg, T, nc, dimg, grad2d);
+  else
+    raster_bwd_kernel<false><<<grid, kBwdThreads, 0, st>>>(a, cam, bg, T, nc, dimg, grad2d);
   SGS_LAUNCH_CHECK("raster_bwd_kernel");
+  return SGS_OK;
+}
+
+int launch_export_lists(const SgsCam& cam, const sgs_workspace* ws, const Layout& lo, const uint32_t* vals,
+                        unsigned long long* keys, uint32_t* out_vals, uint32_t* ranges, cudaStream_t st) {
+  const ListArgs a = list_args(ws, lo, vals);
+  uint2* r = reinterpret_cast<uint2*>(ranges);
+  const uint32_t* dk = at<uint32_t>(ws, lo.depth_key);
+  const bool filt = lo.sort_mode == SGS_SORT_DEPTH_FIRST;
+  for (int pass = 0; pass < 2; ++pass) {
+    if (filt)
+      export_lists_kernel<true><<<lo.n_tiles, kFwdThreads, 0, st>>>(a, cam, pass, dk, r, keys, out_vals);
+    else
+      export_lists_kernel<false><<<lo.n_tiles, kFwdThreads, 0, st>>>(a, cam, pass, dk, r, keys, out_vals);
+    SGS_LAUNCH_CHECK("export_lists_kernel");
+    if (pass == 0) {
+      export_scan_kernel<<<1, 1024, 0, st>>>(r, lo.n_tiles);
+      SGS_LAUNCH_CHECK("export_scan_kernel");
+    }
+  }
   return SGS_OK;
 }
 

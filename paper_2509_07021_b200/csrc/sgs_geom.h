@@ -338,6 +338,30 @@ SGS_HD SgsSpan sgs_span(const float geo[4], const float con[4]) {
   return s;
 }
 
+// The span parameters are cached per primitive by the preprocess: kx in the
+// conic record's 4th slot, (xm, ym) in a float2 (xm < 0 marks an invalid
+// form).  Rebuilding SgsSpan from the cache is bit-identical to sgs_span.
+SGS_HD void sgs_span_cache(const SgsSpan* s, float* kx, float span2[2]) {
+  *kx = s->kx;
+  span2[0] = s->valid ? s->xm : -1.0f;
+  span2[1] = s->ym;
+}
+
+SGS_HD SgsSpan sgs_span_cached(const float geo[4], const float con[4], const float span2[2]) {
+  SgsSpan s;
+  s.mx = geo[0];
+  s.my = geo[1];
+  s.pmin = geo[3];
+  s.A = con[0];
+  s.B = con[1];
+  s.C = con[2];
+  s.kx = con[3];
+  s.valid = span2[0] >= 0.0f;
+  s.xm = s.valid ? span2[0] : 0.0f;
+  s.ym = span2[1];
+  return s;
+}
+
 // x where the ellipse boundary crosses the horizontal line dy (the larger root
 // when `right`, else the smaller); the caller guarantees |dy| <= ym up to
 // rounding, and a slightly negative discriminant is clamped to 0.
@@ -401,6 +425,106 @@ SGS_HD uint32_t sgs_count_tiles(int tx0, int ty0, int tx1, int ty1, const float 
   return n;
 }
 
+// Super-tiles: SGS_SUPER x SGS_SUPER tiles (64 x 64 px).  The depth-first
+// binning sorts (super-tile, primitive) entries -- about a tenth of the
+// (tile, primitive) entries -- and the raster filters each super-tile list
+// down to its own tile with the exact per-tile test above, so the per-tile
+// lists (and everything downstream) are identical to sorting tile entries.
+// A primitive's super-tile set: for each super row, the super columns
+// spanned by [min, max] of its tile rows' spans -- a superset of the super
+// tiles that contain a hit tile, built from the same per-row spans, so no
+// tile hit can be lost to rounding.
+#define SGS_SUPER 4
+
+SGS_HD int sgs_super_row(const SgsSpan* s, const SgsCam* cam, int tx0, int ty0, int tx1, int ty1, int sr,
+                         int* first_sc) {
+  int lo = 0x7fffffff, hi = -1, first;
+  int r0 = sr * SGS_SUPER, r1 = r0 + SGS_SUPER - 1;
+  if (r0 < ty0) r0 = ty0;
+  if (r1 > ty1) r1 = ty1;
+  for (int ty = r0; ty <= r1; ++ty) {
+    const int c = sgs_row_span(s, cam, ty, tx0, tx1, &first);
+    if (c > 0) {
+      const int a = first / SGS_SUPER, b = (first + c - 1) / SGS_SUPER;
+      lo = a < lo ? a : lo;
+      hi = b > hi ? b : hi;
+    }
+  }
+  *first_sc = hi >= lo ? lo : 0;
+  return hi >= lo ? hi - lo + 1 : 0;
+}
+
+// Super row `sr` with its tile rows' spans (first[r], cnt[r]), r = ty - 4 sr
+// (cnt = 0 outside the rectangle), for the per-entry tile masks.
+SGS_HD int sgs_super_row_spans(const SgsSpan* s, const SgsCam* cam, int tx0, int ty0, int tx1, int ty1, int sr,
+                               int first[SGS_SUPER], int cnt[SGS_SUPER], int* first_sc) {
+  int lo = 0x7fffffff, hi = -1;
+  for (int r = 0; r < SGS_SUPER; ++r) {
+    const int ty = sr * SGS_SUPER + r;
+    first[r] = 0;
+    cnt[r] = 0;
+    if (ty < ty0 || ty > ty1) continue;
+    cnt[r] = sgs_row_span(s, cam, ty, tx0, tx1, &first[r]);
+    if (cnt[r] > 0) {
+      const int a = first[r] / SGS_SUPER, b = (first[r] + cnt[r] - 1) / SGS_SUPER;
+      lo = a < lo ? a : lo;
+      hi = b > hi ? b : hi;
+    }
+  }
+  *first_sc = hi >= lo ? lo : 0;
+  return hi >= lo ? hi - lo + 1 : 0;
+}
+
+// 16-bit membership mask of super-tile column sc: bit (r * 4 + c) set iff
+// tile (4 sc + c, 4 sr + r) is in the primitive's tile set.
+SGS_HD uint32_t sgs_super_mask(const int first[SGS_SUPER], const int cnt[SGS_SUPER], int sc) {
+  uint32_t m = 0;
+  for (int r = 0; r < SGS_SUPER; ++r)
+    for (int c = 0; c < SGS_SUPER; ++c) {
+      const int tx = sc * SGS_SUPER + c;
+      if (tx >= first[r] && tx < first[r] + cnt[r]) m |= 1u << (r * SGS_SUPER + c);
+    }
+  return m;
+}
+
+// (tile entries, super-tile entries) of one primitive.
+SGS_HD void sgs_count_hits(int tx0, int ty0, int tx1, int ty1, const float geo[4], const float con[4],
+                           const SgsCam* cam, uint32_t* n_tiles, uint32_t* n_super) {
+  SgsSpan s = sgs_span(geo, con);
+  uint32_t nt = 0, ns = 0;
+  int cur = -1, lo = 0x7fffffff, hi = -1, first;
+  for (int ty = ty0; ty <= ty1; ++ty) {
+    const int sr = ty / SGS_SUPER;
+    if (sr != cur) {
+      if (hi >= lo) ns += (uint32_t)(hi - lo + 1);
+      cur = sr;
+      lo = 0x7fffffff;
+      hi = -1;
+    }
+    const int c = sgs_row_span(&s, cam, ty, tx0, tx1, &first);
+    nt += (uint32_t)c;
+    if (c > 0) {
+      const int a = first / SGS_SUPER, b = (first + c - 1) / SGS_SUPER;
+      lo = a < lo ? a : lo;
+      hi = b > hi ? b : hi;
+    }
+  }
+  if (hi >= lo) ns += (uint32_t)(hi - lo + 1);
+  *n_tiles = nt;
+  *n_super = ns;
+}
+
+// Exact membership of a primitive in tile (tx, ty)'s list (the same test
+// the counts and the CPU restatement use).
+SGS_HD int sgs_tile_member(const float geo[4], const float con[4], const float span2[2], int tx0, int ty0,
+                           int tx1, int ty1, const SgsCam* cam, int tx, int ty) {
+  if (ty < ty0 || ty > ty1 || tx < tx0 || tx > tx1) return 0;
+  SgsSpan s = sgs_span_cached(geo, con, span2);
+  int first;
+  const int c = sgs_row_span(&s, cam, ty, tx0, tx1, &first);
+  return tx >= first && tx < first + c;
+}
+
 // SG color for the camera-to-center view direction (render.py:294-305):
 //   c_pre = diffuse + sum_l m_l a_l exp(s_l (mu_l . v - 1)),  c = max(c_pre, 0)
 // Lobes with mask exactly 0 are skipped (bit-identical to multiplying by 0).
@@ -443,5 +567,5 @@ SGS_HD void sgs_pack_geo(const SgsProj* p, float geo[4], float con[4]) {
   con[0] = F_MUL(k, p->con00);
   con[1] = F_MUL(2.0f * k, p->con01);
   con[2] = F_MUL(k, p->con11);
-  con[3] = 0.0f;
+  con[3] = 0.0f;  // replaced by the span cache's kx (sgs_span_cache)
 }

@@ -56,7 +56,7 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 // must be zeroed.  n = min(*n_ptr, n_cap).  16-byte vector loads.
 template <typename K>
 __global__ void __launch_bounds__(256) rs_histogram(const K* __restrict__ keys, const uint32_t* n_ptr, uint32_t n_cap,
-                                                    int num_passes, uint32_t* __restrict__ hist) {
+                                                    int begin_bit, int num_passes, uint32_t* __restrict__ hist) {
   extern __shared__ uint32_t sh[];  // [num_passes][8 warps][256]
   constexpr int V = 16 / sizeof(K);
   const uint32_t n = min(*n_ptr, n_cap);
@@ -70,11 +70,11 @@ __global__ void __launch_bounds__(256) rs_histogram(const K* __restrict__ keys, 
     const K* ks = reinterpret_cast<const K*>(&raw);
 #pragma unroll
     for (int v = 0; v < V; ++v)
-      for (int p = 0; p < num_passes; ++p) atomicAdd(&sh[(p * 8 + w) * 256 + rs_digit(ks[v], 8 * p)], 1u);
+      for (int p = 0; p < num_passes; ++p) atomicAdd(&sh[(p * 8 + w) * 256 + rs_digit(ks[v], begin_bit + 8 * p)], 1u);
   }
   for (uint32_t i = nvec * V + blockIdx.x * 256u + threadIdx.x; i < n; i += gridDim.x * 256u) {
     K k = keys[i];
-    for (int p = 0; p < num_passes; ++p) atomicAdd(&sh[(p * 8 + w) * 256 + rs_digit(k, 8 * p)], 1u);
+    for (int p = 0; p < num_passes; ++p) atomicAdd(&sh[(p * 8 + w) * 256 + rs_digit(k, begin_bit + 8 * p)], 1u);
   }
   __syncthreads();
   for (int j = threadIdx.x; j < num_passes * 256; j += 256) {
@@ -275,8 +275,8 @@ inline uint64_t rs_parts(uint64_t n) {
   return (n + kRsThreads * IPT - 1) / (kRsThreads * IPT);
 }
 
-// Sort `n_cap`-bounded pairs (count in *n_ptr on the device) over bits
-// [0, bits).  Ping-pongs between (k0, v0) and (k1, v1); *result_in_alt says
+// Sort `n_cap`-bounded pairs (count in *n_ptr on the device) over key bits
+// [begin_bit, begin_bit + bits); lower bits travel with the key unsorted.  Ping-pongs between (k0, v0) and (k1, v1); *result_in_alt says
 // whether the result is in (k1, v1).  iota_values: the input values are the
 // item indices (v0 is not read).  With `rout.ranges`, the last pass writes
 // only values plus the tile ranges.  hist: 16*256 u32; status:
@@ -284,7 +284,8 @@ inline uint64_t rs_parts(uint64_t n) {
 template <typename K, int IPT>
 int radix_sort_pairs(K* k0, uint32_t* v0, K* k1, uint32_t* v1, const uint32_t* n_ptr, uint32_t n_cap, int bits,
                      uint32_t* hist, uint32_t* status, uint32_t* tickets, bool* result_in_alt, cudaStream_t st,
-                     bool iota_values = false, RsRangeOut rout = RsRangeOut{nullptr, 0}) {
+                     bool iota_values = false, RsRangeOut rout = RsRangeOut{nullptr, 0}, int begin_bit = 0,
+                     bool keep_last_keys = false) {
   const int passes = (bits + 7) / 8;
   const uint64_t parts = rs_parts<K, IPT>(n_cap);
   *result_in_alt = false;
@@ -298,7 +299,7 @@ int radix_sort_pairs(K* k0, uint32_t* v0, K* k1, uint32_t* v1, const uint32_t* n
   if (hgrid < 1) hgrid = 1;
   const size_t hsmem = (size_t)passes * 8 * 256 * 4;
   SGS_CUDA(cudaFuncSetAttribute(rs_histogram<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-  rs_histogram<K><<<hgrid, 256, hsmem, st>>>(k0, n_ptr, n_cap, passes, hist);
+  rs_histogram<K><<<hgrid, 256, hsmem, st>>>(k0, n_ptr, n_cap, begin_bit, passes, hist);
   SGS_LAUNCH_CHECK("rs_histogram");
   rs_scan_hist<<<passes, 256, 0, st>>>(hist);
   SGS_LAUNCH_CHECK("rs_scan_hist");
@@ -322,7 +323,8 @@ int radix_sort_pairs(K* k0, uint32_t* v0, K* k1, uint32_t* v1, const uint32_t* n
   for (int p = 0; p < passes; ++p) {
     const bool last = p + 1 == passes;
     rs_onesweep<K, IPT><<<grid, kRsThreads, smem, st>>>(ka, (p == 0 && iota_values) ? nullptr : va,
-                                                  (last && rout.ranges) ? nullptr : kb, vb, n_ptr, n_cap, 8 * p,
+                                                  (last && rout.ranges && !keep_last_keys) ? nullptr : kb, vb, n_ptr,
+                                                  n_cap, begin_bit + 8 * p,
                                                   hist + 256 * p, status + (size_t)parts * 256 * p, tickets + p,
                                                   last ? rout : RsRangeOut{nullptr, 0});
     SGS_LAUNCH_CHECK("rs_onesweep");

@@ -181,7 +181,7 @@ class Rasterizer:
             return self._cap_hint[key]
         if self.initial_capacity is not None:
             return self.initial_capacity
-        return int(min(MAX_CAPACITY, max(1 << 16, 16 * g.n)))
+        return int(min(MAX_CAPACITY, max(1 << 16, 4 * g.n)))
 
     def workspace(self, g, cam, private=False, capacity=None) -> Workspace:
         key = self._key(g, cam)
@@ -228,11 +228,11 @@ class Rasterizer:
             if check:
                 st = ws.stats()
                 if st["overflow"]:
-                    need = int(st["n_entries"] * self.headroom) + 1024
-                    if st["n_entries"] > MAX_CAPACITY:
+                    need = int(st["n_bin_entries"] * self.headroom) + 1024
+                    if st["n_bin_entries"] > MAX_CAPACITY:
                         raise _ffi.CapacityError(
                             "sgs_bin", _ffi.SGS_E_CAPACITY,
-                            f"{st['n_entries']} tile entries exceed one bin call's limit "
+                            f"{st['n_bin_entries']} entries exceed one bin call's limit "
                             f"{MAX_CAPACITY}; render in tile-row strips")
                     self._cap_hint[key] = min(MAX_CAPACITY, need)
                     continue
@@ -294,7 +294,7 @@ class Rasterizer:
     def export_bins(self, frame: Frame):
         """(keys u64 as int64, values int32, ranges (T,2) int32) of the sorted tile list."""
         st = frame.ws.stats()
-        n = int(min(st["n_entries"], st["capacity"]))
+        n = int(st["n_entries"])
         keys = torch.empty(max(n, 1), dtype=torch.int64, device=self.device)
         vals = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
         tiles = ((frame.cam.width + 15) // 16) * ((frame.cam.height + 15) // 16)

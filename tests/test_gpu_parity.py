@@ -129,7 +129,8 @@ def test_capacity_growth():
     g = GaussianTensors.from_arrays(scene)
     frame = rast.forward(g, cams[0])
     ref = tiled.render(scene, cams[0])
-    assert frame.ws.capacity >= ref.n_entries
+    st = frame.stats()
+    assert frame.ws.capacity >= st["n_bin_entries"] > 1000 and not st["overflow"]
     _check_bins(rast, frame, ref)
 
 

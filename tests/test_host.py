@@ -36,7 +36,7 @@ def test_struct_layouts_match_header():
     assert C.sizeof(_ffi.SgsCamera) == 4 * 9 + 4 * 3 + 4 * 5 + 4 * 4 + 4
     assert C.sizeof(_ffi.SgsParams) == 10 * 8 + 8 + 8
     assert C.sizeof(_ffi.SgsWorkspace) == 8 + 8 + 8 + 4 * 4 + 8
-    assert C.sizeof(_ffi.SgsStats) == 7 * 8
+    assert C.sizeof(_ffi.SgsStats) == 8 * 8
 
 
 def _ws(n=1000, L=3, W=256, H=256, cap=1 << 16, mode=0):
