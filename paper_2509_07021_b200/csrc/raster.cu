@@ -57,15 +57,25 @@ __device__ __forceinline__ int list_cell(bool filter, int tx, int ty, int tile, 
   return filter ? (ty / SGS_SUPER) * super_x + tx / SGS_SUPER : tile;
 }
 
+// Shared-memory staging buffer of N records.
+template <int N>
+struct Stage {
+  float4 geo[N];
+  float4 con[N];
+  float4 col[N];
+  uint32_t id[N];
+  uint32_t cand[N];
+  uint32_t wcnt[32];
+};
+
 // Append the members of tile (tx, ty) among candidates [c_lo, c_hi) (at
 // most THREADS * CPT) of the cell list to the shared-memory batch at `base`,
 // in list order.  Depth-first mode reads membership from the 16-bit tile mask
 // carried in each sorted key (bit `local_bit`); 64-bit-key lists are per
 // tile already.  Returns the number appended.  Ends with __syncthreads().
-template <int THREADS, int CPT, bool kFilter, bool kColor>
+template <int THREADS, int CPT, bool kFilter, bool kColor, int N>
 __device__ __forceinline__ int stage_append(uint32_t c_lo, uint32_t c_hi, uint32_t local_bit, const ListArgs& a,
-                                            int base, float4* s_geo, float4* s_con, float4* s_col, uint32_t* s_id,
-                                            uint32_t* s_cand, uint32_t* s_wcnt) {
+                                            int base, Stage<N>& s) {
   constexpr int W = THREADS / 32;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const uint32_t lt = (1u << lane) - 1u;
@@ -76,7 +86,7 @@ __device__ __forceinline__ int stage_append(uint32_t c_lo, uint32_t c_hi, uint32
     bool hit = c < c_hi;
     if (kFilter && hit) hit = (a.keys[c] >> local_bit) & 1u;
     bal[h] = __ballot_sync(0xffffffffu, hit);
-    if (lane == 0) s_wcnt[h * W + warp] = __popc(bal[h]);
+    if (lane == 0) s.wcnt[h * W + warp] = __popc(bal[h]);
   }
   __syncthreads();
   int total = 0;
@@ -84,7 +94,7 @@ __device__ __forceinline__ int stage_append(uint32_t c_lo, uint32_t c_hi, uint32
   for (int h = 0; h < CPT; ++h) {
     int pre = 0;
     for (int j = 0; j < CPT * W; ++j) {
-      const int v = (int)s_wcnt[j];
+      const int v = (int)s.wcnt[j];
       pre += (j < h * W + warp) ? v : 0;
       if (h == 0) total += v;
     }
@@ -92,11 +102,11 @@ __device__ __forceinline__ int stage_append(uint32_t c_lo, uint32_t c_hi, uint32
       const uint32_t c = c_lo + t + h * THREADS;
       const int pos = base + pre + __popc(bal[h] & lt);
       const uint32_t g = a.vals[c];
-      s_geo[pos] = a.geo[g];
-      s_con[pos] = a.con[g];
-      if (kColor) s_col[pos] = a.col[g];
-      s_id[pos] = g;
-      s_cand[pos] = c;
+      s.geo[pos] = a.geo[g];
+      s.con[pos] = a.con[g];
+      if (kColor) s.col[pos] = a.col[g];
+      s.id[pos] = g;
+      s.cand[pos] = c;
     }
   }
   __syncthreads();
@@ -126,12 +136,7 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(ListArgs la, Sg
                                                                  uint32_t* __restrict__ out_nc,
                                                                  float* __restrict__ weight_sums,
                                                                  unsigned long long* __restrict__ pair_count) {
-  __shared__ float4 s_geo[kFwdBuf];
-  __shared__ float4 s_con[kFwdBuf];
-  __shared__ float4 s_col[kFwdBuf];
-  __shared__ uint32_t s_id[kFwdBuf];
-  __shared__ uint32_t s_cand[kFwdBuf];
-  __shared__ uint32_t s_wcnt[kFwdCPT * kFwdThreads / 32];
+  __shared__ Stage<kFwdBuf> s;
   __shared__ uint32_t s_kend;
 
   const int tile = blockIdx.x + cam.tile_y0 * cam.tiles_x;
@@ -158,15 +163,14 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(ListArgs la, Sg
     int nb = 0;
     while (nb < kFwdBatch && cb < ce) {
       const uint32_t chi = cb + kFwdChunk < ce ? cb + kFwdChunk : ce;
-      nb += stage_append<kFwdThreads, kFwdCPT, kFilter, true>(cb, chi, lbit, la, nb, s_geo, s_con, s_col, s_id,
-                                                              s_cand, s_wcnt);
+      nb += stage_append<kFwdThreads, kFwdCPT, kFilter, true>(cb, chi, lbit, la, nb, s);
       cb = chi;
     }
     if (nb == 0) break;
     for (int k = 0; k < nb; ++k) {
       if (!__any_sync(0xffffffffu, live0 || live1)) break;
-      const float4 G = s_geo[k];
-      const float4 K = s_con[k];
+      const float4 G = s.geo[k];
+      const float4 K = s.con[k];
       const float dx = fx - G.x;
       const float dy0 = fy0 - G.y, dy1 = dy0 + 1.0f;
       const float adx = K.x * dx;
@@ -177,14 +181,13 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(ListArgs la, Sg
       if (kCount) reached += (uint32_t)live0 + (uint32_t)live1;
       float w0 = 0.0f, w1 = 0.0f;
       if (__any_sync(0xffffffffu, e0 || e1)) {
-        const float4 c = s_col[k];
+        const float4 c = s.col[k];
         const uint32_t idx = hits_before + (uint32_t)k + 1u;
-        const uint32_t cnext = s_cand[k] + 1u;
         {
           const float a = G.z * ex2_approx(p0);
-          const float Tn = T0 * (a < SGS_ALPHA_MAX ? 1.0f - a : SGS_ONE_MINUS_ALPHA_MAX);
+          const float Tn = T0 * fmaxf(1.0f - a, SGS_ONE_MINUS_ALPHA_MAX);
           const bool keep = e0 && Tn >= SGS_T_KEEP;
-          live0 = live0 && !(e0 && !keep);
+          live0 = live0 && (keep || !e0);
           if (keep) {
             w0 = fminf(a, SGS_ALPHA_MAX) * T0;
             C00 = fmaf(w0, c.x, C00);
@@ -192,14 +195,13 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(ListArgs la, Sg
             C02 = fmaf(w0, c.z, C02);
             T0 = Tn;
             nc0 = idx;
-            kend = cnext;
           }
         }
         {
           const float a = G.z * ex2_approx(p1);
-          const float Tn = T1 * (a < SGS_ALPHA_MAX ? 1.0f - a : SGS_ONE_MINUS_ALPHA_MAX);
+          const float Tn = T1 * fmaxf(1.0f - a, SGS_ONE_MINUS_ALPHA_MAX);
           const bool keep = e1 && Tn >= SGS_T_KEEP;
-          live1 = live1 && !(e1 && !keep);
+          live1 = live1 && (keep || !e1);
           if (keep) {
             w1 = fminf(a, SGS_ALPHA_MAX) * T1;
             C10 = fmaf(w1, c.x, C10);
@@ -207,15 +209,17 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(ListArgs la, Sg
             C12 = fmaf(w1, c.z, C12);
             T1 = Tn;
             nc1 = idx;
-            kend = cnext;
           }
         }
       }
       if (kImportance) {
         const float ws = warp_sum(w0 + w1);
-        if (lane == 0 && ws != 0.0f) atomicAdd(&weight_sums[s_id[k]], ws);
+        if (lane == 0 && ws != 0.0f) atomicAdd(&weight_sums[s.id[k]], ws);
       }
     }
+    // candidate position of this thread's last kept entry (for the backward)
+    const uint32_t mx = nc0 > nc1 ? nc0 : nc1;
+    if (mx > hits_before) kend = s.cand[mx - hits_before - 1] + 1u;
     hits_before += (uint32_t)nb;
     if (cb >= ce) break;
     if (__syncthreads_count(live0 || live1) == 0) break;
@@ -255,12 +259,7 @@ __global__ void __launch_bounds__(kBwdThreads) raster_bwd_kernel(ListArgs la, Sg
                                                                  const uint32_t* __restrict__ ncontrib,
                                                                  const float* __restrict__ dimg,
                                                                  float* __restrict__ grad2d) {
-  __shared__ float4 s_geo[kBwdThreads];
-  __shared__ float4 s_con[kBwdThreads];
-  __shared__ float4 s_col[kBwdThreads];
-  __shared__ uint32_t s_id[kBwdThreads];
-  __shared__ uint32_t s_cand[kBwdThreads];
-  __shared__ uint32_t s_wcnt[kBwdThreads / 32];
+  __shared__ Stage<kBwdThreads> s;
   __shared__ float s_acc[kBwdThreads][kGrad];
   __shared__ uint32_t s_max_nc;
 
@@ -298,14 +297,13 @@ __global__ void __launch_bounds__(kBwdThreads) raster_bwd_kernel(ListArgs la, Sg
     __syncthreads();  // previous batch fully flushed
 #pragma unroll
     for (int c = 0; c < kGrad; ++c) s_acc[t][c] = 0.0f;
-    const int nb = stage_append<kBwdThreads, 1, kFilter, true>(lo, hi, lbit, la, 0, s_geo, s_con, s_col, s_id,
-                                                               s_cand, s_wcnt);
+    const int nb = stage_append<kBwdThreads, 1, kFilter, true>(lo, hi, lbit, la, 0, s);
     const uint32_t base = max_nc - hits_after - (uint32_t)nb;  // per-tile list index of staged entry 0
     for (int k = nb - 1; k >= 0; --k) {
       const uint32_t idx = base + (uint32_t)k;
       if (__all_sync(0xffffffffu, idx >= nc)) continue;
-      const float4 G = s_geo[k];
-      const float4 K = s_con[k];
+      const float4 G = s.geo[k];
+      const float4 K = s.con[k];
       const float dx = fx - G.x, dy = fy - G.y;
       const float p = fmaf(dx, fmaf(K.y, dy, K.x * dx), (K.z * dy) * dy);
       const bool active = idx < nc && p >= G.w;
@@ -313,11 +311,11 @@ __global__ void __launch_bounds__(kBwdThreads) raster_bwd_kernel(ListArgs la, Sg
 #pragma unroll
       for (int c = 0; c < kGrad; ++c) v[c] = 0.0f;
       if (active) {
-        const float4 col = s_col[k];
+        const float4 col = s.col[k];
         const float Gv = ex2_approx(p);
         const float a = G.z * Gv;
         const float alpha = fminf(a, SGS_ALPHA_MAX);
-        const float om = a < SGS_ALPHA_MAX ? 1.0f - a : SGS_ONE_MINUS_ALPHA_MAX;
+        const float om = fmaxf(1.0f - a, SGS_ONE_MINUS_ALPHA_MAX);
         const float Ti = T / om;
         const float w = alpha * Ti;
         const float cg = col.x * g0 + col.y * g1 + col.z * g2;
@@ -349,7 +347,7 @@ __global__ void __launch_bounds__(kBwdThreads) raster_bwd_kernel(ListArgs la, Sg
     }
     __syncthreads();
     if (t < nb) {
-      float* dst = grad2d + (size_t)s_id[t] * kGrad;
+      float* dst = grad2d + (size_t)s.id[t] * kGrad;
 #pragma unroll
       for (int c = 0; c < kGrad; ++c) {
         const float x = s_acc[t][c];
@@ -371,11 +369,7 @@ __global__ void __launch_bounds__(kFwdThreads) export_lists_kernel(ListArgs la, 
                                                                    uint2* __restrict__ tile_ranges,
                                                                    unsigned long long* __restrict__ keys,
                                                                    uint32_t* __restrict__ vals) {
-  __shared__ float4 s_geo[kFwdChunk];
-  __shared__ float4 s_con[kFwdChunk];
-  __shared__ uint32_t s_id[kFwdChunk];
-  __shared__ uint32_t s_cand[kFwdChunk];
-  __shared__ uint32_t s_wcnt[kFwdCPT * kFwdThreads / 32];
+  __shared__ Stage<kFwdChunk> s;
   const int tile = blockIdx.x;
   const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
   const uint2 rg = la.ranges[list_cell(kFilter, tx, ty, tile, la.super_x)];
@@ -384,11 +378,10 @@ __global__ void __launch_bounds__(kFwdThreads) export_lists_kernel(ListArgs la, 
   const uint32_t lbit = tile_local_bit(tx, ty);
   for (uint32_t cb = cs; cb < ce; cb += kFwdChunk) {
     const uint32_t chi = cb + kFwdChunk < ce ? cb + kFwdChunk : ce;
-    const int nb = stage_append<kFwdThreads, kFwdCPT, kFilter, false>(cb, chi, lbit, la, 0, s_geo, s_con, nullptr,
-                                                                       s_id, s_cand, s_wcnt);
+    const int nb = stage_append<kFwdThreads, kFwdCPT, kFilter, false>(cb, chi, lbit, la, 0, s);
     if (pass == 1)
       for (int k = threadIdx.x; k < nb; k += kFwdThreads) {
-        const uint32_t g = s_id[k];
+        const uint32_t g = s.id[k];
         keys[out + k] = ((unsigned long long)tile << 32) | depth_key[g];
         vals[out + k] = g;
       }
