@@ -41,13 +41,15 @@ WORKLOAD = "configs[2]: 1,000,000 Gaussians (64 clusters), 3 SG lobes, 1920x1080
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--views", type=int, default=8)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=1_000_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sort-mode", type=int, default=0)
+    ap.add_argument("--streams", type=int, default=4,
+                    help="concurrent CUDA streams the views of a step are spread over")
     return ap.parse_args()
 
 
@@ -71,7 +73,7 @@ class ClockSampler:
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.fh,
+                 "--format=csv,noheader,nounits", "-lms", "20"], stdout=self.fh,
                 stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -228,11 +230,14 @@ def run_ours(args):
     torch.cuda.synchronize(dev)
     static_bytes = torch.cuda.memory_allocated(dev)
 
-    # warm-up: size the tile-entry capacity on every camera this rank renders
-    imgs = [None] * V
+    # warm-up: size the tile-entry capacity on every camera this rank renders,
+    # on every stream's workspace
+    streams = [torch.cuda.current_stream(dev)] + [torch.cuda.Stream(device=dev)
+                                                  for _ in range(max(args.streams, 1) - 1)]
     for _ in range(max(args.warmup, 3)):
         for k, cam in enumerate(my_cams):
-            imgs[k] = rast.forward(g, cam, check=True).img
+            with torch.cuda.stream(streams[k % len(streams)]):
+                rast.forward(g, cam, check=True)
     torch.cuda.synchronize(dev)
     stats = []
     pairs = torch.zeros(1, dtype=torch.int64, device=dev)
@@ -251,13 +256,15 @@ def run_ours(args):
               C.byref(ws.desc), C.c_void_p(torch.cuda.current_stream(dev).cuda_stream))
     vs = ws.stats()
     model3s = 40 * vs["vram3s_visible"] + 12 * vs["vram3s_entries"]
-    peak_dynamic = torch.cuda.max_memory_allocated(dev) - static_bytes
+    # per-frame dynamic render VRAM: one frame on a fresh workspace
+    from paper_2509_07021_b200.postprocess import measured_render_vram
+    frame_vram = measured_render_vram(g, my_cams[0], rast=rast)
+    inflight_bytes = sum(w.nbytes for w in rast._shared.values())
 
-    # ---- timed region (device time, CUDA events on the launching stream)
+    # ---- timed region (device time, CUDA events on the launching stream).
+    # The views of a step are spread round-robin over `streams` so one view's
+    # latency-bound binning overlaps another view's raster.
     stream = torch.cuda.current_stream(dev)
-    n_ev = args.steps * V
-    r0 = [torch.cuda.Event(enable_timing=True) for _ in range(n_ev)]
-    r1 = [torch.cuda.Event(enable_timing=True) for _ in range(n_ev)]
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     out_bufs = [(torch.empty((c.height, c.width, 3), device=dev),
                  torch.empty((c.height, c.width), device=dev),
@@ -266,17 +273,31 @@ def run_ours(args):
     barrier()
     torch.cuda.synchronize(dev)
     start.record(stream)
-    e = 0
+    for s in streams[1:]:
+        s.wait_stream(stream)
     for _ in range(args.steps):
         for k, cam in enumerate(my_cams):
-            # split forward so the raster kernel can be timed on its stream
-            rast.forward(g, cam, check=False, out=out_bufs[k], _events=(r0[e], r1[e]))
-            e += 1
+            with torch.cuda.stream(streams[k % len(streams)]):
+                rast.forward(g, cam, check=False, out=out_bufs[k])
+    for s in streams[1:]:
+        stream.wait_stream(s)
     stop.record(stream)
     torch.cuda.synchronize(dev)
     barrier()
     clk = clocks.stop()
     t_ms = start.elapsed_time(stop)
+
+    # ---- dominant-kernel timing for the roofline: the same renders on ONE
+    # stream, CUDA events bracketing each raster launch on its stream
+    n_ev = args.steps * V
+    r0 = [torch.cuda.Event(enable_timing=True) for _ in range(n_ev)]
+    r1 = [torch.cuda.Event(enable_timing=True) for _ in range(n_ev)]
+    e = 0
+    for _ in range(args.steps):
+        for k, cam in enumerate(my_cams):
+            rast.forward(g, cam, check=False, out=out_bufs[k], _events=(r0[e], r1[e]))
+            e += 1
+    torch.cuda.synchronize(dev)
     raster_ms = [a.elapsed_time(b) for a, b in zip(r0, r1)]
     # overflow guard: the timed frames reused capacities sized in warm-up
     for cam in my_cams:
@@ -326,11 +347,13 @@ def run_ours(args):
             "data": "synthetic (seeded BASELINE configs[2] distributions, random-init scene)",
             "config": {"workload": WORKLOAD, "views_per_step_per_gpu": V,
                        "parallelism": f"view-sharded x{world}, Gaussians replicated",
+                       "streams_per_gpu": len(streams),
                        "sort_mode": ["depth_first", "key64"][args.sort_mode],
                        "l2": "inputs larger than L2 (140 MB scene + ~0.5 GB key tables per view)"},
             "mpix_per_s": mpix,
-            "vram": {"peak_dynamic_bytes_measured": int(peak_dynamic),
-                     "workspace_bytes": int(rast.workspace(g, my_cams[0]).nbytes),
+            "vram": {"peak_dynamic_bytes_per_frame": int(frame_vram["peak_dynamic_bytes"]),
+                     "workspace_bytes_per_frame": int(frame_vram["workspace_bytes"]),
+                     "workspace_bytes_in_flight": int(inflight_bytes),
                      "reference_model_3sigma_bytes": int(model3s),
                      "static_scene_bytes": int(static_bytes),
                      "tile_entries_per_view": E},

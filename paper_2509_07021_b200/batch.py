@@ -47,10 +47,11 @@ class PinnedScene:
 class BatchRenderer:
     """render_views(pinned_scene, cams) -> list of (H, W, 3) float32 host arrays."""
 
-    def __init__(self, rast: Rasterizer | None = None, device="cuda"):
+    def __init__(self, rast: Rasterizer | None = None, device="cuda", streams: int = 4):
         self.rast = rast or Rasterizer(device=device)
         self.device = torch.device(device)
         self.copy_stream = torch.cuda.Stream(device=self.device)
+        self.streams = [torch.cuda.Stream(device=self.device) for _ in range(max(streams, 1))]
         self._host = {}
 
     def _host_buf(self, k, shape):
@@ -61,23 +62,30 @@ class BatchRenderer:
         return buf
 
     def render_views(self, scene: PinnedScene, cams, background=(0.0, 0.0, 0.0), check=False):
-        g = scene.upload(self.device)
+        """Upload the scene, render every view (spread over the render streams
+        so binning of one view overlaps the raster of another), copy each
+        image back as soon as it is done; returns the pinned host images."""
         main = torch.cuda.current_stream(self.device)
+        g = scene.upload(self.device)
+        up = torch.cuda.Event()
+        up.record(main)
         outs = []
-        imgs = []
         for k, cam in enumerate(cams):
-            frame = self.rast.forward(g, cam, background, check=check)
-            img = frame.img
-            done = torch.cuda.Event()
-            done.record(main)
+            s = self.streams[k % len(self.streams)]
+            s.wait_event(up)
+            with torch.cuda.stream(s):
+                img = self.rast.forward(g, cam, background, check=check).img
+                done = torch.cuda.Event()
+                done.record(s)
             host = self._host_buf(k, tuple(img.shape))
             with torch.cuda.stream(self.copy_stream):
                 self.copy_stream.wait_event(done)
                 host.copy_(img, non_blocking=True)
                 img.record_stream(self.copy_stream)
-            imgs.append(img)
             outs.append(host)
         main.wait_stream(self.copy_stream)
+        for s in self.streams:
+            main.wait_stream(s)
         return outs
 
     @staticmethod

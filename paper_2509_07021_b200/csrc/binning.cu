@@ -282,11 +282,11 @@ __global__ void ranges_fix(uint2* __restrict__ ranges, int n_tiles) {
 // Final location of the sorted values (which ping-pong buffer).
 bool final_in_alt(const Layout& lo) {
   int passes = lo.sort_mode == SGS_SORT_KEY64 ? (32 + tile_sort_bits(lo.n_tiles) + 7) / 8
-                                              : tile_sort_passes(lo.n_super);
+                                              : super_sort_passes(lo.n_super);
   return (passes & 1) != 0;
 }
 
-template <typename KT, int IPT, bool kSuper>
+template <typename KT, int IPT, int RBITS, bool kSuper>
 static int bin_entries(const SgsCam& cam, const sgs_workspace* ws, const Layout& lo, const uint32_t* perm,
                        int key_bits, int tile_shift, cudaStream_t st) {
   Counters* ctr = at<Counters>(ws, lo.counters);
@@ -308,7 +308,7 @@ static int bin_entries(const SgsCam& cam, const sgs_workspace* ws, const Layout&
       at<unsigned long long>(ws, lo.offsets), cam, lo.super_x, cap, &ctr->n_bin, k0, v0);
   SGS_LAUNCH_CHECK("emit_entries");
   bool alt = false;
-  int rc = radix_sort_pairs<KT, IPT>(k0, v0, k1, v1, &ctr->n_sort, cap, key_bits, at<uint32_t>(ws, lo.hist),
+  int rc = radix_sort_pairs<KT, IPT, RBITS>(k0, v0, k1, v1, &ctr->n_sort, cap, key_bits, at<uint32_t>(ws, lo.hist),
                                      at<uint32_t>(ws, lo.status), &ctr->part_counter[8], &alt, st, false,
                                      RsRangeOut{ranges, tile_shift}, kSuper ? 16 : 0, kSuper);
   if (rc) return rc;
@@ -334,7 +334,7 @@ int launch_bin(const SgsCam& cam, const sgs_workspace* ws, const Layout& lo, cud
     SGS_LAUNCH_CHECK("set_count");
     bool alt = false;
     // depth keys are 31-bit (0x7fffffff = not emitting): 4 passes over N
-    int rc = radix_sort_pairs<uint32_t, kDepthSortIPT>(ka, ia, kb, ib, &ctr->n_depth, n, 31, at<uint32_t>(ws, lo.hist),
+    int rc = radix_sort_pairs<uint32_t, kDepthSortIPT, 8>(ka, ia, kb, ib, &ctr->n_depth, n, 31, at<uint32_t>(ws, lo.hist),
                                                         at<uint32_t>(ws, lo.status), &ctr->part_counter[0], &alt, st,
                                                         true);
     if (rc) return rc;
@@ -342,19 +342,21 @@ int launch_bin(const SgsCam& cam, const sgs_workspace* ws, const Layout& lo, cud
     rc = launch_scan(at<uint32_t>(ws, lo.super_touched), perm, n, cap, block_sums, offsets, ctr, st);
     if (rc) return rc;
     // keys (super_id << 16 | 16-bit tile mask), sorted on the super id bits only
-    return bin_entries<uint32_t, kTileSortIPT, true>(cam, ws, lo, perm, tile_sort_bits(lo.n_super), 16, st);
+    const int sbits = tile_sort_bits(lo.n_super);
+    if (sbits <= 9) return bin_entries<uint32_t, kTileSortIPT, 9, true>(cam, ws, lo, perm, sbits, 16, st);
+    return bin_entries<uint32_t, kTileSortIPT, 8, true>(cam, ws, lo, perm, sbits, 16, st);
   }
   int rc = launch_scan(at<uint32_t>(ws, lo.tiles_touched), nullptr, n, cap, block_sums, offsets, ctr, st);
   if (rc) return rc;
-  return bin_entries<unsigned long long, kKey64SortIPT, false>(cam, ws, lo, nullptr, 32 + tile_sort_bits(lo.n_tiles),
-                                                               32, st);
+  return bin_entries<unsigned long long, kKey64SortIPT, 8, false>(cam, ws, lo, nullptr,
+                                                                  32 + tile_sort_bits(lo.n_tiles), 32, st);
 }
 
 // Generic 64-bit pair sort exported through the ABI (for tests / tools).
 uint64_t sort_u64_temp_bytes(uint64_t n, int bits) {
   const uint64_t parts = rs_parts<unsigned long long, kKey64SortIPT>(n);
   const int passes = (bits + 7) / 8;
-  return align256(n * 8) + align256(n * 4) + 16 * 256 * 4 + 256 + parts * 256 * 4 * passes + 64;
+  return align256(n * 8) + align256(n * 4) + 16 * 512 * 4 + 256 + parts * 512 * 4 * passes + 64;
 }
 
 int launch_sort_u64(unsigned long long* keys, uint32_t* vals, uint32_t n, int bits, void* temp, uint64_t temp_bytes,
@@ -370,14 +372,14 @@ int launch_sort_u64(unsigned long long* keys, uint32_t* vals, uint32_t n, int bi
   auto* v1 = reinterpret_cast<uint32_t*>(p);
   p += align256((uint64_t)n * 4);
   uint32_t* hist = reinterpret_cast<uint32_t*>(p);
-  p += 16 * 256 * 4;
+  p += 16 * 512 * 4;
   uint32_t* meta = reinterpret_cast<uint32_t*>(p);  // [0] = n, [1..16] tickets
   p += 256;
   uint32_t* status = reinterpret_cast<uint32_t*>(p);
   set_count<<<1, 1, 0, st>>>(meta, n);
   SGS_LAUNCH_CHECK("set_count");
   bool alt = false;
-  int rc = radix_sort_pairs<unsigned long long, kKey64SortIPT>(keys, vals, k1, v1, meta, n, bits, hist, status,
+  int rc = radix_sort_pairs<unsigned long long, kKey64SortIPT, 8>(keys, vals, k1, v1, meta, n, bits, hist, status,
                                                                meta + 1, &alt, st);
   if (rc) return rc;
   if (alt) {

@@ -75,6 +75,12 @@ inline int tile_sort_bits(int n_tiles) { return n_tiles <= 1 ? 1 : ceil_log2_u64
 
 inline int tile_sort_passes(int n_tiles) { return (tile_sort_bits(n_tiles) + 7) / 8; }
 
+// super-tile id sort: one 9-bit pass when the ids fit (1080p: 510 cells), else 8-bit passes
+inline int super_sort_passes(int n_super) {
+  const int b = tile_sort_bits(n_super);
+  return b <= 9 ? 1 : (b + 7) / 8;
+}
+
 inline uint64_t align256(uint64_t x) { return (x + 255) & ~uint64_t(255); }
 
 inline int make_layout(const sgs_workspace* ws, Layout* lo) {
@@ -127,13 +133,13 @@ inline int make_layout(const sgs_workspace* ws, Layout* lo) {
   lo->ent_val = take(cap * 4);
   lo->ent_val_alt = take(cap * 4);
   lo->ranges = take((uint64_t)lo->n_tiles * 8);
-  lo->hist = take(16 * 256 * 4);
+  lo->hist = take(16 * 512 * 4);
   // onesweep look-back status: per pass, per partition, 256 digits of u32
-  int tile_passes = k64 ? (32 + tile_sort_bits(lo->n_tiles) + 7) / 8 : tile_sort_passes(lo->n_super);
+  int tile_passes = k64 ? (32 + tile_sort_bits(lo->n_tiles) + 7) / 8 : super_sort_passes(lo->n_super);
   int ipt = k64 ? kKey64SortIPT : kTileSortIPT;
   uint64_t parts_tile = (cap + (uint64_t)kRadixThreads * ipt - 1) / ((uint64_t)kRadixThreads * ipt);
   uint64_t parts_depth = (n + (uint64_t)kRadixThreads * kDepthSortIPT - 1) / ((uint64_t)kRadixThreads * kDepthSortIPT);
-  uint64_t st_tile = parts_tile * 256 * 4 * (uint64_t)tile_passes;
+  uint64_t st_tile = parts_tile * 512 * 4 * (uint64_t)tile_passes;
   uint64_t st_depth = k64 ? 0 : parts_depth * 256 * 4 * 4;
   lo->status_bytes = st_tile > st_depth ? st_tile : st_depth;
   lo->status = take(lo->status_bytes);

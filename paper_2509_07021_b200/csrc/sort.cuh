@@ -1,21 +1,22 @@
 // sort.cuh -- stable LSD radix sort of (key, u32 value) pairs, onesweep style:
-// one up-front histogram kernel computes every pass's 256-bin digit counts
-// in a single (vectorised) read of the keys, then each 8-bit pass is ONE
-// kernel that ranks a tile of keys in shared memory (warp ballot-match +
-// per-warp digit counters, order-preserving), publishes its per-digit
-// counts, resolves its global digit offsets by decoupled look-back over
-// earlier tiles, and scatters keys / values through shared memory so the
-// global writes are runs of consecutive addresses.
+// one up-front histogram kernel computes every pass's digit counts in a
+// single (vectorised) read of the keys, then each pass is ONE kernel that
+// ranks a tile of keys in shared memory (warp ballot-match + per-warp digit
+// counters, order-preserving), publishes its per-digit counts, resolves its
+// global digit offsets by decoupled look-back over earlier tiles, and
+// scatters keys / values through shared memory so the global writes are runs
+// of consecutive addresses.  Digits are RBITS wide (8 or 9 bits: a 9-bit key
+// range -- the super-tile ids of a 1080p frame -- sorts in a single pass).
 //
 // Persistent: the grid is at most the number of co-resident CTAs and tiles
 // are claimed in order from an atomic ticket, so look-back only ever waits on
 // a CTA that is running.  Item counts are read from device memory, so a whole
 // frame can be enqueued (or graph-captured) without a host round trip.
 //
-// The final pass of a tile-key sort can skip writing keys and instead emits
-// the per-tile [start, end) ranges: a tile's entries form one contiguous run
-// inside each CTA's shared-memory order, so each run contributes one
-// atomicMin / atomicMax (K4 fused into K3).
+// The final pass of a tile-key sort can also emit the per-cell [start, end)
+// ranges: a cell's entries form one contiguous run inside each CTA's
+// shared-memory order, so each run contributes one atomicMin / atomicMax
+// (K4 fused into K3).
 #pragma once
 
 #include <algorithm>
@@ -28,17 +29,23 @@ namespace sgs {
 // status word: [31:30] flag (0 empty, 1 aggregate, 2 inclusive prefix), [29:0] count
 enum : uint32_t { kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kCountMask = (1u << 30) - 1 };
 
-template <typename K>
+constexpr int kRsThreads = 512;  // 16 warps per CTA
+constexpr int kRsWarps = kRsThreads / 32;
+constexpr int kRsMaxRadix = 512;
+constexpr int kLookback = 32;    // predecessors examined per look-back step
+
+template <typename K, int RBITS>
 __device__ __forceinline__ uint32_t rs_digit(K k, int shift) {
-  return (uint32_t)(k >> shift) & 0xffu;
+  return (uint32_t)(k >> shift) & ((1u << RBITS) - 1u);
 }
 
-// Lanes of the warp holding the same 8-bit digit, from 8 ballots.  Lanes
-// outside `valid` never match.
-__device__ __forceinline__ uint32_t match_digit8(uint32_t d, uint32_t valid) {
+// Lanes of the warp holding the same RBITS-bit digit, from RBITS ballots.
+// Lanes outside `valid` never match.
+template <int RBITS>
+__device__ __forceinline__ uint32_t match_digit(uint32_t d, uint32_t valid) {
   uint32_t peers = valid;
 #pragma unroll
-  for (int b = 0; b < 8; ++b) {
+  for (int b = 0; b < RBITS; ++b) {
     const uint32_t bit = (d >> b) & 1u;
     const uint32_t m = __ballot_sync(0xffffffffu, bit);
     peers &= bit ? m : ~m;
@@ -52,16 +59,17 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   return m;
 }
 
-// Histogram of `num_passes` 8-bit digits; hist is num_passes x 256 u32 and
-// must be zeroed.  n = min(*n_ptr, n_cap).  16-byte vector loads.
-template <typename K>
+// Histogram of `num_passes` RBITS-bit digits starting at begin_bit; hist is
+// num_passes x 2^RBITS u32 and must be zeroed.  n = min(*n_ptr, n_cap).
+template <typename K, int RBITS>
 __global__ void __launch_bounds__(256) rs_histogram(const K* __restrict__ keys, const uint32_t* n_ptr, uint32_t n_cap,
                                                     int begin_bit, int num_passes, uint32_t* __restrict__ hist) {
-  extern __shared__ uint32_t sh[];  // [num_passes][8 warps][256]
+  constexpr int R = 1 << RBITS;
+  extern __shared__ uint32_t sh[];  // [num_passes][8 warps][R]
   constexpr int V = 16 / sizeof(K);
   const uint32_t n = min(*n_ptr, n_cap);
   const int w = threadIdx.x >> 5;
-  for (int j = threadIdx.x; j < num_passes * 8 * 256; j += 256) sh[j] = 0;
+  for (int j = threadIdx.x; j < num_passes * 8 * R; j += 256) sh[j] = 0;
   __syncthreads();
   const uint32_t nvec = n / V;
   const uint4* kv = reinterpret_cast<const uint4*>(keys);
@@ -70,26 +78,30 @@ __global__ void __launch_bounds__(256) rs_histogram(const K* __restrict__ keys, 
     const K* ks = reinterpret_cast<const K*>(&raw);
 #pragma unroll
     for (int v = 0; v < V; ++v)
-      for (int p = 0; p < num_passes; ++p) atomicAdd(&sh[(p * 8 + w) * 256 + rs_digit(ks[v], begin_bit + 8 * p)], 1u);
+      for (int p = 0; p < num_passes; ++p)
+        atomicAdd(&sh[(p * 8 + w) * R + rs_digit<K, RBITS>(ks[v], begin_bit + RBITS * p)], 1u);
   }
   for (uint32_t i = nvec * V + blockIdx.x * 256u + threadIdx.x; i < n; i += gridDim.x * 256u) {
     K k = keys[i];
-    for (int p = 0; p < num_passes; ++p) atomicAdd(&sh[(p * 8 + w) * 256 + rs_digit(k, begin_bit + 8 * p)], 1u);
+    for (int p = 0; p < num_passes; ++p)
+      atomicAdd(&sh[(p * 8 + w) * R + rs_digit<K, RBITS>(k, begin_bit + RBITS * p)], 1u);
   }
   __syncthreads();
-  for (int j = threadIdx.x; j < num_passes * 256; j += 256) {
-    const int p = j >> 8, d = j & 255;
+  for (int j = threadIdx.x; j < num_passes * R; j += 256) {
+    const int p = j / R, d = j % R;
     uint32_t v = 0;
 #pragma unroll
-    for (int ww = 0; ww < 8; ++ww) v += sh[(p * 8 + ww) * 256 + d];
+    for (int ww = 0; ww < 8; ++ww) v += sh[(p * 8 + ww) * R + d];
     if (v) atomicAdd(&hist[j], v);
   }
 }
 
-// In-place exclusive scan of each pass's 256 bins (one CTA per pass).
-__global__ void __launch_bounds__(256) rs_scan_hist(uint32_t* hist) {
-  __shared__ uint32_t warp_tot[8];
-  uint32_t* h = hist + blockIdx.x * 256;
+// In-place exclusive scan of each pass's 2^RBITS bins (one CTA per pass).
+template <int RBITS>
+__global__ void __launch_bounds__(1 << RBITS) rs_scan_hist(uint32_t* hist) {
+  constexpr int R = 1 << RBITS;
+  __shared__ uint32_t warp_tot[R / 32];
+  uint32_t* h = hist + blockIdx.x * R;
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   uint32_t v = h[t], x = v;
 #pragma unroll
@@ -104,37 +116,36 @@ __global__ void __launch_bounds__(256) rs_scan_hist(uint32_t* hist) {
   h[t] = pre + x - v;
 }
 
-constexpr int kRsThreads = 512;  // 16 warps per CTA
-constexpr int kRsWarps = kRsThreads / 32;
-
-template <typename K, int IPT>
+template <typename K, int IPT, int RBITS>
 struct RsSmem {
   static constexpr int kTile = kRsThreads * IPT;
-  uint32_t warp_hist[kRsWarps][256];
-  uint32_t digit_start[256];
-  uint32_t global_base[256];
-  uint32_t warp_tot[8];
+  static constexpr int R = 1 << RBITS;
+  uint32_t warp_hist[kRsWarps][R];
+  uint32_t digit_start[R];
+  uint32_t global_base[R];
+  uint32_t warp_tot[kRsWarps];
   uint32_t part;
   uint32_t vals[kTile];
   K keys[kTile];
 };
 
 struct RsRangeOut {
-  uint2* ranges;   // per-tile [start, end), pre-set to (0xffffffff, 0); null = none
-  int tile_shift;  // tile id = key >> tile_shift
+  uint2* ranges;   // per-cell [start, end), pre-set to (0xffffffff, 0); null = none
+  int tile_shift;  // cell id = key >> tile_shift
 };
 
-// One 8-bit pass.  status: nparts x 256 u32, zeroed; ticket zeroed.
+// One pass.  status: nparts x 2^RBITS u32, zeroed; ticket zeroed.
 // vin == nullptr means values are the item indices (first pass of an argsort).
-// kout == nullptr skips the key writes (last pass).
-template <typename K, int IPT>
+// kout == nullptr skips the key writes.
+template <typename K, int IPT, int RBITS>
 __global__ void __launch_bounds__(kRsThreads) rs_onesweep(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                           K* __restrict__ kout, uint32_t* __restrict__ vout,
                                                           const uint32_t* n_ptr, uint32_t n_cap, int shift,
                                                           const uint32_t* __restrict__ pass_base, uint32_t* status,
                                                           uint32_t* ticket, RsRangeOut rout) {
-  using S = RsSmem<K, IPT>;
+  using S = RsSmem<K, IPT, RBITS>;
   constexpr int kTile = S::kTile;
+  constexpr int R = S::R;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   S& s = *reinterpret_cast<S*>(smem_raw);
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
@@ -144,7 +155,7 @@ __global__ void __launch_bounds__(kRsThreads) rs_onesweep(const K* __restrict__ 
 
   for (;;) {
     if (t == 0) s.part = atomicAdd(ticket, 1u);
-    for (int j = t; j < kRsWarps * 256; j += kRsThreads) (&s.warp_hist[0][0])[j] = 0;
+    for (int j = t; j < kRsWarps * R; j += kRsThreads) (&s.warp_hist[0][0])[j] = 0;
     __syncthreads();
     const uint32_t part = s.part;
     if (part >= nparts) return;
@@ -165,8 +176,8 @@ __global__ void __launch_bounds__(kRsThreads) rs_onesweep(const K* __restrict__ 
     for (int i = 0; i < IPT; ++i) {
       const uint32_t idx = base + i * 32 + lane;
       const bool valid = idx < n;
-      const uint32_t d = rs_digit(keys[i], shift);
-      const uint32_t peers = match_digit8(d, __ballot_sync(0xffffffffu, valid));
+      const uint32_t d = rs_digit<K, RBITS>(keys[i], shift);
+      const uint32_t peers = match_digit<RBITS>(d, __ballot_sync(0xffffffffu, valid));
       const int leader = __ffs(peers) - 1;
       uint32_t old = 0;
       if (valid && lane == leader) old = atomicAdd(&s.warp_hist[w][d], (uint32_t)__popc(peers));
@@ -178,16 +189,16 @@ __global__ void __launch_bounds__(kRsThreads) rs_onesweep(const K* __restrict__ 
     }
     __syncthreads();
 
-    // ---- per digit (threads 0..255): scan over warps, publish, look back
+    // ---- per digit (threads 0..R-1): scan over warps, publish, look back
     uint32_t run = 0, wexcl = 0;
-    if (t < 256) {
+    if (t < R) {
 #pragma unroll
       for (int ww = 0; ww < kRsWarps; ++ww) {
         const uint32_t c = s.warp_hist[ww][t];
         s.warp_hist[ww][t] = run;
         run += c;
       }
-      atomicExch(status + (size_t)part * 256 + t, (part == 0 ? kFlagInc : kFlagAgg) | run);
+      atomicExch(status + (size_t)part * R + t, (part == 0 ? kFlagInc : kFlagAgg) | run);
       uint32_t x = run;  // block exclusive scan of the digit counts -> digit_start
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -198,7 +209,7 @@ __global__ void __launch_bounds__(kRsThreads) rs_onesweep(const K* __restrict__ 
       wexcl = x - run;
     }
     __syncthreads();
-    if (t < 256) {
+    if (t < R) {
       uint32_t pre = 0;
       for (int i = 0; i < w; ++i) pre += s.warp_tot[i];
       s.digit_start[t] = pre + wexcl;
@@ -207,13 +218,12 @@ __global__ void __launch_bounds__(kRsThreads) rs_onesweep(const K* __restrict__ 
         // windowed decoupled look-back: kLookback predecessors are loaded at
         // once, summed from the nearest until the first inclusive prefix; a
         // not-yet-published predecessor restarts the window there.
-        constexpr int kLookback = 16;
         int64_t p = (int64_t)part - 1;
         for (;;) {
           uint32_t v[kLookback];
 #pragma unroll
           for (int j = 0; j < kLookback; ++j)
-            v[j] = (p - j >= 0) ? *reinterpret_cast<volatile uint32_t*>(status + (size_t)(p - j) * 256 + t)
+            v[j] = (p - j >= 0) ? *reinterpret_cast<volatile uint32_t*>(status + (size_t)(p - j) * R + t)
                                 : (uint32_t)kFlagInc;
           int used = 0;
           bool done = false;
@@ -231,7 +241,7 @@ __global__ void __launch_bounds__(kRsThreads) rs_onesweep(const K* __restrict__ 
           if (done) break;
           p -= used;
         }
-        atomicExch(status + (size_t)part * 256 + t, kFlagInc | (excl + run));
+        atomicExch(status + (size_t)part * R + t, kFlagInc | (excl + run));
       }
       s.global_base[t] = pass_base[t] + excl;
     }
@@ -242,7 +252,7 @@ __global__ void __launch_bounds__(kRsThreads) rs_onesweep(const K* __restrict__ 
     for (int i = 0; i < IPT; ++i) {
       const uint32_t idx = base + i * 32 + lane;
       if (idx < n) {
-        const uint32_t d = rs_digit(keys[i], shift);
+        const uint32_t d = rs_digit<K, RBITS>(keys[i], shift);
         const uint32_t pos = s.digit_start[d] + s.warp_hist[w][d] + rank[i];
         s.keys[pos] = keys[i];
         s.vals[pos] = vals[i];
@@ -252,7 +262,7 @@ __global__ void __launch_bounds__(kRsThreads) rs_onesweep(const K* __restrict__ 
     const uint32_t cnt = min((uint32_t)kTile, n - part * kTile);
     for (uint32_t j = t; j < cnt; j += kRsThreads) {
       const K k = s.keys[j];
-      const uint32_t d = rs_digit(k, shift);
+      const uint32_t d = rs_digit<K, RBITS>(k, shift);
       const uint32_t g = s.global_base[d] + j - s.digit_start[d];
       if (kout) kout[g] = k;
       vout[g] = s.vals[j];
@@ -276,41 +286,49 @@ inline uint64_t rs_parts(uint64_t n) {
 }
 
 // Sort `n_cap`-bounded pairs (count in *n_ptr on the device) over key bits
-// [begin_bit, begin_bit + bits); lower bits travel with the key unsorted.  Ping-pongs between (k0, v0) and (k1, v1); *result_in_alt says
-// whether the result is in (k1, v1).  iota_values: the input values are the
-// item indices (v0 is not read).  With `rout.ranges`, the last pass writes
-// only values plus the tile ranges.  hist: 16*256 u32; status:
-// parts*256*passes u32; tickets: >= passes u32; all zeroed here.
-template <typename K, int IPT>
+// [begin_bit, begin_bit + bits) in ceil(bits / RBITS) passes; lower bits
+// travel with the key unsorted.  Ping-pongs between (k0, v0) and (k1, v1);
+// *result_in_alt says whether the result is in (k1, v1).  iota_values: the
+// input values are the item indices (v0 is not read).  With `rout.ranges`,
+// the last pass also writes the cell ranges (and skips its key writes unless
+// keep_last_keys).  hist: 16*512 u32; status: parts*512*passes u32; tickets:
+// >= passes u32; all zeroed here.
+template <typename K, int IPT, int RBITS>
 int radix_sort_pairs(K* k0, uint32_t* v0, K* k1, uint32_t* v1, const uint32_t* n_ptr, uint32_t n_cap, int bits,
                      uint32_t* hist, uint32_t* status, uint32_t* tickets, bool* result_in_alt, cudaStream_t st,
                      bool iota_values = false, RsRangeOut rout = RsRangeOut{nullptr, 0}, int begin_bit = 0,
                      bool keep_last_keys = false) {
-  const int passes = (bits + 7) / 8;
+  constexpr int R = 1 << RBITS;
+  const int passes = (bits + RBITS - 1) / RBITS;
   const uint64_t parts = rs_parts<K, IPT>(n_cap);
   *result_in_alt = false;
   if (n_cap == 0 || passes == 0) return SGS_OK;
-  SGS_CUDA(cudaMemsetAsync(hist, 0, (size_t)passes * 256 * 4, st));
-  SGS_CUDA(cudaMemsetAsync(status, 0, (size_t)parts * 256 * 4 * passes, st));
+  SGS_CUDA(cudaMemsetAsync(hist, 0, (size_t)passes * R * 4, st));
+  SGS_CUDA(cudaMemsetAsync(status, 0, (size_t)parts * R * 4 * passes, st));
   SGS_CUDA(cudaMemsetAsync(tickets, 0, (size_t)passes * 4, st));
   const int sms = device_sm_count();
   constexpr int V = 16 / sizeof(K);
   int hgrid = (int)std::min<uint64_t>((n_cap / V + 256 * 8 - 1) / (256 * 8), (uint64_t)sms * 4);
   if (hgrid < 1) hgrid = 1;
-  const size_t hsmem = (size_t)passes * 8 * 256 * 4;
-  SGS_CUDA(cudaFuncSetAttribute(rs_histogram<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-  rs_histogram<K><<<hgrid, 256, hsmem, st>>>(k0, n_ptr, n_cap, begin_bit, passes, hist);
+  const size_t hsmem = (size_t)passes * 8 * R * 4;
+  static bool hattr = false;
+  if (!hattr) {
+    SGS_CUDA(cudaFuncSetAttribute(rs_histogram<K, RBITS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    hattr = true;
+  }
+  rs_histogram<K, RBITS><<<hgrid, 256, hsmem, st>>>(k0, n_ptr, n_cap, begin_bit, passes, hist);
   SGS_LAUNCH_CHECK("rs_histogram");
-  rs_scan_hist<<<passes, 256, 0, st>>>(hist);
+  rs_scan_hist<RBITS><<<passes, R, 0, st>>>(hist);
   SGS_LAUNCH_CHECK("rs_scan_hist");
-  const size_t smem = sizeof(RsSmem<K, IPT>);
+  const size_t smem = sizeof(RsSmem<K, IPT, RBITS>);
   static bool attr_set = false;
   if (!attr_set) {
-    SGS_CUDA(cudaFuncSetAttribute(rs_onesweep<K, IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SGS_CUDA(cudaFuncSetAttribute(rs_onesweep<K, IPT, RBITS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
     attr_set = true;
   }
   static int per_sm = 0;
-  if (!per_sm) per_sm = resident_ctas_per_sm((const void*)rs_onesweep<K, IPT>, kRsThreads, smem);
+  if (!per_sm) per_sm = resident_ctas_per_sm((const void*)rs_onesweep<K, IPT, RBITS>, kRsThreads, smem);
   if (per_sm < 1) {
     set_error("onesweep kernel cannot be resident");
     return SGS_E_CUDA;
@@ -322,11 +340,10 @@ int radix_sort_pairs(K* k0, uint32_t* v0, K* k1, uint32_t* v1, const uint32_t* n
   uint32_t* vb = v1;
   for (int p = 0; p < passes; ++p) {
     const bool last = p + 1 == passes;
-    rs_onesweep<K, IPT><<<grid, kRsThreads, smem, st>>>(ka, (p == 0 && iota_values) ? nullptr : va,
-                                                  (last && rout.ranges && !keep_last_keys) ? nullptr : kb, vb, n_ptr,
-                                                  n_cap, begin_bit + 8 * p,
-                                                  hist + 256 * p, status + (size_t)parts * 256 * p, tickets + p,
-                                                  last ? rout : RsRangeOut{nullptr, 0});
+    rs_onesweep<K, IPT, RBITS><<<grid, kRsThreads, smem, st>>>(
+        ka, (p == 0 && iota_values) ? nullptr : va, (last && rout.ranges && !keep_last_keys) ? nullptr : kb, vb,
+        n_ptr, n_cap, begin_bit + RBITS * p, hist + R * p, status + (size_t)parts * R * p, tickets + p,
+        last ? rout : RsRangeOut{nullptr, 0});
     SGS_LAUNCH_CHECK("rs_onesweep");
     std::swap(ka, kb);
     std::swap(va, vb);

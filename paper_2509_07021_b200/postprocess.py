@@ -72,13 +72,14 @@ def estimate_vram(scene, cam, tile_px: int = 16) -> VramEstimate:
                         dynamic_bytes=vis * SPLAT2D_RECORD_BYTES + entries * TILE_ENTRY_BYTES)
 
 
-def measured_render_vram(p, cam) -> dict:
+def measured_render_vram(p, cam, rast=None) -> dict:
     """Bytes this renderer allocates for one frame of `p` through `cam`: the
     workspace (projected records, depth-sort and tile-sort buffers, key/value
     entries, ranges) plus the output image / transmittance / contributor
     buffers, and the peak torch allocation seen while rendering."""
-    rast = rasterizer()
-    g = _upload(p)
+    from .rasterizer import GaussianTensors
+    rast = rast or rasterizer()
+    g = p if isinstance(p, GaussianTensors) else _upload(p)
     dev = g.device
     torch.cuda.synchronize(dev)
     base = torch.cuda.memory_allocated(dev)

@@ -184,15 +184,19 @@ class Rasterizer:
         return int(min(MAX_CAPACITY, max(1 << 16, 4 * g.n)))
 
     def workspace(self, g, cam, private=False, capacity=None) -> Workspace:
+        """The shared workspace for this (scene size, image size) on the
+        current stream (one per stream, so views on different streams render
+        concurrently), or a private one."""
         key = self._key(g, cam)
         cap = capacity if capacity is not None else self._capacity(key, g)
         if private:
             return Workspace(*key[:4], cap, self.sort_mode, self.device)
-        ws = self._shared.get(key)
+        skey = key + (_stream_ptr(),)
+        ws = self._shared.get(skey)
         if ws is None or ws.capacity < cap:
-            self._shared.pop(key, None)
+            self._shared.pop(skey, None)
             ws = Workspace(*key[:4], cap, self.sort_mode, self.device)
-            self._shared[key] = ws
+            self._shared[skey] = ws
         return ws
 
     def release(self):
