@@ -191,7 +191,7 @@ int sgs_export_bins(const sgs_workspace* ws, const sgs_camera* cam, uint64_t* ke
 
 /* Export per-primitive preprocess outputs (device buffers, length N):
  * depth bits, packed tile rect (tx0|tx1<<16, ty0|ty1<<16), tile counts and
- * the 12-float raster record [geo(4), conic(4), color(4)]. */
+ * the 16-float raster record [geo(4), conic(4), eigen form(4), color(4)]. */
 int sgs_export_projected(const sgs_workspace* ws, uint32_t* depth_bits,
                          uint32_t* rect, uint32_t* tiles_touched, float* records, void* stream);
 

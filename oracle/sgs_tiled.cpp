@@ -89,21 +89,24 @@ void oracle_preprocess(int64_t n, int L, const float* pos, const float* quat, co
     depth_bits[i] = cnt ? sgs_float_to_bits(pr.depth) : 0x7fffffffu;
     rect[2 * i] = (uint32_t)(pr.tx0 & 0xffff) | ((uint32_t)(pr.tx1 & 0xffff) << 16);
     rect[2 * i + 1] = (uint32_t)(pr.ty0 & 0xffff) | ((uint32_t)(pr.ty1 & 0xffff) << 16);
-    float* rec = records + 12 * i;
-    memset(rec, 0, 12 * sizeof(float));
+    float* rec = records + 16 * i;
+    memset(rec, 0, 16 * sizeof(float));
     if (cnt) {
       ++emit;
       const SgsSpan sp = sgs_span(g, k);
-      float span2[2];
+      float span2[3];
       sgs_span_cache(&sp, &k[3], span2);
       float c_pre[3], c[3];
       sgs_color(pos + 3 * i, diffuse + 3 * i, axis + (size_t)i * L * 3, sharp + (size_t)i * L, amp + (size_t)i * L * 3,
                 lmask + (size_t)i * L, L, &cam, c_pre, c);
+      float e4[4];
+      sgs_pack_eig(&pr, e4);
       memcpy(rec, g, 16);
       memcpy(rec + 4, k, 16);
-      rec[8] = c[0];
-      rec[9] = c[1];
-      rec[10] = c[2];
+      memcpy(rec + 8, e4, 16);
+      rec[12] = c[0];
+      rec[13] = c[1];
+      rec[14] = c[2];
     }
   }
   counts[0] = vis;
@@ -129,7 +132,7 @@ void oracle_bin(int64_t n, const uint32_t* depth_bits, const uint32_t* rect, con
     if (!tiles_touched[i]) continue;
     int tx0 = (int)(rect[2 * i] & 0xffff), tx1 = (int)(int16_t)(rect[2 * i] >> 16);
     int ty0 = (int)(rect[2 * i + 1] & 0xffff), ty1 = (int)(int16_t)(rect[2 * i + 1] >> 16);
-    const float* g = records + 12 * i;
+    const float* g = records + 16 * i;
     const float* k = g + 4;
     const SgsSpan sp = sgs_span(g, k);
     for (int ty = ty0; ty <= ty1; ++ty) {
@@ -168,16 +171,18 @@ void oracle_raster_forward(const uint32_t* ranges, const uint32_t* vals, const f
       float T = 1.0f, C[3] = {0, 0, 0};
       uint32_t nc = 0;
       for (uint32_t j = s; j < e; ++j) {
-        const float* r = records + 12 * (size_t)vals[j];
+        const float* r = records + 16 * (size_t)vals[j];
         const float dx = fx - r[0], dy = fy - r[1];
-        const float p = dx * (r[4] * dx + r[5] * dy) + r[6] * dy * dy;
+        // eigen form, same operation order as the GPU raster
+        const float t1 = fmaf(r[9], dy, r[8] * dx), t2 = fmaf(r[8], dy, -(r[9] * dx));
+        const float p = fmaf(r[10] * t1, t1, (r[11] * t2) * t2);
         if (p < r[3]) continue;
         const float a = r[2] * exp2f(p);
         const float alpha = std::min(a, SGS_ALPHA_MAX);
         const float Tn = T * (a < SGS_ALPHA_MAX ? 1.0f - a : SGS_ONE_MINUS_ALPHA_MAX);
         if (Tn < SGS_T_KEEP) break;
         const float w = alpha * T;
-        for (int c = 0; c < 3; ++c) C[c] += w * r[8 + c];
+        for (int c = 0; c < 3; ++c) C[c] += w * r[12 + c];
         if (weight_sums) weight_sums[vals[j]] += w;
         T = Tn;
         nc = j - s + 1;
@@ -209,9 +214,10 @@ void oracle_raster_backward(const uint32_t* ranges, const uint32_t* vals, const 
       kept.clear();
       double T = 1.0;
       for (uint32_t j = s; j < e; ++j) {
-        const float* r = records + 12 * (size_t)vals[j];
+        const float* r = records + 16 * (size_t)vals[j];
         const double dx = fx - r[0], dy = fy - r[1];
-        const double p = dx * ((double)r[4] * dx + (double)r[5] * dy) + (double)r[6] * dy * dy;
+        const double t1 = (double)r[8] * dx + (double)r[9] * dy, t2 = (double)r[8] * dy - (double)r[9] * dx;
+        const double p = (double)r[10] * t1 * t1 + (double)r[11] * t2 * t2;
         if (p < (double)r[3]) continue;
         const double G = exp2(p);
         const double a = (double)r[2] * G;
@@ -226,8 +232,8 @@ void oracle_raster_backward(const uint32_t* ranges, const uint32_t* vals, const 
       double S = T * (g0 * bg[0] + g1 * bg[1] + g2 * bg[2]);
       for (size_t q = kept.size(); q-- > 0;) {
         const Item& it = kept[q];
-        const float* r = records + 12 * (size_t)it.g;
-        const double cg = r[8] * g0 + r[9] * g1 + r[10] * g2;
+        const float* r = records + 16 * (size_t)it.g;
+        const double cg = r[12] * g0 + r[13] * g1 + r[14] * g2;
         const double w = it.alpha * it.T;
         const double om = 1.0 - it.alpha;
         const double dalpha = it.a < 0.99 ? (it.T * cg - S / om) : 0.0;

@@ -73,7 +73,7 @@ def preprocess(scene, cam, tile_rows=(0, 0), lowpass=0.3):
     r.depth_bits = np.zeros(n, np.uint32)
     r.rect = np.zeros((n, 2), np.uint32)
     r.tiles_touched = np.zeros(n, np.uint32)
-    r.records = np.zeros((n, 12), np.float32)
+    r.records = np.zeros((n, 16), np.float32)
     counts = np.zeros(2, np.int64)
     lib().oracle_preprocess(C.c_int64(n), C.c_int(L), _p(a["position"]), _p(a["quat"]),
                             _p(a["log_scale"]), _p(a["opacity"]), _p(a["diffuse"]),

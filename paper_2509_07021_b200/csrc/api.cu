@@ -274,9 +274,10 @@ int sgs_export_projected(const sgs_workspace* ws, uint32_t* depth_bits, uint32_t
   if (tiles_touched)
     SGS_CUDA(cudaMemcpyAsync(tiles_touched, at<uint32_t>(ws, lo.tiles_touched), n * 4, cudaMemcpyDeviceToDevice, st));
   if (records) {
-    SGS_CUDA(cudaMemcpy2DAsync(records, 48, at<float4>(ws, lo.rec_geo), 16, 16, n, cudaMemcpyDeviceToDevice, st));
-    SGS_CUDA(cudaMemcpy2DAsync(records + 4, 48, at<float4>(ws, lo.rec_con), 16, 16, n, cudaMemcpyDeviceToDevice, st));
-    SGS_CUDA(cudaMemcpy2DAsync(records + 8, 48, at<float4>(ws, lo.rec_col), 16, 16, n, cudaMemcpyDeviceToDevice, st));
+    SGS_CUDA(cudaMemcpy2DAsync(records, 64, at<float4>(ws, lo.rec_geo), 16, 16, n, cudaMemcpyDeviceToDevice, st));
+    SGS_CUDA(cudaMemcpy2DAsync(records + 4, 64, at<float4>(ws, lo.rec_con), 16, 16, n, cudaMemcpyDeviceToDevice, st));
+    SGS_CUDA(cudaMemcpy2DAsync(records + 8, 64, at<float4>(ws, lo.rec_eig), 16, 16, n, cudaMemcpyDeviceToDevice, st));
+    SGS_CUDA(cudaMemcpy2DAsync(records + 12, 64, at<float4>(ws, lo.rec_col), 16, 16, n, cudaMemcpyDeviceToDevice, st));
   }
   return SGS_OK;
 }

@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(256) emit_entries(const uint32_t* __restrict__
                                                     const uint2* __restrict__ rect,
                                                     const float4* __restrict__ rec_geo,
                                                     const float4* __restrict__ rec_con,
-                                                    const float2* __restrict__ rec_span,
+                                                    const float4* __restrict__ rec_span,
                                                     const uint32_t* __restrict__ depth_key,
                                                     const unsigned long long* __restrict__ offsets, SgsCam cam,
                                                     int super_x, uint32_t cap,
@@ -225,9 +225,9 @@ __global__ void __launch_bounds__(256) emit_entries(const uint32_t* __restrict__
       int rf[SGS_SUPER] = {0, 0, 0, 0}, rc[SGS_SUPER] = {0, 0, 0, 0};
       if (k < R) {
         const float4 g4 = rec_geo[og], c4 = rec_con[og];
-        const float2 s2 = rec_span[og];
+        const float4 s2 = rec_span[og];
         const float geo[4] = {g4.x, g4.y, g4.z, g4.w}, con[4] = {c4.x, c4.y, c4.z, c4.w};
-        const float span2[2] = {s2.x, s2.y};
+        const float span2[3] = {s2.x, s2.y, s2.z};
         const SgsSpan sp = sgs_span_cached(geo, con, span2);
         c = kSuper ? (uint32_t)sgs_super_row_spans(&sp, &cam, otx0, oty0, otx1, oty1, row, rf, rc, &first)
                    : (uint32_t)sgs_row_span(&sp, &cam, row, otx0, otx1, &first);
@@ -303,7 +303,7 @@ static int bin_entries(const SgsCam& cam, const sgs_workspace* ws, const Layout&
   SGS_LAUNCH_CHECK("ranges_init");
   emit_entries<KT, kSuper><<<persistent_grid(n, 256, 8), 256, 0, st>>>(
       perm, n, at<uint32_t>(ws, kSuper ? lo.super_touched : lo.tiles_touched), at<uint2>(ws, lo.rect),
-      at<float4>(ws, lo.rec_geo), at<float4>(ws, lo.rec_con), at<float2>(ws, lo.rec_span),
+      at<float4>(ws, lo.rec_geo), at<float4>(ws, lo.rec_con), at<float4>(ws, lo.rec_span),
       at<uint32_t>(ws, lo.depth_key),
       at<unsigned long long>(ws, lo.offsets), cam, lo.super_x, cap, &ctr->n_bin, k0, v0);
   SGS_LAUNCH_CHECK("emit_entries");

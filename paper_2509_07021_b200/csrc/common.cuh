@@ -57,7 +57,7 @@ struct Layout {
   int32_t sort_mode;
   int64_t cap;
   // offsets into the workspace
-  uint64_t counters, rec_geo, rec_con, rec_col, rec_span, depth_key, rect, tiles_touched, super_touched, cand_end;
+  uint64_t counters, rec_geo, rec_con, rec_col, rec_span, rec_eig, depth_key, rect, tiles_touched, super_touched, cand_end;
   uint64_t dkey_alt, dkey_tmp, didx, didx_alt, offsets, scan_blocks;
   uint64_t ent_key, ent_key_alt, ent_val, ent_val_alt, ranges;
   uint64_t hist, status;
@@ -115,7 +115,8 @@ inline int make_layout(const sgs_workspace* ws, Layout* lo) {
   lo->rec_geo = take(n * 16);
   lo->rec_con = take(n * 16);
   lo->rec_col = take(n * 16);
-  lo->rec_span = take(n * 8);
+  lo->rec_span = take(n * 16);
+  lo->rec_eig = take(n * 16);
   lo->depth_key = take(n * 4);
   lo->rect = take(n * 8);
   lo->tiles_touched = take(n * 4);

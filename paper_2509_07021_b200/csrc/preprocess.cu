@@ -17,7 +17,8 @@ __device__ __forceinline__ void warp_count(unsigned long long* ctr, bool pred) {
 
 __global__ void __launch_bounds__(256) preprocess_kernel(sgs_params P, SgsCam cam, float4* __restrict__ rec_geo,
                                                          float4* __restrict__ rec_con, float4* __restrict__ rec_col,
-                                                         float2* __restrict__ rec_span,
+                                                         float4* __restrict__ rec_span,
+                                                         float4* __restrict__ rec_eig,
                                                          uint32_t* __restrict__ depth_key, uint2* __restrict__ rect,
                                                          uint32_t* __restrict__ tiles_touched,
                                                          uint32_t* __restrict__ super_touched, Counters* ctr) {
@@ -41,9 +42,11 @@ __global__ void __launch_bounds__(256) preprocess_kernel(sgs_params P, SgsCam ca
       visible = pr.visible;
       uint32_t nsup = 0;
       float g[4], k[4];
+      SgsSpan sp;
       if (pr.emits) {
         sgs_pack_geo(&pr, g, k);
-        sgs_count_hits(pr.tx0, pr.ty0, pr.tx1, pr.ty1, g, k, &cam, &cnt, &nsup);
+        sp = sgs_span(g, k);
+        sgs_count_hits_span(&sp, pr.tx0, pr.ty0, pr.tx1, pr.ty1, &cam, &cnt, &nsup);
       }
       emitting = cnt > 0;
       tiles_touched[i] = cnt;
@@ -64,12 +67,14 @@ __global__ void __launch_bounds__(256) preprocess_kernel(sgs_params P, SgsCam ca
         }
         float c_pre[3], c[3];
         sgs_color(pos, diffuse, axis, sharp, amp, lm, L, &cam, c_pre, c);
-        const SgsSpan sp = sgs_span(g, k);
-        float span2[2];
+        float span2[3];
         sgs_span_cache(&sp, &k[3], span2);
         rec_geo[i] = make_float4(g[0], g[1], g[2], g[3]);
         rec_con[i] = make_float4(k[0], k[1], k[2], k[3]);
-        rec_span[i] = make_float2(span2[0], span2[1]);
+        rec_span[i] = make_float4(span2[0], span2[1], span2[2], 0.0f);
+        float e4[4];
+        sgs_pack_eig(&pr, e4);
+        rec_eig[i] = make_float4(e4[0], e4[1], e4[2], e4[3]);
         rec_col[i] = make_float4(c[0], c[1], c[2], 0.0f);
       }
     }
@@ -168,7 +173,7 @@ int launch_preprocess(const sgs_params& P, const SgsCam& cam, const sgs_workspac
   Counters* ctr = at<Counters>(ws, lo.counters);
   int grid = persistent_grid((uint64_t)P.n, 256, 8);
   preprocess_kernel<<<grid, 256, 0, st>>>(P, cam, at<float4>(ws, lo.rec_geo), at<float4>(ws, lo.rec_con),
-                                          at<float4>(ws, lo.rec_col), at<float2>(ws, lo.rec_span),
+                                          at<float4>(ws, lo.rec_col), at<float4>(ws, lo.rec_span), at<float4>(ws, lo.rec_eig),
                                           at<uint32_t>(ws, lo.depth_key),
                                           at<uint2>(ws, lo.rect), at<uint32_t>(ws, lo.tiles_touched),
                                           at<uint32_t>(ws, lo.super_touched), ctr);

@@ -48,7 +48,8 @@ struct ListArgs {
   const float4* geo;
   const float4* con;
   const float4* col;
-  const float2* span;
+  const float4* eig;
+  const float4* span;
   uint32_t* cand_end;       // per tile: one past the last candidate any pixel kept
   int super_x;
 };
@@ -103,7 +104,7 @@ __device__ __forceinline__ int stage_append(uint32_t c_lo, uint32_t c_hi, uint32
       const int pos = base + pre + __popc(bal[h] & lt);
       const uint32_t g = a.vals[c];
       s.geo[pos] = a.geo[g];
-      s.con[pos] = a.con[g];
+      s.con[pos] = a.eig[g];
       if (kColor) s.col[pos] = a.col[g];
       s.id[pos] = g;
       s.cand[pos] = c;
@@ -170,12 +171,14 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(ListArgs la, Sg
     for (int k = 0; k < nb; ++k) {
       if (!__any_sync(0xffffffffu, live0 || live1)) break;
       const float4 G = s.geo[k];
-      const float4 K = s.con[k];
+      const float4 E = s.con[k];  // eigen form (ux, uy, a1, a2)
       const float dx = fx - G.x;
       const float dy0 = fy0 - G.y, dy1 = dy0 + 1.0f;
-      const float adx = K.x * dx;
-      const float p0 = fmaf(dx, fmaf(K.y, dy0, adx), (K.z * dy0) * dy0);
-      const float p1 = fmaf(dx, fmaf(K.y, dy1, adx), (K.z * dy1) * dy1);
+      const float uxdx = E.x * dx, uydx = E.y * dx;
+      const float t10 = fmaf(E.y, dy0, uxdx), t20 = fmaf(E.x, dy0, -uydx);
+      const float t11 = fmaf(E.y, dy1, uxdx), t21 = fmaf(E.x, dy1, -uydx);
+      const float p0 = fmaf(E.z * t10, t10, (E.w * t20) * t20);
+      const float p1 = fmaf(E.z * t11, t11, (E.w * t21) * t21);
       const bool e0 = live0 && p0 >= G.w;
       const bool e1 = live1 && p1 >= G.w;
       if (kCount) reached += (uint32_t)live0 + (uint32_t)live1;
@@ -303,9 +306,10 @@ __global__ void __launch_bounds__(kBwdThreads) raster_bwd_kernel(ListArgs la, Sg
       const uint32_t idx = base + (uint32_t)k;
       if (__all_sync(0xffffffffu, idx >= nc)) continue;
       const float4 G = s.geo[k];
-      const float4 K = s.con[k];
+      const float4 E = s.con[k];  // eigen form (ux, uy, a1, a2)
       const float dx = fx - G.x, dy = fy - G.y;
-      const float p = fmaf(dx, fmaf(K.y, dy, K.x * dx), (K.z * dy) * dy);
+      const float t1 = fmaf(E.y, dy, E.x * dx), t2 = fmaf(E.x, dy, -(E.y * dx));
+      const float p = fmaf(E.z * t1, t1, (E.w * t2) * t2);
       const bool active = idx < nc && p >= G.w;
       float v[kGrad];
 #pragma unroll
@@ -427,7 +431,8 @@ static ListArgs list_args(const sgs_workspace* ws, const Layout& lo, const uint3
   a.geo = at<float4>(ws, lo.rec_geo);
   a.con = at<float4>(ws, lo.rec_con);
   a.col = at<float4>(ws, lo.rec_col);
-  a.span = at<float2>(ws, lo.rec_span);
+  a.eig = at<float4>(ws, lo.rec_eig);
+  a.span = at<float4>(ws, lo.rec_span);
   a.cand_end = at<uint32_t>(ws, lo.cand_end);
   a.super_x = lo.super_x;
   return a;

@@ -47,6 +47,11 @@
 #define F_FMA(a, b, c) __fmaf_rn((a), (b), (c))
 #define F_RINT(a) rintf((a))
 #define F_FLOOR(a) floorf((a))
+#define D_MUL(a, b) __dmul_rn((a), (b))
+#define D_ADD(a, b) __dadd_rn((a), (b))
+#define D_SUB(a, b) __dsub_rn((a), (b))
+#define D_DIV(a, b) __ddiv_rn((a), (b))
+#define D_SQRT(a) __dsqrt_rn((a))
 #else
 #define F_MUL(a, b) ((float)(a) * (float)(b))
 #define F_ADD(a, b) ((float)(a) + (float)(b))
@@ -56,6 +61,11 @@
 #define F_FMA(a, b, c) fmaf((a), (b), (c))
 #define F_RINT(a) rintf((a))
 #define F_FLOOR(a) floorf((a))
+#define D_MUL(a, b) ((double)(a) * (double)(b))
+#define D_ADD(a, b) ((double)(a) + (double)(b))
+#define D_SUB(a, b) ((double)(a) - (double)(b))
+#define D_DIV(a, b) ((double)(a) / (double)(b))
+#define D_SQRT(a) sqrt((double)(a))
 #endif
 
 #define SGS_TILE 16
@@ -190,6 +200,9 @@ typedef struct SgsProj {
   float mx, my;
   float cov00, cov01, cov11;
   float con00, con01, con11;
+  // eigen form of the same quadratic: q = t1^2 / lmax + t2^2 / lmin with
+  // t1 = u . d, t2 = u x d (u = unit major axis of cov2d)
+  float ux, uy, ilmax, ilmin;
   float o_eff;
   float qmax;
   int32_t tx0, ty0, tx1, ty1;
@@ -231,67 +244,99 @@ SGS_HD void sgs_project(const float pos[3], const float quat[4], const float ls[
   o->tx1 = o->ty1 = -1;
   if (!o->visible) return;
 
-  o->mx = F_ADD(F_DIV(F_MUL(cam->fx, x), z), cam->cx);
-  o->my = F_ADD(F_DIV(F_MUL(cam->fy, y), z), cam->cy);
+  // one IEEE reciprocal per divisor, then products (the CPU restatement
+  // performs the identical sequence, so results stay bit-identical)
+  float iz = F_DIV(1.0f, z);
+  o->mx = F_ADD(F_MUL(F_MUL(cam->fx, x), iz), cam->cx);
+  o->my = F_ADD(F_MUL(F_MUL(cam->fy, y), iz), cam->cy);
 
   // Sigma = R diag(exp(2 ls)) R^T
   float qn = F_SQRT(F_ADD(F_ADD(F_ADD(F_MUL(quat[0], quat[0]), F_MUL(quat[1], quat[1])),
                                 F_MUL(quat[2], quat[2])), F_MUL(quat[3], quat[3])));
   float R[9];
-  sgs_quat_to_rot(F_DIV(quat[0], qn), F_DIV(quat[1], qn), F_DIV(quat[2], qn),
-                  F_DIV(quat[3], qn), R);
+  float iq = F_DIV(1.0f, qn);
+  sgs_quat_to_rot(F_MUL(quat[0], iq), F_MUL(quat[1], iq), F_MUL(quat[2], iq), F_MUL(quat[3], iq), R);
   float D0 = sgs_expf(F_MUL(2.0f, ls[0]));
   float D1 = sgs_expf(F_MUL(2.0f, ls[1]));
   float D2 = sgs_expf(F_MUL(2.0f, ls[2]));
-  float S[9];
+  double S[9];
   for (int i = 0; i < 3; ++i)
     for (int k = i; k < 3; ++k) {
-      float s = F_ADD(F_ADD(F_MUL(F_MUL(R[3 * i + 0], D0), R[3 * k + 0]),
-                            F_MUL(F_MUL(R[3 * i + 1], D1), R[3 * k + 1])),
-                      F_MUL(F_MUL(R[3 * i + 2], D2), R[3 * k + 2]));
+      double s = D_ADD(D_ADD(D_MUL(D_MUL((double)R[3 * i + 0], (double)D0), (double)R[3 * k + 0]),
+                             D_MUL(D_MUL((double)R[3 * i + 1], (double)D1), (double)R[3 * k + 1])),
+                       D_MUL(D_MUL((double)R[3 * i + 2], (double)D2), (double)R[3 * k + 2]));
       S[3 * i + k] = s;
       S[3 * k + i] = s;
     }
 
-  // J (render.py:278-282), M = J W (2x3)
-  float iz = F_DIV(1.0f, z);
-  float J00 = F_MUL(cam->fx, iz);
-  float J02 = -F_DIV(F_MUL(cam->fx, x), F_MUL(z, z));
-  float J11 = F_MUL(cam->fy, iz);
-  float J12 = -F_DIV(F_MUL(cam->fy, y), F_MUL(z, z));
-  float M0[3], M1[3];
+  // J (render.py:278-282), M = J W, cov2d = M Sigma M^T + lowpass I and its
+  // inverse are formed in float64: for elongated splats cov2d is nearly
+  // singular before the low-pass floor, and float32 cancellation there would
+  // cost ~1e-5 relative in the small eigenvalue.
+  const double dz = (double)z, dx_ = (double)x, dy_ = (double)y;
+  const double diz = D_DIV(1.0, dz), diz2 = D_MUL(diz, diz);
+  const double J00 = D_MUL((double)cam->fx, diz);
+  const double J02 = -D_MUL(D_MUL((double)cam->fx, dx_), diz2);
+  const double J11 = D_MUL((double)cam->fy, diz);
+  const double J12 = -D_MUL(D_MUL((double)cam->fy, dy_), diz2);
+  double M0[3], M1[3];
   for (int k = 0; k < 3; ++k) {
-    M0[k] = F_ADD(F_MUL(J00, W[k]), F_MUL(J02, W[6 + k]));
-    M1[k] = F_ADD(F_MUL(J11, W[3 + k]), F_MUL(J12, W[6 + k]));
+    M0[k] = D_ADD(D_MUL(J00, (double)W[k]), D_MUL(J02, (double)W[6 + k]));
+    M1[k] = D_ADD(D_MUL(J11, (double)W[3 + k]), D_MUL(J12, (double)W[6 + k]));
   }
-  // T = M Sigma, cov = T M^T
-  float T0[3], T1[3];
+  double T0[3], T1[3];
   for (int k = 0; k < 3; ++k) {
-    T0[k] = sgs_dot3(M0[0], M0[1], M0[2], S[k], S[3 + k], S[6 + k]);
-    T1[k] = sgs_dot3(M1[0], M1[1], M1[2], S[k], S[3 + k], S[6 + k]);
+    T0[k] = D_ADD(D_ADD(D_MUL(M0[0], S[k]), D_MUL(M0[1], S[3 + k])), D_MUL(M0[2], S[6 + k]));
+    T1[k] = D_ADD(D_ADD(D_MUL(M1[0], S[k]), D_MUL(M1[1], S[3 + k])), D_MUL(M1[2], S[6 + k]));
   }
-  float a = F_ADD(sgs_dot3(T0[0], T0[1], T0[2], M0[0], M0[1], M0[2]), cam->lowpass);
-  float b = sgs_dot3(T0[0], T0[1], T0[2], M1[0], M1[1], M1[2]);
-  float c = F_ADD(sgs_dot3(T1[0], T1[1], T1[2], M1[0], M1[1], M1[2]), cam->lowpass);
-  o->cov00 = a;
-  o->cov01 = b;
-  o->cov11 = c;
-  float det = F_SUB(F_MUL(a, c), F_MUL(b, b));
-  o->con00 = F_DIV(c, det);
-  o->con01 = -F_DIV(b, det);
-  o->con11 = F_DIV(a, det);
-
+  const double lp = (double)cam->lowpass;
+  const double a = D_ADD(D_ADD(D_ADD(D_MUL(T0[0], M0[0]), D_MUL(T0[1], M0[1])), D_MUL(T0[2], M0[2])), lp);
+  const double b = D_ADD(D_ADD(D_MUL(T0[0], M1[0]), D_MUL(T0[1], M1[1])), D_MUL(T0[2], M1[2]));
+  const double c = D_ADD(D_ADD(D_ADD(D_MUL(T1[0], M1[0]), D_MUL(T1[1], M1[1])), D_MUL(T1[2], M1[2])), lp);
+  o->cov00 = (float)a;
+  o->cov01 = (float)b;
+  o->cov11 = (float)c;
+  const double det = D_SUB(D_MUL(a, c), D_MUL(b, b));
+  const double idet = D_DIV(1.0, det);
+  o->con00 = (float)D_MUL(c, idet);
+  o->con01 = (float)(-D_MUL(b, idet));
+  o->con11 = (float)D_MUL(a, idet);
+  {
+    // eigen decomposition of cov2d (PD): lmax = m + r, lmin = det / lmax,
+    // major axis from whichever of (b, lmax - a), (lmax - c, b) is longer
+    const double m = D_MUL(0.5, D_ADD(a, c));
+    const double h = D_MUL(0.5, D_SUB(a, c));
+    const double r = D_SQRT(D_ADD(D_MUL(h, h), D_MUL(b, b)));
+    const double lmax = D_ADD(m, r);
+    const double lmin = D_DIV(det, lmax);
+    double ex = b, ey = D_SUB(lmax, a);
+    const double fx2 = D_SUB(lmax, c), fy2 = b;
+    if (D_ADD(D_MUL(fx2, fx2), D_MUL(fy2, fy2)) > D_ADD(D_MUL(ex, ex), D_MUL(ey, ey))) {
+      ex = fx2;
+      ey = fy2;
+    }
+    const double en = D_SQRT(D_ADD(D_MUL(ex, ex), D_MUL(ey, ey)));
+    if (en > 0.0) {
+      o->ux = (float)D_DIV(ex, en);
+      o->uy = (float)D_DIV(ey, en);
+    } else {  // isotropic: any axis
+      o->ux = 1.0f;
+      o->uy = 0.0f;
+    }
+    o->ilmax = (float)D_DIV(1.0, lmax);
+    o->ilmin = (float)D_DIV(1.0, lmin);
+  }
   float oe = F_MUL(opacity, pmask);
   o->o_eff = oe;
-  if (!(oe > SGS_EPS) || !(det > 0.0f)) {
+  if (!(oe > SGS_EPS) || !(det > 0.0)) {
     o->qmax = 0.0f;
     return;
   }
   float qmax = F_MUL(2.0f, F_SUB(sgs_logf(oe), SGS_LN_EPS));
   o->qmax = qmax;
   // exact bounding box of {d : d^T cov^-1 d <= qmax} is sqrt(qmax * cov_ii)
-  float rx = F_SQRT(F_MUL(qmax, a));
-  float ry = F_SQRT(F_MUL(qmax, c));
+  float rx = F_SQRT(F_MUL(qmax, o->cov00));
+  float ry = F_SQRT(F_MUL(qmax, o->cov11));
   float x0 = F_SUB(o->mx, rx), x1 = F_ADD(o->mx, rx);
   float y0 = F_SUB(o->my, ry), y1 = F_ADD(o->my, ry);
   if (!(x1 > 0.0f && x0 < (float)cam->width && y1 > 0.0f && y0 < (float)cam->height)) return;
@@ -317,7 +362,7 @@ SGS_HD void sgs_project(const float pos[3], const float quat[4], const float ls[
 // dy = kx dx, its y-extremes on dx = ky dy; xm / ym are the half extents.
 typedef struct SgsSpan {
   float mx, my, A, B, C, pmin;
-  float kx, xm, ym;
+  float kx, xm, ym, i2a;  // i2a = 1 / (2 A)
   int valid;
 } SgsSpan;
 
@@ -333,21 +378,24 @@ SGS_HD SgsSpan sgs_span(const float geo[4], const float con[4]) {
   float D = F_SUB(F_MUL(F_MUL(4.0f, s.A), s.C), F_MUL(s.B, s.B));
   s.valid = D > 0.0f && s.A < 0.0f && s.C < 0.0f && s.pmin < 0.0f;
   s.kx = -F_DIV(s.B, F_MUL(2.0f, s.C));
-  s.xm = s.valid ? F_SQRT(F_DIV(F_MUL(F_MUL(4.0f, s.C), s.pmin), D)) : 0.0f;
-  s.ym = s.valid ? F_SQRT(F_DIV(F_MUL(F_MUL(4.0f, s.A), s.pmin), D)) : 0.0f;
+  const float iD = F_DIV(1.0f, D);
+  s.xm = s.valid ? F_SQRT(F_MUL(F_MUL(F_MUL(4.0f, s.C), s.pmin), iD)) : 0.0f;
+  s.ym = s.valid ? F_SQRT(F_MUL(F_MUL(F_MUL(4.0f, s.A), s.pmin), iD)) : 0.0f;
+  s.i2a = F_DIV(1.0f, F_MUL(2.0f, s.A));
   return s;
 }
 
 // The span parameters are cached per primitive by the preprocess: kx in the
 // conic record's 4th slot, (xm, ym) in a float2 (xm < 0 marks an invalid
 // form).  Rebuilding SgsSpan from the cache is bit-identical to sgs_span.
-SGS_HD void sgs_span_cache(const SgsSpan* s, float* kx, float span2[2]) {
+SGS_HD void sgs_span_cache(const SgsSpan* s, float* kx, float span2[3]) {
   *kx = s->kx;
   span2[0] = s->valid ? s->xm : -1.0f;
   span2[1] = s->ym;
+  span2[2] = s->i2a;
 }
 
-SGS_HD SgsSpan sgs_span_cached(const float geo[4], const float con[4], const float span2[2]) {
+SGS_HD SgsSpan sgs_span_cached(const float geo[4], const float con[4], const float span2[3]) {
   SgsSpan s;
   s.mx = geo[0];
   s.my = geo[1];
@@ -359,6 +407,7 @@ SGS_HD SgsSpan sgs_span_cached(const float geo[4], const float con[4], const flo
   s.valid = span2[0] >= 0.0f;
   s.xm = s.valid ? span2[0] : 0.0f;
   s.ym = span2[1];
+  s.i2a = span2[2];
   return s;
 }
 
@@ -370,8 +419,8 @@ SGS_HD float sgs_span_root(const SgsSpan* s, float dy, int right) {
   float c = F_SUB(F_MUL(F_MUL(s->C, dy), dy), s->pmin);
   float disc = F_SUB(F_MUL(b, b), F_MUL(F_MUL(4.0f, s->A), c));
   float r = F_SQRT(fmaxf(disc, 0.0f));
-  float den = F_MUL(2.0f, s->A);  // < 0: (-b - r)/den is the larger root
-  return right ? F_DIV(F_SUB(-b, r), den) : F_DIV(F_ADD(-b, r), den);
+  // 2A < 0: (-b - r) / (2A) is the larger root
+  return right ? F_MUL(F_SUB(-b, r), s->i2a) : F_MUL(F_ADD(-b, r), s->i2a);
 }
 
 // Tiles of tile-row `ty` (clipped to [tx0, tx1]) whose pixel-center box meets
@@ -488,9 +537,9 @@ SGS_HD uint32_t sgs_super_mask(const int first[SGS_SUPER], const int cnt[SGS_SUP
 }
 
 // (tile entries, super-tile entries) of one primitive.
-SGS_HD void sgs_count_hits(int tx0, int ty0, int tx1, int ty1, const float geo[4], const float con[4],
-                           const SgsCam* cam, uint32_t* n_tiles, uint32_t* n_super) {
-  SgsSpan s = sgs_span(geo, con);
+SGS_HD void sgs_count_hits_span(const SgsSpan* sp, int tx0, int ty0, int tx1, int ty1, const SgsCam* cam,
+                                uint32_t* n_tiles, uint32_t* n_super) {
+  const SgsSpan s = *sp;
   uint32_t nt = 0, ns = 0;
   int cur = -1, lo = 0x7fffffff, hi = -1, first;
   for (int ty = ty0; ty <= ty1; ++ty) {
@@ -514,9 +563,15 @@ SGS_HD void sgs_count_hits(int tx0, int ty0, int tx1, int ty1, const float geo[4
   *n_super = ns;
 }
 
+SGS_HD void sgs_count_hits(int tx0, int ty0, int tx1, int ty1, const float geo[4], const float con[4],
+                           const SgsCam* cam, uint32_t* n_tiles, uint32_t* n_super) {
+  const SgsSpan s = sgs_span(geo, con);
+  sgs_count_hits_span(&s, tx0, ty0, tx1, ty1, cam, n_tiles, n_super);
+}
+
 // Exact membership of a primitive in tile (tx, ty)'s list (the same test
 // the counts and the CPU restatement use).
-SGS_HD int sgs_tile_member(const float geo[4], const float con[4], const float span2[2], int tx0, int ty0,
+SGS_HD int sgs_tile_member(const float geo[4], const float con[4], const float span2[3], int tx0, int ty0,
                            int tx1, int ty1, const SgsCam* cam, int tx, int ty) {
   if (ty < ty0 || ty > ty1 || tx < tx0 || tx > tx1) return 0;
   SgsSpan s = sgs_span_cached(geo, con, span2);
@@ -533,14 +588,16 @@ SGS_HD void sgs_color(const float pos[3], const float diffuse[3], const float* a
                       const SgsCam* cam, float c_pre[3], float c[3]) {
   float d0 = F_SUB(pos[0], cam->C[0]), d1 = F_SUB(pos[1], cam->C[1]), d2 = F_SUB(pos[2], cam->C[2]);
   float r = F_SQRT(sgs_dot3(d0, d1, d2, d0, d1, d2));
-  float v0 = F_DIV(d0, r), v1 = F_DIV(d1, r), v2 = F_DIV(d2, r);
+  float ir = F_DIV(1.0f, r);
+  float v0 = F_MUL(d0, ir), v1 = F_MUL(d1, ir), v2 = F_MUL(d2, ir);
   float acc0 = 0.0f, acc1 = 0.0f, acc2 = 0.0f;
   for (int l = 0; l < L; ++l) {
     float m = lmask[l];
     if (m == 0.0f) continue;
     const float* u = axis + 3 * l;
     float un = F_SQRT(sgs_dot3(u[0], u[1], u[2], u[0], u[1], u[2]));
-    float dot = sgs_dot3(F_DIV(u[0], un), F_DIV(u[1], un), F_DIV(u[2], un), v0, v1, v2);
+    float iun = F_DIV(1.0f, un);
+    float dot = sgs_dot3(F_MUL(u[0], iun), F_MUL(u[1], iun), F_MUL(u[2], iun), v0, v1, v2);
     float e = F_MUL(sgs_expf(F_MUL(sharp[l], F_SUB(dot, 1.0f))), m);
     acc0 = F_ADD(acc0, F_MUL(e, amp[3 * l + 0]));
     acc1 = F_ADD(acc1, F_MUL(e, amp[3 * l + 1]));
@@ -558,6 +615,18 @@ SGS_HD void sgs_color(const float pos[3], const float diffuse[3], const float* a
 //   p2 = A dx^2 + B dx dy + C dy^2  (= -q/2 * log2 e),  G = 2^p2,
 // and skips the pair when p2 < pmin (= -qmax/2 * log2 e), i.e. q > qmax.
 //   geo = (mx, my, o_eff, pmin), con = (A, B, C, 0)
+// Raster record of the eigen form: eig = (ux, uy, a1, a2) with
+//   p2 = a1 (ux dx + uy dy)^2 + a2 (ux dy - uy dx)^2,  a = -log2(e)/2 / l.
+// Both terms are <= 0, so unlike the (A, B, C) form there is no cancellation
+// for elongated splats; this is what the rasterizers evaluate per pixel.
+SGS_HD void sgs_pack_eig(const SgsProj* p, float eig[4]) {
+  const float k = -0.5f * SGS_LOG2E;
+  eig[0] = p->ux;
+  eig[1] = p->uy;
+  eig[2] = F_MUL(k, p->ilmax);
+  eig[3] = F_MUL(k, p->ilmin);
+}
+
 SGS_HD void sgs_pack_geo(const SgsProj* p, float geo[4], float con[4]) {
   const float k = -0.5f * SGS_LOG2E;
   geo[0] = p->mx;

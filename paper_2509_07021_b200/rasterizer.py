@@ -312,7 +312,7 @@ class Rasterizer:
         depth = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
         rect = torch.empty((max(n, 1), 2), dtype=torch.int32, device=self.device)
         tt = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
-        rec = torch.empty((max(n, 1), 12), dtype=torch.float32, device=self.device)
+        rec = torch.empty((max(n, 1), 16), dtype=torch.float32, device=self.device)
         _ffi.call("sgs_export_projected", C.byref(frame.ws.desc), _ptr(depth), _ptr(rect),
                   _ptr(tt), _ptr(rec), C.c_void_p(_stream_ptr()))
         return depth[:n], rect[:n], tt[:n], rec[:n]
