@@ -107,6 +107,15 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def profiled_traffic(kernel: str):
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of
+    `kernel` from the committed `ncu --set full` capture (profiles/traffic.json)."""
+    p = ROOT / "profiles" / "traffic.json"
+    if not p.exists():
+        return None
+    return json.loads(p.read_text()).get(kernel, {}).get("bytes_per_launch")
+
+
 def measured_peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -359,7 +368,7 @@ def run_ours(args):
                      "tile_entries_per_view": E},
             "roofline": {"bound": "fp32_issue", "kernel": "raster_fwd_kernel",
                          "achieved": achieved / 1e9, "peak": peak_pairs / 1e9, "unit": "Gpair/s",
-                         "frac": achieved / peak_pairs, "traffic": None,
+                         "frac": achieved / peak_pairs, "traffic": profiled_traffic("raster_fwd_kernel"),
                          "note": f"pairs/view={pairs_per_view:.4g} (GPU counter); peak = SMs x "
                                  f"{sm_mhz:.0f} MHz ({src} sm_max) x 128/18 pairs/clk/SM",
                          "raster_ms_per_view": float(np.mean(raster_ms))},
