@@ -251,7 +251,7 @@ def run_ours(args):
     stats = []
     pairs = torch.zeros(1, dtype=torch.int64, device=dev)
     for cam in my_cams:
-        f = rast.forward(g, cam, check=True, pair_count=pairs)
+        f = rast.forward(g, cam, check=True, pair_count=pairs, track=False)
         st = f.stats()
         assert not st["overflow"]
         stats.append(st)
@@ -287,7 +287,7 @@ def run_ours(args):
     for _ in range(args.steps):
         for k, cam in enumerate(my_cams):
             with torch.cuda.stream(streams[k % len(streams)]):
-                rast.forward(g, cam, check=False, out=out_bufs[k])
+                rast.forward(g, cam, check=False, out=out_bufs[k], track=False)
     for s in streams[1:]:
         stream.wait_stream(s)
     stop.record(stream)
@@ -304,7 +304,8 @@ def run_ours(args):
     e = 0
     for _ in range(args.steps):
         for k, cam in enumerate(my_cams):
-            rast.forward(g, cam, check=False, out=out_bufs[k], _events=(r0[e], r1[e]))
+            rast.forward(g, cam, check=False, out=out_bufs[k], track=False,
+                         _events=(r0[e], r1[e]))
             e += 1
     torch.cuda.synchronize(dev)
     raster_ms = [a.elapsed_time(b) for a, b in zip(r0, r1)]

@@ -139,6 +139,8 @@ int sgs_bin(const sgs_camera* cam, const sgs_workspace* ws, void* stream);
 /* K5 forward raster -- replaces _chunk_blend + _render_params
  * (render.py:355-408).  out_img (H,W,3), out_T (H,W) final transmittance,
  * out_ncontrib (H,W) number of per-tile entries consumed by each pixel.
+ * out_T and out_ncontrib may be NULL for an image-only render (render.py:411);
+ * sgs_raster_backward needs both from the same frame.
  * weight_sums (N) is ACCUMULATED (like the reference's in-place np.add.at,
  * render.py:406-407) when non-NULL.  pair_count (one device uint64), when
  * non-NULL, is incremented by the number of (pixel, entry) pairs evaluated

@@ -74,7 +74,7 @@ class BatchRenderer:
             s = self.streams[k % len(self.streams)]
             s.wait_event(up)
             with torch.cuda.stream(s):
-                img = self.rast.forward(g, cam, background, check=check).img
+                img = self.rast.forward(g, cam, background, check=check, track=False).img
                 done = torch.cuda.Event()
                 done.record(s)
             host = self._host_buf(k, tuple(img.shape))

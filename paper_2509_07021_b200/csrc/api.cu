@@ -129,7 +129,7 @@ int sgs_raster_forward(const sgs_camera* cam, const float background[3], const s
   int rc = check_ws(ws, &lo);
   if (!rc) rc = make_cam(cam, lo, &c);
   if (rc) return rc;
-  if (!out_img || !out_T || !out_ncontrib || !background) {
+  if (!out_img || !background) {
     set_error("null output buffer");
     return SGS_E_ARG;
   }

@@ -123,14 +123,54 @@ __device__ __forceinline__ uint32_t tile_local_bit(int tx, int ty) {
 // lanes' supports and termination coherent).  Per staged record the two
 // pixels share the record loads, dx and A dx; the per-pixel blend is
 // predicated, and a warp skips a record outright when none of its 64 pixels
-// is inside the record's support.
+// is inside the record's support.  Warp-level termination (every pixel's
+// transmittance fell below the cutoff) is voted once per kVoteEvery records
+// rather than per record: a dead pixel is predicated off anyway, so the vote
+// only bounds the work a finished warp wastes.
+// kTrack: record per-pixel contributor counts and the per-tile candidate end
+// the backward pass walks from; a render that only returns the image skips it.
 constexpr int kFwdThreads = 128;
 constexpr int kFwdCPT = 2;
 constexpr int kFwdChunk = kFwdThreads * kFwdCPT;  // candidates examined per staging step
 constexpr int kFwdBatch = 256;                    // staged entries processed per block sync
 constexpr int kFwdBuf = kFwdBatch + kFwdChunk;
+constexpr int kVoteEvery = 8;
 
-template <bool kImportance, bool kCount, bool kFilter>
+// Warp vote without the compiler's divergence guard (callers are converged).
+__device__ __forceinline__ bool warp_any(bool p) {
+  uint32_t r;
+  asm volatile(
+      "{\n\t.reg .pred P, Q;\n\tsetp.ne.u32 P, %1, 0;\n\tvote.sync.any.pred Q, P, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, Q;\n\t}"
+      : "=r"(r)
+      : "r"((uint32_t)p));
+  return r != 0;
+}
+
+// One pixel's front-to-back step against one record.  Liveness is carried in
+// the sign of T: a pixel whose next transmittance would fall below the cutoff
+// keeps its last kept T, negated, and is never inside a support again.
+__device__ __forceinline__ float blend_px(float p, const float4& G, const float4& c, float& T, float& C0, float& C1,
+                                          float& C2, bool& kept) {
+  const bool e = T > 0.0f && p >= G.w;
+  const float a = G.z * ex2_approx(p);
+  const float Tn = T * fmaxf(1.0f - a, SGS_ONE_MINUS_ALPHA_MAX);
+  const bool cmp = Tn >= SGS_T_KEEP;
+  kept = e && cmp;
+  float w = 0.0f;
+  if (kept) {
+    w = fminf(a, SGS_ALPHA_MAX) * T;
+    C0 = fmaf(w, c.x, C0);
+    C1 = fmaf(w, c.y, C1);
+    C2 = fmaf(w, c.z, C2);
+    T = Tn;
+  } else if (e) {
+    T = -T;
+  }
+  return w;
+}
+
+template <bool kImportance, bool kCount, bool kFilter, bool kTrack>
 __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(ListArgs la, SgsCam cam, float3 bg,
                                                                  float* __restrict__ out_img,
                                                                  float* __restrict__ out_T,
@@ -151,11 +191,12 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(ListArgs la, Sg
   const uint2 rg = la.ranges[list_cell(kFilter, tx, ty, tile, la.super_x)];
   const uint32_t cs = rg.x, ce = rg.y > rg.x ? rg.y : rg.x;
 
-  float T0 = 1.0f, T1 = 1.0f;
+  // T > 0: live; T < 0: terminated with transmittance -T (pixels off the
+  // image start terminated)
+  float T0 = in0 ? 1.0f : -1.0f, T1 = in1 ? 1.0f : -1.0f;
   float C00 = 0.0f, C01 = 0.0f, C02 = 0.0f, C10 = 0.0f, C11 = 0.0f, C12 = 0.0f;
   uint32_t nc0 = 0, nc1 = 0, reached = 0, kend = 0, hits_before = 0;
-  bool live0 = in0, live1 = in1;
-  if (t == 0) s_kend = 0;
+  if (kTrack && t == 0) s_kend = 0;
 
   const uint32_t lbit = tile_local_bit(tx, ty);
   uint32_t cb = cs;
@@ -168,89 +209,85 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(ListArgs la, Sg
       cb = chi;
     }
     if (nb == 0) break;
-    for (int k = 0; k < nb; ++k) {
-      if (!__any_sync(0xffffffffu, live0 || live1)) break;
-      const float4 G = s.geo[k];
-      const float4 E = s.con[k];  // eigen form (ux, uy, a1, a2)
-      const float dx = fx - G.x;
-      const float dy0 = fy0 - G.y, dy1 = dy0 + 1.0f;
-      const float uxdx = E.x * dx, uydx = E.y * dx;
-      const float t10 = fmaf(E.y, dy0, uxdx), t20 = fmaf(E.x, dy0, -uydx);
-      const float t11 = fmaf(E.y, dy1, uxdx), t21 = fmaf(E.x, dy1, -uydx);
-      const float p0 = fmaf(E.z * t10, t10, (E.w * t20) * t20);
-      const float p1 = fmaf(E.z * t11, t11, (E.w * t21) * t21);
-      const bool e0 = live0 && p0 >= G.w;
-      const bool e1 = live1 && p1 >= G.w;
-      if (kCount) reached += (uint32_t)live0 + (uint32_t)live1;
-      float w0 = 0.0f, w1 = 0.0f;
-      if (__any_sync(0xffffffffu, e0 || e1)) {
-        const float4 c = s.col[k];
-        const uint32_t idx = hits_before + (uint32_t)k + 1u;
-        {
-          const float a = G.z * ex2_approx(p0);
-          const float Tn = T0 * fmaxf(1.0f - a, SGS_ONE_MINUS_ALPHA_MAX);
-          const bool keep = e0 && Tn >= SGS_T_KEEP;
-          live0 = live0 && (keep || !e0);
-          if (keep) {
-            w0 = fminf(a, SGS_ALPHA_MAX) * T0;
-            C00 = fmaf(w0, c.x, C00);
-            C01 = fmaf(w0, c.y, C01);
-            C02 = fmaf(w0, c.z, C02);
-            T0 = Tn;
-            nc0 = idx;
-          }
-        }
-        {
-          const float a = G.z * ex2_approx(p1);
-          const float Tn = T1 * fmaxf(1.0f - a, SGS_ONE_MINUS_ALPHA_MAX);
-          const bool keep = e1 && Tn >= SGS_T_KEEP;
-          live1 = live1 && (keep || !e1);
-          if (keep) {
-            w1 = fminf(a, SGS_ALPHA_MAX) * T1;
-            C10 = fmaf(w1, c.x, C10);
-            C11 = fmaf(w1, c.y, C11);
-            C12 = fmaf(w1, c.z, C12);
-            T1 = Tn;
-            nc1 = idx;
-          }
-        }
+    // pad the batch to a whole number of vote groups with records no pixel is
+    // inside (pmin = +inf), so the group loop below needs no bounds checks
+    const int nb_pad = (nb + kVoteEvery - 1) / kVoteEvery * kVoteEvery;
+    if (nb_pad != nb) {
+      if (t < nb_pad - nb) {
+        s.geo[nb + t] = make_float4(0.0f, 0.0f, 0.0f, INFINITY);
+        s.con[nb + t] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
       }
-      if (kImportance) {
-        const float ws = warp_sum(w0 + w1);
-        if (lane == 0 && ws != 0.0f) atomicAdd(&weight_sums[s.id[k]], ws);
+      __syncthreads();
+    }
+    for (int k = 0; k < nb_pad; k += kVoteEvery) {
+      if (!warp_any(T0 > 0.0f || T1 > 0.0f)) break;
+#pragma unroll
+      for (int j = 0; j < kVoteEvery; ++j) {
+        const int kk = k + j;
+        const float4 G = s.geo[kk];
+        const float4 E = s.con[kk];  // eigen form (ux, uy, a1, a2)
+        const float dx = fx - G.x;
+        const float dy0 = fy0 - G.y, dy1 = dy0 + 1.0f;
+        const float uxdx = E.x * dx, uydx = E.y * dx;
+        const float t10 = fmaf(E.y, dy0, uxdx), t20 = fmaf(E.x, dy0, -uydx);
+        const float t11 = fmaf(E.y, dy1, uxdx), t21 = fmaf(E.x, dy1, -uydx);
+        const float p0 = fmaf(E.z * t10, t10, (E.w * t20) * t20);
+        const float p1 = fmaf(E.z * t11, t11, (E.w * t21) * t21);
+        if (kCount && kk < nb) reached += (uint32_t)(T0 > 0.0f) + (uint32_t)(T1 > 0.0f);
+        if (warp_any((T0 > 0.0f && p0 >= G.w) || (T1 > 0.0f && p1 >= G.w))) {
+          const float4 c = s.col[kk];
+          bool k0, k1;
+          const float w0 = blend_px(p0, G, c, T0, C00, C01, C02, k0);
+          const float w1 = blend_px(p1, G, c, T1, C10, C11, C12, k1);
+          if (kTrack) {
+            const uint32_t idx = hits_before + (uint32_t)kk + 1u;
+            if (k0) nc0 = idx;
+            if (k1) nc1 = idx;
+          }
+          if (kImportance) {
+            const float ws = warp_sum(w0 + w1);
+            if (lane == 0 && ws != 0.0f) atomicAdd(&weight_sums[s.id[kk]], ws);
+          }
+        }
       }
     }
-    // candidate position of this thread's last kept entry (for the backward)
-    const uint32_t mx = nc0 > nc1 ? nc0 : nc1;
-    if (mx > hits_before) kend = s.cand[mx - hits_before - 1] + 1u;
+    if (kTrack) {
+      // candidate position of this thread's last kept entry (for the backward)
+      const uint32_t mx = nc0 > nc1 ? nc0 : nc1;
+      if (mx > hits_before) kend = s.cand[mx - hits_before - 1] + 1u;
+    }
     hits_before += (uint32_t)nb;
     if (cb >= ce) break;
-    if (__syncthreads_count(live0 || live1) == 0) break;
+    if (__syncthreads_count(T0 > 0.0f || T1 > 0.0f) == 0) break;
   }
   if (kCount) {
     unsigned long long r = reached;
     for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
     if (lane == 0 && r) atomicAdd(pair_count, r);
   }
-  if (kend) atomicMax(&s_kend, kend);
+  if (kTrack && kend) atomicMax(&s_kend, kend);
+  T0 = fabsf(T0);
+  T1 = fabsf(T1);
   if (in0) {
     const size_t pix = (size_t)py0 * cam.width + px;
     out_img[3 * pix + 0] = C00 + T0 * bg.x;
     out_img[3 * pix + 1] = C01 + T0 * bg.y;
     out_img[3 * pix + 2] = C02 + T0 * bg.z;
-    out_T[pix] = T0;
-    out_nc[pix] = nc0;
+    if (out_T) out_T[pix] = T0;
+    if (kTrack) out_nc[pix] = nc0;
   }
   if (in1) {
     const size_t pix = (size_t)(py0 + 1) * cam.width + px;
     out_img[3 * pix + 0] = C10 + T1 * bg.x;
     out_img[3 * pix + 1] = C11 + T1 * bg.y;
     out_img[3 * pix + 2] = C12 + T1 * bg.z;
-    out_T[pix] = T1;
-    out_nc[pix] = nc1;
+    if (out_T) out_T[pix] = T1;
+    if (kTrack) out_nc[pix] = nc1;
   }
-  __syncthreads();
-  if (t == 0) la.cand_end[tile] = s_kend ? s_kend : cs;
+  if (kTrack) {
+    __syncthreads();
+    if (t == 0) la.cand_end[tile] = s_kend ? s_kend : cs;
+  }
 }
 
 constexpr int kGrad = 9;
@@ -444,19 +481,22 @@ int launch_raster_fwd(const SgsCam& cam, float3 bg, const sgs_workspace* ws, con
   const int grid = (cam.tile_y1 - cam.tile_y0) * cam.tiles_x;
   const ListArgs a = list_args(ws, lo, vals);
   const bool filt = lo.sort_mode == SGS_SORT_DEPTH_FIRST;
-#define SGS_FWD(I, C, F) \
-  raster_fwd_kernel<I, C, F><<<grid, kFwdThreads, 0, st>>>(a, cam, bg, img, T, nc, weight_sums, pairs)
+#define SGS_FWD(I, C, F, K) \
+  raster_fwd_kernel<I, C, F, K><<<grid, kFwdThreads, 0, st>>>(a, cam, bg, img, T, nc, weight_sums, pairs)
+#define SGS_FWD_TRACK(I, C, F) \
+  if (nc) SGS_FWD(I, C, F, true); else SGS_FWD(I, C, F, false)
   if (filt) {
-    if (weight_sums && pairs) SGS_FWD(true, true, true);
-    else if (weight_sums) SGS_FWD(true, false, true);
-    else if (pairs) SGS_FWD(false, true, true);
-    else SGS_FWD(false, false, true);
+    if (weight_sums && pairs) SGS_FWD_TRACK(true, true, true);
+    else if (weight_sums) SGS_FWD_TRACK(true, false, true);
+    else if (pairs) SGS_FWD_TRACK(false, true, true);
+    else SGS_FWD_TRACK(false, false, true);
   } else {
-    if (weight_sums && pairs) SGS_FWD(true, true, false);
-    else if (weight_sums) SGS_FWD(true, false, false);
-    else if (pairs) SGS_FWD(false, true, false);
-    else SGS_FWD(false, false, false);
+    if (weight_sums && pairs) SGS_FWD_TRACK(true, true, false);
+    else if (weight_sums) SGS_FWD_TRACK(true, false, false);
+    else if (pairs) SGS_FWD_TRACK(false, true, false);
+    else SGS_FWD_TRACK(false, false, false);
   }
+#undef SGS_FWD_TRACK
 #undef SGS_FWD
   SGS_LAUNCH_CHECK("raster_fwd_kernel");
   return SGS_OK;

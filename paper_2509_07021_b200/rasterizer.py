@@ -147,7 +147,7 @@ class Frame:
 
     img: torch.Tensor          # (H, W, 3) float32
     final_T: torch.Tensor      # (H, W) float32
-    ncontrib: torch.Tensor     # (H, W) int32 (uint32 on the device)
+    ncontrib: torch.Tensor | None  # (H, W) int32 (uint32 on the device); None if not tracked
     ws: Workspace
     cam: _ffi.SgsCamera
     bg: tuple
@@ -205,10 +205,12 @@ class Rasterizer:
     # ------------------------------------------------------------------ forward
     def forward(self, g: GaussianTensors, cam, background=(0.0, 0.0, 0.0), weight_sums=None,
                 check=True, private=False, tile_rows=None, out=None, pair_count=None,
-                _events=None) -> Frame:
+                track=True, _events=None) -> Frame:
         """Render one view.  ``weight_sums`` (N float32 device tensor) is
         accumulated in place (render.py:406-407).  ``out`` may supply
-        preallocated (img, T, nc) tensors."""
+        preallocated (img, T, nc) tensors.  ``track=False`` renders the image
+        (and T) only, skipping the per-pixel contributor counts the backward
+        needs (an image-only render, render.py:411)."""
         c_cam = to_sgs(cam, tile_rows)
         bg = tuple(float(v) for v in np.asarray(background, dtype=np.float64).reshape(3))
         c_bg = (C.c_float * 3)(*bg)
@@ -216,9 +218,11 @@ class Rasterizer:
         if out is None:
             img = torch.empty((H, W, 3), dtype=torch.float32, device=self.device)
             T = torch.empty((H, W), dtype=torch.float32, device=self.device)
-            nc = torch.empty((H, W), dtype=torch.int32, device=self.device)
+            nc = torch.empty((H, W), dtype=torch.int32, device=self.device) if track else None
         else:
             img, T, nc = out
+            if not track:
+                nc = None
         if weight_sums is not None:
             if weight_sums.dtype != torch.float32 or tuple(weight_sums.shape) != (g.n,):
                 raise ValueError("weight_sums must be a float32 (N,) tensor")
@@ -256,6 +260,8 @@ class Rasterizer:
         shaped like the parameters (+ 'lobe_mask' / 'prim_mask' when
         ``mask_grads``) and 'grad2d' (N,9)."""
         dimg = dimg.to(device=self.device, dtype=torch.float32).contiguous()
+        if frame.ncontrib is None:
+            raise ValueError("frame was rendered with track=False; the backward needs track=True")
         if tuple(dimg.shape) != tuple(frame.img.shape):
             raise ValueError(f"dimg shape {tuple(dimg.shape)} != image {tuple(frame.img.shape)}")
         stream = C.c_void_p(_stream_ptr())

@@ -210,7 +210,7 @@ def _render_params(p, cam, background, weight_sums: np.ndarray | None = None) ->
     ws = None
     if weight_sums is not None:
         ws = torch.zeros(g.n, dtype=torch.float32, device=rast.device)
-    frame = rast.forward(g, cam, _bg(background), weight_sums=ws)
+    frame = rast.forward(g, cam, _bg(background), weight_sums=ws, track=False)
     img = _to_np64(frame.img)
     if weight_sums is not None:
         weight_sums += _to_np64(ws)
@@ -232,7 +232,7 @@ def accumulate_importance_params(p, cams, background=(0.0, 0.0, 0.0)) -> np.ndar
     g = _upload(p)
     ws = torch.zeros(g.n, dtype=torch.float32, device=rast.device)
     for cam in cams:
-        rast.forward(g, cam, _bg(background), weight_sums=ws)
+        rast.forward(g, cam, _bg(background), weight_sums=ws, track=False)
     return _to_np64(ws)
 
 

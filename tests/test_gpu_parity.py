@@ -180,3 +180,19 @@ def test_backward_matches_oracle(bg):
               "amplitude", "lobe_mask", "prim_mask"):
         ok = _composite_ok(grads[k].cpu().numpy(), og[k])
         assert ok.mean() == 1.0, f"{k}: {np.count_nonzero(~ok)} of {ok.size} outside tolerance"
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_untracked_render_equals_tracked(mode):
+    """The image-only forward (no contributor counts) renders the same bits."""
+    scene, cams = scenes.config1(n=20_000)
+    cam = cams[0]
+    rast = Rasterizer(sort_mode=mode)
+    g = GaussianTensors.from_arrays(scene)
+    a = rast.forward(g, cam, (0.1, 0.2, 0.3))
+    img_a, T_a = a.img.clone(), a.final_T.clone()
+    b = rast.forward(g, cam, (0.1, 0.2, 0.3), track=False)
+    assert b.ncontrib is None
+    assert torch.equal(img_a, b.img) and torch.equal(T_a, b.final_T)
+    with pytest.raises(ValueError):
+        rast.backward(g, b, torch.zeros_like(b.img))
