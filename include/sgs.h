@@ -193,7 +193,8 @@ int sgs_export_bins(const sgs_workspace* ws, const sgs_camera* cam, uint64_t* ke
 
 /* Export per-primitive preprocess outputs (device buffers, length N):
  * depth bits, packed tile rect (tx0|tx1<<16, ty0|ty1<<16), tile counts and
- * the 16-float raster record [geo(4), conic(4), eigen form(4), color(4)]. */
+ * the 16-float raster record [geo(4) = (mean x, mean y, log2 o_eff, pmin),
+ * conic(4) = (A, B, C, kx), scaled eigen form(4), color(4)] (sgs_geom.h). */
 int sgs_export_projected(const sgs_workspace* ws, uint32_t* depth_bits,
                          uint32_t* rect, uint32_t* tiles_touched, float* records, void* stream);
 

@@ -173,11 +173,12 @@ void oracle_raster_forward(const uint32_t* ranges, const uint32_t* vals, const f
       for (uint32_t j = s; j < e; ++j) {
         const float* r = records + 16 * (size_t)vals[j];
         const float dx = fx - r[0], dy = fy - r[1];
-        // eigen form, same operation order as the GPU raster
-        const float t1 = fmaf(r[9], dy, r[8] * dx), t2 = fmaf(r[8], dy, -(r[9] * dx));
-        const float p = fmaf(r[10] * t1, t1, (r[11] * t2) * t2);
-        if (p < r[3]) continue;
-        const float a = r[2] * exp2f(p);
+        // scaled eigen form with log2(o_eff) folded in (sgs_pack_eig), same
+        // operation order as the GPU raster: p = log2(o_eff G)
+        const float t1 = fmaf(r[9], dy, r[8] * dx), t2 = fmaf(r[10], dy, -(r[11] * dx));
+        const float p = fmaf(-t1, t1, fmaf(-t2, t2, r[2]));
+        // every listed primitive is blended (alpha < 1e-7 outside its support)
+        const float a = exp2f(p);
         const float alpha = std::min(a, SGS_ALPHA_MAX);
         const float Tn = T * (a < SGS_ALPHA_MAX ? 1.0f - a : SGS_ONE_MINUS_ALPHA_MAX);
         if (Tn < SGS_T_KEEP) break;
@@ -216,11 +217,10 @@ void oracle_raster_backward(const uint32_t* ranges, const uint32_t* vals, const 
       for (uint32_t j = s; j < e; ++j) {
         const float* r = records + 16 * (size_t)vals[j];
         const double dx = fx - r[0], dy = fy - r[1];
-        const double t1 = (double)r[8] * dx + (double)r[9] * dy, t2 = (double)r[8] * dy - (double)r[9] * dx;
-        const double p = (double)r[10] * t1 * t1 + (double)r[11] * t2 * t2;
-        if (p < (double)r[3]) continue;
-        const double G = exp2(p);
-        const double a = (double)r[2] * G;
+        const double t1 = (double)r[8] * dx + (double)r[9] * dy, t2 = (double)r[10] * dy - (double)r[11] * dx;
+        const double p = (double)r[2] - t1 * t1 - t2 * t2;  // log2(o_eff G)
+        const double a = exp2(p);
+        const double G = a;  // o_eff G: dq below is -1/2 o G dalpha
         const double alpha = std::min(a, 0.99);
         const double Tn = T * (1.0 - alpha);
         if (Tn < (double)SGS_T_KEEP) break;
@@ -238,7 +238,7 @@ void oracle_raster_backward(const uint32_t* ranges, const uint32_t* vals, const 
         const double om = 1.0 - it.alpha;
         const double dalpha = it.a < 0.99 ? (it.T * cg - S / om) : 0.0;
         S += w * cg;
-        const double dq = -0.5 * (double)r[2] * it.G * dalpha;
+        const double dq = -0.5 * it.G * dalpha;
         double* d = grad2d + 9 * (size_t)it.g;
         d[0] += w * g0;
         d[1] += w * g1;

@@ -147,27 +147,31 @@ __device__ __forceinline__ bool warp_any(bool p) {
   return r != 0;
 }
 
-// One pixel's front-to-back step against one record.  Liveness is carried in
-// the sign of T: a pixel whose next transmittance would fall below the cutoff
-// keeps its last kept T, negated, and is never inside a support again.
-__device__ __forceinline__ float blend_px(float p, const float4& G, const float4& c, float& T, float& C0, float& C1,
-                                          float& C2, bool& kept) {
-  const bool e = T > 0.0f && p >= G.w;
-  const float a = G.z * ex2_approx(p);
+// One pixel's front-to-back step against one record of its tile's list;
+// p = log2(o G) (see sgs_pack_eig).  Every listed record is blended into every
+// pixel of the tile, as the reference blends every primitive into every pixel
+// (render.py:355-390); the lists hold the primitives whose support o G >= 1e-7
+// meets the tile (binning), so a listed record outside a pixel's support
+// contributes alpha < 1e-7, like the reference.
+// Liveness is carried in the sign of T: a pixel whose next transmittance
+// would fall below the cutoff keeps its last kept T, negated.  A terminated
+// pixel needs no separate test: its Tn is negative, so it is never kept
+// again, and re-terminating leaves -|T| unchanged.
+//   a = 2^p,  Tn = T max(1 - a, 0.01)
+//   keep = Tn >= T_keep:  C += min(a, 0.99) T c,  T = Tn;   else T = -|T|
+__device__ __forceinline__ bool blend_px(float p, const float4& c, float& T, float& C0, float& C1, float& C2,
+                                         float& w) {
+  const float a = ex2_approx(p);
   const float Tn = T * fmaxf(1.0f - a, SGS_ONE_MINUS_ALPHA_MAX);
-  const bool cmp = Tn >= SGS_T_KEEP;
-  kept = e && cmp;
-  float w = 0.0f;
-  if (kept) {
-    w = fminf(a, SGS_ALPHA_MAX) * T;
+  const bool keep = Tn >= SGS_T_KEEP;
+  w = fminf(a, SGS_ALPHA_MAX) * T;
+  if (keep) {
     C0 = fmaf(w, c.x, C0);
     C1 = fmaf(w, c.y, C1);
     C2 = fmaf(w, c.z, C2);
-    T = Tn;
-  } else if (e) {
-    T = -T;
   }
-  return w;
+  T = keep ? Tn : -fabsf(T);
+  return keep;
 }
 
 template <bool kImportance, bool kCount, bool kFilter, bool kTrack>
@@ -209,13 +213,14 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(ListArgs la, Sg
       cb = chi;
     }
     if (nb == 0) break;
-    // pad the batch to a whole number of vote groups with records no pixel is
-    // inside (pmin = +inf), so the group loop below needs no bounds checks
+    // pad the batch to a whole number of vote groups with records of zero
+    // opacity (log2 o = -inf), so the group loop below needs no bounds checks
     const int nb_pad = (nb + kVoteEvery - 1) / kVoteEvery * kVoteEvery;
     if (nb_pad != nb) {
       if (t < nb_pad - nb) {
-        s.geo[nb + t] = make_float4(0.0f, 0.0f, 0.0f, INFINITY);
+        s.geo[nb + t] = make_float4(0.0f, 0.0f, -INFINITY, 0.0f);
         s.con[nb + t] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        s.col[nb + t] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
       }
       __syncthreads();
     }
@@ -224,29 +229,33 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(ListArgs la, Sg
 #pragma unroll
       for (int j = 0; j < kVoteEvery; ++j) {
         const int kk = k + j;
-        const float4 G = s.geo[kk];
-        const float4 E = s.con[kk];  // eigen form (ux, uy, a1, a2)
+        const float4 G = s.geo[kk];  // (mx, my, log2 o_eff, -)
+        const float4 E = s.con[kk];  // scaled eigen form (s1 ux, s1 uy, s2 ux, s2 uy)
         const float dx = fx - G.x;
         const float dy0 = fy0 - G.y, dy1 = dy0 + 1.0f;
-        const float uxdx = E.x * dx, uydx = E.y * dx;
-        const float t10 = fmaf(E.y, dy0, uxdx), t20 = fmaf(E.x, dy0, -uydx);
-        const float t11 = fmaf(E.y, dy1, uxdx), t21 = fmaf(E.x, dy1, -uydx);
-        const float p0 = fmaf(E.z * t10, t10, (E.w * t20) * t20);
-        const float p1 = fmaf(E.z * t11, t11, (E.w * t21) * t21);
+        const float e1dx = E.x * dx, e3dx = E.w * dx;
+        const float t10 = fmaf(E.y, dy0, e1dx), t20 = fmaf(E.z, dy0, -e3dx);
+        const float t11 = fmaf(E.y, dy1, e1dx), t21 = fmaf(E.z, dy1, -e3dx);
+        const float p0 = fmaf(-t10, t10, fmaf(-t20, t20, G.z));
+        const float p1 = fmaf(-t11, t11, fmaf(-t21, t21, G.z));
         if (kCount && kk < nb) reached += (uint32_t)(T0 > 0.0f) + (uint32_t)(T1 > 0.0f);
-        if (warp_any((T0 > 0.0f && p0 >= G.w) || (T1 > 0.0f && p1 >= G.w))) {
+        {
           const float4 c = s.col[kk];
-          bool k0, k1;
-          const float w0 = blend_px(p0, G, c, T0, C00, C01, C02, k0);
-          const float w1 = blend_px(p1, G, c, T1, C10, C11, C12, k1);
-          if (kTrack) {
+          float w0, w1;
+          const bool k0 = blend_px(p0, c, T0, C00, C01, C02, w0);
+          const bool k1 = blend_px(p1, c, T1, C10, C11, C12, w1);
+          if (kTrack && kk < nb) {  // padding records are never counted
             const uint32_t idx = hits_before + (uint32_t)kk + 1u;
             if (k0) nc0 = idx;
             if (k1) nc1 = idx;
           }
           if (kImportance) {
-            const float ws = warp_sum(w0 + w1);
-            if (lane == 0 && ws != 0.0f) atomicAdd(&weight_sums[s.id[kk]], ws);
+            w0 = k0 ? w0 : 0.0f;
+            w1 = k1 ? w1 : 0.0f;
+            if (warp_any(w0 != 0.0f || w1 != 0.0f)) {
+              const float ws = warp_sum(w0 + w1);
+              if (lane == 0 && ws != 0.0f) atomicAdd(&weight_sums[s.id[kk]], ws);
+            }
           }
         }
       }
@@ -342,19 +351,18 @@ __global__ void __launch_bounds__(kBwdThreads) raster_bwd_kernel(ListArgs la, Sg
     for (int k = nb - 1; k >= 0; --k) {
       const uint32_t idx = base + (uint32_t)k;
       if (__all_sync(0xffffffffu, idx >= nc)) continue;
-      const float4 G = s.geo[k];
-      const float4 E = s.con[k];  // eigen form (ux, uy, a1, a2)
+      const float4 G = s.geo[k];  // (mx, my, log2 o_eff, -)
+      const float4 E = s.con[k];  // scaled eigen form (s1 ux, s1 uy, s2 ux, s2 uy)
       const float dx = fx - G.x, dy = fy - G.y;
-      const float t1 = fmaf(E.y, dy, E.x * dx), t2 = fmaf(E.x, dy, -(E.y * dx));
-      const float p = fmaf(E.z * t1, t1, (E.w * t2) * t2);
-      const bool active = idx < nc && p >= G.w;
+      const float t1 = fmaf(E.y, dy, E.x * dx), t2 = fmaf(E.z, dy, -(E.w * dx));
+      const float p = fmaf(-t1, t1, fmaf(-t2, t2, G.z));
+      const bool active = idx < nc;
       float v[kGrad];
 #pragma unroll
       for (int c = 0; c < kGrad; ++c) v[c] = 0.0f;
       if (active) {
         const float4 col = s.col[k];
-        const float Gv = ex2_approx(p);
-        const float a = G.z * Gv;
+        const float a = ex2_approx(p);
         const float alpha = fminf(a, SGS_ALPHA_MAX);
         const float om = fmaxf(1.0f - a, SGS_ONE_MINUS_ALPHA_MAX);
         const float Ti = T / om;
@@ -363,7 +371,7 @@ __global__ void __launch_bounds__(kBwdThreads) raster_bwd_kernel(ListArgs la, Sg
         const float dalpha = (a < SGS_ALPHA_MAX) ? (Ti * cg - S / om) : 0.0f;
         S += w * cg;
         T = Ti;
-        const float dq = -0.5f * G.z * Gv * dalpha;
+        const float dq = -0.5f * a * dalpha;
         v[0] = w * g0;
         v[1] = w * g1;
         v[2] = w * g2;

@@ -611,27 +611,34 @@ SGS_HD void sgs_color(const float pos[3], const float diffuse[3], const float* a
   c[2] = fmaxf(c_pre[2], 0.0f);
 }
 
-// Raster record packing: the forward kernel evaluates
-//   p2 = A dx^2 + B dx dy + C dy^2  (= -q/2 * log2 e),  G = 2^p2,
-// and skips the pair when p2 < pmin (= -qmax/2 * log2 e), i.e. q > qmax.
-//   geo = (mx, my, o_eff, pmin), con = (A, B, C, 0)
-// Raster record of the eigen form: eig = (ux, uy, a1, a2) with
-//   p2 = a1 (ux dx + uy dy)^2 + a2 (ux dy - uy dx)^2,  a = -log2(e)/2 / l.
-// Both terms are <= 0, so unlike the (A, B, C) form there is no cancellation
-// for elongated splats; this is what the rasterizers evaluate per pixel.
+// Raster record packing.  The binning stage reads
+//   geo = (mx, my, lo, pmin), con = (A, B, C, kx)
+// where p2 = A dx^2 + B dx dy + C dy^2 (= -q/2 * log2 e) and pmin = -qmax/2 *
+// log2 e bound the support (sgs_span).  The rasterizers evaluate the same
+// quadratic in a scaled eigen form, with the opacity folded in:
+//   eig = (s1 ux, s1 uy, s2 ux, s2 uy),  s_i = sqrt(log2(e) / (2 l_i)),
+//   t1 = s1 (ux dx + uy dy),  t2 = s2 (ux dy - uy dx),
+//   p  = lo - t1^2 - t2^2 = log2(o_eff G),   alpha = min(2^p, 0.99),
+// with lo = log2(o_eff).  Every term is <= 0, so there is no cancellation for
+// elongated splats, and the support test o_eff G >= SGS_EPS is the constant
+// comparison p >= SGS_LOG2_EPS.
+#define SGS_LOG2_EPS (-23.253496664211536f)  // log2(1e-7)
+
 SGS_HD void sgs_pack_eig(const SgsProj* p, float eig[4]) {
-  const float k = -0.5f * SGS_LOG2E;
-  eig[0] = p->ux;
-  eig[1] = p->uy;
-  eig[2] = F_MUL(k, p->ilmax);
-  eig[3] = F_MUL(k, p->ilmin);
+  const float k = 0.5f * SGS_LOG2E;
+  const float s1 = F_SQRT(F_MUL(k, p->ilmax));
+  const float s2 = F_SQRT(F_MUL(k, p->ilmin));
+  eig[0] = F_MUL(s1, p->ux);
+  eig[1] = F_MUL(s1, p->uy);
+  eig[2] = F_MUL(s2, p->ux);
+  eig[3] = F_MUL(s2, p->uy);
 }
 
 SGS_HD void sgs_pack_geo(const SgsProj* p, float geo[4], float con[4]) {
   const float k = -0.5f * SGS_LOG2E;
   geo[0] = p->mx;
   geo[1] = p->my;
-  geo[2] = p->o_eff;
+  geo[2] = F_MUL(sgs_logf(p->o_eff), SGS_LOG2E);
   geo[3] = F_MUL(k, p->qmax);
   con[0] = F_MUL(k, p->con00);
   con[1] = F_MUL(2.0f * k, p->con01);
