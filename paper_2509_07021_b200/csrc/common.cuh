@@ -58,6 +58,7 @@ struct Layout {
   int64_t cap;
   // offsets into the workspace
   uint64_t counters, rec_geo, rec_con, rec_col, rec_span, rec_eig, depth_key, rect, tiles_touched, super_touched, cand_end;
+  uint64_t cell_order;
   uint64_t dkey_alt, dkey_tmp, didx, didx_alt, offsets, scan_blocks;
   uint64_t ent_key, ent_key_alt, ent_val, ent_val_alt, ranges;
   uint64_t hist, status;
@@ -122,6 +123,7 @@ inline int make_layout(const sgs_workspace* ws, Layout* lo) {
   lo->tiles_touched = take(n * 4);
   lo->super_touched = take(n * 4);
   lo->cand_end = take((uint64_t)lo->n_tiles * 4);
+  lo->cell_order = take((uint64_t)(lo->n_tiles > lo->n_super ? lo->n_tiles : lo->n_super) * 4);
   lo->dkey_alt = take(n * 4);
   lo->dkey_tmp = take(n * 4);
   lo->didx = take(n * 4);

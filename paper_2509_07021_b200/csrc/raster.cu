@@ -51,11 +51,74 @@ struct ListArgs {
   const float4* eig;
   const float4* span;
   uint32_t* cand_end;       // per tile: one past the last candidate any pixel kept
+  const uint32_t* order;    // raster dispatch order of the window's cells (longest list first)
   int super_x;
+  int cell_base;            // first cell of the tile-row window
 };
 
 __device__ __forceinline__ int list_cell(bool filter, int tx, int ty, int tile, int super_x) {
   return filter ? (ty / SGS_SUPER) * super_x + tx / SGS_SUPER : tile;
+}
+
+// Tile of CTA `b` in cost order: the forward raster's CTAs walk the window's
+// cells longest list first (cell_order_kernel), so the heaviest tiles start in
+// the first wave instead of forming the tail.  In depth-first mode a cell is
+// a 4x4-tile super-tile and 16 consecutive CTAs take its tiles.  Returns false
+// for tiles outside the image or the tile-row window.
+template <bool kFilter>
+__device__ __forceinline__ bool ordered_tile(const ListArgs& la, const SgsCam& cam, uint32_t b, int& tx, int& ty) {
+  if (kFilter) {
+    const int cell = (int)la.order[b >> 4] + la.cell_base;
+    const int sub = (int)(b & 15u);
+    tx = (cell % la.super_x) * SGS_SUPER + (sub & 3);
+    ty = (cell / la.super_x) * SGS_SUPER + (sub >> 2);
+  } else {
+    const int tile = (int)la.order[b] + la.cell_base;
+    tx = tile % cam.tiles_x;
+    ty = tile / cam.tiles_x;
+  }
+  return tx < cam.tiles_x && ty >= cam.tile_y0 && ty < cam.tile_y1;
+}
+
+// Dispatch order of the window's n cells, by decreasing list length (ties by
+// index): a bitonic sort of (~len, index) pairs in shared memory.  Windows
+// of more than kOrderMax cells keep the identity order.
+constexpr int kOrderMax = 8192;
+__global__ void __launch_bounds__(1024) cell_order_kernel(const uint2* __restrict__ ranges, int base, int n,
+                                                          uint32_t* __restrict__ order) {
+  extern __shared__ unsigned long long sk[];
+  if (n > kOrderMax) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) order[i] = (uint32_t)i;
+    return;
+  }
+  int P = 1;
+  while (P < n) P <<= 1;
+  for (int i = threadIdx.x; i < P; i += blockDim.x) {
+    unsigned long long v = ~0ull;
+    if (i < n) {
+      const uint2 r = ranges[base + i];
+      const uint32_t len = r.y > r.x ? r.y - r.x : 0u;
+      v = ((unsigned long long)(0xffffffffu - len) << 32) | (uint32_t)i;
+    }
+    sk[i] = v;
+  }
+  __syncthreads();
+  for (int k = 2; k <= P; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        const int l = i ^ j;
+        if (l > i) {
+          const unsigned long long a = sk[i], c = sk[l];
+          const bool up = (i & k) == 0;
+          if ((a > c) == up) {
+            sk[i] = c;
+            sk[l] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) order[i] = (uint32_t)sk[i];
 }
 
 // Shared-memory staging buffer of N records.
@@ -184,8 +247,9 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(ListArgs la, Sg
   __shared__ Stage<kFwdBuf> s;
   __shared__ uint32_t s_kend;
 
-  const int tile = blockIdx.x + cam.tile_y0 * cam.tiles_x;
-  const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
+  int tx, ty;
+  if (!ordered_tile<kFilter>(la, cam, blockIdx.x, tx, ty)) return;
+  const int tile = ty * cam.tiles_x + tx;
   const int t = threadIdx.x, lane = t & 31;
   const int px = tx * SGS_TILE + (t & 15);
   const int py0 = ty * SGS_TILE + 2 * (t >> 4);  // rows py0 and py0 + 1
@@ -479,16 +543,42 @@ static ListArgs list_args(const sgs_workspace* ws, const Layout& lo, const uint3
   a.eig = at<float4>(ws, lo.rec_eig);
   a.span = at<float4>(ws, lo.rec_span);
   a.cand_end = at<uint32_t>(ws, lo.cand_end);
+  a.order = at<uint32_t>(ws, lo.cell_order);
   a.super_x = lo.super_x;
+  a.cell_base = 0;
   return a;
 }
 
 int launch_raster_fwd(const SgsCam& cam, float3 bg, const sgs_workspace* ws, const Layout& lo, const uint32_t* vals,
                       float* img, float* T, uint32_t* nc, float* weight_sums, unsigned long long* pairs,
                       cudaStream_t st) {
-  const int grid = (cam.tile_y1 - cam.tile_y0) * cam.tiles_x;
-  const ListArgs a = list_args(ws, lo, vals);
+  ListArgs a = list_args(ws, lo, vals);
   const bool filt = lo.sort_mode == SGS_SORT_DEPTH_FIRST;
+  // cells of the tile-row window, then their dispatch order
+  int n_cells, grid;
+  if (filt) {
+    const int sr0 = cam.tile_y0 / SGS_SUPER, sr1 = (cam.tile_y1 - 1) / SGS_SUPER;
+    a.cell_base = sr0 * lo.super_x;
+    n_cells = (sr1 - sr0 + 1) * lo.super_x;
+    grid = n_cells * SGS_SUPER * SGS_SUPER;
+  } else {
+    a.cell_base = cam.tile_y0 * cam.tiles_x;
+    n_cells = (cam.tile_y1 - cam.tile_y0) * cam.tiles_x;
+    grid = n_cells;
+  }
+  {
+    static bool attr_set = false;
+    const int smem = kOrderMax * (int)sizeof(unsigned long long);
+    if (!attr_set) {
+      SGS_CUDA(cudaFuncSetAttribute(cell_order_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      attr_set = true;
+    }
+    int P = 1;
+    while (P < n_cells) P <<= 1;
+    const size_t dyn = n_cells > kOrderMax ? 0 : (size_t)P * sizeof(unsigned long long);
+    cell_order_kernel<<<1, 1024, dyn, st>>>(a.ranges, a.cell_base, n_cells, at<uint32_t>(ws, lo.cell_order));
+    SGS_LAUNCH_CHECK("cell_order_kernel");
+  }
 #define SGS_FWD(I, C, F, K) \
   raster_fwd_kernel<I, C, F, K><<<grid, kFwdThreads, 0, st>>>(a, cam, bg, img, T, nc, weight_sums, pairs)
 #define SGS_FWD_TRACK(I, C, F) \
