@@ -147,26 +147,6 @@ __device__ __forceinline__ KT make_key(uint32_t tile, uint32_t dbits) {
   return (KT)tile;
 }
 
-// Largest lane L with x_L <= k, for x non-decreasing across lanes and x_0 <= k.
-__device__ __forceinline__ int lane_search(uint32_t x, uint32_t k) {
-  int L = 0;
-#pragma unroll
-  for (int step = 16; step >= 1; step >>= 1) {
-    const int c = L + step;
-    if (__shfl_sync(0xffffffffu, x, c & 31) <= k && c < 32) L = c;
-  }
-  return L;
-}
-
-__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
-    if (lane >= o) v += y;
-  }
-  return v;
-}
-
 // Emission (K2), warp-cooperative and load-balanced.  A warp takes 32
 // consecutive primitives in rank order; their entries form one contiguous
 // output range, ordered by (primitive, row, column).  The warp flattens the

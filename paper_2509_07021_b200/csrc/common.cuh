@@ -13,8 +13,8 @@ namespace sgs {
 
 constexpr int kNumSMs = 148;
 constexpr int kRadixThreads = 512;  // = kRsThreads in sort.cuh
-constexpr int kTileSortIPT = 8;   // items per thread, tile-key onesweep passes (4096 per CTA)
-constexpr int kDepthSortIPT = 8;
+constexpr int kTileSortIPT = 16;  // items per thread, tile-key onesweep passes (8192 per CTA)
+constexpr int kDepthSortIPT = 16;  // 1M depth keys = 123 tiles: one wave of one CTA per SM
 constexpr int kKey64SortIPT = 6;
 constexpr uint32_t kMaxEntries = (1u << 30) - 1;  // look-back status packs 30-bit counts
 
@@ -203,6 +203,48 @@ inline int make_cam(const sgs_camera* c, const Layout& lo, SgsCam* out) {
   out->lowpass = c->lowpass;
   return SGS_OK;
 }
+
+
+// ------------------------------------------------------------ warp helpers
+#ifdef __CUDACC__
+// Largest lane L with x_L <= k, for x non-decreasing across lanes and x_0 <= k.
+__device__ __forceinline__ int lane_search(uint32_t x, uint32_t k) {
+  int L = 0;
+#pragma unroll
+  for (int step = 16; step >= 1; step >>= 1) {
+    const int c = L + step;
+    if (__shfl_sync(0xffffffffu, x, c & 31) <= k && c < 32) L = c;
+  }
+  return L;
+}
+
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += y;
+  }
+  return v;
+}
+
+
+// Broadcast lane `src`'s span record to every lane.
+__device__ __forceinline__ SgsSpan shfl_span(const SgsSpan& s, int src) {
+  SgsSpan o;
+  o.mx = __shfl_sync(0xffffffffu, s.mx, src);
+  o.my = __shfl_sync(0xffffffffu, s.my, src);
+  o.A = __shfl_sync(0xffffffffu, s.A, src);
+  o.B = __shfl_sync(0xffffffffu, s.B, src);
+  o.C = __shfl_sync(0xffffffffu, s.C, src);
+  o.pmin = __shfl_sync(0xffffffffu, s.pmin, src);
+  o.kx = __shfl_sync(0xffffffffu, s.kx, src);
+  o.xm = __shfl_sync(0xffffffffu, s.xm, src);
+  o.ym = __shfl_sync(0xffffffffu, s.ym, src);
+  o.i2a = __shfl_sync(0xffffffffu, s.i2a, src);
+  o.valid = __shfl_sync(0xffffffffu, s.valid, src);
+  return o;
+}
+#endif
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 

@@ -15,40 +15,86 @@ __device__ __forceinline__ void warp_count(unsigned long long* ctr, bool pred) {
   if ((threadIdx.x & 31) == 0 && m) atomicAdd(ctr, (unsigned long long)__popc(m));
 }
 
-__global__ void __launch_bounds__(256) preprocess_kernel(sgs_params P, SgsCam cam, float4* __restrict__ rec_geo,
+// The exact tile counts are the expensive part: one ellipse-row span (two
+// quadratic roots) per tile row the support rectangle covers, and the row
+// count varies 1..>10 across a warp.  They are computed warp-cooperatively:
+// the warp's primitives' super-tile rows (4 tile rows each) are flattened
+// into one list and processed 32 at a time, lane = super row, and each row's
+// tile and super-tile counts are summed into its primitive's shared-memory
+// slot.  The spans are sgs_super_row_spans -- the definition the emission and
+// the CPU restatement use -- so the counts agree bit for bit.
+template <int kL>
+__global__ void __launch_bounds__(256, 3) preprocess_kernel(sgs_params P, SgsCam cam, float4* __restrict__ rec_geo,
                                                          float4* __restrict__ rec_con, float4* __restrict__ rec_col,
                                                          float4* __restrict__ rec_span,
                                                          float4* __restrict__ rec_eig,
                                                          uint32_t* __restrict__ depth_key, uint2* __restrict__ rect,
                                                          uint32_t* __restrict__ tiles_touched,
                                                          uint32_t* __restrict__ super_touched, Counters* ctr) {
+  __shared__ uint32_t s_cnt[8][32], s_sup[8][32];
   const int64_t n = P.n;
-  const int L = P.n_lobes;
+  const int L = kL > 0 ? kL : P.n_lobes;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  // iterate whole warps so the ballot counters see converged warps
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // iterate whole warps so the ballots and the cooperative row loop see converged warps
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
     const int64_t i = base + threadIdx.x;
-    bool live = i < n;
-    bool visible = false, emitting = false;
-    uint32_t cnt = 0;
+    const bool live = i < n;
+    bool visible = false;
+    SgsProj pr;
+    pr.emits = 0;
+    pr.tx0 = pr.ty0 = 0;
+    pr.tx1 = pr.ty1 = -1;
+    float pos[3] = {0.0f, 0.0f, 0.0f};
+    float g[4], k[4];
+    SgsSpan sp;
+    sp.valid = 0;
     if (live) {
-      float pos[3] = {P.position[3 * i], P.position[3 * i + 1], P.position[3 * i + 2]};
+      pos[0] = P.position[3 * i];
+      pos[1] = P.position[3 * i + 1];
+      pos[2] = P.position[3 * i + 2];
       float4 q4 = reinterpret_cast<const float4*>(P.quat)[i];
       float quat[4] = {q4.x, q4.y, q4.z, q4.w};
       float ls[3] = {P.log_scale[3 * i], P.log_scale[3 * i + 1], P.log_scale[3 * i + 2]};
       float pm = P.prim_mask ? P.prim_mask[i] : 1.0f;
-      SgsProj pr;
       sgs_project(pos, quat, ls, P.opacity[i], pm, &cam, &pr);
       visible = pr.visible;
-      uint32_t nsup = 0;
-      float g[4], k[4];
-      SgsSpan sp;
       if (pr.emits) {
         sgs_pack_geo(&pr, g, k);
         sp = sgs_span(g, k);
-        sgs_count_hits_span(&sp, pr.tx0, pr.ty0, pr.tx1, pr.ty1, &cam, &cnt, &nsup);
       }
-      emitting = cnt > 0;
+    }
+    // ---- exact counts, one super-tile row per lane
+    const uint32_t nitems = pr.emits ? (uint32_t)(pr.ty1 / SGS_SUPER - pr.ty0 / SGS_SUPER + 1) : 0u;
+    s_cnt[warp][lane] = 0;
+    s_sup[warp][lane] = 0;
+    __syncwarp();
+    const uint32_t incl = warp_incl_scan(nitems, lane);
+    const uint32_t start = incl - nitems;
+    const uint32_t R = __shfl_sync(0xffffffffu, incl, 31);
+    for (uint32_t k0 = 0; k0 < R; k0 += 32) {
+      const uint32_t kk = k0 + lane;
+      const int owner = lane_search(start, kk < R ? kk : R - 1);
+      const SgsSpan os = shfl_span(sp, owner);
+      const int otx0 = __shfl_sync(0xffffffffu, pr.tx0, owner);
+      const int oty0 = __shfl_sync(0xffffffffu, pr.ty0, owner);
+      const int otx1 = __shfl_sync(0xffffffffu, pr.tx1, owner);
+      const int oty1 = __shfl_sync(0xffffffffu, pr.ty1, owner);
+      const uint32_t ostart = __shfl_sync(0xffffffffu, start, owner);
+      if (kk < R) {
+        const int sr = oty0 / SGS_SUPER + (int)(kk - ostart);
+        int rf[SGS_SUPER], rc[SGS_SUPER], fsc;
+        const int nsc = sgs_super_row_spans(&os, &cam, otx0, oty0, otx1, oty1, sr, rf, rc, &fsc);
+        const uint32_t nt = (uint32_t)(rc[0] + rc[1] + rc[2] + rc[3]);
+        if (nt) atomicAdd(&s_cnt[warp][owner], nt);
+        if (nsc) atomicAdd(&s_sup[warp][owner], (uint32_t)nsc);
+      }
+    }
+    __syncwarp();
+    const uint32_t cnt = s_cnt[warp][lane];
+    const uint32_t nsup = s_sup[warp][lane];
+    const bool emitting = cnt > 0;
+    if (live) {
       tiles_touched[i] = cnt;
       super_touched[i] = nsup;
       depth_key[i] = emitting ? sgs_float_to_bits(pr.depth) : 0x7fffffffu;
@@ -57,9 +103,12 @@ __global__ void __launch_bounds__(256) preprocess_kernel(sgs_params P, SgsCam ca
       if (emitting) {
         float diffuse[3] = {P.diffuse[3 * i], P.diffuse[3 * i + 1], P.diffuse[3 * i + 2]};
         float axis[3 * SGS_MAX_LOBES], sharp[SGS_MAX_LOBES], amp[3 * SGS_MAX_LOBES], lm[SGS_MAX_LOBES];
-        for (int l = 0; l < L; ++l) {
+#pragma unroll
+        for (int l = 0; l < (kL > 0 ? kL : SGS_MAX_LOBES); ++l) {
+          if (kL == 0 && l >= L) break;
           sharp[l] = P.sharpness[i * L + l];
           lm[l] = P.lobe_mask[i * L + l];
+#pragma unroll
           for (int kk = 0; kk < 3; ++kk) {
             axis[3 * l + kk] = P.axis_raw[(i * L + l) * 3 + kk];
             amp[3 * l + kk] = P.amplitude[(i * L + l) * 3 + kk];
@@ -82,7 +131,7 @@ __global__ void __launch_bounds__(256) preprocess_kernel(sgs_params P, SgsCam ca
     warp_count(&ctr->n_emitting, emitting);
     unsigned long long e = cnt;
     for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
-    if ((threadIdx.x & 31) == 0 && e) atomicAdd(&ctr->n_entries, e);
+    if (lane == 0 && e) atomicAdd(&ctr->n_entries, e);
   }
 }
 
@@ -171,12 +220,18 @@ int launch_project_records(const sgs_params& P, const SgsCam& cam, float* out, c
 int launch_preprocess(const sgs_params& P, const SgsCam& cam, const sgs_workspace* ws, const Layout& lo,
                       cudaStream_t st) {
   Counters* ctr = at<Counters>(ws, lo.counters);
-  int grid = persistent_grid((uint64_t)P.n, 256, 8);
-  preprocess_kernel<<<grid, 256, 0, st>>>(P, cam, at<float4>(ws, lo.rec_geo), at<float4>(ws, lo.rec_con),
-                                          at<float4>(ws, lo.rec_col), at<float4>(ws, lo.rec_span), at<float4>(ws, lo.rec_eig),
-                                          at<uint32_t>(ws, lo.depth_key),
-                                          at<uint2>(ws, lo.rect), at<uint32_t>(ws, lo.tiles_touched),
-                                          at<uint32_t>(ws, lo.super_touched), ctr);
+  int grid = persistent_grid((uint64_t)P.n, 256, 3);  // one wave at 3 resident CTAs per SM
+#define SGS_PRE(KL)                                                                                             \
+  preprocess_kernel<KL><<<grid, 256, 0, st>>>(P, cam, at<float4>(ws, lo.rec_geo), at<float4>(ws, lo.rec_con),    \
+                                              at<float4>(ws, lo.rec_col), at<float4>(ws, lo.rec_span),           \
+                                              at<float4>(ws, lo.rec_eig), at<uint32_t>(ws, lo.depth_key),        \
+                                              at<uint2>(ws, lo.rect), at<uint32_t>(ws, lo.tiles_touched),        \
+                                              at<uint32_t>(ws, lo.super_touched), ctr)
+  if (P.n_lobes == 3)
+    SGS_PRE(3);
+  else
+    SGS_PRE(0);
+#undef SGS_PRE
   SGS_LAUNCH_CHECK("preprocess_kernel");
   return SGS_OK;
 }

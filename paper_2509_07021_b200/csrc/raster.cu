@@ -91,6 +91,26 @@ __global__ void __launch_bounds__(1024) cell_order_kernel(const uint2* __restric
     for (int i = threadIdx.x; i < n; i += blockDim.x) order[i] = (uint32_t)i;
     return;
   }
+  if (n <= (int)blockDim.x) {
+    // small windows (1080p: 510 cells): rank by counting, one cell per thread
+    const int i = threadIdx.x;
+    uint32_t len = 0;
+    if (i < n) {
+      const uint2 r = ranges[base + i];
+      len = r.y > r.x ? r.y - r.x : 0u;
+      sk[i] = len;
+    }
+    __syncthreads();
+    if (i < n) {
+      int rank = 0;
+      for (int j = 0; j < n; ++j) {
+        const uint32_t lj = (uint32_t)sk[j];
+        rank += (lj > len || (lj == len && j < i)) ? 1 : 0;
+      }
+      order[rank] = (uint32_t)i;
+    }
+    return;
+  }
   int P = 1;
   while (P < n) P <<= 1;
   for (int i = threadIdx.x; i < P; i += blockDim.x) {
@@ -575,7 +595,7 @@ int launch_raster_fwd(const SgsCam& cam, float3 bg, const sgs_workspace* ws, con
     }
     int P = 1;
     while (P < n_cells) P <<= 1;
-    const size_t dyn = n_cells > kOrderMax ? 0 : (size_t)P * sizeof(unsigned long long);
+    const size_t dyn = n_cells > kOrderMax ? 0 : (size_t)(P > 1024 ? P : 1024) * sizeof(unsigned long long);
     cell_order_kernel<<<1, 1024, dyn, st>>>(a.ranges, a.cell_base, n_cells, at<uint32_t>(ws, lo.cell_order));
     SGS_LAUNCH_CHECK("cell_order_kernel");
   }
