@@ -80,65 +80,48 @@ __device__ __forceinline__ bool ordered_tile(const ListArgs& la, const SgsCam& c
   return tx < cam.tiles_x && ty >= cam.tile_y0 && ty < cam.tile_y1;
 }
 
-// Dispatch order of the window's n cells, by decreasing list length (ties by
-// index): a bitonic sort of (~len, index) pairs in shared memory.  Windows
-// of more than kOrderMax cells keep the identity order.
-constexpr int kOrderMax = 8192;
+// Dispatch order of the window's n cells, longest lists first: a counting
+// sort on 64 length classes (log2 of the length with one mantissa bit),
+// descending.  Only the raster's CTA scheduling depends on this order (not
+// any result), so ties within a class are placed by shared-memory atomics.
+constexpr int kOrderClasses = 64;
+__device__ __forceinline__ int length_class(uint32_t len) {
+  if (len == 0) return 0;
+  const int e = 31 - __clz(len);                                 // floor(log2 len)
+  const int half = e > 0 ? (int)((len >> (e - 1)) & 1u) : 0;    // next bit
+  const int c = 2 * e + half + 1;
+  return c < kOrderClasses ? c : kOrderClasses - 1;
+}
+
 __global__ void __launch_bounds__(1024) cell_order_kernel(const uint2* __restrict__ ranges, int base, int n,
                                                           uint32_t* __restrict__ order) {
-  extern __shared__ unsigned long long sk[];
-  if (n > kOrderMax) {
-    for (int i = threadIdx.x; i < n; i += blockDim.x) order[i] = (uint32_t)i;
-    return;
-  }
-  if (n <= (int)blockDim.x) {
-    // small windows (1080p: 510 cells): rank by counting, one cell per thread
-    const int i = threadIdx.x;
-    uint32_t len = 0;
-    if (i < n) {
-      const uint2 r = ranges[base + i];
-      len = r.y > r.x ? r.y - r.x : 0u;
-      sk[i] = len;
-    }
-    __syncthreads();
-    if (i < n) {
-      int rank = 0;
-      for (int j = 0; j < n; ++j) {
-        const uint32_t lj = (uint32_t)sk[j];
-        rank += (lj > len || (lj == len && j < i)) ? 1 : 0;
-      }
-      order[rank] = (uint32_t)i;
-    }
-    return;
-  }
-  int P = 1;
-  while (P < n) P <<= 1;
-  for (int i = threadIdx.x; i < P; i += blockDim.x) {
-    unsigned long long v = ~0ull;
-    if (i < n) {
-      const uint2 r = ranges[base + i];
-      const uint32_t len = r.y > r.x ? r.y - r.x : 0u;
-      v = ((unsigned long long)(0xffffffffu - len) << 32) | (uint32_t)i;
-    }
-    sk[i] = v;
+  __shared__ uint32_t hist[kOrderClasses];
+  __shared__ uint32_t cursor[kOrderClasses];
+  const int t = threadIdx.x;
+  if (t < kOrderClasses) hist[t] = 0;
+  __syncthreads();
+  for (int i = t; i < n; i += blockDim.x) {
+    const uint2 r = ranges[base + i];
+    atomicAdd(&hist[length_class(r.y > r.x ? r.y - r.x : 0u)], 1u);
   }
   __syncthreads();
-  for (int k = 2; k <= P; k <<= 1)
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < P; i += blockDim.x) {
-        const int l = i ^ j;
-        if (l > i) {
-          const unsigned long long a = sk[i], c = sk[l];
-          const bool up = (i & k) == 0;
-          if ((a > c) == up) {
-            sk[i] = c;
-            sk[l] = a;
-          }
-        }
-      }
-      __syncthreads();
+  if (t < 32) {  // exclusive scan over classes, longest class first
+    const uint32_t a = hist[kOrderClasses - 1 - 2 * t], b = hist[kOrderClasses - 2 - 2 * t];
+    uint32_t x = a + b;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (t >= o) x += y;
     }
-  for (int i = threadIdx.x; i < n; i += blockDim.x) order[i] = (uint32_t)sk[i];
+    const uint32_t excl = x - a - b;
+    cursor[kOrderClasses - 1 - 2 * t] = excl;
+    cursor[kOrderClasses - 2 - 2 * t] = excl + a;
+  }
+  __syncthreads();
+  for (int i = t; i < n; i += blockDim.x) {
+    const uint2 r = ranges[base + i];
+    order[atomicAdd(&cursor[length_class(r.y > r.x ? r.y - r.x : 0u)], 1u)] = (uint32_t)i;
+  }
 }
 
 // Shared-memory staging buffer of N records.
@@ -587,16 +570,7 @@ int launch_raster_fwd(const SgsCam& cam, float3 bg, const sgs_workspace* ws, con
     grid = n_cells;
   }
   {
-    static bool attr_set = false;
-    const int smem = kOrderMax * (int)sizeof(unsigned long long);
-    if (!attr_set) {
-      SGS_CUDA(cudaFuncSetAttribute(cell_order_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      attr_set = true;
-    }
-    int P = 1;
-    while (P < n_cells) P <<= 1;
-    const size_t dyn = n_cells > kOrderMax ? 0 : (size_t)(P > 1024 ? P : 1024) * sizeof(unsigned long long);
-    cell_order_kernel<<<1, 1024, dyn, st>>>(a.ranges, a.cell_base, n_cells, at<uint32_t>(ws, lo.cell_order));
+    cell_order_kernel<<<1, 1024, 0, st>>>(a.ranges, a.cell_base, n_cells, at<uint32_t>(ws, lo.cell_order));
     SGS_LAUNCH_CHECK("cell_order_kernel");
   }
 #define SGS_FWD(I, C, F, K) \

@@ -433,35 +433,33 @@ SGS_HD float sgs_span_root(const SgsSpan* s, float dy, int right) {
 // oracle, so counts, keys and ranges agree bit for bit.  Returns the count
 // and the first hit column.
 SGS_HD int sgs_row_span(const SgsSpan* s, const SgsCam* cam, int ty, int tx0, int tx1, int* first) {
-  *first = 0;
-  if (!s->valid) return 0;
-  float yc0 = (float)(ty * SGS_TILE) + 0.5f;
-  float yc1 = (float)min_i32_(ty * SGS_TILE + SGS_TILE - 1, cam->height - 1) + 0.5f;
-  float dy0 = F_SUB(yc0, s->my), dy1 = F_SUB(yc1, s->my);
-  if (dy1 < -s->ym || dy0 > s->ym) return 0;
-  float dyr = F_MUL(s->kx, s->xm);  // dy of the rightmost point; leftmost is at -dyr
-  float xr, xl;
-  if (dyr >= dy0 && dyr <= dy1) {
-    xr = s->xm;
-  } else {
-    xr = sgs_span_root(s, dyr < dy0 ? dy0 : dy1, 1);
-  }
-  float dyl = -dyr;
-  if (dyl >= dy0 && dyl <= dy1) {
-    xl = -s->xm;
-  } else {
-    xl = sgs_span_root(s, dyl < dy0 ? dy0 : dy1, 0);
-  }
-  float XL = F_ADD(s->mx, xl), XR = F_ADD(s->mx, xr);
-  if (!(XR >= 0.5f && XL <= (float)cam->width - 0.5f && XL <= XR)) return 0;
+  // Branch-free: both crossings are always evaluated and the early outs are
+  // folded into `hit`, so the lanes of a warp never diverge here.  The values
+  // selected are exactly those of the branching definition above.
+  const float yc0 = (float)(ty * SGS_TILE) + 0.5f;
+  const float yc1 = (float)min_i32_(ty * SGS_TILE + SGS_TILE - 1, cam->height - 1) + 0.5f;
+  const float dy0 = F_SUB(yc0, s->my), dy1 = F_SUB(yc1, s->my);
+  int hit = s->valid && !(dy1 < -s->ym || dy0 > s->ym);
+  const float dyr = F_MUL(s->kx, s->xm);  // dy of the rightmost point; leftmost is at -dyr
+  const float dyl = -dyr;
+  const int rin = dyr >= dy0 && dyr <= dy1;
+  const int lin = dyl >= dy0 && dyl <= dy1;
+  const float rr = sgs_span_root(s, dyr < dy0 ? dy0 : dy1, 1);
+  const float rl = sgs_span_root(s, dyl < dy0 ? dy0 : dy1, 0);
+  const float xr = rin ? s->xm : rr;
+  const float xl = lin ? -s->xm : rl;
+  const float XL = F_ADD(s->mx, xl), XR = F_ADD(s->mx, xr);
+  hit = hit && (XR >= 0.5f && XL <= (float)cam->width - 0.5f && XL <= XR);
   const float inv_tile = 1.0f / SGS_TILE;
-  float flo = ceilf(F_MUL(F_SUB(XL, 15.5f), inv_tile));
-  float fhi = F_FLOOR(F_MUL(F_SUB(XR, 0.5f), inv_tile));
-  int lo = flo < (float)tx0 ? tx0 : (int)flo;
-  int hi = fhi > (float)tx1 ? tx1 : (int)fhi;
-  if (hi < lo) return 0;
-  *first = lo;
-  return hi - lo + 1;
+  const float flo = ceilf(F_MUL(F_SUB(XL, 15.5f), inv_tile));
+  const float fhi = F_FLOOR(F_MUL(F_SUB(XR, 0.5f), inv_tile));
+  // clamp to [tx0, tx1 + 1] / [tx0 - 1, tx1] before converting (integral
+  // floats, so identical to clamping after; NaN-safe via fmin/fmax)
+  const int lo = (int)fminf(fmaxf(flo, (float)tx0), (float)tx1 + 1.0f);
+  const int hi = (int)fmaxf(fminf(fhi, (float)tx1), (float)tx0 - 1.0f);
+  hit = hit && hi >= lo;
+  *first = hit ? lo : 0;
+  return hit ? hi - lo + 1 : 0;
 }
 
 // Number of tiles whose box meets the support, over the rectangle rows.
@@ -509,11 +507,14 @@ SGS_HD int sgs_super_row_spans(const SgsSpan* s, const SgsCam* cam, int tx0, int
                                int first[SGS_SUPER], int cnt[SGS_SUPER], int* first_sc) {
   int lo = 0x7fffffff, hi = -1;
   for (int r = 0; r < SGS_SUPER; ++r) {
+    // rows outside the rectangle are evaluated on a clamped row and masked
+    // (no divergence); their count is 0
     const int ty = sr * SGS_SUPER + r;
-    first[r] = 0;
-    cnt[r] = 0;
-    if (ty < ty0 || ty > ty1) continue;
-    cnt[r] = sgs_row_span(s, cam, ty, tx0, tx1, &first[r]);
+    const int in = ty >= ty0 && ty <= ty1;
+    int f;
+    const int c = sgs_row_span(s, cam, in ? ty : ty0, tx0, tx1, &f);
+    first[r] = in ? f : 0;
+    cnt[r] = in ? c : 0;
     if (cnt[r] > 0) {
       const int a = first[r] / SGS_SUPER, b = (first[r] + cnt[r] - 1) / SGS_SUPER;
       lo = a < lo ? a : lo;
