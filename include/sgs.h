@@ -211,6 +211,29 @@ int sgs_sort_temp_size(int64_t n, int32_t key_bits, uint64_t* bytes_out);
 int sgs_sort_pairs_u64(uint64_t* keys, uint32_t* values, int64_t n, int32_t key_bits, void* temp,
                        uint64_t temp_bytes, void* stream);
 
+/* Image loss (render.py:197-205, 433-509): (1 - lambda) L1 + lambda (1 - SSIM)
+ * with a normalised Gaussian window (odd, <= 31 taps) and zero padding. */
+typedef struct sgs_loss_config {
+  double lambda_ssim; /* LossConfig.lambda_ssim (0.2) */
+  int32_t window;     /* LossConfig.window (11) */
+  double sigma;       /* LossConfig.sigma (1.5) */
+  double c1, c2;      /* LossConfig.c1 / c2 (0.01^2, 0.03^2) */
+} sgs_loss_config;
+
+/* Device scratch bytes for sgs_image_loss on an H x W x 3 image. */
+int sgs_loss_workspace_size(int32_t height, int32_t width, uint64_t* bytes_out);
+
+/* Fused loss + dL/dimg -- replaces loss / ssim / _ssim_grad / _loss_and_dimg
+ * (render.py:464-509).  img and target are (H,W,3) device arrays, float32 or
+ * float64 (the *_is_f64 flags).  out (device, 3 doubles) receives
+ * [loss, mean |img - target|, mean SSIM].  dimg (float32) / dimg_f64 / ssim_map
+ * (float64, (H,W,3)) are optional (NULL to skip).  Statistics are accumulated
+ * in float64.  Never synchronises. */
+int sgs_image_loss(const void* img, int32_t img_is_f64, const void* target, int32_t target_is_f64,
+                   int32_t height, int32_t width, const sgs_loss_config* cfg, float* dimg,
+                   double* dimg_f64, double* ssim_map, double* out, void* workspace,
+                   uint64_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

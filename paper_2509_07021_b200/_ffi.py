@@ -54,6 +54,11 @@ class SgsStats(C.Structure):
                 ("n_bin_entries", C.c_uint64)]
 
 
+class SgsLossConfig(C.Structure):
+    _fields_ = [("lambda_ssim", C.c_double), ("window", C.c_int32), ("sigma", C.c_double),
+                ("c1", C.c_double), ("c2", C.c_double)]
+
+
 # every exported symbol and its signature (tests check the .so exports all of them)
 _P = C.POINTER
 SIGNATURES = {
@@ -83,6 +88,10 @@ SIGNATURES = {
     "sgs_sort_temp_size": (C.c_int, [C.c_int64, C.c_int32, _P(C.c_uint64)]),
     "sgs_sort_pairs_u64": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p,
                                      C.c_uint64, C.c_void_p]),
+    "sgs_loss_workspace_size": (C.c_int, [C.c_int32, C.c_int32, _P(C.c_uint64)]),
+    "sgs_image_loss": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+                                 _P(SgsLossConfig), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                 C.c_void_p, C.c_uint64, C.c_void_p]),
 }
 
 

@@ -80,6 +80,11 @@ static const uint32_t* final_vals(const sgs_workspace* ws, const Layout& lo) {
   return at<uint32_t>(ws, final_in_alt(lo) ? lo.ent_val_alt : lo.ent_val);
 }
 
+uint64_t loss_workspace_bytes(int H, int W);
+int launch_image_loss(const void* img, int img_f64, const void* tgt, int tgt_f64, int H, int W,
+                      const sgs_loss_config* cfg, float* dimg, double* dimg64, double* smap, double* out,
+                      void* workspace, uint64_t ws_bytes, cudaStream_t st);
+
 }  // namespace sgs
 
 using namespace sgs;
@@ -317,6 +322,22 @@ int sgs_sort_pairs_u64(uint64_t* keys, uint32_t* values, int64_t n, int32_t key_
   if (n == 0) return SGS_OK;
   return launch_sort_u64(reinterpret_cast<unsigned long long*>(keys), values, (uint32_t)n, key_bits, temp, temp_bytes,
                          as_stream(stream));
+}
+
+int sgs_loss_workspace_size(int32_t height, int32_t width, uint64_t* bytes_out) {
+  if (height < 1 || width < 1 || !bytes_out) {
+    set_error("invalid image size");
+    return SGS_E_ARG;
+  }
+  *bytes_out = loss_workspace_bytes(height, width);
+  return SGS_OK;
+}
+
+int sgs_image_loss(const void* img, int32_t img_is_f64, const void* target, int32_t target_is_f64, int32_t height,
+                   int32_t width, const sgs_loss_config* cfg, float* dimg, double* dimg_f64, double* ssim_map,
+                   double* out, void* workspace, uint64_t workspace_bytes, void* stream) {
+  return launch_image_loss(img, img_is_f64, target, target_is_f64, height, width, cfg, dimg, dimg_f64, ssim_map, out,
+                           workspace, workspace_bytes, as_stream(stream));
 }
 
 }  // extern "C"

@@ -3,7 +3,7 @@
 
 Same names, signatures, argument meaning, return types and errors as the
 reference; the work runs in libsgs.so (hand-written sm_100a CUDA) through the
-C ABI, the L1/SSIM loss runs on the GPU in float64 PyTorch.  Inputs are the
+C ABI, the L1/SSIM loss runs in the fused CUDA loss kernel (float64 statistics).  Inputs are the
 reference's float64 numpy arrays; they are rounded to float32 at the
 boundary (the GPU computes in fp32) and results come back as float64.
 
@@ -23,6 +23,7 @@ accepted for compatibility and ignored (the tiled renderer has no chunks).
 
 from __future__ import annotations
 
+import dataclasses
 from dataclasses import dataclass
 
 import numpy as np
@@ -30,6 +31,7 @@ import torch
 
 from . import _ffi
 from .camera import Camera, to_sgs
+from .loss import image_loss
 from .rasterizer import GRAD_FIELDS, GaussianTensors, Rasterizer
 
 ALPHA_MAX = 0.99
@@ -237,41 +239,12 @@ def accumulate_importance_params(p, cams, background=(0.0, 0.0, 0.0)) -> np.ndar
 
 
 # --------------------------------------------------------------------- loss
-def _gauss_window(window: int, sigma: float, device) -> torch.Tensor:
-    t = torch.arange(window, dtype=torch.float64, device=device) - (window - 1) / 2.0
-    g = torch.exp(-0.5 * (t / sigma) ** 2)
-    return g / g.sum()
-
-
-def _filt(x: torch.Tensor, k: torch.Tensor) -> torch.Tensor:
-    """Separable zero-padded correlation of (C, 1, H, W) planes."""
-    r = k.numel() // 2
-    x = torch.nn.functional.conv2d(x, k.view(1, 1, -1, 1), padding=(r, 0))
-    return torch.nn.functional.conv2d(x, k.view(1, 1, 1, -1), padding=(0, r))
-
-
-def _ssim_map(img: torch.Tensor, target: torch.Tensor, cfg: LossConfig) -> torch.Tensor:
-    k = _gauss_window(cfg.window, cfg.sigma, img.device)
-    x = img.permute(2, 0, 1).unsqueeze(1)
-    y = target.permute(2, 0, 1).unsqueeze(1)
-    mx, my = _filt(x, k), _filt(y, k)
-    sx = _filt(x * x, k) - mx * mx
-    sy = _filt(y * y, k) - my * my
-    sxy = _filt(x * y, k) - mx * my
-    return ((2 * mx * my + cfg.c1) * (2 * sxy + cfg.c2)) / ((mx * mx + my * my + cfg.c1) * (sx + sy + cfg.c2))
-
-
+# All loss math runs in the fused SSIM + L1 kernel (csrc/loss.cu, loss.py):
+# float64 statistics on the device, exact dL/dimg (render.py:469-509).
 def _t64(a) -> torch.Tensor:
     if isinstance(a, torch.Tensor):
         return a.to(device=_device(), dtype=torch.float64)
     return torch.as_tensor(np.asarray(a, dtype=np.float64), device=_device())
-
-
-def _loss_t(img: torch.Tensor, target: torch.Tensor, cfg: LossConfig) -> torch.Tensor:
-    l1 = (img - target).abs().mean()
-    if cfg.lambda_ssim == 0.0:
-        return (1.0 - cfg.lambda_ssim) * l1
-    return (1.0 - cfg.lambda_ssim) * l1 + cfg.lambda_ssim * (1.0 - _ssim_map(img, target, cfg).mean())
 
 
 def _check_shapes(img, target):
@@ -279,39 +252,35 @@ def _check_shapes(img, target):
         raise ValueError(f"image shape {tuple(np.shape(img))} != target {tuple(np.shape(target))}")
 
 
+def _with_ssim(cfg: LossConfig) -> LossConfig:
+    """The same window / constants with lambda = 1 (pure SSIM term)."""
+    return dataclasses.replace(cfg, lambda_ssim=1.0)
+
+
 def ssim(img, target, cfg: LossConfig = LossConfig()) -> float:
     _check_shapes(img, target)
-    return float(_ssim_map(_t64(img), _t64(target), cfg).mean())
+    out, _, _ = image_loss(_t64(img), _t64(target), _with_ssim(cfg), grad=None)
+    return float(out[2])
 
 
 def loss(img, target, cfg: LossConfig = LossConfig()) -> float:
     _check_shapes(img, target)
-    return float(_loss_t(_t64(img), _t64(target), cfg))
-
-
-def _loss_and_dimg_t(img: torch.Tensor, target: torch.Tensor, cfg: LossConfig):
-    """Loss and its exact gradient w.r.t. the image (float64 autograd of the
-    same formula; the L1 subgradient is sign(diff)/size as in render.py:504)."""
-    x = img.detach().to(torch.float64).requires_grad_(True)
-    y = target.detach().to(torch.float64)
-    val = _loss_t(x, y, cfg)
-    (dimg,) = torch.autograd.grad(val, x)
-    return float(val.detach()), dimg
+    out, _, _ = image_loss(_t64(img), _t64(target), cfg, grad=None)
+    return float(out[0])
 
 
 def _loss_and_dimg(img, target, cfg: LossConfig):
     _check_shapes(img, target)
-    val, d = _loss_and_dimg_t(_t64(img), _t64(target), cfg)
-    return val, _to_np64(d)
+    out, d, _ = image_loss(_t64(img), _t64(target), cfg, grad="f64")
+    return float(out[0]), _to_np64(d)
 
 
 def _ssim_grad(img, target, cfg: LossConfig):
     """d(mean SSIM)/d(img) and the SSIM map (render.py:469-486)."""
     _check_shapes(img, target)
-    x = _t64(img).requires_grad_(True)
-    smap = _ssim_map(x, _t64(target), cfg)
-    (g,) = torch.autograd.grad(smap.mean(), x)
-    return _to_np64(g), _to_np64(smap.squeeze(1).permute(1, 2, 0))
+    # with lambda = 1 the kernel's dL/dimg is -d(mean SSIM)/dimg
+    _, d, smap = image_loss(_t64(img), _t64(target), _with_ssim(cfg), grad="f64", ssim_map=True)
+    return -_to_np64(d), _to_np64(smap)
 
 
 def psnr(img: np.ndarray, target: np.ndarray) -> float:
@@ -331,12 +300,15 @@ def _grads_to_set(gr: dict) -> GradientSet:
 
 def loss_and_grads_device(g: GaussianTensors, cam, target: torch.Tensor, cfg: LossConfig = LossConfig(),
                           background=(0.0, 0.0, 0.0), rast: Rasterizer | None = None,
-                          mask_grads: bool = False):
-    """Device-resident variant: (loss float, dict of float32 gradient tensors)."""
+                          mask_grads: bool = False, sync: bool = True):
+    """Device-resident variant: (loss, dict of float32 gradient tensors).  The
+    loss is a float, or a 0-dim float64 device tensor with ``sync=False`` (no
+    host round trip)."""
     rast = rast or rasterizer()
     frame = rast.forward(g, cam, _bg(background))
-    val, dimg = _loss_and_dimg_t(frame.img, target, cfg)
-    return val, rast.backward(g, frame, dimg.to(torch.float32), mask_grads=mask_grads)
+    out, dimg, _ = image_loss(frame.img, target, cfg, grad="f32")
+    grads = rast.backward(g, frame, dimg, mask_grads=mask_grads)
+    return (float(out[0]) if sync else out[0]), grads
 
 
 def loss_and_grads(p, cam, target: np.ndarray, cfg: LossConfig = LossConfig(),

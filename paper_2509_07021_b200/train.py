@@ -72,7 +72,7 @@ class SoftPruneTrainer:
             return self.grad_fn(g, cam, target)
         from .render import LossConfig, loss_and_grads_device
         return loss_and_grads_device(g, cam, target, LossConfig(lambda_ssim=self.cfg.lambda_ssim),
-                                     rast=self.rast, mask_grads=True)
+                                     rast=self.rast, mask_grads=True, sync=False)
 
     def step(self, cams, targets, rank: int = 0, world: int = 1, apply: bool = True) -> float:
         """One step over all views (this rank renders its round-robin share);

@@ -83,6 +83,21 @@ def test_null_and_mismatched_arguments_fail_without_touching_the_device():
     assert lib.sgs_project_records(C.byref(p), C.byref(bad), None, None) == _ffi.SGS_E_ARG
 
 
+def test_loss_entry_validates_before_touching_the_device():
+    lib = _ffi.load()
+    nb = C.c_uint64()
+    assert lib.sgs_loss_workspace_size(720, 1280, C.byref(nb)) == _ffi.SGS_OK
+    assert nb.value == 3 * 720 * 1280 * 3 * 8
+    assert lib.sgs_loss_workspace_size(0, 4, C.byref(nb)) == _ffi.SGS_E_ARG
+    cfg = _ffi.SgsLossConfig(0.2, 10, 1.5, 1e-4, 9e-4)  # even window
+    out = C.c_void_p(1)
+    assert lib.sgs_image_loss(1, 0, 1, 0, 4, 4, C.byref(cfg), None, None, None, out, 1, 1 << 20,
+                              None) == _ffi.SGS_E_ARG
+    cfg.window = 11
+    assert lib.sgs_image_loss(1, 0, 1, 0, 4, 4, C.byref(cfg), None, None, None, out, 1, 8,
+                              None) == _ffi.SGS_E_WORKSPACE
+
+
 def test_camera_conventions_match_reference():
     cam = Camera.look_at(eye=(0.0, -2.5, 0.3), target=(0, 0, 0), width=16, height=16, fx=20)
     R = cam.rotation
