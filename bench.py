@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--sort-mode", type=int, default=0)
     ap.add_argument("--streams", type=int, default=4,
                     help="concurrent CUDA streams the views of a step are spread over")
+    ap.add_argument("--workload", default="render", choices=["render", "train", "stress"],
+                    help="render: configs[2] headline; train: configs[3] training step; "
+                         "stress: configs[4] 4K frame in tile strips")
     return ap.parse_args()
 
 
@@ -317,13 +320,15 @@ def run_ours(args):
     pinned = PinnedScene(scene)
     br = BatchRenderer(rast, device=dev)
     for _ in range(2):
-        br.render_views(pinned, my_cams)
+        br.render_views(pinned, my_cams, wait=False)
     torch.cuda.synchronize(dev)
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
-        br.render_views(pinned, my_cams)
+        # every step uploads the whole scene and reads back every image; the
+        # next step's upload overlaps this step's renders (double-buffered)
+        br.render_views(pinned, my_cams, wait=False)
     e1.record(stream)
     torch.cuda.synchronize(dev)
     barrier()
@@ -392,10 +397,184 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+# -------------------------------------------------------- configs[3] training
+def run_train(args):
+    """configs[3]: 500k Gaussians, 8 views 1280x720 per step, forward + fused
+    L1/SSIM loss + backward per view, mask gradients through the sigmoid,
+    gradients all-reduced (NCCL) over ranks.  Views are split over the ranks
+    (strong scaling: the 8-view step is fixed)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2509_07021_b200 import scenes
+    from paper_2509_07021_b200.render import LossConfig, loss_and_grads_device
+    from paper_2509_07021_b200.train import SoftPruneTrainer
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    group = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        group = dist.group.WORLD
+    n = args.n if args.n != 1_000_000 else 500_000
+    scene, cams = scenes.config3(n=n)
+    targets = [torch.from_numpy(scenes.target_image(0, c.height, c.width, v)).to(dev)
+               for v, c in enumerate(cams)]
+    tr = SoftPruneTrainer(scene, scene.extra["prim_logit"], scene.extra["lobe_logit"], device=dev,
+                          group=group)
+    for _ in range(max(args.warmup, 3)):
+        tr.step(cams, targets, rank, world, apply=False)
+    torch.cuda.synchronize(dev)
+    stream = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0.record(stream)
+    for _ in range(args.steps):
+        tr.step(cams, targets, rank, world, apply=True)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    clk = clocks.stop()
+    t_ms = e0.elapsed_time(e1)
+    # per-phase device time of one view (camera 0) on one stream
+    g = tr.gaussians()
+    rast = tr.rast
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    phases = {"forward": [], "loss": [], "backward": []}
+    from paper_2509_07021_b200.loss import image_loss
+    for _ in range(5):
+        ev[0].record(stream)
+        fr = rast.forward(g, cams[0], check=False)
+        ev[1].record(stream)
+        out, dimg, _ = image_loss(fr.img, targets[0], LossConfig())
+        ev[2].record(stream)
+        rast.backward(g, fr, dimg, mask_grads=True)
+        ev[3].record(stream)
+        torch.cuda.synchronize(dev)
+        phases["forward"].append(ev[0].elapsed_time(ev[1]))
+        phases["loss"].append(ev[1].elapsed_time(ev[2]))
+        phases["backward"].append(ev[2].elapsed_time(ev[3]))
+    t = torch.tensor([t_ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_ms = float(t[0])
+    views = len(cams) * args.steps
+    if rank == 0:
+        line = {"metric": "training views/s (configs[3]: fwd + L1/SSIM + bwd + mask grads + allreduce)",
+                "value": views / (t_ms / 1e3), "unit": "views/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms / args.steps,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic (seeded configs[3] distributions, U(0,1) targets)",
+                "config": {"workload": f"configs[3]: {n} Gaussians, 3 lobes, 8 views 1280x720, "
+                                       "soft masks, lambda_ssim 0.2",
+                           "parallelism": f"views split over {world} ranks, NCCL gradient allreduce"},
+                "phase_ms_per_view": {k: float(np.median(v)) for k, v in phases.items()},
+                "clocks": clk}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ------------------------------------------------------------ configs[4] stress
+def run_stress(args):
+    """configs[4]: 5M Gaussians, one 3840x2160 frame split into horizontal
+    tile strips balanced by a per-row cost estimate; rank r renders strip r
+    (Gaussians replicated, no collective).  One GPU renders all strips."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2509_07021_b200 import scenes
+    from paper_2509_07021_b200.rasterizer import GaussianTensors, Rasterizer
+    from paper_2509_07021_b200.sharding import balanced_strips, row_costs_from_rects
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n = args.n if args.n != 1_000_000 else 5_000_000
+    scene, (cam,) = scenes.config4(n=n)
+    rast = Rasterizer(device=dev)
+    g = GaussianTensors.from_arrays(scene, device=dev)
+    tiles_y = (cam.height + 15) // 16
+    # cost estimate from one preprocess pass (host-side strip planning)
+    f0 = rast.forward(g, cam, check=True, tile_rows=(0, 1), track=False)
+    _, rect, tt, _ = rast.export_projected(f0)
+    cost = row_costs_from_rects(rect.cpu().numpy().view(np.uint32), tt.cpu().numpy().view(np.uint32),
+                                tiles_y)
+    img = torch.empty((cam.height, cam.width, 3), device=dev)
+    T = torch.empty((cam.height, cam.width), device=dev)
+    # strips per rank: as few as keep one bin call under its entry limit
+    from paper_2509_07021_b200._ffi import CapacityError
+    per_rank = 1
+    while True:
+        strips = balanced_strips(cost, world * per_rank)[rank * per_rank:(rank + 1) * per_rank]
+        ok = 1.0
+        try:
+            for y0, y1 in strips:
+                rast.forward(g, cam, check=True, tile_rows=(y0, y1), out=(img, T, None), track=False)
+        except CapacityError:
+            ok = 0.0
+        if world > 1:  # every rank must use the same strip partition
+            f = torch.tensor([ok], device=dev)
+            dist.all_reduce(f, op=dist.ReduceOp.MIN)
+            ok = float(f[0])
+        if ok:
+            break
+        per_rank *= 2
+
+    def frame():
+        for y0, y1 in strips:
+            rast.forward(g, cam, check=False, tile_rows=(y0, y1), out=(img, T, None), track=False)
+
+    for _ in range(max(args.warmup, 3)):
+        frame()
+    torch.cuda.synchronize(dev)
+    stream = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0.record(stream)
+    for _ in range(args.steps):
+        frame()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    clk = clocks.stop()
+    t = torch.tensor([e0.elapsed_time(e1)], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_ms = float(t[0])
+    ent = 0
+    for y0, y1 in strips:
+        ent += rast.forward(g, cam, check=True, tile_rows=(y0, y1), out=(img, T, None),
+                            track=False).stats()["n_entries"]
+    if rank == 0:
+        line = {"metric": "frames/s (configs[4]: 5M Gaussians, 3840x2160, tile strips)",
+                "value": args.steps / (t_ms / 1e3), "unit": "frames/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms / args.steps,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic (seeded configs[4] distributions)",
+                "config": {"workload": f"configs[4]: {n} Gaussians, 3840x2160, FoV 60, radius 2.5",
+                           "strips": [list(s) for s in strips], "ranks": world},
+                "tile_entries_rank0": int(ent), "clocks": clk}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.workload == "train":
+        run_train(args)
+    elif args.workload == "stress":
+        run_stress(args)
     else:
         run_ours(args)
 

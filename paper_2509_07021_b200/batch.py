@@ -45,14 +45,24 @@ class PinnedScene:
 
 
 class BatchRenderer:
-    """render_views(pinned_scene, cams) -> list of (H, W, 3) float32 host arrays."""
+    """render_views(pinned_scene, cams) -> list of (H, W, 3) float32 host arrays.
+
+    Scenes are uploaded into one of two device-resident copies on a dedicated
+    host-to-device stream, so with ``wait=False`` the upload of the next
+    call's scene overlaps the renders and image read-backs of this one (the
+    copy engines run both directions at once).  Every call still moves its
+    whole scene host -> device and every image device -> host."""
 
     def __init__(self, rast: Rasterizer | None = None, device="cuda", streams: int = 4):
         self.rast = rast or Rasterizer(device=device)
         self.device = torch.device(device)
         self.copy_stream = torch.cuda.Stream(device=self.device)
+        self.h2d_stream = torch.cuda.Stream(device=self.device)
         self.streams = [torch.cuda.Stream(device=self.device) for _ in range(max(streams, 1))]
         self._host = {}
+        self._dev = [None, None]      # two device copies of the scene
+        self._free = [None, None]     # event: renders of the copy's last use finished
+        self._calls = 0
 
     def _host_buf(self, k, shape):
         buf = self._host.get(k)
@@ -61,14 +71,40 @@ class BatchRenderer:
             self._host[k] = buf
         return buf
 
-    def render_views(self, scene: PinnedScene, cams, background=(0.0, 0.0, 0.0), check=False):
+    def _upload(self, scene: PinnedScene, slot: int) -> GaussianTensors:
+        dev = self._dev[slot]
+        if dev is None or any(tuple(getattr(dev, f).shape) != tuple(t.shape)
+                              for f, t in scene.arrays.items()):
+            with torch.cuda.stream(self.h2d_stream):
+                arrs = {f: torch.empty(t.shape, dtype=torch.float32, device=self.device)
+                        for f, t in scene.arrays.items()}
+                pm = None if scene.prim_mask is None else torch.empty(
+                    scene.prim_mask.shape, dtype=torch.float32, device=self.device)
+            dev = GaussianTensors(**arrs, prim_mask=pm)
+            self._dev[slot] = dev
+        with torch.cuda.stream(self.h2d_stream):
+            if self._free[slot] is not None:
+                self.h2d_stream.wait_event(self._free[slot])
+            for f, t in scene.arrays.items():
+                getattr(dev, f).copy_(t, non_blocking=True)
+            if scene.prim_mask is not None:
+                dev.prim_mask.copy_(scene.prim_mask, non_blocking=True)
+        return dev
+
+    def render_views(self, scene: PinnedScene, cams, background=(0.0, 0.0, 0.0), check=False,
+                     wait: bool = True):
         """Upload the scene, render every view (spread over the render streams
         so binning of one view overlaps the raster of another), copy each
-        image back as soon as it is done; returns the pinned host images."""
+        image back as soon as it is done; returns the pinned host images.
+        With ``wait=False`` the call returns once everything is enqueued: the
+        images are complete after the next device synchronisation, and the
+        host buffers are reused by the call after next."""
+        slot = self._calls % 2
+        self._calls += 1
         main = torch.cuda.current_stream(self.device)
-        g = scene.upload(self.device)
+        g = self._upload(scene, slot)  # waits only for the renders that last used this copy
         up = torch.cuda.Event()
-        up.record(main)
+        up.record(self.h2d_stream)
         outs = []
         for k, cam in enumerate(cams):
             s = self.streams[k % len(self.streams)]
@@ -77,15 +113,21 @@ class BatchRenderer:
                 img = self.rast.forward(g, cam, background, check=check, track=False).img
                 done = torch.cuda.Event()
                 done.record(s)
-            host = self._host_buf(k, tuple(img.shape))
+            host = self._host_buf((slot, k), tuple(img.shape))
             with torch.cuda.stream(self.copy_stream):
                 self.copy_stream.wait_event(done)
                 host.copy_(img, non_blocking=True)
                 img.record_stream(self.copy_stream)
             outs.append(host)
-        main.wait_stream(self.copy_stream)
+        # the device copy may be overwritten once this call's renders are done
+        freed = torch.cuda.Event()
         for s in self.streams:
             main.wait_stream(s)
+        freed.record(main)
+        self._free[slot] = freed
+        main.wait_stream(self.copy_stream)
+        if wait:
+            main.synchronize()
         return outs
 
     @staticmethod
