@@ -367,108 +367,171 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(ListArgs la, Sg
 }
 
 constexpr int kGrad = 9;
-constexpr int kBwdThreads = 256;
+constexpr int kBwdThreads = 128;
+constexpr int kBwdCPT = 2;
+constexpr int kBwdChunk = kBwdThreads * kBwdCPT;  // candidates staged per batch
 
+// Sum of nine per-lane values over the warp by recursive halving: each
+// exchange level sends the half of the values the partner keeps (5 + 3 + 2
+// + 1 + 1 = 12 shuffles instead of 9 x 5).  Returns the total of value
+// kBwdLaneValue(lane) (pairs of lanes hold the same total; -1 = padding).
+__device__ __forceinline__ float warp_reduce9(const float v[kGrad], int lane) {
+  const bool u16 = lane & 16, u8 = lane & 8, u4 = lane & 4, u2 = lane & 2;
+  float a[5];
+#pragma unroll
+  for (int j = 0; j < 5; ++j) {
+    const float hi = j + 5 < kGrad ? v[j + 5] : 0.0f;
+    const float send = u16 ? v[j] : hi, keep = u16 ? hi : v[j];
+    a[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+  float b[3];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    const float hi = j + 3 < 5 ? a[j + 3] : 0.0f;
+    const float send = u8 ? a[j] : hi, keep = u8 ? hi : a[j];
+    b[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  float c[2];
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const float hi = j + 2 < 3 ? b[j + 2] : 0.0f;
+    const float send = u4 ? b[j] : hi, keep = u4 ? hi : b[j];
+    c[j] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  const float send = u2 ? c[0] : c[1], keep = u2 ? c[1] : c[0];
+  float d = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+  return d + __shfl_xor_sync(0xffffffffu, d, 1);
+}
+
+// Value index held by each even lane after warp_reduce9 (4 bits per even
+// lane, 15 = padding), from simulating the halving schedule above.
+__device__ __forceinline__ int reduce9_index(int lane) {
+  constexpr unsigned long long kLut = 0xfff8f765ff43f210ull;
+  return (lane & 1) ? 15 : (int)((kLut >> (2 * lane)) & 15ull);
+}
+
+// Backward raster: 128 threads per tile, two vertically adjacent pixels per
+// thread (a warp covers 16x4 pixels, as in the forward), walking the tile's
+// list back to front from the last entry any pixel kept.  Per record each
+// thread sums its two pixels' nine partials, the warp reduces them with
+// warp_reduce9, and nine lanes add the totals into the batch's shared
+// accumulators (4 warps per record); each batch is flushed with one global
+// atomic per (record, partial).  T is recovered with one correctly rounded
+// reciprocal per pixel-record: T_i = T_{i+1} / (1 - alpha_i).
 template <bool kFilter>
 __global__ void __launch_bounds__(kBwdThreads) raster_bwd_kernel(ListArgs la, SgsCam cam, float3 bg,
                                                                  const float* __restrict__ final_T,
                                                                  const uint32_t* __restrict__ ncontrib,
                                                                  const float* __restrict__ dimg,
                                                                  float* __restrict__ grad2d) {
-  __shared__ Stage<kBwdThreads> s;
-  __shared__ float s_acc[kBwdThreads][kGrad];
+  __shared__ Stage<kBwdChunk> s;
+  __shared__ float s_acc[kBwdChunk][kGrad + 1];
   __shared__ uint32_t s_max_nc;
 
   const int tile = blockIdx.x + cam.tile_y0 * cam.tiles_x;
   const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
   const int t = threadIdx.x, lane = t & 31;
-  const int px = tx * SGS_TILE + (t & 15), py = ty * SGS_TILE + (t >> 4);
-  const bool inside = px < cam.width && py < cam.height;
-  const float fx = (float)px + 0.5f, fy = (float)py + 0.5f;
+  const int px = tx * SGS_TILE + (t & 15);
+  const int py0 = ty * SGS_TILE + 2 * (t >> 4);
+  const bool in0 = px < cam.width && py0 < cam.height;
+  const bool in1 = px < cam.width && py0 + 1 < cam.height;
+  const float fx = (float)px + 0.5f, fy0 = (float)py0 + 0.5f;
   const uint2 rg = la.ranges[list_cell(kFilter, tx, ty, tile, la.super_x)];
   const uint32_t cs = rg.x;
   const uint32_t cend = la.cand_end[tile];
 
-  float T = 1.0f, g0 = 0.0f, g1 = 0.0f, g2 = 0.0f, S = 0.0f;
-  uint32_t nc = 0;
+  float T0 = 1.0f, T1 = 1.0f, S0 = 0.0f, S1 = 0.0f;
+  float g00 = 0.0f, g01 = 0.0f, g02 = 0.0f, g10 = 0.0f, g11 = 0.0f, g12 = 0.0f;
+  uint32_t nc0 = 0, nc1 = 0;
   if (t == 0) s_max_nc = 0;
   __syncthreads();
-  if (inside) {
-    const size_t pix = (size_t)py * cam.width + px;
-    T = final_T[pix];
-    nc = ncontrib[pix];
-    g0 = dimg[3 * pix + 0];
-    g1 = dimg[3 * pix + 1];
-    g2 = dimg[3 * pix + 2];
-    S = T * (g0 * bg.x + g1 * bg.y + g2 * bg.z);
-    atomicMax(&s_max_nc, nc);
+  if (in0) {
+    const size_t pix = (size_t)py0 * cam.width + px;
+    T0 = final_T[pix];
+    nc0 = ncontrib[pix];
+    g00 = dimg[3 * pix + 0];
+    g01 = dimg[3 * pix + 1];
+    g02 = dimg[3 * pix + 2];
+    S0 = T0 * (g00 * bg.x + g01 * bg.y + g02 * bg.z);
   }
+  if (in1) {
+    const size_t pix = (size_t)(py0 + 1) * cam.width + px;
+    T1 = final_T[pix];
+    nc1 = ncontrib[pix];
+    g10 = dimg[3 * pix + 0];
+    g11 = dimg[3 * pix + 1];
+    g12 = dimg[3 * pix + 2];
+    S1 = T1 * (g10 * bg.x + g11 * bg.y + g12 * bg.z);
+  }
+  const uint32_t ncm = nc0 > nc1 ? nc0 : nc1;
+  if (ncm) atomicMax(&s_max_nc, ncm);
   __syncthreads();
   const uint32_t max_nc = s_max_nc;
+  const uint32_t warp_nc = __reduce_max_sync(0xffffffffu, ncm);
   const uint32_t lbit = tile_local_bit(tx, ty);
+  const int vidx = reduce9_index(lane);
   uint32_t hits_after = 0;
 
   for (uint32_t hi = cend; hi > cs;) {
-    const uint32_t lo = hi - cs > (uint32_t)kBwdThreads ? hi - kBwdThreads : cs;
+    const uint32_t lo = hi - cs > (uint32_t)kBwdChunk ? hi - kBwdChunk : cs;
     __syncthreads();  // previous batch fully flushed
-#pragma unroll
-    for (int c = 0; c < kGrad; ++c) s_acc[t][c] = 0.0f;
-    const int nb = stage_append<kBwdThreads, 1, kFilter, true>(lo, hi, lbit, la, 0, s);
+    for (int i = t; i < kBwdChunk * (kGrad + 1); i += kBwdThreads) (&s_acc[0][0])[i] = 0.0f;
+    const int nb = stage_append<kBwdThreads, kBwdCPT, kFilter, true>(lo, hi, lbit, la, 0, s);
     const uint32_t base = max_nc - hits_after - (uint32_t)nb;  // per-tile list index of staged entry 0
     for (int k = nb - 1; k >= 0; --k) {
       const uint32_t idx = base + (uint32_t)k;
-      if (__all_sync(0xffffffffu, idx >= nc)) continue;
+      if (idx >= warp_nc) continue;  // warp-uniform: no pixel of this warp kept the record
       const float4 G = s.geo[k];  // (mx, my, log2 o_eff, -)
       const float4 E = s.con[k];  // scaled eigen form (s1 ux, s1 uy, s2 ux, s2 uy)
-      const float dx = fx - G.x, dy = fy - G.y;
-      const float t1 = fmaf(E.y, dy, E.x * dx), t2 = fmaf(E.z, dy, -(E.w * dx));
-      const float p = fmaf(-t1, t1, fmaf(-t2, t2, G.z));
-      const bool active = idx < nc;
+      const float4 col = s.col[k];
+      const float dx = fx - G.x;
+      const float dy0 = fy0 - G.y, dy1 = dy0 + 1.0f;
+      const float e1dx = E.x * dx, e3dx = E.w * dx;
       float v[kGrad];
 #pragma unroll
       for (int c = 0; c < kGrad; ++c) v[c] = 0.0f;
-      if (active) {
-        const float4 col = s.col[k];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const float dy = q ? dy1 : dy0;
+        const bool act = idx < (q ? nc1 : nc0);
+        const float t1 = fmaf(E.y, dy, e1dx), t2 = fmaf(E.z, dy, -e3dx);
+        const float p = fmaf(-t1, t1, fmaf(-t2, t2, G.z));
         const float a = ex2_approx(p);
         const float alpha = fminf(a, SGS_ALPHA_MAX);
         const float om = fmaxf(1.0f - a, SGS_ONE_MINUS_ALPHA_MAX);
-        const float Ti = T / om;
+        const float rom = __frcp_rn(om);
+        float& T = q ? T1 : T0;
+        float& S = q ? S1 : S0;
+        const float gx = q ? g10 : g00, gy = q ? g11 : g01, gz = q ? g12 : g02;
+        const float Ti = T * rom;
         const float w = alpha * Ti;
-        const float cg = col.x * g0 + col.y * g1 + col.z * g2;
-        const float dalpha = (a < SGS_ALPHA_MAX) ? (Ti * cg - S / om) : 0.0f;
-        S += w * cg;
-        T = Ti;
-        const float dq = -0.5f * a * dalpha;
-        v[0] = w * g0;
-        v[1] = w * g1;
-        v[2] = w * g2;
-        v[3] = dq;
-        v[4] = dq * dx;
-        v[5] = dq * dy;
-        v[6] = dq * dx * dx;
-        v[7] = dq * dx * dy;
-        v[8] = dq * dy * dy;
-      }
-      if (__any_sync(0xffffffffu, active)) {
-#pragma unroll
-        for (int c = 0; c < kGrad; ++c) v[c] = warp_sum(v[c]);
-        if (lane < kGrad) {
-          float mine = v[0];
-#pragma unroll
-          for (int c = 1; c < kGrad; ++c)
-            if (lane == c) mine = v[c];
-          atomicAdd(&s_acc[k][lane], mine);
+        const float cg = fmaf(col.x, gx, fmaf(col.y, gy, col.z * gz));
+        const float dal = (a < SGS_ALPHA_MAX) ? fmaf(Ti, cg, -S * rom) : 0.0f;
+        const float dq = act ? -0.5f * a * dal : 0.0f;
+        const float ww = act ? w : 0.0f;
+        if (act) {
+          S = fmaf(w, cg, S);
+          T = Ti;
         }
+        v[0] = fmaf(ww, gx, v[0]);
+        v[1] = fmaf(ww, gy, v[1]);
+        v[2] = fmaf(ww, gz, v[2]);
+        v[3] += dq;
+        const float qx = dq * dx, qy = dq * dy;
+        v[4] += qx;
+        v[5] += qy;
+        v[6] = fmaf(qx, dx, v[6]);
+        v[7] = fmaf(qx, dy, v[7]);
+        v[8] = fmaf(qy, dy, v[8]);
       }
+      const float tot = warp_reduce9(v, lane);
+      if (vidx < kGrad) atomicAdd(&s_acc[k][vidx], tot);
     }
     __syncthreads();
-    if (t < nb) {
-      float* dst = grad2d + (size_t)s.id[t] * kGrad;
-#pragma unroll
-      for (int c = 0; c < kGrad; ++c) {
-        const float x = s_acc[t][c];
-        if (x != 0.0f) atomicAdd(dst + c, x);
-      }
+    for (int i = t; i < nb * kGrad; i += kBwdThreads) {
+      const int k = i / kGrad, c = i - k * kGrad;
+      const float x = s_acc[k][c];
+      if (x != 0.0f) atomicAdd(grad2d + (size_t)s.id[k] * kGrad + c, x);
     }
     hits_after += (uint32_t)nb;
     hi = lo;
