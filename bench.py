@@ -36,6 +36,11 @@ sys.path.insert(0, str(ROOT))
 METRIC = "frames/s & Mpix/s at 1080p, 1M Gaussians, 3 SG lobes (1/2/4/8 B200); peak render VRAM"
 UNIT = "frames/s"
 WORKLOAD = "configs[2]: 1,000,000 Gaussians (64 clusters), 3 SG lobes, 1920x1080, FoV 60"
+# libsgs kernels per forward frame (depth-first mode, 1080p): preprocess; set_count,
+# histogram, histogram scan, 4 onesweep passes (depth sort); 3 scan kernels;
+# ranges_init, emit_entries; histogram, histogram scan, 1 onesweep pass (super-tile
+# sort + ranges); ranges_fix; cell_order, raster_fwd
+KERNELS_PER_FRAME = 19
 
 
 def parse():
@@ -302,16 +307,16 @@ def run_ours(args):
     # ---- dominant-kernel timing for the roofline: the same renders on ONE
     # stream, CUDA events bracketing each raster launch on its stream
     n_ev = args.steps * V
-    r0 = [torch.cuda.Event(enable_timing=True) for _ in range(n_ev)]
-    r1 = [torch.cuda.Event(enable_timing=True) for _ in range(n_ev)]
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(n_ev)]
     e = 0
     for _ in range(args.steps):
         for k, cam in enumerate(my_cams):
-            rast.forward(g, cam, check=False, out=out_bufs[k], track=False,
-                         _events=(r0[e], r1[e]))
+            rast.forward(g, cam, check=False, out=out_bufs[k], track=False, _events=ev[e])
             e += 1
     torch.cuda.synchronize(dev)
-    raster_ms = [a.elapsed_time(b) for a, b in zip(r0, r1)]
+    raster_ms = [a[0].elapsed_time(a[1]) for a in ev]
+    prep_ms = [a[2].elapsed_time(a[3]) for a in ev]
+    bin_ms = [a[3].elapsed_time(a[0]) for a in ev]   # sgs_bin: depth sort, scan, emission, tile sort
     # overflow guard: the timed frames reused capacities sized in warm-up
     for cam in my_cams:
         assert not rast.forward(g, cam, check=True).stats()["overflow"]
@@ -355,6 +360,29 @@ def run_ours(args):
         peak_pairs = n_sm * sm_mhz * 1e6 * min(128.0 / 18.0, 16.0)
         achieved = pairs_per_view / (float(np.mean(raster_ms)) / 1e3)
         E = float(np.mean([s["n_entries"] for s in stats]))
+        Es = float(np.mean([s["n_bin_entries"] for s in stats]))
+        n_emit = float(np.mean([s["n_emitting"] for s in stats]))
+        N = float(args.n)
+        hbm = float(peaks.get("hbm_gbs", 6549.1))
+
+        def stage(ms_list, nbytes, what):
+            ms = float(np.mean(ms_list))
+            gbs = nbytes / (ms / 1e3) / 1e9
+            return {"ms_per_view": ms, "algorithmic_bytes": int(nbytes), "GB_per_s": gbs,
+                    "frac_of_hbm": gbs / hbm, "bytes_model": what}
+        # algorithmic bytes per view: preprocess reads the
+        # 152 B SoA row and writes 20 B of keys/rects/counts for every
+        # primitive plus 80 B of records for every emitting one; binning =
+        # depth sort (copy 8 + histogram 4 + 4 passes x 16 B per primitive),
+        # offsets scan (24 B), emission reads (76 B per primitive) and writes
+        # 8 B per super-tile entry, and the super-tile sort (histogram 4 +
+        # pass 12 B per entry)
+        stages = {
+            "preprocess": stage(prep_ms, N * (152 + 20) + n_emit * 80,
+                                "152 B read + 20 B written per primitive + 80 B records per emitting"),
+            "binning": stage(bin_ms, N * (8 + 4 + 64 + 24 + 76) + Es * (8 + 16),
+                             "176 B per primitive + 24 B per super-tile entry"),
+        }
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
@@ -380,7 +408,9 @@ def run_ours(args):
                          "raster_ms_per_view": float(np.mean(raster_ms))},
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(pinned.nbytes),
                     "d2h_bytes_per_step": int(BatchRenderer.d2h_bytes(my_cams))},
-            "gpu_launches": int(args.steps * V * 18),
+            "stages": stages,
+            "super_tile_entries_per_view": Es,
+            "gpu_launches": int(args.steps * V * KERNELS_PER_FRAME),
             "clocks": clk,
         }
         if not args.no_cpu_baseline:

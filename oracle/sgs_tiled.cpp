@@ -180,9 +180,9 @@ void oracle_raster_forward(const uint32_t* ranges, const uint32_t* vals, const f
         // every listed primitive is blended (alpha < 1e-7 outside its support)
         const float a = exp2f(p);
         const float alpha = std::min(a, SGS_ALPHA_MAX);
-        const float Tn = T * (a < SGS_ALPHA_MAX ? 1.0f - a : SGS_ONE_MINUS_ALPHA_MAX);
-        if (Tn < SGS_T_KEEP) break;
         const float w = alpha * T;
+        const float Tn = T - w;  // the GPU's blend step (sgs_geom.h SGS_T_KEEP)
+        if (Tn < SGS_T_KEEP) break;
         for (int c = 0; c < 3; ++c) C[c] += w * r[12 + c];
         if (weight_sums) weight_sums[vals[j]] += w;
         T = Tn;

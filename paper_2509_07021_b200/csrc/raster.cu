@@ -223,14 +223,14 @@ __device__ __forceinline__ bool warp_any(bool p) {
 // would fall below the cutoff keeps its last kept T, negated.  A terminated
 // pixel needs no separate test: its Tn is negative, so it is never kept
 // again, and re-terminating leaves -|T| unchanged.
-//   a = 2^p,  Tn = T max(1 - a, 0.01)
-//   keep = Tn >= T_keep:  C += min(a, 0.99) T c,  T = Tn;   else T = -|T|
+//   alpha = min(2^p, 0.99),  w = alpha T,  Tn = T - w   (sgs_geom.h SGS_T_KEEP)
+//   keep = Tn >= T_keep:  C += w c,  T = Tn;   else T = -|T|
 __device__ __forceinline__ bool blend_px(float p, const float4& c, float& T, float& C0, float& C1, float& C2,
                                          float& w) {
-  const float a = ex2_approx(p);
-  const float Tn = T * fmaxf(1.0f - a, SGS_ONE_MINUS_ALPHA_MAX);
+  const float alpha = fminf(ex2_approx(p), SGS_ALPHA_MAX);
+  w = alpha * T;
+  const float Tn = T - w;
   const bool keep = Tn >= SGS_T_KEEP;
-  w = fminf(a, SGS_ALPHA_MAX) * T;
   if (keep) {
     C0 = fmaf(w, c.x, C0);
     C1 = fmaf(w, c.y, C1);
@@ -498,7 +498,7 @@ __global__ void __launch_bounds__(kBwdThreads) raster_bwd_kernel(ListArgs la, Sg
         const float p = fmaf(-t1, t1, fmaf(-t2, t2, G.z));
         const float a = ex2_approx(p);
         const float alpha = fminf(a, SGS_ALPHA_MAX);
-        const float om = fmaxf(1.0f - a, SGS_ONE_MINUS_ALPHA_MAX);
+        const float om = 1.0f - alpha;  // the forward's T_next = T - alpha T
         const float rom = __frcp_rn(om);
         float& T = q ? T1 : T0;
         float& S = q ? S1 : S0;

@@ -71,19 +71,16 @@
 #define SGS_TILE 16
 #define SGS_ALPHA_MAX 0.99f      // render.py:24
 #define SGS_T_CUTOFF 1e-4f       // render.py:25
-// 1 - alpha for a clamped alpha.  float64 gives 1 - 0.99 = 0.010000000000000009;
-// float32 1 - 0.99f = 0.0099999905 is 1e-6 (relative) lower, which decides
-// the keep test below for stacks of opaque primitives, so the clamped branch
-// uses 0.01f (0.0099999998) instead.
-#define SGS_ONE_MINUS_ALPHA_MAX 0.01f
-// The fp32 keep test `T_next >= SGS_T_KEEP`.  The reference keeps a primitive
-// iff its float64 T_next >= 1e-4 (render.py:384).  The most common boundary
-// is structural, not random: two alpha-clamped primitives give T = 0.01^2,
-// which float64 rounds to 1.0000000000000018e-4 (kept) but float32 to
-// 9.99999955e-5 (dropped).  Lowering the fp32 threshold by a relative 1e-6
-// reproduces the float64 decision there; the price is a 1e-6-wide band where
-// fp32 now keeps what float64 drops, each such pair contributing <= 1e-4 |c|.
-#define SGS_T_KEEP 9.99999e-5f
+// The fp32 blend step is  w = min(a, 0.99) T,  T_next = T - w  (the real
+// value T (1 - alpha) of the reference's cumprod, render.py:374-384, in one
+// FMUL + one FADD), and a primitive is kept iff T_next >= SGS_T_KEEP.  The
+// reference keeps iff its float64 T_next >= 1e-4.  The common boundary is
+// structural, not random: two alpha-clamped primitives give T = 0.01^2,
+// which float64 rounds to 1.0000000000000018e-4 (kept) but this fp32 step to
+// 9.999983e-5.  Lowering the fp32 threshold by a relative 2e-6 reproduces the
+// float64 decision there; the price is a 2e-6-wide band where fp32 keeps what
+// float64 drops, each such pair contributing <= 1e-4 |c|.
+#define SGS_T_KEEP 9.99998e-5f
 #define SGS_LOWPASS 0.3f         // render.py:26
 #define SGS_EPS 1e-7f            // opacity-aware support threshold
 #define SGS_LN_EPS (-16.11809565095832f)  // ln(1e-7)

@@ -206,6 +206,8 @@ class Rasterizer:
     def forward(self, g: GaussianTensors, cam, background=(0.0, 0.0, 0.0), weight_sums=None,
                 check=True, private=False, tile_rows=None, out=None, pair_count=None,
                 track=True, _events=None) -> Frame:
+        # _events (timing hooks): (raster start, raster end[, preprocess start,
+        # preprocess end]) CUDA events recorded on the current stream
         """Render one view.  ``weight_sums`` (N float32 device tensor) is
         accumulated in place (render.py:406-407).  ``out`` may supply
         preallocated (img, T, nc) tensors.  ``track=False`` renders the image
@@ -231,7 +233,11 @@ class Rasterizer:
         key = self._key(g, cam)
         while True:
             ws = self.workspace(g, cam, private=private)
+            if _events is not None and len(_events) > 2:
+                _events[2].record()
             _ffi.call("sgs_preprocess", C.byref(params), C.byref(c_cam), C.byref(ws.desc), stream)
+            if _events is not None and len(_events) > 2:
+                _events[3].record()
             _ffi.call("sgs_bin", C.byref(c_cam), C.byref(ws.desc), stream)
             if check:
                 st = ws.stats()
