@@ -234,6 +234,14 @@ int sgs_image_loss(const void* img, int32_t img_is_f64, const void* target, int3
                    double* dimg_f64, double* ssim_map, double* out, void* workspace,
                    uint64_t workspace_bytes, void* stream);
 
+/* ADMM proximal projection support (prune.py:204-213, _top_k_mask): keep[i] =
+ * 1 for the k largest of n float64 device scores, ties keeping the lower
+ * index (np.argsort(-scores, kind="stable")[:k]); keep is a device uint8
+ * array of n.  temp: sgs_topk_mask_temp_size() bytes of device scratch. */
+int sgs_topk_mask_temp_size(int64_t n, uint64_t* bytes_out);
+int sgs_topk_mask(const double* scores, int64_t n, int64_t k, uint8_t* keep, void* temp,
+                  uint64_t temp_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -89,6 +89,9 @@ SIGNATURES = {
     "sgs_sort_pairs_u64": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p,
                                      C.c_uint64, C.c_void_p]),
     "sgs_loss_workspace_size": (C.c_int, [C.c_int32, C.c_int32, _P(C.c_uint64)]),
+    "sgs_topk_mask_temp_size": (C.c_int, [C.c_int64, _P(C.c_uint64)]),
+    "sgs_topk_mask": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, C.c_uint64,
+                                C.c_void_p]),
     "sgs_image_loss": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
                                  _P(SgsLossConfig), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                  C.c_void_p, C.c_uint64, C.c_void_p]),

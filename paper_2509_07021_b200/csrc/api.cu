@@ -85,6 +85,10 @@ int launch_image_loss(const void* img, int img_f64, const void* tgt, int tgt_f64
                       const sgs_loss_config* cfg, float* dimg, double* dimg64, double* smap, double* out,
                       void* workspace, uint64_t ws_bytes, cudaStream_t st);
 
+uint64_t topk_temp_bytes(uint64_t n);
+int launch_topk_mask(const double* scores, uint32_t n, uint32_t k, uint8_t* keep, void* temp, uint64_t temp_bytes,
+                     cudaStream_t st);
+
 }  // namespace sgs
 
 using namespace sgs;
@@ -338,6 +342,25 @@ int sgs_image_loss(const void* img, int32_t img_is_f64, const void* target, int3
                    double* out, void* workspace, uint64_t workspace_bytes, void* stream) {
   return launch_image_loss(img, img_is_f64, target, target_is_f64, height, width, cfg, dimg, dimg_f64, ssim_map, out,
                            workspace, workspace_bytes, as_stream(stream));
+}
+
+int sgs_topk_mask_temp_size(int64_t n, uint64_t* bytes_out) {
+  if (n < 0 || n > (int64_t)kMaxEntries || !bytes_out) {
+    set_error("invalid top-k size");
+    return SGS_E_ARG;
+  }
+  *bytes_out = topk_temp_bytes((uint64_t)n);
+  return SGS_OK;
+}
+
+int sgs_topk_mask(const double* scores, int64_t n, int64_t k, uint8_t* keep, void* temp, uint64_t temp_bytes,
+                  void* stream) {
+  if (n < 0 || n > (int64_t)kMaxEntries || k < 0 || k > n || (n > 0 && (!scores || !keep || !temp))) {
+    set_error("invalid top-k arguments (need 0 <= k <= n)");
+    return SGS_E_ARG;
+  }
+  if (n == 0) return SGS_OK;
+  return launch_topk_mask(scores, (uint32_t)n, (uint32_t)k, keep, temp, temp_bytes, as_stream(stream));
 }
 
 }  // extern "C"

@@ -206,7 +206,47 @@ def gen_vram():
     save("vram_model", **out)
 
 
+def gen_admm():
+    """The reference ADMM loop (prune.run_state) on a small scene: 3 views of
+    24x20 crops, 8 iterations, proximal event every 3 (magnitude and range
+    operators), plus one prox_project on random scores with ties."""
+    from sgsplat import prune as PR
+    s, cams = scenes.config0(n=300, seed=3)
+    views = []
+    for k, (x0, y0) in enumerate([(116, 118), (100, 110), (130, 124)]):
+        cam = cams[0].crop(x0, y0, 24, 20)
+        tgt = scenes.target_image(7, cam.height, cam.width, view=k)
+        views.append((cam, tgt))
+    out = {}
+    for op in ("sharpness", "range"):
+        p = ref_params(s)
+        p.lobe_mask = np.asarray(s.lobe_mask) > 0.5
+        cfg = PR.PrunerConfig.from_keep_ratios(s.n, int(p.lobe_mask.sum()), 0.6, 0.5, delta=5e-3,
+                                               iters=8, prox_every=3, sharpness_operator=op, seed=1)
+        st = PR.PrunerState.init(p)
+        trace = PR.run_state(st, [(ref_cam(c), t.astype(np.float64)) for c, t in views], cfg)
+        for f in FIELDS:
+            out[f"{op}_{f}"] = getattr(p, f)
+        out[f"{op}_proxy_o"], out[f"{op}_proxy_s"] = st.proxy_o, st.proxy_s
+        out[f"{op}_dual_o"], out[f"{op}_dual_s"] = st.dual_o, st.dual_s
+        out[f"{op}_trace"] = np.array([[r.iteration, r.loss, r.residual_o, r.residual_s,
+                                        r.active_primitives, r.active_lobes, r.budget_units]
+                                       for r in trace])
+        out[f"{op}_kappa"] = np.array([cfg.kappa, cfg.kappa_o, cfg.kappa_s])
+    rng = np.random.default_rng(4)
+    o_in = np.round(rng.normal(size=500), 1)        # many ties
+    s_in = np.round(rng.normal(size=(500, 3)), 1)
+    cfgp = PR.PrunerConfig(kappa=11 * 137 + 7 * 611, kappa_o=137, kappa_s=611)
+    po, ps = PR.prox_project(o_in, s_in, cfgp)
+    out.update(prox_o_in=o_in, prox_s_in=s_in, prox_o=po, prox_s=ps)
+    for k, (c, t) in enumerate(views):
+        out.update({f"v{k}_{key}": v for key, v in cam_dict(c).items()})
+        out[f"v{k}_target"] = t
+    save("admm", **out, **scene_dict(s))
+
+
 GENERATORS = {
+    "admm": gen_admm,
     "accept_grads": gen_accept_grads,
     "vram_model": gen_vram,
     "masks_grads": gen_masks,
