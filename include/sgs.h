@@ -35,6 +35,8 @@ extern "C" {
 #define SGS_E_CUDA (-2)       /* CUDA runtime error */
 #define SGS_E_WORKSPACE (-3)  /* workspace too small for N / image size */
 #define SGS_E_CAPACITY (-4)   /* tile-entry capacity exceeded; grow and retry */
+#define SGS_E_FORMAT (-5)     /* malformed scene file (the reference raises SceneFormatError) */
+#define SGS_E_TRUNCATED (-6)  /* scene file shorter than its header promises (TruncatedFileError) */
 
 #define SGS_SORT_DEPTH_FIRST 0  /* global depth sort of primitives + stable tile bucketing */
 #define SGS_SORT_KEY64 1        /* (tile<<32 | depth_bits) keys, 64-bit onesweep radix sort */
@@ -241,6 +243,34 @@ int sgs_image_loss(const void* img, int32_t img_is_f64, const void* target, int3
 int sgs_topk_mask_temp_size(int64_t n, uint64_t* bytes_out);
 int sgs_topk_mask(const double* scores, int64_t n, int64_t k, uint8_t* keep, void* temp,
                   uint64_t temp_bytes, void* stream);
+
+/* MEGS2 compact scene files (io.py:1-15 layout, 173-214 read_compact) into
+ * the renderer's device SoA.  Host side: sgs_compact_header reads the
+ * primitive count; sgs_compact_index walks the variable-length records of a
+ * HOST buffer into count + 1 byte offsets (host array) and the largest lobe
+ * count, with the reference's checks (bad magic / version / trailing bytes
+ * -> SGS_E_FORMAT, short payload -> SGS_E_TRUNCATED).  Device side:
+ * sgs_compact_decode reads the uploaded bytes and offsets (device arrays)
+ * and writes the SceneParams arrays (render.py:135-145) for n_lobes slots:
+ * log_scale = log(scale), unused slots axis (0,0,1), zero sharpness /
+ * amplitude, lobe_mask 0/1. */
+typedef struct sgs_scene_soa {
+  float* position;  /* (N,3) */
+  float* quat;      /* (N,4) */
+  float* log_scale; /* (N,3) */
+  float* opacity;   /* (N) */
+  float* diffuse;   /* (N,3) */
+  float* axis_raw;  /* (N,L,3) */
+  float* sharpness; /* (N,L) */
+  float* amplitude; /* (N,L,3) */
+  float* lobe_mask; /* (N,L) */
+} sgs_scene_soa;
+
+int sgs_compact_header(const uint8_t* data, uint64_t size, int64_t* count_out);
+int sgs_compact_index(const uint8_t* data, uint64_t size, uint64_t* offsets, int64_t offsets_cap,
+                      int32_t* max_lobes_out);
+int sgs_compact_decode(const uint8_t* data, const uint64_t* offsets, int64_t n, int32_t n_lobes,
+                       const sgs_scene_soa* out, void* stream);
 
 #ifdef __cplusplus
 }

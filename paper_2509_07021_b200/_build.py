@@ -19,7 +19,7 @@ PKG_DIR = Path(__file__).resolve().parent
 CSRC = PKG_DIR / "csrc"
 LIB_DIR = PKG_DIR / "_lib"
 LIB_PATH = LIB_DIR / "libsgs.so"
-SOURCES = ["api.cu", "preprocess.cu", "binning.cu", "raster.cu", "preprocess_bwd.cu", "loss.cu", "select.cu"]
+SOURCES = ["api.cu", "preprocess.cu", "binning.cu", "raster.cu", "preprocess_bwd.cu", "loss.cu", "select.cu", "compact.cu"]
 HEADERS = ["common.cuh", "sgs_geom.h", "sort.cuh"]
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-shared",

@@ -16,6 +16,8 @@ SGS_E_ARG = -1
 SGS_E_CUDA = -2
 SGS_E_WORKSPACE = -3
 SGS_E_CAPACITY = -4
+SGS_E_FORMAT = -5
+SGS_E_TRUNCATED = -6
 SORT_DEPTH_FIRST = 0
 SORT_KEY64 = 1
 
@@ -54,6 +56,11 @@ class SgsStats(C.Structure):
                 ("n_bin_entries", C.c_uint64)]
 
 
+class SgsSceneSoa(C.Structure):
+    _fields_ = [(f, C.c_void_p) for f in ("position", "quat", "log_scale", "opacity", "diffuse",
+                                           "axis_raw", "sharpness", "amplitude", "lobe_mask")]
+
+
 class SgsLossConfig(C.Structure):
     _fields_ = [("lambda_ssim", C.c_double), ("window", C.c_int32), ("sigma", C.c_double),
                 ("c1", C.c_double), ("c2", C.c_double)]
@@ -90,6 +97,10 @@ SIGNATURES = {
                                      C.c_uint64, C.c_void_p]),
     "sgs_loss_workspace_size": (C.c_int, [C.c_int32, C.c_int32, _P(C.c_uint64)]),
     "sgs_topk_mask_temp_size": (C.c_int, [C.c_int64, _P(C.c_uint64)]),
+    "sgs_compact_header": (C.c_int, [C.c_char_p, C.c_uint64, _P(C.c_int64)]),
+    "sgs_compact_index": (C.c_int, [C.c_char_p, C.c_uint64, C.c_void_p, C.c_int64, _P(C.c_int32)]),
+    "sgs_compact_decode": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, _P(SgsSceneSoa),
+                                     C.c_void_p]),
     "sgs_topk_mask": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, C.c_uint64,
                                 C.c_void_p]),
     "sgs_image_loss": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,

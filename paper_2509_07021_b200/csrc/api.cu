@@ -89,6 +89,11 @@ uint64_t topk_temp_bytes(uint64_t n);
 int launch_topk_mask(const double* scores, uint32_t n, uint32_t k, uint8_t* keep, void* temp, uint64_t temp_bytes,
                      cudaStream_t st);
 
+int compact_header(const uint8_t* data, uint64_t size, int64_t* count);
+int compact_index(const uint8_t* data, uint64_t size, uint64_t* offsets, int64_t cap, int32_t* max_lobes);
+int launch_compact_decode(const uint8_t* data, const uint64_t* offsets, int64_t n, int L, const sgs_scene_soa* out,
+                          cudaStream_t st);
+
 }  // namespace sgs
 
 using namespace sgs;
@@ -361,6 +366,27 @@ int sgs_topk_mask(const double* scores, int64_t n, int64_t k, uint8_t* keep, voi
   }
   if (n == 0) return SGS_OK;
   return launch_topk_mask(scores, (uint32_t)n, (uint32_t)k, keep, temp, temp_bytes, as_stream(stream));
+}
+
+int sgs_compact_header(const uint8_t* data, uint64_t size, int64_t* count_out) {
+  return compact_header(data, size, count_out);
+}
+
+int sgs_compact_index(const uint8_t* data, uint64_t size, uint64_t* offsets, int64_t offsets_cap,
+                      int32_t* max_lobes_out) {
+  return compact_index(data, size, offsets, offsets_cap, max_lobes_out);
+}
+
+int sgs_compact_decode(const uint8_t* data, const uint64_t* offsets, int64_t n, int32_t n_lobes,
+                       const sgs_scene_soa* out, void* stream) {
+  if (n < 0 || n_lobes < 0 || n_lobes > 255 || !out ||
+      (n > 0 && (!data || !offsets || !out->position || !out->quat || !out->log_scale || !out->opacity ||
+                 !out->diffuse || !out->lobe_mask ||
+                 (n_lobes > 0 && (!out->axis_raw || !out->sharpness || !out->amplitude))))) {
+    set_error("invalid compact decode arguments");
+    return SGS_E_ARG;
+  }
+  return launch_compact_decode(data, offsets, n, n_lobes, out, as_stream(stream));
 }
 
 }  // extern "C"

@@ -245,7 +245,39 @@ def gen_admm():
     save("admm", **out, **scene_dict(s))
 
 
+def gen_compact():
+    """A MEGS2 compact file written by the reference (io.write_compact) and
+    what its read_compact + SceneParams.from_scene make of it: varying lobe
+    counts (0..5, so max_lobes exceeds the default 3)."""
+    from sgsplat import io as IO
+    from sgsplat.scene import SGLobe
+    rng = np.random.default_rng(21)
+    prims = []
+    for i in range(257):
+        nl = int(rng.integers(0, 4)) if i != 100 else 5
+        q = rng.normal(size=4)
+        lobes = []
+        for _ in range(nl):
+            ax = rng.normal(size=3)
+            lobes.append(SGLobe(axis=ax / np.linalg.norm(ax), sharpness=float(rng.uniform(0, 40)),
+                                amplitude=rng.normal(0, 0.3, 3)))
+        prims.append(GaussianPrimitive(position=rng.uniform(-1, 1, 3), rotation=q / np.linalg.norm(q),
+                                       scale=np.exp(rng.normal(-3, 0.5, 3)), opacity=float(rng.uniform()),
+                                       diffuse=rng.uniform(0, 1, 3), lobes=lobes))
+    sc = Scene(prims, ColorModel.sg(5))
+    data = IO.write_compact(sc)
+    back = IO.read_compact(data)
+    p = R.SceneParams.from_scene(back)
+    out = {f: getattr(p, f) for f in FIELDS}
+    out["lobe_mask"] = p.lobe_mask
+    out["raw"] = np.frombuffer(data, np.uint8)
+    out["scale"] = np.stack([q.scale for q in prims])
+    out["n_lobes"] = np.array([len(q.lobes) for q in prims])
+    save("compact", **out)
+
+
 GENERATORS = {
+    "compact": gen_compact,
     "admm": gen_admm,
     "accept_grads": gen_accept_grads,
     "vram_model": gen_vram,
