@@ -53,7 +53,8 @@ class BatchRenderer:
     copy engines run both directions at once).  Every call still moves its
     whole scene host -> device and every image device -> host."""
 
-    def __init__(self, rast: Rasterizer | None = None, device="cuda", streams: int = 4):
+    def __init__(self, rast: Rasterizer | None = None, device="cuda", streams: int = 4,
+                 graphs: bool = True):
         self.rast = rast or Rasterizer(device=device)
         self.device = torch.device(device)
         self.copy_stream = torch.cuda.Stream(device=self.device)
@@ -63,6 +64,8 @@ class BatchRenderer:
         self._dev = [None, None]      # two device copies of the scene
         self._free = [None, None]     # event: renders of the copy's last use finished
         self._calls = 0
+        self.graphs = graphs          # replay each (copy, view) render from a CUDA graph
+        self._dev_out = {}
 
     def _host_buf(self, k, shape):
         buf = self._host.get(k)
@@ -110,7 +113,17 @@ class BatchRenderer:
             s = self.streams[k % len(self.streams)]
             s.wait_event(up)
             with torch.cuda.stream(s):
-                img = self.rast.forward(g, cam, background, check=check, track=False).img
+                if self.graphs and not check:
+                    H, W = int(cam.height), int(cam.width)
+                    buf = self._dev_out.get((slot, k))
+                    if buf is None or tuple(buf[0].shape) != (H, W, 3):
+                        buf = (torch.empty((H, W, 3), dtype=torch.float32, device=self.device),
+                               torch.empty((H, W), dtype=torch.float32, device=self.device))
+                        self._dev_out[(slot, k)] = buf
+                    self.rast.graph_forward(g, cam, buf, background)
+                    img = buf[0]
+                else:
+                    img = self.rast.forward(g, cam, background, check=check, track=False).img
                 done = torch.cuda.Event()
                 done.record(s)
             host = self._host_buf((slot, k), tuple(img.shape))

@@ -200,6 +200,7 @@ class Rasterizer:
         return ws
 
     def release(self):
+        self.release_graphs()
         self._shared.clear()
 
     # ------------------------------------------------------------------ forward
@@ -258,6 +259,48 @@ class Rasterizer:
         if _events is not None:
             _events[1].record()
         return Frame(img=img, final_T=T, ncontrib=nc, ws=ws, cam=c_cam, bg=bg)
+
+    # ------------------------------------------------------- graph forward
+    def graph_forward(self, g: GaussianTensors, cam, out, background=(0.0, 0.0, 0.0),
+                      tile_rows=None) -> None:
+        """Image-only forward of one view replayed from a CUDA graph on the
+        current stream (one graph launch instead of ~20 kernel launches and
+        ~3 FFI calls of host work per view).  The graph is captured on first
+        use for this (scene buffers, camera, output buffers, stream) and
+        re-reads the scene tensors at every replay, so in-place parameter
+        updates are seen.  ``out`` = (img, T) device tensors.  The tile-entry
+        capacity is sized before capture; a later frame that outgrows it
+        sets the overflow counter (Frame.stats / ensure via forward(check=True))."""
+        c = to_sgs(cam, tile_rows)
+        stream = torch.cuda.current_stream(self.device)
+        key = (bytes(c), g.position.data_ptr(), g.n, g.n_lobes, out[0].data_ptr(), out[1].data_ptr(),
+               stream.cuda_stream, tuple(float(v) for v in background))
+        graphs = self.__dict__.setdefault("_graphs", {})
+        gr = graphs.get(key)
+        if gr is None:
+            # capture on a private (non-default) stream paired with the caller's
+            # stream; its workspace belongs to that pairing, so graphs replayed
+            # concurrently on different streams never share scratch
+            caps = self.__dict__.setdefault("_capture_streams", {})
+            cap = caps.get(stream.cuda_stream)
+            if cap is None:
+                cap = torch.cuda.Stream(device=self.device)
+                caps[stream.cuda_stream] = cap
+            cap.wait_stream(stream)
+            with torch.cuda.stream(cap):
+                self.forward(g, cam, background, check=True, tile_rows=tile_rows,
+                             out=(out[0], out[1], None), track=False)
+            cap.synchronize()
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr, stream=cap):
+                self.forward(g, cam, background, check=False, tile_rows=tile_rows,
+                             out=(out[0], out[1], None), track=False)
+            stream.wait_stream(cap)
+            graphs[key] = gr
+        gr.replay()
+
+    def release_graphs(self):
+        self.__dict__.pop("_graphs", None)
 
     # ----------------------------------------------------------------- backward
     def backward(self, g: GaussianTensors, frame: Frame, dimg: torch.Tensor,

@@ -46,3 +46,19 @@ def test_pipelined_calls_render_their_own_scene():
     for got, want in zip(snaps, (wb, wa)):
         for a, b in zip(got, want):
             assert np.array_equal(a, b)
+
+
+def test_graph_forward_replays_current_scene():
+    """A captured view re-reads the scene buffers at every replay."""
+    scene, cams = scenes.config1(n=20_000)
+    cam = cams[0].crop(200, 100, 320, 200)
+    rast = Rasterizer()
+    g = GaussianTensors.from_arrays(scene)
+    out = (torch.empty((200, 320, 3), device="cuda"), torch.empty((200, 320), device="cuda"))
+    rast.graph_forward(g, cam, out)
+    want = rast.forward(g, cam, track=False).img
+    assert torch.equal(out[0], want)
+    g.diffuse.mul_(0.5)  # in-place parameter update, same buffers
+    rast.graph_forward(g, cam, out)
+    want2 = rast.forward(g, cam, track=False).img
+    assert torch.equal(out[0], want2) and not torch.equal(want, want2)
