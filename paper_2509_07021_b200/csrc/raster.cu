@@ -24,6 +24,8 @@
 // Per-primitive partials are reduced across the warp with shuffles, across
 // warps in shared memory, and flushed to HBM with one atomic per value per
 // (primitive, tile).
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace sgs {
@@ -225,9 +227,14 @@ __device__ __forceinline__ bool warp_any(bool p) {
 // again, and re-terminating leaves -|T| unchanged.
 //   alpha = min(2^p, 0.99),  w = alpha T,  Tn = T - w   (sgs_geom.h SGS_T_KEEP)
 //   keep = Tn >= T_keep:  C += w c,  T = Tn;   else T = -|T|
+// kClamp = false when no record of the batch can reach alpha 0.99 (the
+// staging checks log2 o_eff < kLog2AlphaSafe), which drops the clamp.
+constexpr float kLog2AlphaSafe = -0.0146f;  // 2^x = 0.98993 < 0.99 with ex2.approx's error
+template <bool kClamp>
 __device__ __forceinline__ bool blend_px(float p, const float4& c, float& T, float& C0, float& C1, float& C2,
                                          float& w) {
-  const float alpha = fminf(ex2_approx(p), SGS_ALPHA_MAX);
+  const float a = ex2_approx(p);
+  const float alpha = kClamp ? fminf(a, SGS_ALPHA_MAX) : a;
   w = alpha * T;
   const float Tn = T - w;
   const bool keep = Tn >= SGS_T_KEEP;
@@ -254,8 +261,12 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(ListArgs la, Sg
   if (!ordered_tile<kFilter>(la, cam, blockIdx.x, tx, ty)) return;
   const int tile = ty * cam.tiles_x + tx;
   const int t = threadIdx.x, lane = t & 31;
-  const int px = tx * SGS_TILE + (t & 15);
-  const int py0 = ty * SGS_TILE + 2 * (t >> 4);  // rows py0 and py0 + 1
+  // warp w covers the 8x8 quadrant (w & 1, w >> 1) of the tile: lane l owns
+  // column l & 7 and rows 2 (l >> 3), 2 (l >> 3) + 1 of it (square blocks
+  // keep a warp's supports and termination more coherent than 16x4 strips)
+  const int wq = t >> 5, lq = t & 31;
+  const int px = tx * SGS_TILE + (wq & 1) * 8 + (lq & 7);
+  const int py0 = ty * SGS_TILE + (wq >> 1) * 8 + 2 * (lq >> 3);  // rows py0 and py0 + 1
   const bool in0 = px < cam.width && py0 < cam.height;
   const bool in1 = px < cam.width && py0 + 1 < cam.height;
   const float fx = (float)px + 0.5f, fy0 = (float)py0 + 0.5f;
@@ -283,14 +294,17 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(ListArgs la, Sg
     // pad the batch to a whole number of vote groups with records of zero
     // opacity (log2 o = -inf), so the group loop below needs no bounds checks
     const int nb_pad = (nb + kVoteEvery - 1) / kVoteEvery * kVoteEvery;
-    if (nb_pad != nb) {
-      if (t < nb_pad - nb) {
-        s.geo[nb + t] = make_float4(0.0f, 0.0f, -INFINITY, 0.0f);
-        s.con[nb + t] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-        s.col[nb + t] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-      }
-      __syncthreads();
+    if (t < nb_pad - nb) {
+      s.geo[nb + t] = make_float4(0.0f, 0.0f, -INFINITY, 0.0f);
+      s.con[nb + t] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+      s.col[nb + t] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
     }
+    // can any staged record reach the alpha clamp?  (almost never: o_eff >= 0.99)
+    bool clampable = false;
+    for (int i = t; i < nb; i += kFwdThreads) clampable |= s.geo[i].z >= kLog2AlphaSafe;
+    const bool batch_clamp = __syncthreads_or(clampable);
+    auto run_batch = [&](auto clamp_tag) {
+    constexpr bool kClamp = decltype(clamp_tag)::value;
     for (int k = 0; k < nb_pad; k += kVoteEvery) {
       if (!warp_any(T0 > 0.0f || T1 > 0.0f)) break;
 #pragma unroll
@@ -309,8 +323,8 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(ListArgs la, Sg
         {
           const float4 c = s.col[kk];
           float w0, w1;
-          const bool k0 = blend_px(p0, c, T0, C00, C01, C02, w0);
-          const bool k1 = blend_px(p1, c, T1, C10, C11, C12, w1);
+          const bool k0 = blend_px<kClamp>(p0, c, T0, C00, C01, C02, w0);
+          const bool k1 = blend_px<kClamp>(p1, c, T1, C10, C11, C12, w1);
           if (kTrack && kk < nb) {  // padding records are never counted
             const uint32_t idx = hits_before + (uint32_t)kk + 1u;
             if (k0) nc0 = idx;
@@ -327,6 +341,11 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(ListArgs la, Sg
         }
       }
     }
+    };
+    if (batch_clamp)
+      run_batch(std::true_type{});
+    else
+      run_batch(std::false_type{});
     if (kTrack) {
       // candidate position of this thread's last kept entry (for the backward)
       const uint32_t mx = nc0 > nc1 ? nc0 : nc1;
