@@ -129,6 +129,7 @@ __global__ void __launch_bounds__(1024) cell_order_kernel(const uint2* __restric
 // Shared-memory staging buffer of N records.
 template <int N>
 struct Stage {
+  static constexpr bool kIds = true;
   float4 geo[N];
   float4 con[N];
   float4 col[N];
@@ -137,14 +138,25 @@ struct Stage {
   uint32_t wcnt[32];
 };
 
+// Stage without primitive ids / candidate positions (image-only forward):
+// 8 KB less shared memory per CTA.
+template <int N>
+struct StageNoIds {
+  static constexpr bool kIds = false;
+  float4 geo[N];
+  float4 con[N];
+  float4 col[N];
+  uint32_t wcnt[32];
+};
+
 // Append the members of tile (tx, ty) among candidates [c_lo, c_hi) (at
 // most THREADS * CPT) of the cell list to the shared-memory batch at `base`,
 // in list order.  Depth-first mode reads membership from the 16-bit tile mask
 // carried in each sorted key (bit `local_bit`); 64-bit-key lists are per
 // tile already.  Returns the number appended.  Ends with __syncthreads().
-template <int THREADS, int CPT, bool kFilter, bool kColor, int N>
+template <int THREADS, int CPT, bool kFilter, bool kColor, class S>
 __device__ __forceinline__ int stage_append(uint32_t c_lo, uint32_t c_hi, uint32_t local_bit, const ListArgs& a,
-                                            int base, Stage<N>& s) {
+                                            int base, S& s) {
   constexpr int W = THREADS / 32;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const uint32_t lt = (1u << lane) - 1u;
@@ -174,8 +186,10 @@ __device__ __forceinline__ int stage_append(uint32_t c_lo, uint32_t c_hi, uint32
       s.geo[pos] = a.geo[g];
       s.con[pos] = a.eig[g];
       if (kColor) s.col[pos] = a.col[g];
-      s.id[pos] = g;
-      s.cand[pos] = c;
+      if constexpr (S::kIds) {
+        s.id[pos] = g;
+        s.cand[pos] = c;
+      }
     }
   }
   __syncthreads();
@@ -254,7 +268,7 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(ListArgs la, Sg
                                                                  uint32_t* __restrict__ out_nc,
                                                                  float* __restrict__ weight_sums,
                                                                  unsigned long long* __restrict__ pair_count) {
-  __shared__ Stage<kFwdBuf> s;
+  __shared__ std::conditional_t<kImportance || kTrack, Stage<kFwdBuf>, StageNoIds<kFwdBuf>> s;
   __shared__ uint32_t s_kend;
 
   int tx, ty;
@@ -330,7 +344,7 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(ListArgs la, Sg
             if (k0) nc0 = idx;
             if (k1) nc1 = idx;
           }
-          if (kImportance) {
+          if constexpr (kImportance) {
             w0 = k0 ? w0 : 0.0f;
             w1 = k1 ? w1 : 0.0f;
             if (warp_any(w0 != 0.0f || w1 != 0.0f)) {
@@ -346,7 +360,7 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(ListArgs la, Sg
       run_batch(std::true_type{});
     else
       run_batch(std::false_type{});
-    if (kTrack) {
+    if constexpr (kTrack) {
       // candidate position of this thread's last kept entry (for the backward)
       const uint32_t mx = nc0 > nc1 ? nc0 : nc1;
       if (mx > hits_before) kend = s.cand[mx - hits_before - 1] + 1u;
