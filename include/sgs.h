@@ -135,7 +135,9 @@ int sgs_preprocess(const sgs_params* params, const sgs_camera* cam, const sgs_wo
  * ws->sort_mode picks SGS_SORT_DEPTH_FIRST or SGS_SORT_KEY64; both produce
  * bit-identical results.  Never synchronises: when E exceeds the workspace's
  * entry capacity only the first `capacity` entries are kept and
- * sgs_stats.overflow is set -- grow the workspace and redo the frame. */
+ * sgs_stats.overflow is set -- grow the workspace and redo the frame.
+ * In SGS_SORT_DEPTH_FIRST mode the depth-digit histograms are accumulated by
+ * sgs_preprocess, so each sgs_bin must follow its own sgs_preprocess. */
 int sgs_bin(const sgs_camera* cam, const sgs_workspace* ws, void* stream);
 
 /* K5 forward raster -- replaces _chunk_blend + _render_params

@@ -167,7 +167,15 @@ __global__ void __launch_bounds__(256) emit_entries(const uint32_t* __restrict__
                                                     const unsigned long long* __restrict__ offsets, SgsCam cam,
                                                     int super_x, uint32_t cap,
                                                     const unsigned long long* __restrict__ total_ptr,
-                                                    KT* __restrict__ keys_out, uint32_t* __restrict__ vals_out) {
+                                                    KT* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
+                                                    uint32_t* __restrict__ cell_hist) {
+  // cell_hist (single-pass super-tile sort): counts of the 9-bit cell digit
+  // of every written entry, accumulated per CTA in shared memory
+  __shared__ uint32_t s_hist[512];
+  if (cell_hist) {
+    for (int j = threadIdx.x; j < 512; j += blockDim.x) s_hist[j] = 0;
+    __syncthreads();
+  }
   const int lane = threadIdx.x & 31;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -235,8 +243,10 @@ __global__ void __launch_bounds__(256) emit_entries(const uint32_t* __restrict__
           if (o < lim) {
             const uint32_t col = (uint32_t)rfirst + (j - rex);
             const uint32_t cell = (uint32_t)(rrow * row_w) + col;
-            if (kSuper)
+            if (kSuper) {
               keys_out[o] = (KT)((cell << 16) | sgs_super_mask(mf, mc, (int)col));
+              if (cell_hist) atomicAdd(&s_hist[cell & 511u], 1u);
+            }
             else
               keys_out[o] = make_key<KT>(cell, sizeof(KT) == 8 ? depth_key[rg] : 0u);
             vals_out[o] = rg;
@@ -245,6 +255,11 @@ __global__ void __launch_bounds__(256) emit_entries(const uint32_t* __restrict__
       }
       out += Ctot;
     }
+  }
+  if (cell_hist) {
+    __syncthreads();
+    for (int j = threadIdx.x; j < 512; j += blockDim.x)
+      if (s_hist[j]) atomicAdd(&cell_hist[j], s_hist[j]);
   }
 }
 
@@ -269,6 +284,8 @@ bool final_in_alt(const Layout& lo) {
 template <typename KT, int IPT, int RBITS, bool kSuper>
 static int bin_entries(const SgsCam& cam, const sgs_workspace* ws, const Layout& lo, const uint32_t* perm,
                        int key_bits, int tile_shift, cudaStream_t st) {
+  // the emission accumulates the histogram when the cell sort is one 9-bit pass
+  const bool fused_hist = kSuper && RBITS == 9 && key_bits <= 9;
   Counters* ctr = at<Counters>(ws, lo.counters);
   const uint32_t n = (uint32_t)lo.n;
   const uint32_t cap = (uint32_t)lo.cap;
@@ -285,12 +302,14 @@ static int bin_entries(const SgsCam& cam, const sgs_workspace* ws, const Layout&
       perm, n, at<uint32_t>(ws, kSuper ? lo.super_touched : lo.tiles_touched), at<uint2>(ws, lo.rect),
       at<float4>(ws, lo.rec_geo), at<float4>(ws, lo.rec_con), at<float4>(ws, lo.rec_span),
       at<uint32_t>(ws, lo.depth_key),
-      at<unsigned long long>(ws, lo.offsets), cam, lo.super_x, cap, &ctr->n_bin, k0, v0);
+      at<unsigned long long>(ws, lo.offsets), cam, lo.super_x, cap, &ctr->n_bin, k0, v0,
+      fused_hist ? at<uint32_t>(ws, lo.hist) + kSuperHistOff : nullptr);
   SGS_LAUNCH_CHECK("emit_entries");
   bool alt = false;
-  int rc = radix_sort_pairs<KT, IPT, RBITS>(k0, v0, k1, v1, &ctr->n_sort, cap, key_bits, at<uint32_t>(ws, lo.hist),
+  uint32_t* hist = at<uint32_t>(ws, lo.hist) + (fused_hist ? kSuperHistOff : 0);
+  int rc = radix_sort_pairs<KT, IPT, RBITS>(k0, v0, k1, v1, &ctr->n_sort, cap, key_bits, hist,
                                      at<uint32_t>(ws, lo.status), &ctr->part_counter[8], &alt, st, false,
-                                     RsRangeOut{ranges, tile_shift}, kSuper ? 16 : 0, kSuper);
+                                     RsRangeOut{ranges, tile_shift}, kSuper ? 16 : 0, kSuper, fused_hist);
   if (rc) return rc;
   ranges_fix<<<rgrid, 256, 0, st>>>(ranges, n_cells);
   SGS_LAUNCH_CHECK("ranges_fix");
@@ -314,9 +333,11 @@ int launch_bin(const SgsCam& cam, const sgs_workspace* ws, const Layout& lo, cud
     SGS_LAUNCH_CHECK("set_count");
     bool alt = false;
     // depth keys are 31-bit (0x7fffffff = not emitting): 4 passes over N
-    int rc = radix_sort_pairs<uint32_t, kDepthSortIPT, 8>(ka, ia, kb, ib, &ctr->n_depth, n, 31, at<uint32_t>(ws, lo.hist),
+    // the preprocess accumulated the four depth-digit histograms
+    int rc = radix_sort_pairs<uint32_t, kDepthSortIPT, 8>(ka, ia, kb, ib, &ctr->n_depth, n, 31,
+                                                        at<uint32_t>(ws, lo.hist) + kDepthHistOff,
                                                         at<uint32_t>(ws, lo.status), &ctr->part_counter[0], &alt, st,
-                                                        true);
+                                                        true, RsRangeOut{nullptr, 0}, 0, false, true);
     if (rc) return rc;
     const uint32_t* perm = alt ? ib : ia;
     rc = launch_scan(at<uint32_t>(ws, lo.super_touched), perm, n, cap, block_sums, offsets, ctr, st);

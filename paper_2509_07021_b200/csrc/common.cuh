@@ -17,6 +17,12 @@ constexpr int kTileSortIPT = 16;  // items per thread, tile-key onesweep passes 
 constexpr int kDepthSortIPT = 16;  // 1M depth keys = 123 tiles: one wave of one CTA per SM
 constexpr int kKey64SortIPT = 6;
 constexpr uint32_t kMaxEntries = (1u << 30) - 1;  // look-back status packs 30-bit counts
+// Digit histograms accumulated by producer kernels (depth-first mode): the
+// preprocess counts the 4 depth-key digits, the emission the 9-bit
+// super-tile digit.  Both live in the workspace's hist buffer, zeroed by
+// sgs_preprocess.
+constexpr int kDepthHistOff = 0;      // 4 x 256 u32
+constexpr int kSuperHistOff = 1024;   // 512 u32
 
 void set_error(const char* fmt, ...);
 int cuda_fail(cudaError_t e, const char* what);

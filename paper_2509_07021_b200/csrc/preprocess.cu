@@ -30,8 +30,14 @@ __global__ void __launch_bounds__(256, 3) preprocess_kernel(sgs_params P, SgsCam
                                                          float4* __restrict__ rec_eig,
                                                          uint32_t* __restrict__ depth_key, uint2* __restrict__ rect,
                                                          uint32_t* __restrict__ tiles_touched,
-                                                         uint32_t* __restrict__ super_touched, Counters* ctr) {
+                                                         uint32_t* __restrict__ super_touched,
+                                                         uint32_t* __restrict__ depth_hist, Counters* ctr) {
   __shared__ uint32_t s_cnt[8][32], s_sup[8][32];
+  __shared__ uint32_t s_hist[4][256];  // depth-key digit counts of this CTA's primitives
+  if (depth_hist) {
+    for (int j = threadIdx.x; j < 4 * 256; j += blockDim.x) (&s_hist[0][0])[j] = 0;
+    __syncthreads();
+  }
   const int64_t n = P.n;
   const int L = kL > 0 ? kL : P.n_lobes;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -97,7 +103,12 @@ __global__ void __launch_bounds__(256, 3) preprocess_kernel(sgs_params P, SgsCam
     if (live) {
       tiles_touched[i] = cnt;
       super_touched[i] = nsup;
-      depth_key[i] = emitting ? sgs_float_to_bits(pr.depth) : 0x7fffffffu;
+      const uint32_t dk = emitting ? sgs_float_to_bits(pr.depth) : 0x7fffffffu;
+      depth_key[i] = dk;
+      if (depth_hist) {
+#pragma unroll
+        for (int d = 0; d < 4; ++d) atomicAdd(&s_hist[d][(dk >> (8 * d)) & 0xffu], 1u);
+      }
       rect[i] = make_uint2((uint32_t)(pr.tx0 & 0xffff) | ((uint32_t)(pr.tx1 & 0xffff) << 16),
                            (uint32_t)(pr.ty0 & 0xffff) | ((uint32_t)(pr.ty1 & 0xffff) << 16));
       if (emitting) {
@@ -132,6 +143,13 @@ __global__ void __launch_bounds__(256, 3) preprocess_kernel(sgs_params P, SgsCam
     unsigned long long e = cnt;
     for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
     if (lane == 0 && e) atomicAdd(&ctr->n_entries, e);
+  }
+  if (depth_hist) {
+    __syncthreads();
+    for (int j = threadIdx.x; j < 4 * 256; j += blockDim.x) {
+      const uint32_t v = (&s_hist[0][0])[j];
+      if (v) atomicAdd(&depth_hist[j], v);
+    }
   }
 }
 
@@ -226,7 +244,9 @@ int launch_preprocess(const sgs_params& P, const SgsCam& cam, const sgs_workspac
                                               at<float4>(ws, lo.rec_col), at<float4>(ws, lo.rec_span),           \
                                               at<float4>(ws, lo.rec_eig), at<uint32_t>(ws, lo.depth_key),        \
                                               at<uint2>(ws, lo.rect), at<uint32_t>(ws, lo.tiles_touched),        \
-                                              at<uint32_t>(ws, lo.super_touched), ctr)
+                                              at<uint32_t>(ws, lo.super_touched),                                 \
+                                              lo.sort_mode == SGS_SORT_DEPTH_FIRST                                 \
+                                                  ? at<uint32_t>(ws, lo.hist) + kDepthHistOff : nullptr, ctr)
   if (P.n_lobes == 3)
     SGS_PRE(3);
   else

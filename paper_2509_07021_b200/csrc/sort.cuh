@@ -292,18 +292,20 @@ inline uint64_t rs_parts(uint64_t n) {
 // input values are the item indices (v0 is not read).  With `rout.ranges`,
 // the last pass also writes the cell ranges (and skips its key writes unless
 // keep_last_keys).  hist: 16*512 u32; status: parts*512*passes u32; tickets:
-// >= passes u32; all zeroed here.
+// >= passes u32; all zeroed here (hist only when !hist_ready).
 template <typename K, int IPT, int RBITS>
 int radix_sort_pairs(K* k0, uint32_t* v0, K* k1, uint32_t* v1, const uint32_t* n_ptr, uint32_t n_cap, int bits,
                      uint32_t* hist, uint32_t* status, uint32_t* tickets, bool* result_in_alt, cudaStream_t st,
                      bool iota_values = false, RsRangeOut rout = RsRangeOut{nullptr, 0}, int begin_bit = 0,
-                     bool keep_last_keys = false) {
+                     bool keep_last_keys = false, bool hist_ready = false) {
   constexpr int R = 1 << RBITS;
   const int passes = (bits + RBITS - 1) / RBITS;
   const uint64_t parts = rs_parts<K, IPT>(n_cap);
   *result_in_alt = false;
   if (n_cap == 0 || passes == 0) return SGS_OK;
-  SGS_CUDA(cudaMemsetAsync(hist, 0, (size_t)passes * R * 4, st));
+  // hist_ready: the producer kernel already accumulated every pass's digit
+  // counts into the (zeroed) hist; only the exclusive scan remains
+  if (!hist_ready) SGS_CUDA(cudaMemsetAsync(hist, 0, (size_t)passes * R * 4, st));
   SGS_CUDA(cudaMemsetAsync(status, 0, (size_t)parts * R * 4 * passes, st));
   SGS_CUDA(cudaMemsetAsync(tickets, 0, (size_t)passes * 4, st));
   const int sms = device_sm_count();
@@ -316,8 +318,10 @@ int radix_sort_pairs(K* k0, uint32_t* v0, K* k1, uint32_t* v1, const uint32_t* n
     SGS_CUDA(cudaFuncSetAttribute(rs_histogram<K, RBITS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     hattr = true;
   }
-  rs_histogram<K, RBITS><<<hgrid, 256, hsmem, st>>>(k0, n_ptr, n_cap, begin_bit, passes, hist);
-  SGS_LAUNCH_CHECK("rs_histogram");
+  if (!hist_ready) {
+    rs_histogram<K, RBITS><<<hgrid, 256, hsmem, st>>>(k0, n_ptr, n_cap, begin_bit, passes, hist);
+    SGS_LAUNCH_CHECK("rs_histogram");
+  }
   rs_scan_hist<RBITS><<<passes, R, 0, st>>>(hist);
   SGS_LAUNCH_CHECK("rs_scan_hist");
   const size_t smem = sizeof(RsSmem<K, IPT, RBITS>);
