@@ -464,8 +464,9 @@ __global__ void __launch_bounds__(kBwdThreads) raster_bwd_kernel(ListArgs la, Sg
   const int tile = blockIdx.x + cam.tile_y0 * cam.tiles_x;
   const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
   const int t = threadIdx.x, lane = t & 31;
-  const int px = tx * SGS_TILE + (t & 15);
-  const int py0 = ty * SGS_TILE + 2 * (t >> 4);
+  const int wq = t >> 5, lq = t & 31;  // 8x8 quadrants per warp, as in the forward
+  const int px = tx * SGS_TILE + (wq & 1) * 8 + (lq & 7);
+  const int py0 = ty * SGS_TILE + (wq >> 1) * 8 + 2 * (lq >> 3);
   const bool in0 = px < cam.width && py0 < cam.height;
   const bool in1 = px < cam.width && py0 + 1 < cam.height;
   const float fx = (float)px + 0.5f, fy0 = (float)py0 + 0.5f;
@@ -520,6 +521,17 @@ __global__ void __launch_bounds__(kBwdThreads) raster_bwd_kernel(ListArgs la, Sg
       const float dx = fx - G.x;
       const float dy0 = fy0 - G.y, dy1 = dy0 + 1.0f;
       const float e1dx = E.x * dx, e3dx = E.w * dx;
+      float pq[2];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const float dy = q ? dy1 : dy0;
+        const float t1 = fmaf(E.y, dy, e1dx), t2 = fmaf(E.z, dy, -e3dx);
+        pq[q] = fmaf(-t1, t1, fmaf(-t2, t2, G.z));
+      }
+      // A record outside the support of every active pixel of the warp
+      // (alpha < 1e-7 for all of them) contributes < 1e-7 of any partial and
+      // changes T by a factor within 1e-7 of 1: skip it whole.
+      if (!warp_any((idx < nc0 && pq[0] >= SGS_LOG2_EPS) || (idx < nc1 && pq[1] >= SGS_LOG2_EPS))) continue;
       float v[kGrad];
 #pragma unroll
       for (int c = 0; c < kGrad; ++c) v[c] = 0.0f;
@@ -527,8 +539,7 @@ __global__ void __launch_bounds__(kBwdThreads) raster_bwd_kernel(ListArgs la, Sg
       for (int q = 0; q < 2; ++q) {
         const float dy = q ? dy1 : dy0;
         const bool act = idx < (q ? nc1 : nc0);
-        const float t1 = fmaf(E.y, dy, e1dx), t2 = fmaf(E.z, dy, -e3dx);
-        const float p = fmaf(-t1, t1, fmaf(-t2, t2, G.z));
+        const float p = pq[q];
         const float a = ex2_approx(p);
         const float alpha = fminf(a, SGS_ALPHA_MAX);
         const float om = 1.0f - alpha;  // the forward's T_next = T - alpha T
