@@ -36,6 +36,12 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -449,8 +455,8 @@ __device__ __forceinline__ int reduce9_index(int lane) {
 // thread sums its two pixels' nine partials, the warp reduces them with
 // warp_reduce9, and nine lanes add the totals into the batch's shared
 // accumulators (4 warps per record); each batch is flushed with one global
-// atomic per (record, partial).  T is recovered with one correctly rounded
-// reciprocal per pixel-record: T_i = T_{i+1} / (1 - alpha_i).
+// atomic per (record, partial).  T is recovered with one hardware reciprocal
+// per pixel-record, T_i = T_{i+1} rcp(1 - alpha_i) (~1 ulp per record).
 template <bool kFilter>
 __global__ void __launch_bounds__(kBwdThreads) raster_bwd_kernel(ListArgs la, SgsCam cam, float3 bg,
                                                                  const float* __restrict__ final_T,
@@ -543,7 +549,7 @@ __global__ void __launch_bounds__(kBwdThreads) raster_bwd_kernel(ListArgs la, Sg
         const float a = ex2_approx(p);
         const float alpha = fminf(a, SGS_ALPHA_MAX);
         const float om = 1.0f - alpha;  // the forward's T_next = T - alpha T
-        const float rom = __frcp_rn(om);
+        const float rom = rcp_approx(om);  // om in [0.0099, 1]: MUFU.RCP, ~1 ulp
         float& T = q ? T1 : T0;
         float& S = q ? S1 : S0;
         const float gx = q ? g10 : g00, gy = q ? g11 : g01, gz = q ? g12 : g02;

@@ -155,6 +155,15 @@ class Frame:
     def stats(self) -> dict:
         return self.ws.stats()
 
+    def record_overflow(self, dst: torch.Tensor) -> None:
+        """Copy this frame's (overflow, binned entries) counters into the int64
+        device tensor ``dst`` (2 elements) without a host round trip, so a
+        caller can check many frames with one read (Counters layout,
+        common.cuh: overflow at u64 slot 4, n_bin at slot 7)."""
+        c = self.ws.buf[:64].view(torch.int64)
+        dst[0].copy_(c[4])
+        dst[1].copy_(c[7])
+
 
 MAX_CAPACITY = (1 << 30) - 1
 
@@ -198,6 +207,15 @@ class Rasterizer:
             ws = Workspace(*key[:4], cap, self.sort_mode, self.device)
             self._shared[skey] = ws
         return ws
+
+    def grow_capacity(self, g, cam, n_entries: int) -> None:
+        """Size the tile-entry capacity for ``n_entries`` binned entries (the
+        deferred form of forward(check=True)'s retry)."""
+        if n_entries > MAX_CAPACITY:
+            raise _ffi.CapacityError("sgs_bin", _ffi.SGS_E_CAPACITY,
+                                     f"{n_entries} entries exceed one bin call's limit {MAX_CAPACITY}")
+        key = self._key(g, cam)
+        self._cap_hint[key] = min(MAX_CAPACITY, int(n_entries * self.headroom) + 1024)
 
     def release(self):
         self.release_graphs()

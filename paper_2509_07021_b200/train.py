@@ -67,12 +67,12 @@ class SoftPruneTrainer:
             return SimpleNamespace(**self.params, lobe_mask=m_l.contiguous(), prim_mask=m_p.contiguous())
         return GaussianTensors(**self.params, lobe_mask=m_l.contiguous(), prim_mask=m_p.contiguous())
 
-    def _view_grads(self, g: GaussianTensors, cam, target):
+    def _view_grads(self, g: GaussianTensors, cam, target, overflow=None):
         if self.grad_fn is not None:
             return self.grad_fn(g, cam, target)
         from .render import LossConfig, loss_and_grads_device
         return loss_and_grads_device(g, cam, target, LossConfig(lambda_ssim=self.cfg.lambda_ssim),
-                                     rast=self.rast, mask_grads=True, sync=False)
+                                     rast=self.rast, mask_grads=True, sync=False, overflow_out=overflow)
 
     def step(self, cams, targets, rank: int = 0, world: int = 1, apply: bool = True) -> float:
         """One step over all views (this rank renders its round-robin share);
@@ -83,8 +83,11 @@ class SoftPruneTrainer:
         g = self.gaussians()
         m_p, m_l = g.prim_mask, g.lobe_mask
         loss_sum = torch.zeros((), dtype=torch.float64, device=self.device)
-        for v in mine:
-            val, gr = self._view_grads(g, cams[v], targets[v])
+        # tile-entry overflow is checked once per step (no host round trip per view)
+        ovf = None if self.grad_fn is not None else torch.zeros((len(mine), 2), dtype=torch.int64,
+                                                                device=self.device)
+        for j, v in enumerate(mine):
+            val, gr = self._view_grads(g, cams[v], targets[v], None if ovf is None else ovf[j])
             loss_sum += val
             d_mp = gr.pop("prim_mask")
             d_ml = gr.pop("lobe_mask")
@@ -92,6 +95,20 @@ class SoftPruneTrainer:
             self.bucket.add_(gr)
             self.bucket.view("prim_logit").add_(d_mp * m_p * (1 - m_p))
             self.bucket.view("lobe_logit").add_(d_ml * m_l * (1 - m_l))
+        if ovf is not None:
+            # some view outgrew its capacity: size it and redo the step (on every
+            # rank together, so the collectives below stay matched)
+            import torch.distributed as dist
+            need = (ovf[:, 0].max() if len(mine) else torch.zeros((), dtype=torch.int64,
+                                                                   device=self.device)).reshape(1)
+            if dist.is_available() and dist.is_initialized() and dist.get_world_size(self.group) > 1:
+                dist.all_reduce(need, op=dist.ReduceOp.MAX, group=self.group)
+            if int(need.item()):
+                o = ovf.cpu()
+                for j, v in enumerate(mine):
+                    if o[j, 0]:
+                        self.rast.grow_capacity(g, cams[v], int(o[j, 1]))
+                return self.step(cams, targets, rank, world, apply)
         # all-reduce the summed view gradients and the loss, then average
         stats = torch.stack([loss_sum, torch.tensor(float(len(mine)), dtype=torch.float64,
                                                     device=self.device)])

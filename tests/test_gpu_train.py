@@ -50,3 +50,25 @@ def test_train_steps_reduce_loss():
     losses = [tr.step(cams, targets) for _ in range(6)]
     assert losses[-1] < losses[0]
     assert all(np.isfinite(losses))
+
+
+def test_step_redoes_views_that_outgrow_capacity():
+    """A deliberately tiny tile-entry capacity: the deferred per-step check
+    grows it and redoes the step, matching a step with ample capacity."""
+    import numpy as np
+    import torch
+    from paper_2509_07021_b200 import scenes
+    from paper_2509_07021_b200.rasterizer import Rasterizer
+    from paper_2509_07021_b200.train import SoftPruneTrainer
+    scene, cams = scenes.config3(n=3000, n_views=2)
+    cams = [c.crop(400, 200, 256, 160) for c in cams]
+    tg = [torch.from_numpy(scenes.target_image(0, c.height, c.width, v)).cuda() for v, c in enumerate(cams)]
+    out = []
+    for cap in (64, None):
+        tr = SoftPruneTrainer(scene, scene.extra["prim_logit"], scene.extra["lobe_logit"])
+        tr.rast = Rasterizer(initial_capacity=cap)
+        loss = tr.step(cams, tg, apply=False)
+        out.append((loss, {k: v.clone() for k, v in tr.grads().items()}))
+    assert out[0][0] == pytest.approx(out[1][0], rel=1e-6)
+    for k in out[0][1]:
+        np.testing.assert_allclose(out[0][1][k].cpu().numpy(), out[1][1][k].cpu().numpy(), rtol=1e-4, atol=1e-7)
