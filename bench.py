@@ -36,11 +36,12 @@ sys.path.insert(0, str(ROOT))
 METRIC = "frames/s & Mpix/s at 1080p, 1M Gaussians, 3 SG lobes (1/2/4/8 B200); peak render VRAM"
 UNIT = "frames/s"
 WORKLOAD = "configs[2]: 1,000,000 Gaussians (64 clusters), 3 SG lobes, 1920x1080, FoV 60"
-# libsgs kernels per forward frame (depth-first mode, 1080p): preprocess; set_count,
-# histogram, histogram scan, 4 onesweep passes (depth sort); 3 scan kernels;
-# ranges_init, emit_entries; histogram, histogram scan, 1 onesweep pass (super-tile
-# sort + ranges); ranges_fix; cell_order, raster_fwd
-KERNELS_PER_FRAME = 19
+# libsgs kernels per forward frame (depth-first mode, 1080p): preprocess (also
+# accumulates the depth-digit histograms); set_count, histogram scan, 4 onesweep
+# passes (depth sort); 3 offsets-scan kernels; ranges_init, emit_entries (also the
+# cell histogram); histogram scan + 1 onesweep pass (super-tile sort + ranges);
+# ranges_fix; cell_order, raster_fwd
+KERNELS_PER_FRAME = 17
 
 
 def parse():
@@ -419,7 +420,10 @@ def run_ours(args):
                          "achieved": achieved / 1e9, "peak": peak_pairs / 1e9, "unit": "Gpair/s",
                          "frac": achieved / peak_pairs, "traffic": profiled_traffic("raster_fwd_kernel"),
                          "note": f"pairs/view={pairs_per_view:.4g} (GPU counter); peak = SMs x "
-                                 f"{sm_mhz:.0f} MHz ({src} sm_max) x 128/18 pairs/clk/SM",
+                                 f"{sm_mhz:.0f} MHz ({src} sm_max) x 128/18 pairs/clk/SM; the "
+                                 f"kernel's DRAM traffic is "
+                                 f"{(profiled_traffic('raster_fwd_kernel') or 0) / (float(np.mean(raster_ms)) / 1e3) / 1e9:.0f}"
+                                 f" GB/s ({(profiled_traffic('raster_fwd_kernel') or 0) / (float(np.mean(raster_ms)) / 1e3) / 1e9 / float(peaks.get('hbm_gbs', 6549.1)):.3f} of HBM): not memory-bound",
                          "raster_ms_per_view": float(np.mean(raster_ms))},
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(pinned.nbytes),
                     "d2h_bytes_per_step": int(BatchRenderer.d2h_bytes(my_cams))},
