@@ -168,7 +168,9 @@ __global__ void __launch_bounds__(256) emit_entries(const uint32_t* __restrict__
                                                     int super_x, uint32_t cap,
                                                     const unsigned long long* __restrict__ total_ptr,
                                                     KT* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
-                                                    uint32_t* __restrict__ cell_hist) {
+                                                    uint32_t* __restrict__ cell_hist,
+                                                    const uint32_t* __restrict__ row_off,
+                                                    const uint16_t* __restrict__ row_spans) {
   // cell_hist (single-pass super-tile sort): counts of the 9-bit cell digit
   // of every written entry, accumulated per CTA in shared memory
   __shared__ uint32_t s_hist[512];
@@ -186,11 +188,12 @@ __global__ void __launch_bounds__(256) emit_entries(const uint32_t* __restrict__
     unsigned long long out = offsets[base];  // uniform: every lane reads the same word
     if (out >= lim) continue;
     const uint32_t r = base + lane;
-    uint32_t g = 0, nrows = 0;
+    uint32_t g = 0, nrows = 0, roff = kNoRows;
     int tx0 = 0, ty0 = 0, tx1 = -1, ty1 = -1;
     if (r < n) {
       g = perm ? perm[r] : r;
       if (counts[g]) {
+        if (kSuper && row_off) roff = row_off[g];
         unpack_rect(rect[g], tx0, ty0, tx1, ty1);
         nrows = kSuper ? (uint32_t)(ty1 / SGS_SUPER - ty0 / SGS_SUPER + 1) : (uint32_t)(ty1 - ty0 + 1);
       }
@@ -207,18 +210,39 @@ __global__ void __launch_bounds__(256) emit_entries(const uint32_t* __restrict__
       const int otx0 = __shfl_sync(0xffffffffu, tx0, owner);
       const int otx1 = __shfl_sync(0xffffffffu, tx1, owner);
       const uint32_t ors = __shfl_sync(0xffffffffu, rstart, owner);
+      const uint32_t ooff = __shfl_sync(0xffffffffu, roff, owner);
       const int row = (kSuper ? oty0 / SGS_SUPER : oty0) + (int)(k - ors);
       uint32_t c = 0;
       int first = 0;
       int rf[SGS_SUPER] = {0, 0, 0, 0}, rc[SGS_SUPER] = {0, 0, 0, 0};
       if (k < R) {
-        const float4 g4 = rec_geo[og], c4 = rec_con[og];
-        const float4 s2 = rec_span[og];
-        const float geo[4] = {g4.x, g4.y, g4.z, g4.w}, con[4] = {c4.x, c4.y, c4.z, c4.w};
-        const float span2[3] = {s2.x, s2.y, s2.z};
-        const SgsSpan sp = sgs_span_cached(geo, con, span2);
-        c = kSuper ? (uint32_t)sgs_super_row_spans(&sp, &cam, otx0, oty0, otx1, oty1, row, rf, rc, &first)
-                   : (uint32_t)sgs_row_span(&sp, &cam, row, otx0, otx1, &first);
+        if (kSuper && ooff != kNoRows) {
+          // the preprocess's stored row spans (the values sgs_super_row_spans gives)
+          int lo = 0x7fffffff, hi = -1;
+#pragma unroll
+          for (int q = 0; q < SGS_SUPER; ++q) {
+            const int ty = row * SGS_SUPER + q;
+            const bool in = ty >= oty0 && ty <= oty1;
+            const uint32_t e = in ? (uint32_t)row_spans[ooff + (uint32_t)(ty - oty0)] : 0u;
+            rc[q] = (int)(e >> 8);
+            rf[q] = rc[q] > 0 ? otx0 + (int)(e & 0xffu) : 0;
+            if (rc[q] > 0) {
+              const int a = rf[q] / SGS_SUPER, b = (rf[q] + rc[q] - 1) / SGS_SUPER;
+              lo = a < lo ? a : lo;
+              hi = b > hi ? b : hi;
+            }
+          }
+          first = hi >= lo ? lo : 0;
+          c = hi >= lo ? (uint32_t)(hi - lo + 1) : 0u;
+        } else {
+          const float4 g4 = rec_geo[og], c4 = rec_con[og];
+          const float4 s2 = rec_span[og];
+          const float geo[4] = {g4.x, g4.y, g4.z, g4.w}, con[4] = {c4.x, c4.y, c4.z, c4.w};
+          const float span2[3] = {s2.x, s2.y, s2.z};
+          const SgsSpan sp = sgs_span_cached(geo, con, span2);
+          c = kSuper ? (uint32_t)sgs_super_row_spans(&sp, &cam, otx0, oty0, otx1, oty1, row, rf, rc, &first)
+                     : (uint32_t)sgs_row_span(&sp, &cam, row, otx0, otx1, &first);
+        }
       }
       const uint32_t cincl = warp_incl_scan(c, lane);
       const uint32_t cexcl = cincl - c;
@@ -303,7 +327,8 @@ static int bin_entries(const SgsCam& cam, const sgs_workspace* ws, const Layout&
       at<float4>(ws, lo.rec_geo), at<float4>(ws, lo.rec_con), at<float4>(ws, lo.rec_span),
       at<uint32_t>(ws, lo.depth_key),
       at<unsigned long long>(ws, lo.offsets), cam, lo.super_x, cap, &ctr->n_bin, k0, v0,
-      fused_hist ? at<uint32_t>(ws, lo.hist) + kSuperHistOff : nullptr);
+      fused_hist ? at<uint32_t>(ws, lo.hist) + kSuperHistOff : nullptr,
+      lo.row_cap ? at<uint32_t>(ws, lo.row_off) : nullptr, lo.row_cap ? at<uint16_t>(ws, lo.row_spans) : nullptr);
   SGS_LAUNCH_CHECK("emit_entries");
   bool alt = false;
   uint32_t* hist = at<uint32_t>(ws, lo.hist) + (fused_hist ? kSuperHistOff : 0);

@@ -16,6 +16,8 @@ constexpr int kRadixThreads = 512;  // = kRsThreads in sort.cuh
 constexpr int kTileSortIPT = 16;  // items per thread, tile-key onesweep passes (8192 per CTA)
 constexpr int kDepthSortIPT = 16;  // 1M depth keys = 123 tiles: one wave of one CTA per SM
 constexpr int kKey64SortIPT = 6;
+constexpr int kRowSpansPerPrim = 8;   // row-span store capacity, u16 entries per primitive
+constexpr uint32_t kNoRows = 0xffffffffu;  // row_off of a primitive whose spans are not stored
 constexpr uint32_t kMaxEntries = (1u << 30) - 1;  // look-back status packs 30-bit counts
 // Digit histograms accumulated by producer kernels (depth-first mode): the
 // preprocess counts the 4 depth-key digits, the emission the 9-bit
@@ -52,7 +54,8 @@ struct Counters {
   uint32_t n_sort;                   // min(E, capacity): items the tile sort processes
   uint32_t n_depth;                  // primitives entering the depth sort
   uint32_t part_counter[16];         // onesweep partition tickets, one per pass
-  uint32_t pad1[14];
+  uint32_t row_alloc;                // row-span store: entries handed out by the preprocess
+  uint32_t pad1[13];
 };
 
 // Carved workspace.  All sub-buffers 256-byte aligned.
@@ -64,7 +67,8 @@ struct Layout {
   int64_t cap;
   // offsets into the workspace
   uint64_t counters, rec_geo, rec_con, rec_col, rec_span, rec_eig, depth_key, rect, tiles_touched, super_touched, cand_end;
-  uint64_t cell_order;
+  uint64_t cell_order, row_off, row_spans;
+  uint64_t row_cap;
   uint64_t dkey_alt, dkey_tmp, didx, didx_alt, offsets, scan_blocks;
   uint64_t ent_key, ent_key_alt, ent_val, ent_val_alt, ranges;
   uint64_t hist, status;
@@ -128,6 +132,12 @@ inline int make_layout(const sgs_workspace* ws, Layout* lo) {
   lo->rect = take(n * 8);
   lo->tiles_touched = take(n * 4);
   lo->super_touched = take(n * 4);
+  // row-span store (depth-first mode): the preprocess's exact tile-row spans,
+  // one u16 per row, read back by the emission instead of re-solving them
+  lo->row_cap = ws->sort_mode == SGS_SORT_DEPTH_FIRST ? (uint64_t)kRowSpansPerPrim * n : 0;
+  if (lo->row_cap > 0xfffffff0ull) lo->row_cap = 0xfffffff0ull;  // u32 offsets
+  lo->row_off = take(n * 4);
+  lo->row_spans = take(lo->row_cap * 2);
   lo->cand_end = take((uint64_t)lo->n_tiles * 4);
   lo->cell_order = take((uint64_t)(lo->n_tiles > lo->n_super ? lo->n_tiles : lo->n_super) * 4);
   lo->dkey_alt = take(n * 4);

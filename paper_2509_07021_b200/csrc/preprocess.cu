@@ -31,7 +31,9 @@ __global__ void __launch_bounds__(256, 3) preprocess_kernel(sgs_params P, SgsCam
                                                          uint32_t* __restrict__ depth_key, uint2* __restrict__ rect,
                                                          uint32_t* __restrict__ tiles_touched,
                                                          uint32_t* __restrict__ super_touched,
-                                                         uint32_t* __restrict__ depth_hist, Counters* ctr) {
+                                                         uint32_t* __restrict__ depth_hist,
+                                                         uint32_t* __restrict__ row_off, uint16_t* __restrict__ row_spans,
+                                                         uint32_t row_cap, Counters* ctr) {
   __shared__ uint32_t s_cnt[8][32], s_sup[8][32];
   __shared__ uint32_t s_hist[4][256];  // depth-key digit counts of this CTA's primitives
   if (depth_hist) {
@@ -78,6 +80,19 @@ __global__ void __launch_bounds__(256, 3) preprocess_kernel(sgs_params P, SgsCam
     const uint32_t incl = warp_incl_scan(nitems, lane);
     const uint32_t start = incl - nitems;
     const uint32_t R = __shfl_sync(0xffffffffu, incl, 31);
+    // row-span store: one u16 (first column - tx0 | count << 8) per tile row of
+    // the support rectangle, space handed out per warp; primitives that do not
+    // fit (store full, or wider than 255 tiles) are re-solved by the emission
+    uint32_t my_off = kNoRows;
+    if (row_spans) {
+      const uint32_t nrows = pr.emits && pr.tx1 - pr.tx0 < 255 ? (uint32_t)(pr.ty1 - pr.ty0 + 1) : 0u;
+      const uint32_t rincl = warp_incl_scan(nrows, lane);
+      const uint32_t rtot = __shfl_sync(0xffffffffu, rincl, 31);
+      uint32_t rbase = 0;
+      if (lane == 31 && rtot) rbase = atomicAdd(&ctr->row_alloc, rtot);
+      rbase = __shfl_sync(0xffffffffu, rbase, 31);
+      if (nrows && (uint64_t)rbase + rincl <= row_cap) my_off = rbase + rincl - nrows;
+    }
     for (uint32_t k0 = 0; k0 < R; k0 += 32) {
       const uint32_t kk = k0 + lane;
       const int owner = lane_search(start, kk < R ? kk : R - 1);
@@ -87,6 +102,7 @@ __global__ void __launch_bounds__(256, 3) preprocess_kernel(sgs_params P, SgsCam
       const int otx1 = __shfl_sync(0xffffffffu, pr.tx1, owner);
       const int oty1 = __shfl_sync(0xffffffffu, pr.ty1, owner);
       const uint32_t ostart = __shfl_sync(0xffffffffu, start, owner);
+      const uint32_t ooff = __shfl_sync(0xffffffffu, my_off, owner);
       if (kk < R) {
         const int sr = oty0 / SGS_SUPER + (int)(kk - ostart);
         int rf[SGS_SUPER], rc[SGS_SUPER], fsc;
@@ -94,6 +110,15 @@ __global__ void __launch_bounds__(256, 3) preprocess_kernel(sgs_params P, SgsCam
         const uint32_t nt = (uint32_t)(rc[0] + rc[1] + rc[2] + rc[3]);
         if (nt) atomicAdd(&s_cnt[warp][owner], nt);
         if (nsc) atomicAdd(&s_sup[warp][owner], (uint32_t)nsc);
+        if (ooff != kNoRows) {
+#pragma unroll
+          for (int j = 0; j < SGS_SUPER; ++j) {
+            const int ty = sr * SGS_SUPER + j;
+            if (ty >= oty0 && ty <= oty1)
+              row_spans[ooff + (uint32_t)(ty - oty0)] =
+                  (uint16_t)(rc[j] > 0 ? (((rf[j] - otx0) & 0xff) | (rc[j] << 8)) : 0);
+          }
+        }
       }
     }
     __syncwarp();
@@ -103,6 +128,7 @@ __global__ void __launch_bounds__(256, 3) preprocess_kernel(sgs_params P, SgsCam
     if (live) {
       tiles_touched[i] = cnt;
       super_touched[i] = nsup;
+      if (row_off) row_off[i] = cnt ? my_off : kNoRows;
       const uint32_t dk = emitting ? sgs_float_to_bits(pr.depth) : 0x7fffffffu;
       depth_key[i] = dk;
       if (depth_hist) {
@@ -246,7 +272,10 @@ int launch_preprocess(const sgs_params& P, const SgsCam& cam, const sgs_workspac
                                               at<uint2>(ws, lo.rect), at<uint32_t>(ws, lo.tiles_touched),        \
                                               at<uint32_t>(ws, lo.super_touched),                                 \
                                               lo.sort_mode == SGS_SORT_DEPTH_FIRST                                 \
-                                                  ? at<uint32_t>(ws, lo.hist) + kDepthHistOff : nullptr, ctr)
+                                                  ? at<uint32_t>(ws, lo.hist) + kDepthHistOff : nullptr,   \
+                                              lo.row_cap ? at<uint32_t>(ws, lo.row_off) : nullptr,                 \
+                                              lo.row_cap ? at<uint16_t>(ws, lo.row_spans) : nullptr,               \
+                                              (uint32_t)lo.row_cap, ctr)
   if (P.n_lobes == 3)
     SGS_PRE(3);
   else
