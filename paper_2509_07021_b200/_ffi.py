@@ -129,7 +129,8 @@ def load(path: Path | None = None) -> C.CDLL:
     global _lib
     if _lib is not None and path is None:
         return _lib
-    p = Path(path) if path is not None else LIB_PATH
+    import os
+    p = Path(path) if path is not None else Path(os.environ.get("SGS_LIB", LIB_PATH))
     if not p.exists():
         from ._build import build_lib
         build_lib()

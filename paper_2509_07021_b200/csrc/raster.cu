@@ -220,9 +220,15 @@ __device__ __forceinline__ uint32_t tile_local_bit(int tx, int ty) {
 constexpr int kFwdThreads = 128;
 constexpr int kFwdCPT = 2;
 constexpr int kFwdChunk = kFwdThreads * kFwdCPT;  // candidates examined per staging step
-constexpr int kFwdBatch = 256;                    // staged entries processed per block sync
+#ifndef SGS_FWD_BATCH
+#define SGS_FWD_BATCH 128
+#endif
+#ifndef SGS_VOTE_EVERY
+#define SGS_VOTE_EVERY 8
+#endif
+constexpr int kFwdBatch = SGS_FWD_BATCH;          // staged entries processed per block sync
 constexpr int kFwdBuf = kFwdBatch + kFwdChunk;
-constexpr int kVoteEvery = 8;
+constexpr int kVoteEvery = SGS_VOTE_EVERY;
 
 // Warp vote without the compiler's divergence guard (callers are converged).
 __device__ __forceinline__ bool warp_any(bool p) {

@@ -201,6 +201,7 @@ typedef struct SgsProj {
   // t1 = u . d, t2 = u x d (u = unit major axis of cov2d)
   float ux, uy, ilmax, ilmin;
   float o_eff;
+  float ln_o;        // ln(o_eff) (sgs_logf), valid when emits
   float qmax;
   int32_t tx0, ty0, tx1, ty1;
   int32_t visible;   // z > near (render.py:263)
@@ -329,7 +330,8 @@ SGS_HD void sgs_project(const float pos[3], const float quat[4], const float ls[
     o->qmax = 0.0f;
     return;
   }
-  float qmax = F_MUL(2.0f, F_SUB(sgs_logf(oe), SGS_LN_EPS));
+  o->ln_o = sgs_logf(oe);
+  float qmax = F_MUL(2.0f, F_SUB(o->ln_o, SGS_LN_EPS));
   o->qmax = qmax;
   // exact bounding box of {d : d^T cov^-1 d <= qmax} is sqrt(qmax * cov_ii)
   float rx = F_SQRT(F_MUL(qmax, o->cov00));
@@ -636,7 +638,7 @@ SGS_HD void sgs_pack_geo(const SgsProj* p, float geo[4], float con[4]) {
   const float k = -0.5f * SGS_LOG2E;
   geo[0] = p->mx;
   geo[1] = p->my;
-  geo[2] = F_MUL(sgs_logf(p->o_eff), SGS_LOG2E);
+  geo[2] = F_MUL(p->ln_o, SGS_LOG2E);
   geo[3] = F_MUL(k, p->qmax);
   con[0] = F_MUL(k, p->con00);
   con[1] = F_MUL(2.0f * k, p->con01);
