@@ -202,6 +202,70 @@ __device__ __forceinline__ int stage_append(uint32_t c_lo, uint32_t c_hi, uint32
   return total;
 }
 
+// A chunk of candidates [lo, hi) whose list keys and primitive indices are
+// held in registers: the forward raster loads the next chunk before blending
+// the current batch, so the list loads overlap the blend instead of stalling
+// the next staging step.
+template <int CPT>
+struct ChunkRegs {
+  uint32_t key[CPT], val[CPT];
+  uint32_t lo, hi;
+};
+
+template <int THREADS, int CPT, bool kFilter>
+__device__ __forceinline__ void load_chunk(ChunkRegs<CPT>& r, uint32_t lo, uint32_t hi, const ListArgs& a) {
+  r.lo = lo;
+  r.hi = hi;
+#pragma unroll
+  for (int h = 0; h < CPT; ++h) {
+    const uint32_t c = lo + threadIdx.x + h * THREADS;
+    r.key[h] = (kFilter && c < hi) ? a.keys[c] : 0u;
+    r.val[h] = c < hi ? a.vals[c] : 0u;
+  }
+}
+
+// stage_append on a register chunk (same result).
+template <int THREADS, int CPT, bool kFilter, class S>
+__device__ __forceinline__ int stage_append_regs(const ChunkRegs<CPT>& r, uint32_t local_bit, const ListArgs& a,
+                                                 int base, S& s) {
+  constexpr int W = THREADS / 32;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const uint32_t lt = (1u << lane) - 1u;
+  uint32_t bal[CPT];
+#pragma unroll
+  for (int h = 0; h < CPT; ++h) {
+    const uint32_t c = r.lo + t + h * THREADS;
+    bool hit = c < r.hi;
+    if (kFilter) hit = hit && ((r.key[h] >> local_bit) & 1u);
+    bal[h] = __ballot_sync(0xffffffffu, hit);
+    if (lane == 0) s.wcnt[h * W + warp] = __popc(bal[h]);
+  }
+  __syncthreads();
+  int total = 0;
+#pragma unroll
+  for (int h = 0; h < CPT; ++h) {
+    int pre = 0;
+    for (int j = 0; j < CPT * W; ++j) {
+      const int v = (int)s.wcnt[j];
+      pre += (j < h * W + warp) ? v : 0;
+      if (h == 0) total += v;
+    }
+    if ((bal[h] >> lane) & 1u) {
+      const int pos = base + pre + __popc(bal[h] & lt);
+      const uint32_t g = r.val[h];
+      s.geo[pos] = a.geo[g];
+      s.con[pos] = a.eig[g];
+      s.col[pos] = a.col[g];
+      if constexpr (S::kIds) {
+        s.id[pos] = g;
+        s.cand[pos] = r.lo + t + h * THREADS;
+      }
+    }
+  }
+  __syncthreads();
+  return total;
+}
+
 __device__ __forceinline__ uint32_t tile_local_bit(int tx, int ty) {
   return (uint32_t)((ty % SGS_SUPER) * SGS_SUPER + (tx % SGS_SUPER));
 }
@@ -308,15 +372,24 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(ListArgs la, Sg
 
   const uint32_t lbit = tile_local_bit(tx, ty);
   uint32_t cb = cs;
+  ChunkRegs<kFwdCPT> pf;
+  bool have_pf = false;
   for (;;) {
     // stage until a full batch of this tile's entries (or the list ends)
     int nb = 0;
     while (nb < kFwdBatch && cb < ce) {
       const uint32_t chi = cb + kFwdChunk < ce ? cb + kFwdChunk : ce;
-      nb += stage_append<kFwdThreads, kFwdCPT, kFilter, true>(cb, chi, lbit, la, nb, s);
+      if (!have_pf) load_chunk<kFwdThreads, kFwdCPT, kFilter>(pf, cb, chi, la);
+      have_pf = false;
+      nb += stage_append_regs<kFwdThreads, kFwdCPT, kFilter>(pf, lbit, la, nb, s);
       cb = chi;
     }
     if (nb == 0) break;
+    // the next chunk's keys / indices load while this batch blends
+    if (cb < ce) {
+      load_chunk<kFwdThreads, kFwdCPT, kFilter>(pf, cb, cb + kFwdChunk < ce ? cb + kFwdChunk : ce, la);
+      have_pf = true;
+    }
     // pad the batch to a whole number of vote groups with records of zero
     // opacity (log2 o = -inf), so the group loop below needs no bounds checks
     const int nb_pad = (nb + kVoteEvery - 1) / kVoteEvery * kVoteEvery;
