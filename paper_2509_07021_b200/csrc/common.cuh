@@ -249,10 +249,9 @@ __device__ __forceinline__ SgsSpan shfl_span(const SgsSpan& s, int src) {
   SgsSpan o;
   o.mx = __shfl_sync(0xffffffffu, s.mx, src);
   o.my = __shfl_sync(0xffffffffu, s.my, src);
-  o.A = __shfl_sync(0xffffffffu, s.A, src);
-  o.B = __shfl_sync(0xffffffffu, s.B, src);
-  o.C = __shfl_sync(0xffffffffu, s.C, src);
-  o.pmin = __shfl_sync(0xffffffffu, s.pmin, src);
+  o.kb = __shfl_sync(0xffffffffu, s.kb, src);
+  o.D = __shfl_sync(0xffffffffu, s.D, src);
+  o.Q = __shfl_sync(0xffffffffu, s.Q, src);
   o.kx = __shfl_sync(0xffffffffu, s.kx, src);
   o.xm = __shfl_sync(0xffffffffu, s.xm, src);
   o.ym = __shfl_sync(0xffffffffu, s.ym, src);

@@ -360,33 +360,40 @@ SGS_HD void sgs_project(const float pos[3], const float quat[4], const float ls[
 // with (dx, dy) = pixel center - mean.  Its x-extreme points lie on the line
 // dy = kx dx, its y-extremes on dx = ky dy; xm / ym are the half extents.
 typedef struct SgsSpan {
-  float mx, my, A, B, C, pmin;
+  float mx, my;
   float kx, xm, ym, i2a;  // i2a = 1 / (2 A)
+  // crossing of the boundary with the line dy:  A x^2 + B dy x + (C dy^2 - pmin) = 0
+  //   x = kb dy -/+ sqrt(Q - D dy^2) i2a,  kb = -B i2a,  D = 4AC - B^2,  Q = 4A pmin
+  float kb, D, Q;
   int valid;
 } SgsSpan;
 
-SGS_HD SgsSpan sgs_span(const float geo[4], const float con[4]) {
+SGS_HD SgsSpan sgs_span_from(float mx, float my, float A, float B, float C, float pmin) {
   SgsSpan s;
-  s.mx = geo[0];
-  s.my = geo[1];
-  s.pmin = geo[3];
-  s.A = con[0];
-  s.B = con[1];
-  s.C = con[2];
+  s.mx = mx;
+  s.my = my;
   // D = 4AC - B^2 > 0 for a negative-definite form
-  float D = F_SUB(F_MUL(F_MUL(4.0f, s.A), s.C), F_MUL(s.B, s.B));
-  s.valid = D > 0.0f && s.A < 0.0f && s.C < 0.0f && s.pmin < 0.0f;
-  s.kx = -F_DIV(s.B, F_MUL(2.0f, s.C));
+  const float D = F_SUB(F_MUL(F_MUL(4.0f, A), C), F_MUL(B, B));
+  s.valid = D > 0.0f && A < 0.0f && C < 0.0f && pmin < 0.0f;
+  s.kx = -F_DIV(B, F_MUL(2.0f, C));
   const float iD = F_DIV(1.0f, D);
-  s.xm = s.valid ? F_SQRT(F_MUL(F_MUL(F_MUL(4.0f, s.C), s.pmin), iD)) : 0.0f;
-  s.ym = s.valid ? F_SQRT(F_MUL(F_MUL(F_MUL(4.0f, s.A), s.pmin), iD)) : 0.0f;
-  s.i2a = F_DIV(1.0f, F_MUL(2.0f, s.A));
+  s.xm = s.valid ? F_SQRT(F_MUL(F_MUL(F_MUL(4.0f, C), pmin), iD)) : 0.0f;
+  s.ym = s.valid ? F_SQRT(F_MUL(F_MUL(F_MUL(4.0f, A), pmin), iD)) : 0.0f;
+  s.i2a = F_DIV(1.0f, F_MUL(2.0f, A));
+  s.kb = F_MUL(-B, s.i2a);
+  s.D = D;
+  s.Q = F_MUL(F_MUL(4.0f, A), pmin);
   return s;
 }
 
+SGS_HD SgsSpan sgs_span(const float geo[4], const float con[4]) {
+  return sgs_span_from(geo[0], geo[1], con[0], con[1], con[2], geo[3]);
+}
+
 // The span parameters are cached per primitive by the preprocess: kx in the
-// conic record's 4th slot, (xm, ym) in a float2 (xm < 0 marks an invalid
-// form).  Rebuilding SgsSpan from the cache is bit-identical to sgs_span.
+// conic record's 4th slot, (xm, ym, i2a) in rec_span (xm < 0 marks an invalid
+// form); kb, D, Q are recomputed from the conic with the same operations.
+// Rebuilding SgsSpan from the cache is bit-identical to sgs_span.
 SGS_HD void sgs_span_cache(const SgsSpan* s, float* kx, float span2[3]) {
   *kx = s->kx;
   span2[0] = s->valid ? s->xm : -1.0f;
@@ -398,15 +405,14 @@ SGS_HD SgsSpan sgs_span_cached(const float geo[4], const float con[4], const flo
   SgsSpan s;
   s.mx = geo[0];
   s.my = geo[1];
-  s.pmin = geo[3];
-  s.A = con[0];
-  s.B = con[1];
-  s.C = con[2];
   s.kx = con[3];
   s.valid = span2[0] >= 0.0f;
   s.xm = s.valid ? span2[0] : 0.0f;
   s.ym = span2[1];
   s.i2a = span2[2];
+  s.kb = F_MUL(-con[1], s.i2a);
+  s.D = F_SUB(F_MUL(F_MUL(4.0f, con[0]), con[2]), F_MUL(con[1], con[1]));
+  s.Q = F_MUL(F_MUL(4.0f, con[0]), geo[3]);
   return s;
 }
 
@@ -414,12 +420,10 @@ SGS_HD SgsSpan sgs_span_cached(const float geo[4], const float con[4], const flo
 // when `right`, else the smaller); the caller guarantees |dy| <= ym up to
 // rounding, and a slightly negative discriminant is clamped to 0.
 SGS_HD float sgs_span_root(const SgsSpan* s, float dy, int right) {
-  float b = F_MUL(s->B, dy);
-  float c = F_SUB(F_MUL(F_MUL(s->C, dy), dy), s->pmin);
-  float disc = F_SUB(F_MUL(b, b), F_MUL(F_MUL(4.0f, s->A), c));
-  float r = F_SQRT(fmaxf(disc, 0.0f));
-  // 2A < 0: (-b - r) / (2A) is the larger root
-  return right ? F_MUL(F_SUB(-b, r), s->i2a) : F_MUL(F_ADD(-b, r), s->i2a);
+  const float disc = F_FMA(-s->D, F_MUL(dy, dy), s->Q);
+  const float ri = F_MUL(F_SQRT(fmaxf(disc, 0.0f)), s->i2a);
+  // i2a < 0: kb dy - r i2a is the larger root
+  return F_FMA(s->kb, dy, right ? -ri : ri);
 }
 
 // Tiles of tile-row `ty` (clipped to [tx0, tx1]) whose pixel-center box meets
