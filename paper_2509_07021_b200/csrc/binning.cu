@@ -359,7 +359,7 @@ int launch_bin(const SgsCam& cam, const sgs_workspace* ws, const Layout& lo, cud
     bool alt = false;
     // depth keys are 31-bit (0x7fffffff = not emitting): 4 passes over N
     // the preprocess accumulated the four depth-digit histograms
-    int rc = radix_sort_pairs<uint32_t, kDepthSortIPT, 8>(ka, ia, kb, ib, &ctr->n_depth, n, 31,
+    int rc = radix_sort_pairs<uint32_t, kDepthSortIPT, 8, kDepthSortThreads>(ka, ia, kb, ib, &ctr->n_depth, n, 31,
                                                         at<uint32_t>(ws, lo.hist) + kDepthHistOff,
                                                         at<uint32_t>(ws, lo.status), &ctr->part_counter[0], &alt, st,
                                                         true, RsRangeOut{nullptr, 0}, 0, false, true);

@@ -14,7 +14,11 @@ namespace sgs {
 constexpr int kNumSMs = 148;
 constexpr int kRadixThreads = 512;  // = kRsThreads in sort.cuh
 constexpr int kTileSortIPT = 16;  // items per thread, tile-key onesweep passes (8192 per CTA)
-constexpr int kDepthSortIPT = 16;  // 1M depth keys = 123 tiles: one wave of one CTA per SM
+constexpr int kDepthSortIPT = 16;
+#ifndef SGS_DEPTH_SORT_THREADS
+#define SGS_DEPTH_SORT_THREADS 512
+#endif
+constexpr int kDepthSortThreads = SGS_DEPTH_SORT_THREADS;  // 256 (co-resident with rasters) measured no faster  // 1M depth keys = 123 tiles: one wave of one CTA per SM
 constexpr int kKey64SortIPT = 6;
 constexpr int kRowSpansPerPrim = 8;   // row-span store capacity, u16 entries per primitive
 constexpr uint32_t kNoRows = 0xffffffffu;  // row_off of a primitive whose spans are not stored
@@ -157,7 +161,8 @@ inline int make_layout(const sgs_workspace* ws, Layout* lo) {
   int tile_passes = k64 ? (32 + tile_sort_bits(lo->n_tiles) + 7) / 8 : super_sort_passes(lo->n_super);
   int ipt = k64 ? kKey64SortIPT : kTileSortIPT;
   uint64_t parts_tile = (cap + (uint64_t)kRadixThreads * ipt - 1) / ((uint64_t)kRadixThreads * ipt);
-  uint64_t parts_depth = (n + (uint64_t)kRadixThreads * kDepthSortIPT - 1) / ((uint64_t)kRadixThreads * kDepthSortIPT);
+  uint64_t parts_depth =
+      (n + (uint64_t)kDepthSortThreads * kDepthSortIPT - 1) / ((uint64_t)kDepthSortThreads * kDepthSortIPT);
   uint64_t st_tile = parts_tile * 512 * 4 * (uint64_t)tile_passes;
   uint64_t st_depth = k64 ? 0 : parts_depth * 256 * 4 * 4;
   lo->status_bytes = st_tile > st_depth ? st_tile : st_depth;

@@ -29,8 +29,8 @@ namespace sgs {
 // status word: [31:30] flag (0 empty, 1 aggregate, 2 inclusive prefix), [29:0] count
 enum : uint32_t { kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kCountMask = (1u << 30) - 1 };
 
-constexpr int kRsThreads = 512;  // 16 warps per CTA
-constexpr int kRsWarps = kRsThreads / 32;
+constexpr int kRsThreads = 512;  // default CTA size: 16 warps
+
 constexpr int kRsMaxRadix = 512;
 constexpr int kLookback = 32;    // predecessors examined per look-back step
 
@@ -116,14 +116,15 @@ __global__ void __launch_bounds__(1 << RBITS) rs_scan_hist(uint32_t* hist) {
   h[t] = pre + x - v;
 }
 
-template <typename K, int IPT, int RBITS>
+template <typename K, int IPT, int RBITS, int NT = kRsThreads>
 struct RsSmem {
-  static constexpr int kTile = kRsThreads * IPT;
+  static constexpr int kTile = NT * IPT;
   static constexpr int R = 1 << RBITS;
-  uint32_t warp_hist[kRsWarps][R];
+  static constexpr int kWarps = NT / 32;
+  uint32_t warp_hist[kWarps][R];
   uint32_t digit_start[R];
   uint32_t global_base[R];
-  uint32_t warp_tot[kRsWarps];
+  uint32_t warp_tot[kWarps];
   uint32_t part;
   uint32_t vals[kTile];
   K keys[kTile];
@@ -137,13 +138,15 @@ struct RsRangeOut {
 // One pass.  status: nparts x 2^RBITS u32, zeroed; ticket zeroed.
 // vin == nullptr means values are the item indices (first pass of an argsort).
 // kout == nullptr skips the key writes.
-template <typename K, int IPT, int RBITS>
-__global__ void __launch_bounds__(kRsThreads) rs_onesweep(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
+template <typename K, int IPT, int RBITS, int NT = kRsThreads>
+__global__ void __launch_bounds__(NT) rs_onesweep(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                           K* __restrict__ kout, uint32_t* __restrict__ vout,
                                                           const uint32_t* n_ptr, uint32_t n_cap, int shift,
                                                           const uint32_t* __restrict__ pass_base, uint32_t* status,
                                                           uint32_t* ticket, RsRangeOut rout) {
-  using S = RsSmem<K, IPT, RBITS>;
+  static_assert((1 << RBITS) <= NT, "one thread per digit");
+  using S = RsSmem<K, IPT, RBITS, NT>;
+  constexpr int kRsWarps = S::kWarps;
   constexpr int kTile = S::kTile;
   constexpr int R = S::R;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -155,7 +158,7 @@ __global__ void __launch_bounds__(kRsThreads) rs_onesweep(const K* __restrict__ 
 
   for (;;) {
     if (t == 0) s.part = atomicAdd(ticket, 1u);
-    for (int j = t; j < kRsWarps * R; j += kRsThreads) (&s.warp_hist[0][0])[j] = 0;
+    for (int j = t; j < kRsWarps * R; j += NT) (&s.warp_hist[0][0])[j] = 0;
     __syncthreads();
     const uint32_t part = s.part;
     if (part >= nparts) return;
@@ -260,7 +263,7 @@ __global__ void __launch_bounds__(kRsThreads) rs_onesweep(const K* __restrict__ 
     }
     __syncthreads();
     const uint32_t cnt = min((uint32_t)kTile, n - part * kTile);
-    for (uint32_t j = t; j < cnt; j += kRsThreads) {
+    for (uint32_t j = t; j < cnt; j += NT) {
       const K k = s.keys[j];
       const uint32_t d = rs_digit<K, RBITS>(k, shift);
       const uint32_t g = s.global_base[d] + j - s.digit_start[d];
@@ -280,9 +283,9 @@ __global__ void __launch_bounds__(kRsThreads) rs_onesweep(const K* __restrict__ 
 int resident_ctas_per_sm(const void* kernel, int threads, size_t smem);
 int device_sm_count();
 
-template <typename K, int IPT>
+template <typename K, int IPT, int NT = kRsThreads>
 inline uint64_t rs_parts(uint64_t n) {
-  return (n + kRsThreads * IPT - 1) / (kRsThreads * IPT);
+  return (n + NT * IPT - 1) / (NT * IPT);
 }
 
 // Sort `n_cap`-bounded pairs (count in *n_ptr on the device) over key bits
@@ -293,14 +296,14 @@ inline uint64_t rs_parts(uint64_t n) {
 // the last pass also writes the cell ranges (and skips its key writes unless
 // keep_last_keys).  hist: 16*512 u32; status: parts*512*passes u32; tickets:
 // >= passes u32; all zeroed here (hist only when !hist_ready).
-template <typename K, int IPT, int RBITS>
+template <typename K, int IPT, int RBITS, int NT = kRsThreads>
 int radix_sort_pairs(K* k0, uint32_t* v0, K* k1, uint32_t* v1, const uint32_t* n_ptr, uint32_t n_cap, int bits,
                      uint32_t* hist, uint32_t* status, uint32_t* tickets, bool* result_in_alt, cudaStream_t st,
                      bool iota_values = false, RsRangeOut rout = RsRangeOut{nullptr, 0}, int begin_bit = 0,
                      bool keep_last_keys = false, bool hist_ready = false) {
   constexpr int R = 1 << RBITS;
   const int passes = (bits + RBITS - 1) / RBITS;
-  const uint64_t parts = rs_parts<K, IPT>(n_cap);
+  const uint64_t parts = rs_parts<K, IPT, NT>(n_cap);
   *result_in_alt = false;
   if (n_cap == 0 || passes == 0) return SGS_OK;
   // hist_ready: the producer kernel already accumulated every pass's digit
@@ -324,15 +327,15 @@ int radix_sort_pairs(K* k0, uint32_t* v0, K* k1, uint32_t* v1, const uint32_t* n
   }
   rs_scan_hist<RBITS><<<passes, R, 0, st>>>(hist);
   SGS_LAUNCH_CHECK("rs_scan_hist");
-  const size_t smem = sizeof(RsSmem<K, IPT, RBITS>);
+  const size_t smem = sizeof(RsSmem<K, IPT, RBITS, NT>);
   static bool attr_set = false;
   if (!attr_set) {
-    SGS_CUDA(cudaFuncSetAttribute(rs_onesweep<K, IPT, RBITS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    SGS_CUDA(cudaFuncSetAttribute(rs_onesweep<K, IPT, RBITS, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem));
     attr_set = true;
   }
   static int per_sm = 0;
-  if (!per_sm) per_sm = resident_ctas_per_sm((const void*)rs_onesweep<K, IPT, RBITS>, kRsThreads, smem);
+  if (!per_sm) per_sm = resident_ctas_per_sm((const void*)rs_onesweep<K, IPT, RBITS, NT>, NT, smem);
   if (per_sm < 1) {
     set_error("onesweep kernel cannot be resident");
     return SGS_E_CUDA;
@@ -344,7 +347,7 @@ int radix_sort_pairs(K* k0, uint32_t* v0, K* k1, uint32_t* v1, const uint32_t* n
   uint32_t* vb = v1;
   for (int p = 0; p < passes; ++p) {
     const bool last = p + 1 == passes;
-    rs_onesweep<K, IPT, RBITS><<<grid, kRsThreads, smem, st>>>(
+    rs_onesweep<K, IPT, RBITS, NT><<<grid, NT, smem, st>>>(
         ka, (p == 0 && iota_values) ? nullptr : va, (last && rout.ranges && !keep_last_keys) ? nullptr : kb, vb,
         n_ptr, n_cap, begin_bit + RBITS * p, hist + R * p, status + (size_t)parts * R * p, tickets + p,
         last ? rout : RsRangeOut{nullptr, 0});
