@@ -18,7 +18,9 @@ constexpr int kDepthSortIPT = 16;
 #ifndef SGS_DEPTH_SORT_THREADS
 #define SGS_DEPTH_SORT_THREADS 512
 #endif
-constexpr int kDepthSortThreads = SGS_DEPTH_SORT_THREADS;  // 256 (co-resident with rasters) measured no faster  // 1M depth keys = 123 tiles: one wave of one CTA per SM
+// 1M depth keys = 123 tiles of 8192: one wave of one CTA per SM (256-thread CTAs,
+// which leave room for co-resident rasters, measured no faster)
+constexpr int kDepthSortThreads = SGS_DEPTH_SORT_THREADS;
 constexpr int kKey64SortIPT = 6;
 constexpr int kRowSpansPerPrim = 8;   // row-span store capacity, u16 entries per primitive
 constexpr uint32_t kNoRows = 0xffffffffu;  // row_off of a primitive whose spans are not stored

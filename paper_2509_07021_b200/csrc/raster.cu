@@ -10,7 +10,7 @@
 //
 // One CTA per 16x16 tile.  The tile's primitive list is read from its cell's
 // sorted list -- the super-tile list in depth-first mode, filtered to this
-// tile with the exact per-tile membership test (sgs_tile_member), or the
+// tile by the tile's bit of the exact 16-bit membership mask each entry carries, or the
 // tile's own list in 64-bit-key mode -- in batches that are compacted
 // (stable) into shared memory.  The per-tile list index of a staged entry is
 // its rank among the tile's hits, identical in both modes.

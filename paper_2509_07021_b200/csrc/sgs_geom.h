@@ -486,24 +486,6 @@ SGS_HD uint32_t sgs_count_tiles(int tx0, int ty0, int tx1, int ty1, const float 
 // tile hit can be lost to rounding.
 #define SGS_SUPER 4
 
-SGS_HD int sgs_super_row(const SgsSpan* s, const SgsCam* cam, int tx0, int ty0, int tx1, int ty1, int sr,
-                         int* first_sc) {
-  int lo = 0x7fffffff, hi = -1, first;
-  int r0 = sr * SGS_SUPER, r1 = r0 + SGS_SUPER - 1;
-  if (r0 < ty0) r0 = ty0;
-  if (r1 > ty1) r1 = ty1;
-  for (int ty = r0; ty <= r1; ++ty) {
-    const int c = sgs_row_span(s, cam, ty, tx0, tx1, &first);
-    if (c > 0) {
-      const int a = first / SGS_SUPER, b = (first + c - 1) / SGS_SUPER;
-      lo = a < lo ? a : lo;
-      hi = b > hi ? b : hi;
-    }
-  }
-  *first_sc = hi >= lo ? lo : 0;
-  return hi >= lo ? hi - lo + 1 : 0;
-}
-
 // Super row `sr` with its tile rows' spans (first[r], cnt[r]), r = ty - 4 sr
 // (cnt = 0 outside the rectangle), for the per-entry tile masks.
 SGS_HD int sgs_super_row_spans(const SgsSpan* s, const SgsCam* cam, int tx0, int ty0, int tx1, int ty1, int sr,
@@ -538,50 +520,6 @@ SGS_HD uint32_t sgs_super_mask(const int first[SGS_SUPER], const int cnt[SGS_SUP
       if (tx >= first[r] && tx < first[r] + cnt[r]) m |= 1u << (r * SGS_SUPER + c);
     }
   return m;
-}
-
-// (tile entries, super-tile entries) of one primitive.
-SGS_HD void sgs_count_hits_span(const SgsSpan* sp, int tx0, int ty0, int tx1, int ty1, const SgsCam* cam,
-                                uint32_t* n_tiles, uint32_t* n_super) {
-  const SgsSpan s = *sp;
-  uint32_t nt = 0, ns = 0;
-  int cur = -1, lo = 0x7fffffff, hi = -1, first;
-  for (int ty = ty0; ty <= ty1; ++ty) {
-    const int sr = ty / SGS_SUPER;
-    if (sr != cur) {
-      if (hi >= lo) ns += (uint32_t)(hi - lo + 1);
-      cur = sr;
-      lo = 0x7fffffff;
-      hi = -1;
-    }
-    const int c = sgs_row_span(&s, cam, ty, tx0, tx1, &first);
-    nt += (uint32_t)c;
-    if (c > 0) {
-      const int a = first / SGS_SUPER, b = (first + c - 1) / SGS_SUPER;
-      lo = a < lo ? a : lo;
-      hi = b > hi ? b : hi;
-    }
-  }
-  if (hi >= lo) ns += (uint32_t)(hi - lo + 1);
-  *n_tiles = nt;
-  *n_super = ns;
-}
-
-SGS_HD void sgs_count_hits(int tx0, int ty0, int tx1, int ty1, const float geo[4], const float con[4],
-                           const SgsCam* cam, uint32_t* n_tiles, uint32_t* n_super) {
-  const SgsSpan s = sgs_span(geo, con);
-  sgs_count_hits_span(&s, tx0, ty0, tx1, ty1, cam, n_tiles, n_super);
-}
-
-// Exact membership of a primitive in tile (tx, ty)'s list (the same test
-// the counts and the CPU restatement use).
-SGS_HD int sgs_tile_member(const float geo[4], const float con[4], const float span2[3], int tx0, int ty0,
-                           int tx1, int ty1, const SgsCam* cam, int tx, int ty) {
-  if (ty < ty0 || ty > ty1 || tx < tx0 || tx > tx1) return 0;
-  SgsSpan s = sgs_span_cached(geo, con, span2);
-  int first;
-  const int c = sgs_row_span(&s, cam, ty, tx0, tx1, &first);
-  return tx >= first && tx < first + c;
 }
 
 // SG color for the camera-to-center view direction (render.py:294-305):
