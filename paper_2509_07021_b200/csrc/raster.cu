@@ -486,7 +486,7 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(ListArgs la, Sg
 
 constexpr int kGrad = 9;
 constexpr int kBwdThreads = 128;
-constexpr int kBwdCPT = 2;
+constexpr int kBwdCPT = 1;
 constexpr int kBwdChunk = kBwdThreads * kBwdCPT;  // candidates staged per batch
 
 // Sum of nine per-lane values over the warp by recursive halving: each
@@ -532,9 +532,9 @@ __device__ __forceinline__ int reduce9_index(int lane) {
 // thread (a warp covers 16x4 pixels, as in the forward), walking the tile's
 // list back to front from the last entry any pixel kept.  Per record each
 // thread sums its two pixels' nine partials, the warp reduces them with
-// warp_reduce9, and nine lanes add the totals into the batch's shared
-// accumulators (4 warps per record); each batch is flushed with one global
-// atomic per (record, partial).  T is recovered with one hardware reciprocal
+// warp_reduce9, and nine lanes store the totals into the warp's slot of the
+// batch's shared partials; each batch is flushed by summing the 4 warps'
+// partials with one global atomic per (record, partial).  T is recovered with one hardware reciprocal
 // per pixel-record, T_i = T_{i+1} rcp(1 - alpha_i) (~1 ulp per record).
 template <bool kFilter>
 __global__ void __launch_bounds__(kBwdThreads) raster_bwd_kernel(ListArgs la, SgsCam cam, float3 bg,
@@ -543,7 +543,9 @@ __global__ void __launch_bounds__(kBwdThreads) raster_bwd_kernel(ListArgs la, Sg
                                                                  const float* __restrict__ dimg,
                                                                  float* __restrict__ grad2d) {
   __shared__ Stage<kBwdChunk> s;
-  __shared__ float s_acc[kBwdChunk][kGrad + 1];
+  // per-warp partial totals (plain stores; shared-memory float atomics are CAS
+  // loops on sm_100), summed over the 4 warps when the batch is flushed
+  __shared__ float s_part[kBwdThreads / 32][kBwdChunk][kGrad];
   __shared__ uint32_t s_max_nc;
 
   const int tile = blockIdx.x + cam.tile_y0 * cam.tiles_x;
@@ -594,12 +596,15 @@ __global__ void __launch_bounds__(kBwdThreads) raster_bwd_kernel(ListArgs la, Sg
   for (uint32_t hi = cend; hi > cs;) {
     const uint32_t lo = hi - cs > (uint32_t)kBwdChunk ? hi - kBwdChunk : cs;
     __syncthreads();  // previous batch fully flushed
-    for (int i = t; i < kBwdChunk * (kGrad + 1); i += kBwdThreads) (&s_acc[0][0])[i] = 0.0f;
     const int nb = stage_append<kBwdThreads, kBwdCPT, kFilter, true>(lo, hi, lbit, la, 0, s);
     const uint32_t base = max_nc - hits_after - (uint32_t)nb;  // per-tile list index of staged entry 0
     for (int k = nb - 1; k >= 0; --k) {
       const uint32_t idx = base + (uint32_t)k;
-      if (idx >= warp_nc) continue;  // warp-uniform: no pixel of this warp kept the record
+      const int wq_ = t >> 5;
+      if (idx >= warp_nc) {  // warp-uniform: no pixel of this warp kept the record
+        if (vidx < kGrad) s_part[wq_][k][vidx] = 0.0f;
+        continue;
+      }
       const float4 G = s.geo[k];  // (mx, my, log2 o_eff, -)
       const float4 E = s.con[k];  // scaled eigen form (s1 ux, s1 uy, s2 ux, s2 uy)
       const float4 col = s.col[k];
@@ -616,7 +621,10 @@ __global__ void __launch_bounds__(kBwdThreads) raster_bwd_kernel(ListArgs la, Sg
       // A record outside the support of every active pixel of the warp
       // (alpha < 1e-7 for all of them) contributes < 1e-7 of any partial and
       // changes T by a factor within 1e-7 of 1: skip it whole.
-      if (!warp_any((idx < nc0 && pq[0] >= SGS_LOG2_EPS) || (idx < nc1 && pq[1] >= SGS_LOG2_EPS))) continue;
+      if (!warp_any((idx < nc0 && pq[0] >= SGS_LOG2_EPS) || (idx < nc1 && pq[1] >= SGS_LOG2_EPS))) {
+        if (vidx < kGrad) s_part[wq_][k][vidx] = 0.0f;
+        continue;
+      }
       float v[kGrad];
 #pragma unroll
       for (int c = 0; c < kGrad; ++c) v[c] = 0.0f;
@@ -654,12 +662,14 @@ __global__ void __launch_bounds__(kBwdThreads) raster_bwd_kernel(ListArgs la, Sg
         v[8] = fmaf(qy, dy, v[8]);
       }
       const float tot = warp_reduce9(v, lane);
-      if (vidx < kGrad) atomicAdd(&s_acc[k][vidx], tot);
+      if (vidx < kGrad) s_part[wq_][k][vidx] = tot;
     }
     __syncthreads();
     for (int i = t; i < nb * kGrad; i += kBwdThreads) {
       const int k = i / kGrad, c = i - k * kGrad;
-      const float x = s_acc[k][c];
+      float x = 0.0f;
+#pragma unroll
+      for (int w = 0; w < kBwdThreads / 32; ++w) x += s_part[w][k][c];
       if (x != 0.0f) atomicAdd(grad2d + (size_t)s.id[k] * kGrad + c, x);
     }
     hits_after += (uint32_t)nb;
