@@ -653,14 +653,16 @@ __global__ void __launch_bounds__(kBwdThreads) raster_bwd_kernel(ListArgs la, Sg
         v[0] = fmaf(ww, gx, v[0]);
         v[1] = fmaf(ww, gy, v[1]);
         v[2] = fmaf(ww, gz, v[2]);
+        // the thread's pixels share dx: accumulate sum dq, sum dq dy, sum dq dy^2
+        // and apply the dx factors once per record below
         v[3] += dq;
-        const float qx = dq * dx, qy = dq * dy;
-        v[4] += qx;
+        const float qy = dq * dy;
         v[5] += qy;
-        v[6] = fmaf(qx, dx, v[6]);
-        v[7] = fmaf(qx, dy, v[7]);
         v[8] = fmaf(qy, dy, v[8]);
       }
+      v[4] = v[3] * dx;  // sum dq dx
+      v[6] = v[4] * dx;  // sum dq dx^2
+      v[7] = v[5] * dx;  // sum dq dx dy
       const float tot = warp_reduce9(v, lane);
       if (vidx < kGrad) s_part[wq_][k][vidx] = tot;
     }
