@@ -337,6 +337,30 @@ __device__ __forceinline__ bool blend_px(float p, const float4& c, float& T, flo
   return keep;
 }
 
+// blend_px for the thread's two pixels at once with packed FP32x2 arithmetic
+// (FFMA2 / FMUL2 / FADD2 on sm_100: one instruction for both pixels, each
+// lane IEEE-rounded exactly as the scalar operation).  T2 = (T0, T1) and the
+// colour accumulators are packed per channel: Cr = (C0.r, C1.r), ...
+__device__ __forceinline__ float2 f2(float x) { return make_float2(x, x); }
+__device__ __forceinline__ float2 neg2(float2 v) { return make_float2(-v.x, -v.y); }
+
+template <bool kClamp>
+__device__ __forceinline__ void blend2(float2 p, const float4& c, float2& T2, float2& Cr, float2& Cg, float2& Cb,
+                                       bool& k0, bool& k1, float2& w) {
+  float2 alpha = make_float2(ex2_approx(p.x), ex2_approx(p.y));
+  if (kClamp) alpha = make_float2(fminf(alpha.x, SGS_ALPHA_MAX), fminf(alpha.y, SGS_ALPHA_MAX));
+  w = __fmul2_rn(alpha, T2);
+  const float2 Tn = __fadd2_rn(T2, neg2(w));  // T - w
+  k0 = Tn.x >= SGS_T_KEEP;
+  k1 = Tn.y >= SGS_T_KEEP;
+  const float2 we = make_float2(k0 ? w.x : 0.0f, k1 ? w.y : 0.0f);  // C + 0 c = C exactly
+  Cr = __ffma2_rn(we, f2(c.x), Cr);
+  Cg = __ffma2_rn(we, f2(c.y), Cg);
+  Cb = __ffma2_rn(we, f2(c.z), Cb);
+  T2 = make_float2(k0 ? Tn.x : -fabsf(T2.x), k1 ? Tn.y : -fabsf(T2.y));
+  w = we;
+}
+
 template <bool kImportance, bool kCount, bool kFilter, bool kTrack>
 __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(ListArgs la, SgsCam cam, float3 bg,
                                                                  float* __restrict__ out_img,
@@ -365,8 +389,9 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(ListArgs la, Sg
 
   // T > 0: live; T < 0: terminated with transmittance -T (pixels off the
   // image start terminated)
-  float T0 = in0 ? 1.0f : -1.0f, T1 = in1 ? 1.0f : -1.0f;
-  float C00 = 0.0f, C01 = 0.0f, C02 = 0.0f, C10 = 0.0f, C11 = 0.0f, C12 = 0.0f;
+  float2 T2 = make_float2(in0 ? 1.0f : -1.0f, in1 ? 1.0f : -1.0f);
+  float2 Cr = make_float2(0.0f, 0.0f), Cg = Cr, Cb = Cr;
+  const float2 fyv = make_float2(fy0, fy0 + 1.0f);  // the two pixels' row centres
   uint32_t nc0 = 0, nc1 = 0, reached = 0, kend = 0, hits_before = 0;
   if (kTrack && t == 0) s_kend = 0;
 
@@ -405,33 +430,31 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(ListArgs la, Sg
     auto run_batch = [&](auto clamp_tag) {
     constexpr bool kClamp = decltype(clamp_tag)::value;
     for (int k = 0; k < nb_pad; k += kVoteEvery) {
-      if (!warp_any(T0 > 0.0f || T1 > 0.0f)) break;
+      if (!warp_any(T2.x > 0.0f || T2.y > 0.0f)) break;
 #pragma unroll
       for (int j = 0; j < kVoteEvery; ++j) {
         const int kk = k + j;
         const float4 G = s.geo[kk];  // (mx, my, log2 o_eff, -)
         const float4 E = s.con[kk];  // scaled eigen form (s1 ux, s1 uy, s2 ux, s2 uy)
         const float dx = fx - G.x;
-        const float dy0 = fy0 - G.y, dy1 = dy0 + 1.0f;
+        const float2 dy = __fadd2_rn(fyv, f2(-G.y));
         const float e1dx = E.x * dx, e3dx = E.w * dx;
-        const float t10 = fmaf(E.y, dy0, e1dx), t20 = fmaf(E.z, dy0, -e3dx);
-        const float t11 = fmaf(E.y, dy1, e1dx), t21 = fmaf(E.z, dy1, -e3dx);
-        const float p0 = fmaf(-t10, t10, fmaf(-t20, t20, G.z));
-        const float p1 = fmaf(-t11, t11, fmaf(-t21, t21, G.z));
-        if (kCount && kk < nb) reached += (uint32_t)(T0 > 0.0f) + (uint32_t)(T1 > 0.0f);
+        const float2 t1 = __ffma2_rn(f2(E.y), dy, f2(e1dx));
+        const float2 t2 = __ffma2_rn(f2(E.z), dy, f2(-e3dx));
+        const float2 p = __ffma2_rn(neg2(t1), t1, __ffma2_rn(neg2(t2), t2, f2(G.z)));
+        if (kCount && kk < nb) reached += (uint32_t)(T2.x > 0.0f) + (uint32_t)(T2.y > 0.0f);
         {
           const float4 c = s.col[kk];
-          float w0, w1;
-          const bool k0 = blend_px<kClamp>(p0, c, T0, C00, C01, C02, w0);
-          const bool k1 = blend_px<kClamp>(p1, c, T1, C10, C11, C12, w1);
+          bool k0, k1;
+          float2 w;
+          blend2<kClamp>(p, c, T2, Cr, Cg, Cb, k0, k1, w);
           if (kTrack && kk < nb) {  // padding records are never counted
             const uint32_t idx = hits_before + (uint32_t)kk + 1u;
             if (k0) nc0 = idx;
             if (k1) nc1 = idx;
           }
           if constexpr (kImportance) {
-            w0 = k0 ? w0 : 0.0f;
-            w1 = k1 ? w1 : 0.0f;
+            const float w0 = w.x, w1 = w.y;
             if (warp_any(w0 != 0.0f || w1 != 0.0f)) {
               const float ws = warp_sum(w0 + w1);
               if (lane == 0 && ws != 0.0f) atomicAdd(&weight_sums[s.id[kk]], ws);
@@ -452,7 +475,7 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(ListArgs la, Sg
     }
     hits_before += (uint32_t)nb;
     if (cb >= ce) break;
-    if (__syncthreads_count(T0 > 0.0f || T1 > 0.0f) == 0) break;
+    if (__syncthreads_count(T2.x > 0.0f || T2.y > 0.0f) == 0) break;
   }
   if (kCount) {
     unsigned long long r = reached;
@@ -460,8 +483,8 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(ListArgs la, Sg
     if (lane == 0 && r) atomicAdd(pair_count, r);
   }
   if (kTrack && kend) atomicMax(&s_kend, kend);
-  T0 = fabsf(T0);
-  T1 = fabsf(T1);
+  const float T0 = fabsf(T2.x), T1 = fabsf(T2.y);
+  const float C00 = Cr.x, C01 = Cg.x, C02 = Cb.x, C10 = Cr.y, C11 = Cg.y, C12 = Cb.y;
   if (in0) {
     const size_t pix = (size_t)py0 * cam.width + px;
     out_img[3 * pix + 0] = C00 + T0 * bg.x;
