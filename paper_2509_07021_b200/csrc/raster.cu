@@ -607,6 +607,10 @@ __global__ void __launch_bounds__(kBwdThreads) raster_bwd_kernel(ListArgs la, Sg
     g12 = dimg[3 * pix + 2];
     S1 = T1 * (g10 * bg.x + g11 * bg.y + g12 * bg.z);
   }
+  float2 T2 = make_float2(T0, T1), S2 = make_float2(S0, S1);
+  const float2 gx2 = make_float2(g00, g10), gy2 = make_float2(g01, g11), gz2 = make_float2(g02, g12);
+  const float2 gxy0 = make_float2(g00, g01), gxy1 = make_float2(g10, g11);
+  const float2 fyv = make_float2(fy0, fy0 + 1.0f);
   const uint32_t ncm = nc0 > nc1 ? nc0 : nc1;
   if (ncm) atomicMax(&s_max_nc, ncm);
   __syncthreads();
@@ -631,58 +635,48 @@ __global__ void __launch_bounds__(kBwdThreads) raster_bwd_kernel(ListArgs la, Sg
       const float4 G = s.geo[k];  // (mx, my, log2 o_eff, -)
       const float4 E = s.con[k];  // scaled eigen form (s1 ux, s1 uy, s2 ux, s2 uy)
       const float4 col = s.col[k];
+      // the thread's two pixels packed per quantity (FFMA2/FMUL2/FADD2), as in the forward
       const float dx = fx - G.x;
-      const float dy0 = fy0 - G.y, dy1 = dy0 + 1.0f;
+      const float2 dy = __fadd2_rn(fyv, f2(-G.y));
       const float e1dx = E.x * dx, e3dx = E.w * dx;
-      float pq[2];
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const float dy = q ? dy1 : dy0;
-        const float t1 = fmaf(E.y, dy, e1dx), t2 = fmaf(E.z, dy, -e3dx);
-        pq[q] = fmaf(-t1, t1, fmaf(-t2, t2, G.z));
-      }
+      const float2 t1 = __ffma2_rn(f2(E.y), dy, f2(e1dx));
+      const float2 t2 = __ffma2_rn(f2(E.z), dy, f2(-e3dx));
+      const float2 p = __ffma2_rn(neg2(t1), t1, __ffma2_rn(neg2(t2), t2, f2(G.z)));
+      const bool act0 = idx < nc0, act1 = idx < nc1;
       // A record outside the support of every active pixel of the warp
       // (alpha < 1e-7 for all of them) contributes < 1e-7 of any partial and
       // changes T by a factor within 1e-7 of 1: skip it whole.
-      if (!warp_any((idx < nc0 && pq[0] >= SGS_LOG2_EPS) || (idx < nc1 && pq[1] >= SGS_LOG2_EPS))) {
+      if (!warp_any((act0 && p.x >= SGS_LOG2_EPS) || (act1 && p.y >= SGS_LOG2_EPS))) {
         if (vidx < kGrad) s_part[wq_][k][vidx] = 0.0f;
         continue;
       }
+      const float2 a = make_float2(ex2_approx(p.x), ex2_approx(p.y));
+      const float2 alpha = make_float2(fminf(a.x, SGS_ALPHA_MAX), fminf(a.y, SGS_ALPHA_MAX));
+      const float2 om = __fadd2_rn(f2(1.0f), neg2(alpha));  // the forward's T_next = T - alpha T
+      // om in [0.0099, 1]: MUFU.RCP, ~1 ulp
+      const float2 rom = make_float2(rcp_approx(om.x), rcp_approx(om.y));
+      const float2 Ti = __fmul2_rn(T2, rom);
+      const float2 w = __fmul2_rn(alpha, Ti);
+      const float2 cg = __ffma2_rn(f2(col.x), gx2, __ffma2_rn(f2(col.y), gy2, __fmul2_rn(f2(col.z), gz2)));
+      const float2 dal = __ffma2_rn(Ti, cg, neg2(__fmul2_rn(S2, rom)));
+      const float2 dq = __fmul2_rn(__fmul2_rn(f2(-0.5f), a), dal);
+      const float2 Sn = __ffma2_rn(w, cg, S2);
+      const bool l0 = act0 && a.x < SGS_ALPHA_MAX, l1 = act1 && a.y < SGS_ALPHA_MAX;
+      const float2 dqa = make_float2(l0 ? dq.x : 0.0f, l1 ? dq.y : 0.0f);
+      const float ww0 = act0 ? w.x : 0.0f, ww1 = act1 ? w.y : 0.0f;
+      S2 = make_float2(act0 ? Sn.x : S2.x, act1 ? Sn.y : S2.y);
+      T2 = make_float2(act0 ? Ti.x : T2.x, act1 ? Ti.y : T2.y);
       float v[kGrad];
-#pragma unroll
-      for (int c = 0; c < kGrad; ++c) v[c] = 0.0f;
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const float dy = q ? dy1 : dy0;
-        const bool act = idx < (q ? nc1 : nc0);
-        const float p = pq[q];
-        const float a = ex2_approx(p);
-        const float alpha = fminf(a, SGS_ALPHA_MAX);
-        const float om = 1.0f - alpha;  // the forward's T_next = T - alpha T
-        const float rom = rcp_approx(om);  // om in [0.0099, 1]: MUFU.RCP, ~1 ulp
-        float& T = q ? T1 : T0;
-        float& S = q ? S1 : S0;
-        const float gx = q ? g10 : g00, gy = q ? g11 : g01, gz = q ? g12 : g02;
-        const float Ti = T * rom;
-        const float w = alpha * Ti;
-        const float cg = fmaf(col.x, gx, fmaf(col.y, gy, col.z * gz));
-        const float dal = (a < SGS_ALPHA_MAX) ? fmaf(Ti, cg, -S * rom) : 0.0f;
-        const float dq = act ? -0.5f * a * dal : 0.0f;
-        const float ww = act ? w : 0.0f;
-        if (act) {
-          S = fmaf(w, cg, S);
-          T = Ti;
-        }
-        v[0] = fmaf(ww, gx, v[0]);
-        v[1] = fmaf(ww, gy, v[1]);
-        v[2] = fmaf(ww, gz, v[2]);
-        // the thread's pixels share dx: accumulate sum dq, sum dq dy, sum dq dy^2
-        // and apply the dx factors once per record below
-        v[3] += dq;
-        const float qy = dq * dy;
-        v[5] += qy;
-        v[8] = fmaf(qy, dy, v[8]);
-      }
+      const float2 vxy = __ffma2_rn(f2(ww1), gxy1, __fmul2_rn(f2(ww0), gxy0));
+      v[0] = vxy.x;
+      v[1] = vxy.y;
+      v[2] = fmaf(ww1, g12, ww0 * g02);
+      // the thread's pixels share dx: accumulate sum dq, sum dq dy, sum dq dy^2
+      // and apply the dx factors once per record
+      const float2 qy = __fmul2_rn(dqa, dy);
+      v[3] = dqa.x + dqa.y;
+      v[5] = qy.x + qy.y;
+      v[8] = fmaf(qy.y, dy.y, qy.x * dy.x);
       v[4] = v[3] * dx;  // sum dq dx
       v[6] = v[4] * dx;  // sum dq dx^2
       v[7] = v[5] * dx;  // sum dq dx dy
