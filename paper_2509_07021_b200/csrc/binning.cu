@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(256) emit_entries(const uint32_t* __restrict__
             const uint32_t col = (uint32_t)rfirst + (j - rex);
             const uint32_t cell = (uint32_t)(rrow * row_w) + col;
             if (kSuper) {
-              keys_out[o] = (KT)((cell << 16) | sgs_super_mask(mf, mc, (int)col));
+              keys_out[o] = (KT)((cell << 16) | sgs_super_mask_fast(mf, mc, (int)col));
               if (cell_hist) atomicAdd(&s_hist[cell & 511u], 1u);
             }
             else

@@ -290,6 +290,9 @@ constexpr int kFwdChunk = kFwdThreads * kFwdCPT;  // candidates examined per sta
 #ifndef SGS_VOTE_EVERY
 #define SGS_VOTE_EVERY 8
 #endif
+#ifndef SGS_FWD_MIN_BLOCKS
+#define SGS_FWD_MIN_BLOCKS 1
+#endif
 constexpr int kFwdBatch = SGS_FWD_BATCH;          // staged entries processed per block sync
 constexpr int kFwdBuf = kFwdBatch + kFwdChunk;
 constexpr int kVoteEvery = SGS_VOTE_EVERY;
@@ -362,7 +365,7 @@ __device__ __forceinline__ void blend2(float2 p, const float4& c, float2& T2, fl
 }
 
 template <bool kImportance, bool kCount, bool kFilter, bool kTrack>
-__global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(ListArgs la, SgsCam cam, float3 bg,
+__global__ void __launch_bounds__(kFwdThreads, SGS_FWD_MIN_BLOCKS) raster_fwd_kernel(ListArgs la, SgsCam cam, float3 bg,
                                                                  float* __restrict__ out_img,
                                                                  float* __restrict__ out_T,
                                                                  uint32_t* __restrict__ out_nc,

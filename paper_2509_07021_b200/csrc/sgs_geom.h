@@ -522,6 +522,22 @@ SGS_HD uint32_t sgs_super_mask(const int first[SGS_SUPER], const int cnt[SGS_SUP
   return m;
 }
 
+// sgs_super_mask with per-row bit arithmetic (same value): row r's members
+// are tile columns [max(first, 4 sc), min(first + cnt, 4 sc + 4)) of the
+// super column, a run of bits ((1 << hi) - (1 << lo)) in nibble r.
+SGS_HD uint32_t sgs_super_mask_fast(const int first[SGS_SUPER], const int cnt[SGS_SUPER], int sc) {
+  uint32_t m = 0;
+  const int x0 = sc * SGS_SUPER;
+  for (int r = 0; r < SGS_SUPER; ++r) {
+    int lo = first[r] - x0, hi = first[r] + cnt[r] - x0;
+    lo = lo < 0 ? 0 : lo;
+    hi = hi > SGS_SUPER ? SGS_SUPER : hi;
+    const uint32_t run = hi > lo ? (1u << hi) - (1u << lo) : 0u;
+    m |= run << (r * SGS_SUPER);
+  }
+  return m;
+}
+
 // SG color for the camera-to-center view direction (render.py:294-305):
 //   c_pre = diffuse + sum_l m_l a_l exp(s_l (mu_l . v - 1)),  c = max(c_pre, 0)
 // Lobes with mask exactly 0 are skipped (bit-identical to multiplying by 0).
