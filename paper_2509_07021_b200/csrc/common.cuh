@@ -13,8 +13,14 @@ namespace sgs {
 
 constexpr int kNumSMs = 148;
 constexpr int kRadixThreads = 512;  // = kRsThreads in sort.cuh
-constexpr int kTileSortIPT = 16;  // items per thread, tile-key onesweep passes (8192 per CTA)
-constexpr int kDepthSortIPT = 16;
+#ifndef SGS_TILE_SORT_IPT
+#define SGS_TILE_SORT_IPT 16
+#endif
+#ifndef SGS_DEPTH_SORT_IPT
+#define SGS_DEPTH_SORT_IPT 16
+#endif
+constexpr int kTileSortIPT = SGS_TILE_SORT_IPT;  // items per thread, tile-key onesweep passes (8192 per CTA)
+constexpr int kDepthSortIPT = SGS_DEPTH_SORT_IPT;
 #ifndef SGS_DEPTH_SORT_THREADS
 #define SGS_DEPTH_SORT_THREADS 512
 #endif
