@@ -515,43 +515,43 @@ constexpr int kBwdThreads = 128;
 constexpr int kBwdCPT = 1;
 constexpr int kBwdChunk = kBwdThreads * kBwdCPT;  // candidates staged per batch
 
-// Sum of nine per-lane values over the warp by recursive halving: each
-// exchange level sends the half of the values the partner keeps (5 + 3 + 2
-// + 1 + 1 = 12 shuffles instead of 9 x 5).  Returns the total of value
-// kBwdLaneValue(lane) (pairs of lanes hold the same total; -1 = padding).
-__device__ __forceinline__ float warp_reduce9(const float v[kGrad], int lane) {
+// The nine per-record partials summed over the warp.  A lane's two pixels
+// share the column (dx); the four lanes of a column (lane bits 3, 4) are
+// summed first on the six dx-free partials -- colour sums c0..c2 = sum w g
+// and dq moments m0 = sum dq, m1 = sum dq dy, m2 = sum dq dy^2 -- by
+// recursive halving (3 + 2 shuffles), the column sums are turned into the
+// dx moments there (sum dq dx = dx m0, ...), and the eight columns (lane
+// bits 0..2) are summed by halving again (2 + 1 + 1 shuffles): 9 shuffles in
+// all instead of 12.  Returns the total of value reduce9_index(lane).
+__device__ __forceinline__ float warp_reduce9(float c0, float c1, float c2, float m0, float m1, float m2, float dx,
+                                              int lane) {
   const bool u16 = lane & 16, u8 = lane & 8, u4 = lane & 4, u2 = lane & 2;
-  float a[5];
-#pragma unroll
-  for (int j = 0; j < 5; ++j) {
-    const float hi = j + 5 < kGrad ? v[j + 5] : 0.0f;
-    const float send = u16 ? v[j] : hi, keep = u16 ? hi : v[j];
-    a[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-  }
-  float b[3];
-#pragma unroll
-  for (int j = 0; j < 3; ++j) {
-    const float hi = j + 3 < 5 ? a[j + 3] : 0.0f;
-    const float send = u8 ? a[j] : hi, keep = u8 ? hi : a[j];
-    b[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-  }
-  float c[2];
-#pragma unroll
-  for (int j = 0; j < 2; ++j) {
-    const float hi = j + 2 < 3 ? b[j + 2] : 0.0f;
-    const float send = u4 ? b[j] : hi, keep = u4 ? hi : b[j];
-    c[j] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-  }
-  const float send = u2 ? c[0] : c[1], keep = u2 ? c[1] : c[0];
-  float d = keep + __shfl_xor_sync(0xffffffffu, send, 2);
-  return d + __shfl_xor_sync(0xffffffffu, d, 1);
+  // rows, bit 4: colours stay on u16 = 0, moments on u16 = 1
+  const float x0 = (u16 ? m0 : c0) + __shfl_xor_sync(0xffffffffu, u16 ? c0 : m0, 16);
+  const float x1 = (u16 ? m1 : c1) + __shfl_xor_sync(0xffffffffu, u16 ? c1 : m1, 16);
+  const float x2 = (u16 ? m2 : c2) + __shfl_xor_sync(0xffffffffu, u16 ? c2 : m2, 16);
+  // rows, bit 3: (x0, x1) split, x2 summed on both
+  const float y0 = (u8 ? x1 : x0) + __shfl_xor_sync(0xffffffffu, u8 ? x0 : x1, 8);
+  const float y1 = x2 + __shfl_xor_sync(0xffffffffu, x2, 8);
+  // column sums: (u16, u8) = 00: c0, c2 | 01: c1 | 10: m0, dx m0, dx^2 m0 | 11: m1, dx m1, m2
+  const float ydx = y0 * dx;
+  const float z0 = y0;
+  const float z1 = u16 ? ydx : (u8 ? 0.0f : y1);
+  const float z2 = u16 ? (u8 ? y1 : ydx * dx) : 0.0f;
+  // columns, bit 2: (z0, z1) split, z2 summed on both; bits 1, 0
+  const float p0 = (u4 ? z1 : z0) + __shfl_xor_sync(0xffffffffu, u4 ? z0 : z1, 4);
+  const float p1 = z2 + __shfl_xor_sync(0xffffffffu, z2, 4);
+  const float q = (u2 ? p1 : p0) + __shfl_xor_sync(0xffffffffu, u2 ? p0 : p1, 2);
+  return q + __shfl_xor_sync(0xffffffffu, q, 1);
 }
 
-// Value index held by each even lane after warp_reduce9 (4 bits per even
-// lane, 15 = padding), from simulating the halving schedule above.
+// Partial index held by each even lane after warp_reduce9 (4 bits per lane
+// pair, 15 = padding or a duplicate): pair i = lane >> 1 has (u16, u8, u4,
+// u2) = bits (3, 2, 1, 0) of i and holds u2 ? z2 : (u4 ? z1 : z0) with the
+// partial order (w gx, w gy, w gz, dq, dq dx, dq dy, dq dx^2, dq dx dy, dq dy^2).
 __device__ __forceinline__ int reduce9_index(int lane) {
-  constexpr unsigned long long kLut = 0xfff8f765ff43f210ull;
-  return (lane & 1) ? 15 : (int)((kLut >> (2 * lane)) & 15ull);
+  constexpr unsigned long long kLut = 0xf785f463fff1f2f0ull;
+  return (lane & 1) ? 15 : (int)((kLut >> (4 * (lane >> 1))) & 15ull);
 }
 
 // Backward raster: 128 threads per tile, two vertically adjacent pixels per
@@ -669,21 +669,12 @@ __global__ void __launch_bounds__(kBwdThreads) raster_bwd_kernel(ListArgs la, Sg
       const float ww0 = act0 ? w.x : 0.0f, ww1 = act1 ? w.y : 0.0f;
       S2 = make_float2(act0 ? Sn.x : S2.x, act1 ? Sn.y : S2.y);
       T2 = make_float2(act0 ? Ti.x : T2.x, act1 ? Ti.y : T2.y);
-      float v[kGrad];
       const float2 vxy = __ffma2_rn(f2(ww1), gxy1, __fmul2_rn(f2(ww0), gxy0));
-      v[0] = vxy.x;
-      v[1] = vxy.y;
-      v[2] = fmaf(ww1, g12, ww0 * g02);
-      // the thread's pixels share dx: accumulate sum dq, sum dq dy, sum dq dy^2
-      // and apply the dx factors once per record
+      // the column's pixels share dx: the dq moments are summed in dy only and
+      // the dx factors applied to the column sums inside the reduction
       const float2 qy = __fmul2_rn(dqa, dy);
-      v[3] = dqa.x + dqa.y;
-      v[5] = qy.x + qy.y;
-      v[8] = fmaf(qy.y, dy.y, qy.x * dy.x);
-      v[4] = v[3] * dx;  // sum dq dx
-      v[6] = v[4] * dx;  // sum dq dx^2
-      v[7] = v[5] * dx;  // sum dq dx dy
-      const float tot = warp_reduce9(v, lane);
+      const float tot = warp_reduce9(vxy.x, vxy.y, fmaf(ww1, g12, ww0 * g02), dqa.x + dqa.y, qy.x + qy.y,
+                                     fmaf(qy.y, dy.y, qy.x * dy.x), dx, lane);
       if (vidx < kGrad) s_part[wq_][k][vidx] = tot;
     }
     __syncthreads();
