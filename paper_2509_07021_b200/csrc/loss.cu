@@ -27,7 +27,10 @@
 
 namespace sgs {
 
-constexpr int kLossTW = 32, kLossTH = 8, kLossThreads = 256;
+#ifndef SGS_LOSS_TH
+#define SGS_LOSS_TH 16
+#endif
+constexpr int kLossTW = 32, kLossTH = SGS_LOSS_TH, kLossThreads = kLossTW * kLossTH;
 constexpr int kMaxWindow = 31;
 
 struct LossParams {
@@ -59,14 +62,17 @@ __host__ __device__ inline size_t loss_smem_doubles(int r, int nplanes_in, int n
   return (size_t)nplanes_in * (kLossTH + 2 * r) * (kLossTW + 2 * r) + (size_t)nplanes_h * (kLossTH + 2 * r) * kLossTW;
 }
 
-template <typename TI, typename TT>
+// R > 0: the window radius as a compile-time constant (the default 11-tap
+// window, R = 5: unrolled taps, weights as constant-bank immediates, halo
+// index arithmetic by constants); R = 0 reads it from P.
+template <typename TI, typename TT, int R>
 __global__ void __launch_bounds__(kLossThreads) ssim_fwd_kernel(const TI* __restrict__ img, const TT* __restrict__ tgt,
                                                                 LossParams P, double* __restrict__ dmu,
                                                                 double* __restrict__ dxx, double* __restrict__ dxy,
                                                                 double* __restrict__ smap, double* __restrict__ sums) {
   extern __shared__ double sh[];
   __shared__ double red[kLossThreads / 32];
-  const int r = P.r, HW = kLossTW + 2 * r, HH = kLossTH + 2 * r;
+  const int r = R > 0 ? R : P.r, HW = kLossTW + 2 * r, HH = kLossTH + 2 * r;
   double* sx = sh;
   double* sy = sx + HH * HW;
   double* hs = sy + HH * HW;  // 5 planes of HH x TW
@@ -88,7 +94,8 @@ __global__ void __launch_bounds__(kLossThreads) ssim_fwd_kernel(const TI* __rest
     for (int i = t; i < HH * kLossTW; i += kLossThreads) {
       const int row = i / kLossTW, col = i % kLossTW;
       double a = 0, b = 0, aa = 0, bb = 0, ab = 0;
-      for (int k = 0; k <= 2 * r; ++k) {
+      #pragma unroll
+        for (int k = 0; k <= 2 * r; ++k) {
         const double wx = P.w[k];
         const double u = sx[row * HW + col + k], v = sy[row * HW + col + k];
         a = fma(wx, u, a);
@@ -107,7 +114,8 @@ __global__ void __launch_bounds__(kLossThreads) ssim_fwd_kernel(const TI* __rest
     __syncthreads();
     if (inside) {
       double mx = 0, my = 0, mxx = 0, myy = 0, mxy = 0;
-      for (int k = 0; k <= 2 * r; ++k) {
+      #pragma unroll
+        for (int k = 0; k <= 2 * r; ++k) {
         const double wy = P.w[k];
         const int o = (oy + k) * kLossTW + ox;
         mx = fma(wy, hs[o], mx);
@@ -121,7 +129,8 @@ __global__ void __launch_bounds__(kLossThreads) ssim_fwd_kernel(const TI* __rest
       const double B1 = mx * mx + my * my + P.c1, B2 = sxv + syv + P.c2;
       const double inv = 1.0 / (B1 * B2);
       const double S = A1 * A2 * inv;
-      const double dA1 = A2 * inv, dA2 = A1 * inv, dB1 = -S / B1, dB2 = -S / B2;
+      // 1 / B1 = B2 inv, 1 / B2 = B1 inv: one division
+      const double dA1 = A2 * inv, dA2 = A1 * inv, dB1 = -S * (B2 * inv), dB2 = -S * (B1 * inv);
       const size_t g = ((size_t)py * P.W + px) * 3 + c;
       dmu[g] = 2.0 * my * dA1 + 2.0 * mx * dB1 - 2.0 * mx * dB2 - 2.0 * my * dA2;
       dxx[g] = dB2;
@@ -141,14 +150,14 @@ __global__ void __launch_bounds__(kLossThreads) ssim_fwd_kernel(const TI* __rest
   }
 }
 
-template <typename TI, typename TT>
+template <typename TI, typename TT, int R>
 __global__ void __launch_bounds__(kLossThreads) ssim_bwd_kernel(const TI* __restrict__ img, const TT* __restrict__ tgt,
                                                                 LossParams P, const double* __restrict__ dmu,
                                                                 const double* __restrict__ dxx,
                                                                 const double* __restrict__ dxy, float* __restrict__ dimg,
                                                                 double* __restrict__ dimg64) {
   extern __shared__ double sh[];
-  const int r = P.r, HW = kLossTW + 2 * r, HH = kLossTH + 2 * r;
+  const int r = R > 0 ? R : P.r, HW = kLossTW + 2 * r, HH = kLossTH + 2 * r;
   double* s0 = sh;
   double* s1 = s0 + HH * HW;
   double* s2 = s1 + HH * HW;
@@ -172,6 +181,7 @@ __global__ void __launch_bounds__(kLossThreads) ssim_bwd_kernel(const TI* __rest
       for (int i = t; i < HH * kLossTW; i += kLossThreads) {
         const int row = i / kLossTW, col = i % kLossTW;
         double a = 0, b = 0, d = 0;
+        #pragma unroll
         for (int k = 0; k <= 2 * r; ++k) {
           const double wx = P.w[k];
           const int o = row * HW + col + k;
@@ -193,6 +203,7 @@ __global__ void __launch_bounds__(kLossThreads) ssim_bwd_kernel(const TI* __rest
       double out = (1.0 - P.lam) * (double)((diff > 0.0) - (diff < 0.0)) * P.inv_size;
       if (P.lam != 0.0) {
         double fa = 0, fb = 0, fd = 0;
+        #pragma unroll
         for (int k = 0; k <= 2 * r; ++k) {
           const double wy = P.w[k];
           const int o = (oy + k) * kLossTW + ox;
@@ -239,8 +250,13 @@ static int run_loss(const TI* img, const TT* tgt, const LossParams& P, float* di
   const dim3 grid((P.W + kLossTW - 1) / kLossTW, (P.H + kLossTH - 1) / kLossTH);
   if (P.lam != 0.0) {
     const size_t smem = loss_smem_doubles(P.r, 2, 5) * sizeof(double);
-    SGS_CUDA(cudaFuncSetAttribute(ssim_fwd_kernel<TI, TT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    ssim_fwd_kernel<TI, TT><<<grid, kLossThreads, smem, st>>>(img, tgt, P, dmu, dxx, dxy, smap, out + 3);
+    if (P.r == 5) {
+      SGS_CUDA(cudaFuncSetAttribute(ssim_fwd_kernel<TI, TT, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      ssim_fwd_kernel<TI, TT, 5><<<grid, kLossThreads, smem, st>>>(img, tgt, P, dmu, dxx, dxy, smap, out + 3);
+    } else {
+      SGS_CUDA(cudaFuncSetAttribute(ssim_fwd_kernel<TI, TT, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      ssim_fwd_kernel<TI, TT, 0><<<grid, kLossThreads, smem, st>>>(img, tgt, P, dmu, dxx, dxy, smap, out + 3);
+    }
     SGS_LAUNCH_CHECK("ssim_fwd_kernel");
   } else {
     const int g = persistent_grid(n, kLossThreads * 8, 4);
@@ -251,8 +267,13 @@ static int run_loss(const TI* img, const TT* tgt, const LossParams& P, float* di
   SGS_LAUNCH_CHECK("loss_finish_kernel");
   if (dimg || dimg64) {
     const size_t smem = P.lam != 0.0 ? loss_smem_doubles(P.r, 3, 3) * sizeof(double) : 0;
-    SGS_CUDA(cudaFuncSetAttribute(ssim_bwd_kernel<TI, TT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    ssim_bwd_kernel<TI, TT><<<grid, kLossThreads, smem, st>>>(img, tgt, P, dmu, dxx, dxy, dimg, dimg64);
+    if (P.r == 5) {
+      SGS_CUDA(cudaFuncSetAttribute(ssim_bwd_kernel<TI, TT, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      ssim_bwd_kernel<TI, TT, 5><<<grid, kLossThreads, smem, st>>>(img, tgt, P, dmu, dxx, dxy, dimg, dimg64);
+    } else {
+      SGS_CUDA(cudaFuncSetAttribute(ssim_bwd_kernel<TI, TT, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      ssim_bwd_kernel<TI, TT, 0><<<grid, kLossThreads, smem, st>>>(img, tgt, P, dmu, dxx, dxy, dimg, dimg64);
+    }
     SGS_LAUNCH_CHECK("ssim_bwd_kernel");
   }
   return SGS_OK;
