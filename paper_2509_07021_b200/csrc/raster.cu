@@ -451,10 +451,9 @@ __global__ void __launch_bounds__(kFwdThreads, SGS_FWD_MIN_BLOCKS) raster_fwd_ke
           bool k0, k1;
           float2 w;
           blend2<kClamp>(p, c, T2, Cr, Cg, Cb, k0, k1, w);
-          if (kTrack && kk < nb) {  // padding records are never counted
-            const uint32_t idx = hits_before + (uint32_t)kk + 1u;
-            if (k0) nc0 = idx;
-            if (k1) nc1 = idx;
+          if constexpr (kTrack) {  // kept records form a prefix: count them
+            nc0 += (uint32_t)k0;
+            nc1 += (uint32_t)k1;
           }
           if constexpr (kImportance) {
             const float w0 = w.x, w1 = w.y;
@@ -472,6 +471,10 @@ __global__ void __launch_bounds__(kFwdThreads, SGS_FWD_MIN_BLOCKS) raster_fwd_ke
     else
       run_batch(std::false_type{});
     if constexpr (kTrack) {
+      // the zero-opacity padding records count as kept for pixels still alive
+      const uint32_t lim = hits_before + (uint32_t)nb;
+      nc0 = nc0 < lim ? nc0 : lim;
+      nc1 = nc1 < lim ? nc1 : lim;
       // candidate position of this thread's last kept entry (for the backward)
       const uint32_t mx = nc0 > nc1 ? nc0 : nc1;
       if (mx > hits_before) kend = s.cand[mx - hits_before - 1] + 1u;
