@@ -615,7 +615,6 @@ __global__ void __launch_bounds__(kBwdThreads) raster_bwd_kernel(ListArgs la, Sg
   }
   float2 T2 = make_float2(T0, T1), S2 = make_float2(S0, S1);
   const float2 gx2 = make_float2(g00, g10), gy2 = make_float2(g01, g11), gz2 = make_float2(g02, g12);
-  const float2 gxy0 = make_float2(g00, g01), gxy1 = make_float2(g10, g11);
   const float2 fyv = make_float2(fy0, fy0 + 1.0f);
   const uint32_t ncm = nc0 > nc1 ? nc0 : nc1;
   if (ncm) atomicMax(&s_max_nc, ncm);
@@ -672,11 +671,12 @@ __global__ void __launch_bounds__(kBwdThreads) raster_bwd_kernel(ListArgs la, Sg
       const float ww0 = act0 ? w.x : 0.0f, ww1 = act1 ? w.y : 0.0f;
       S2 = make_float2(act0 ? Sn.x : S2.x, act1 ? Sn.y : S2.y);
       T2 = make_float2(act0 ? Ti.x : T2.x, act1 ? Ti.y : T2.y);
-      const float2 vxy = __ffma2_rn(f2(ww1), gxy1, __fmul2_rn(f2(ww0), gxy0));
+      const float2 ww = make_float2(ww0, ww1);
+      const float2 wgx = __fmul2_rn(ww, gx2), wgy = __fmul2_rn(ww, gy2), wgz = __fmul2_rn(ww, gz2);
       // the column's pixels share dx: the dq moments are summed in dy only and
       // the dx factors applied to the column sums inside the reduction
       const float2 qy = __fmul2_rn(dqa, dy);
-      const float tot = warp_reduce9(vxy.x, vxy.y, fmaf(ww1, g12, ww0 * g02), dqa.x + dqa.y, qy.x + qy.y,
+      const float tot = warp_reduce9(wgx.x + wgx.y, wgy.x + wgy.y, wgz.x + wgz.y, dqa.x + dqa.y, qy.x + qy.y,
                                      fmaf(qy.y, dy.y, qy.x * dy.x), dx, lane);
       if (vidx < kGrad) s_part[wq_][k][vidx] = tot;
     }
