@@ -473,7 +473,7 @@ def run_train(args):
     tr = SoftPruneTrainer(scene, scene.extra["prim_logit"], scene.extra["lobe_logit"], device=dev,
                           group=group)
     for _ in range(max(args.warmup, 3)):
-        tr.step(cams, targets, rank, world, apply=False)
+        tr.step(cams, targets, rank, world, apply=True)  # steady state: capacities sized
     torch.cuda.synchronize(dev)
     stream = torch.cuda.current_stream(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
