@@ -85,7 +85,12 @@ typedef struct sgs_grads {
   float* amplitude;
   float* lobe_mask;
   float* prim_mask;
+  int32_t flags;  /* SGS_GRADS_* bits; 0 = overwrite every output row */
 } sgs_grads;
+
+/* sgs_grads.flags */
+#define SGS_GRADS_ACCUMULATE 1  /* add into the outputs (a multi-view gradient sum) */
+#define SGS_GRADS_MASK_LOGIT 2  /* mask gradients w.r.t. logits: x m (1 - m), m = sigmoid(logit) = the mask */
 
 /* Device workspace descriptor.  `base` is ONE caller-allocated device buffer
  * of at least sgs_workspace_size() bytes for the same (n, n_lobes, width,

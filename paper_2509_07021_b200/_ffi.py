@@ -40,7 +40,11 @@ class SgsGrads(C.Structure):
     _fields_ = [("position", C.c_void_p), ("quat", C.c_void_p), ("log_scale", C.c_void_p),
                 ("opacity", C.c_void_p), ("diffuse", C.c_void_p), ("axis_raw", C.c_void_p),
                 ("sharpness", C.c_void_p), ("amplitude", C.c_void_p), ("lobe_mask", C.c_void_p),
-                ("prim_mask", C.c_void_p)]
+                ("prim_mask", C.c_void_p), ("flags", C.c_int32)]
+
+
+GRADS_ACCUMULATE = 1   # SGS_GRADS_ACCUMULATE
+GRADS_MASK_LOGIT = 2   # SGS_GRADS_MASK_LOGIT
 
 
 class SgsWorkspace(C.Structure):

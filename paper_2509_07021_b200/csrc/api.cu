@@ -192,6 +192,11 @@ int sgs_preprocess_backward(const sgs_params* params, const sgs_camera* cam, con
     set_error("null gradient buffer");
     return SGS_E_ARG;
   }
+  if ((grads->flags & ~(SGS_GRADS_ACCUMULATE | SGS_GRADS_MASK_LOGIT)) != 0 ||
+      (reinterpret_cast<uintptr_t>(grads->quat) & 15u) != 0) {
+    set_error("invalid gradient flags or unaligned quaternion gradient (16-byte rows)");
+    return SGS_E_ARG;
+  }
   Layout lo{};
   lo.W = cam ? cam->width : 0;
   lo.H = cam ? cam->height : 0;

@@ -6,15 +6,29 @@
 //   dL/dm_p = o   dL/do_eff          (o_eff = m_p o)
 //   dL/dm_l = (dL/dc_pre . a_l) e_l  (c_pre = diffuse + sum_l m_l a_l e_l)
 // One thread per primitive; every output row is written (zeros for
-// primitives no pixel kept), so outputs need no memset.
+// primitives no pixel kept), so outputs need no memset.  With
+// SGS_GRADS_ACCUMULATE the rows are added to the outputs instead (a training
+// step sums its views straight into one gradient bucket), and with
+// SGS_GRADS_MASK_LOGIT the mask gradients are taken through the sigmoid that
+// produced the masks: dL/dlogit = dL/dm m (1 - m).
 #include "common.cuh"
 
 namespace sgs {
 
 constexpr int kG2 = 9;
 
+template <bool kAcc>
+__device__ __forceinline__ void put(float* p, int64_t i, float v) {
+  if (kAcc)
+    p[i] += v;
+  else
+    p[i] = v;
+}
+
+template <bool kAcc>
 __global__ void __launch_bounds__(128) preprocess_bwd_kernel(sgs_params P, SgsCam cam,
                                                              const float* __restrict__ grad2d, sgs_grads out) {
+  const bool logit = (out.flags & SGS_GRADS_MASK_LOGIT) != 0;
   const int64_t n = P.n;
   const int L = P.n_lobes;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -154,19 +168,19 @@ __global__ void __launch_bounds__(128) preprocess_bwd_kernel(sgs_params P, SgsCa
       const float s = P.sharpness[i * L + l];
       const float da = dcp[0] * a[0] + dcp[1] * a[1] + dcp[2] * a[2];
       const float em = e[l] * m;
-      for (int c = 0; c < 3; ++c) out.amplitude[(i * L + l) * 3 + c] = dcp[c] * em;
+      for (int c = 0; c < 3; ++c) put<kAcc>(out.amplitude, (i * L + l) * 3 + c, dcp[c] * em);
       const float ga = da * em;
-      out.sharpness[i * L + l] = ga * (dotv[l] - 1.0f);
-      if (out.lobe_mask) out.lobe_mask[i * L + l] = da * e[l];
+      put<kAcc>(out.sharpness, i * L + l, ga * (dotv[l] - 1.0f));
+      if (out.lobe_mask) put<kAcc>(out.lobe_mask, i * L + l, logit ? da * e[l] * (m * (1.0f - m)) : da * e[l]);
       const float un = sqrtf(u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
       const float mu0 = u[0] / un, mu1 = u[1] / un, mu2 = u[2] / un;
       // d mu = ga s v ; d u = (I - mu mu^T) d mu / |u|
       const float gs = ga * s;
       const float dm0 = gs * v0, dm1 = gs * v1, dm2 = gs * v2;
       const float pr = mu0 * dm0 + mu1 * dm1 + mu2 * dm2;
-      out.axis_raw[(i * L + l) * 3 + 0] = (dm0 - mu0 * pr) / un;
-      out.axis_raw[(i * L + l) * 3 + 1] = (dm1 - mu1 * pr) / un;
-      out.axis_raw[(i * L + l) * 3 + 2] = (dm2 - mu2 * pr) / un;
+      put<kAcc>(out.axis_raw, (i * L + l) * 3 + 0, (dm0 - mu0 * pr) / un);
+      put<kAcc>(out.axis_raw, (i * L + l) * 3 + 1, (dm1 - mu1 * pr) / un);
+      put<kAcc>(out.axis_raw, (i * L + l) * 3 + 2, (dm2 - mu2 * pr) / un);
       dv[0] += gs * mu0;
       dv[1] += gs * mu1;
       dv[2] += gs * mu2;
@@ -177,20 +191,28 @@ __global__ void __launch_bounds__(128) preprocess_bwd_kernel(sgs_params P, SgsCa
     d_pos[2] += (dv[2] - v2 * pv) / rd;
 
     for (int k = 0; k < 3; ++k) {
-      out.position[3 * i + k] = d_pos[k];
-      out.log_scale[3 * i + k] = d_ls[k];
-      out.diffuse[3 * i + k] = d_diff[k];
+      put<kAcc>(out.position, 3 * i + k, d_pos[k]);
+      put<kAcc>(out.log_scale, 3 * i + k, d_ls[k]);
+      put<kAcc>(out.diffuse, 3 * i + k, d_diff[k]);
     }
-    reinterpret_cast<float4*>(out.quat)[i] = make_float4(d_q[0], d_q[1], d_q[2], d_q[3]);
-    out.opacity[i] = d_op;
-    if (out.prim_mask) out.prim_mask[i] = d_pm;
+    float4 q = make_float4(d_q[0], d_q[1], d_q[2], d_q[3]);
+    if (kAcc) {
+      const float4 o = reinterpret_cast<const float4*>(out.quat)[i];
+      q = make_float4(o.x + q.x, o.y + q.y, o.z + q.z, o.w + q.w);
+    }
+    reinterpret_cast<float4*>(out.quat)[i] = q;
+    put<kAcc>(out.opacity, i, d_op);
+    if (out.prim_mask) put<kAcc>(out.prim_mask, i, logit ? d_pm * (pm * (1.0f - pm)) : d_pm);
   }
 }
 
 int launch_preprocess_bwd(const sgs_params& P, const SgsCam& cam, const float* grad2d, const sgs_grads& g,
                           cudaStream_t st) {
   int grid = persistent_grid((uint64_t)P.n, 128, 16);
-  preprocess_bwd_kernel<<<grid, 128, 0, st>>>(P, cam, grad2d, g);
+  if (g.flags & SGS_GRADS_ACCUMULATE)
+    preprocess_bwd_kernel<true><<<grid, 128, 0, st>>>(P, cam, grad2d, g);
+  else
+    preprocess_bwd_kernel<false><<<grid, 128, 0, st>>>(P, cam, grad2d, g);
   SGS_LAUNCH_CHECK("preprocess_bwd_kernel");
   return SGS_OK;
 }

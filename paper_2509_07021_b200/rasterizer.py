@@ -322,10 +322,15 @@ class Rasterizer:
 
     # ----------------------------------------------------------------- backward
     def backward(self, g: GaussianTensors, frame: Frame, dimg: torch.Tensor,
-                 mask_grads: bool = True) -> dict:
+                 mask_grads: bool = True, out: dict | None = None, accumulate: bool = False,
+                 mask_logit: bool = False) -> dict:
         """dL/dparams for dL/dimg (H,W,3).  Returns a dict of float32 tensors
         shaped like the parameters (+ 'lobe_mask' / 'prim_mask' when
-        ``mask_grads``) and 'grad2d' (N,9)."""
+        ``mask_grads``) and 'grad2d' (N,9).  ``out`` supplies the output
+        tensors (contiguous float32, parameter-shaped, 'quat' 16-byte
+        aligned); with ``accumulate`` the gradients are added into them, and
+        with ``mask_logit`` the mask gradients are taken with respect to the
+        logits whose sigmoids are the masks (x m (1 - m))."""
         dimg = dimg.to(device=self.device, dtype=torch.float32).contiguous()
         if frame.ncontrib is None:
             raise ValueError("frame was rendered with track=False; the backward needs track=True")
@@ -337,15 +342,27 @@ class Rasterizer:
         _ffi.call("sgs_raster_backward", C.byref(frame.cam), c_bg, C.byref(frame.ws.desc),
                   _ptr(frame.img), _ptr(frame.final_T), _ptr(frame.ncontrib), _ptr(dimg),
                   _ptr(grad2d), stream)
-        out = {f: torch.empty_like(getattr(g, f)) for f in GRAD_FIELDS}
-        if mask_grads:
-            out["lobe_mask"] = torch.empty_like(g.lobe_mask)
-            out["prim_mask"] = torch.empty((g.n,), dtype=torch.float32, device=self.device)
+        if out is None:
+            if accumulate:
+                raise ValueError("accumulate=True needs the output tensors")
+            out = {f: torch.empty_like(getattr(g, f)) for f in GRAD_FIELDS}
+            if mask_grads:
+                out["lobe_mask"] = torch.empty_like(g.lobe_mask)
+                out["prim_mask"] = torch.empty((g.n,), dtype=torch.float32, device=self.device)
+        else:
+            out = dict(out)
+            for f in GRAD_FIELDS + (("lobe_mask", "prim_mask") if mask_grads else ()):
+                t = out.get(f)
+                numel = g.n if f == "prim_mask" else getattr(g, f).numel()
+                if t is None or t.dtype != torch.float32 or not t.is_contiguous() or t.numel() != numel:
+                    raise ValueError(f"gradient output '{f}' must be a contiguous float32 tensor "
+                                     f"of {numel} elements")
         cg = _ffi.SgsGrads()
+        cg.flags = (_ffi.GRADS_ACCUMULATE if accumulate else 0) | (_ffi.GRADS_MASK_LOGIT if mask_logit else 0)
         for f in GRAD_FIELDS:
             setattr(cg, f, _ptr(out[f]))
-        cg.lobe_mask = _ptr(out.get("lobe_mask"))
-        cg.prim_mask = _ptr(out.get("prim_mask"))
+        cg.lobe_mask = _ptr(out.get("lobe_mask")) if mask_grads else None
+        cg.prim_mask = _ptr(out.get("prim_mask")) if mask_grads else None
         params = g.c_params()
         _ffi.call("sgs_preprocess_backward", C.byref(params), C.byref(frame.cam), _ptr(grad2d),
                   C.byref(cg), stream)

@@ -300,18 +300,22 @@ def _grads_to_set(gr: dict) -> GradientSet:
 
 def loss_and_grads_device(g: GaussianTensors, cam, target: torch.Tensor, cfg: LossConfig = LossConfig(),
                           background=(0.0, 0.0, 0.0), rast: Rasterizer | None = None,
-                          mask_grads: bool = False, sync: bool = True, overflow_out=None):
+                          mask_grads: bool = False, sync: bool = True, overflow_out=None,
+                          grads_out: dict | None = None, accumulate: bool = False, mask_logit: bool = False):
     """Device-resident variant: (loss, dict of float32 gradient tensors).  The
     loss is a float, or a 0-dim float64 device tensor with ``sync=False`` (no
     host round trip).  With ``overflow_out`` (int64 device tensor of 2) the
     tile-entry capacity is not checked here: the frame's (overflow, entries)
-    counters land in it and the caller checks them later (Frame.record_overflow)."""
+    counters land in it and the caller checks them later (Frame.record_overflow).
+    ``grads_out`` / ``accumulate`` / ``mask_logit``: see Rasterizer.backward
+    (a training step sums its views straight into one gradient bucket)."""
     rast = rast or rasterizer()
     frame = rast.forward(g, cam, _bg(background), check=overflow_out is None)
     if overflow_out is not None:
         frame.record_overflow(overflow_out)
     out, dimg, _ = image_loss(frame.img, target, cfg, grad="f32")
-    grads = rast.backward(g, frame, dimg, mask_grads=mask_grads)
+    grads = rast.backward(g, frame, dimg, mask_grads=mask_grads, out=grads_out, accumulate=accumulate,
+                          mask_logit=mask_logit)
     return (float(out[0]) if sync else out[0]), grads
 
 

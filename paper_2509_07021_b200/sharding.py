@@ -80,7 +80,7 @@ class GradBucket:
         off = 0
         for k in self.keys:
             self.offsets[k] = off
-            off += self.sizes[k]
+            off += (self.sizes[k] + 3) // 4 * 4  # 16-byte aligned views (float4 rows)
         self.numel = off
         self.flat = torch.zeros(off, device=device, dtype=dtype)
 

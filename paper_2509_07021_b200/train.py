@@ -67,12 +67,30 @@ class SoftPruneTrainer:
             return SimpleNamespace(**self.params, lobe_mask=m_l.contiguous(), prim_mask=m_p.contiguous())
         return GaussianTensors(**self.params, lobe_mask=m_l.contiguous(), prim_mask=m_p.contiguous())
 
+    def _bucket_out(self) -> dict:
+        out = {f: self.bucket.view(f) for f in GRAD_FIELDS}
+        out["prim_mask"] = self.bucket.view("prim_logit")
+        out["lobe_mask"] = self.bucket.view("lobe_logit")
+        return out
+
     def _view_grads(self, g: GaussianTensors, cam, target, overflow=None):
+        """Loss of one view; its gradients are added to the bucket (mask
+        gradients through the sigmoid, i.e. with respect to the logits)."""
         if self.grad_fn is not None:
-            return self.grad_fn(g, cam, target)
+            val, gr = self.grad_fn(g, cam, target)
+            m_p, m_l = g.prim_mask, g.lobe_mask
+            d_mp = gr.pop("prim_mask")
+            d_ml = gr.pop("lobe_mask")
+            gr.pop("grad2d", None)
+            self.bucket.add_(gr)
+            self.bucket.view("prim_logit").add_(d_mp * m_p * (1 - m_p))
+            self.bucket.view("lobe_logit").add_(d_ml * m_l * (1 - m_l))
+            return val
         from .render import LossConfig, loss_and_grads_device
-        return loss_and_grads_device(g, cam, target, LossConfig(lambda_ssim=self.cfg.lambda_ssim),
-                                     rast=self.rast, mask_grads=True, sync=False, overflow_out=overflow)
+        val, _ = loss_and_grads_device(g, cam, target, LossConfig(lambda_ssim=self.cfg.lambda_ssim),
+                                       rast=self.rast, mask_grads=True, sync=False, overflow_out=overflow,
+                                       grads_out=self._bucket_out(), accumulate=True, mask_logit=True)
+        return val
 
     def step(self, cams, targets, rank: int = 0, world: int = 1, apply: bool = True) -> float:
         """One step over all views (this rank renders its round-robin share);
@@ -87,14 +105,7 @@ class SoftPruneTrainer:
         ovf = None if self.grad_fn is not None else torch.zeros((len(mine), 2), dtype=torch.int64,
                                                                 device=self.device)
         for j, v in enumerate(mine):
-            val, gr = self._view_grads(g, cams[v], targets[v], None if ovf is None else ovf[j])
-            loss_sum += val
-            d_mp = gr.pop("prim_mask")
-            d_ml = gr.pop("lobe_mask")
-            gr.pop("grad2d", None)
-            self.bucket.add_(gr)
-            self.bucket.view("prim_logit").add_(d_mp * m_p * (1 - m_p))
-            self.bucket.view("lobe_logit").add_(d_ml * m_l * (1 - m_l))
+            loss_sum += self._view_grads(g, cams[v], targets[v], None if ovf is None else ovf[j])
         if ovf is not None:
             # some view outgrew its capacity: size it and redo the step (on every
             # rank together, so the collectives below stay matched)

@@ -72,3 +72,31 @@ def test_step_redoes_views_that_outgrow_capacity():
     assert out[0][0] == pytest.approx(out[1][0], rel=1e-6)
     for k in out[0][1]:
         np.testing.assert_allclose(out[0][1][k].cpu().numpy(), out[1][1][k].cpu().numpy(), rtol=1e-4, atol=1e-7)
+
+
+def test_backward_accumulate_and_mask_logit_flags():
+    """SGS_GRADS_ACCUMULATE adds into the outputs; SGS_GRADS_MASK_LOGIT takes
+    the mask gradients through the sigmoid (x m (1 - m))."""
+    from paper_2509_07021_b200.rasterizer import GRAD_FIELDS, GaussianTensors, Rasterizer
+    scene, cams, targets = _setup(n=3000, views=1)
+    g = GaussianTensors.from_arrays(scene)
+    g.prim_mask = torch.sigmoid(torch.as_tensor(scene.extra["prim_logit"], device="cuda")).float().contiguous()
+    g.lobe_mask = torch.sigmoid(torch.as_tensor(scene.extra["lobe_logit"], device="cuda")).float().contiguous()
+    rast = Rasterizer()
+    fr = rast.forward(g, cams[0])
+    dimg = torch.randn_like(fr.img)
+    ref = rast.backward(g, fr, dimg, mask_grads=True)
+    acc = {f: torch.full_like(ref[f], 0.5) for f in GRAD_FIELDS + ("lobe_mask", "prim_mask")}
+    # (float4 quaternion rows need 16-byte alignment; fresh torch allocations have it)
+    rast.backward(g, fr, dimg, mask_grads=True, out=acc, accumulate=True, mask_logit=True)
+    rast.backward(g, fr, dimg, mask_grads=True, out=acc, accumulate=True, mask_logit=True)
+    # the raster's float atomics sum in a different order on every call
+    for f in GRAD_FIELDS:
+        want = 0.5 + 2 * ref[f]
+        assert torch.allclose(acc[f], want, rtol=1e-4, atol=1e-5 * float(ref[f].abs().max())), f
+    for f in ("lobe_mask", "prim_mask"):
+        m = getattr(g, f)
+        want = 0.5 + 2 * ref[f] * m * (1 - m)
+        assert torch.allclose(acc[f], want, rtol=1e-4, atol=1e-5 * float(ref[f].abs().max())), f
+    with pytest.raises(ValueError):
+        rast.backward(g, fr, dimg, accumulate=True)
