@@ -27,109 +27,119 @@
 namespace sgs {
 
 // ---------------------------------------------------------------- scan (u64)
-// offsets[r] = sum_{r' < r} tiles_touched[perm ? perm[r'] : r'] ; totals -> counters
-constexpr int kScanItems = 2048;  // per CTA (256 threads x 8)
+// offsets[r] = sum_{r' < r} tiles_touched[perm ? perm[r'] : r'] ; totals -> counters.
+// One kernel, decoupled look-back: partitions of kScanItems ranks are claimed
+// in order from a ticket, each publishes its sum, then its inclusive prefix
+// once warp 0 has summed the predecessors' published values 32 at a time.
+constexpr int kScanThreads = 256, kScanPer = 8;
+constexpr int kScanItems = kScanThreads * kScanPer;  // 2048 ranks per partition
+constexpr unsigned long long kScanAgg = 1ull << 62, kScanInc = 2ull << 62, kScanVal = (1ull << 62) - 1;
 
 __device__ __forceinline__ uint32_t scan_load(const uint32_t* tt, const uint32_t* perm, uint32_t r) {
   return tt[perm ? perm[r] : r];
 }
 
-__global__ void __launch_bounds__(256) scan_reduce(const uint32_t* __restrict__ tt, const uint32_t* __restrict__ perm,
-                                                   uint32_t n, unsigned long long* __restrict__ block_sums) {
-  __shared__ unsigned long long warp_sum[8];
-  const uint32_t b0 = blockIdx.x * kScanItems;
-  unsigned long long s = 0;
-  for (int i = threadIdx.x; i < kScanItems; i += 256) {
-    uint32_t r = b0 + i;
-    if (r < n) s += scan_load(tt, perm, r);
-  }
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if ((threadIdx.x & 31) == 0) warp_sum[threadIdx.x >> 5] = s;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long t = 0;
-    for (int w = 0; w < 8; ++w) t += warp_sum[w];
-    block_sums[blockIdx.x] = t;
-  }
-}
-
-// single CTA: exclusive scan of block sums; writes E, n_sort, overflow
-__global__ void __launch_bounds__(1024) scan_blocks(unsigned long long* block_sums, uint32_t nb, uint32_t cap,
-                                                    Counters* ctr) {
-  __shared__ unsigned long long warp_tot[32];
-  __shared__ unsigned long long carry;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (uint32_t base = 0; base < nb; base += 1024) {
-    uint32_t i = base + threadIdx.x;
-    unsigned long long v = i < nb ? block_sums[i] : 0ull, x = v;
+__global__ void __launch_bounds__(kScanThreads) scan_onepass(const uint32_t* __restrict__ tt,
+                                                            const uint32_t* __restrict__ perm, uint32_t n,
+                                                            uint32_t cap, unsigned long long* status,
+                                                            uint32_t* ticket,
+                                                            unsigned long long* __restrict__ offsets,
+                                                            Counters* ctr) {
+  __shared__ unsigned long long warp_tot[kScanThreads / 32];
+  __shared__ unsigned long long s_excl;
+  __shared__ uint32_t s_part;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const uint32_t nparts = (n + kScanItems - 1) / kScanItems;
+  for (;;) {
+    if (t == 0) s_part = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const uint32_t part = s_part;
+    if (part >= nparts) return;
+    // each thread owns kScanPer consecutive ranks
+    const uint32_t r0 = part * kScanItems + (uint32_t)t * kScanPer;
+    uint32_t v[kScanPer];
+    unsigned long long sum = 0;
+#pragma unroll
+    for (int k = 0; k < kScanPer; ++k) {
+      v[k] = r0 + k < n ? scan_load(tt, perm, r0 + k) : 0u;
+      sum += v[k];
+    }
+    unsigned long long x = sum;
+#pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
       if (lane >= o) x += y;
     }
     if (lane == 31) warp_tot[w] = x;
     __syncthreads();
-    unsigned long long pre = carry;
-    for (int k = 0; k < w; ++k) pre += warp_tot[k];
-    if (i < nb) block_sums[i] = pre + x - v;
+    unsigned long long pre = 0, agg = 0;
+#pragma unroll
+    for (int k = 0; k < kScanThreads / 32; ++k) {
+      pre += k < w ? warp_tot[k] : 0ull;
+      agg += warp_tot[k];
+    }
+    if (w == 0) {
+      unsigned long long excl = 0;
+      if (part == 0) {
+        if (lane == 0) atomicExch(&status[0], kScanInc | agg);
+      } else {
+        if (lane == 0) atomicExch(&status[part], kScanAgg | agg);
+        int64_t p = (int64_t)part - 1;
+        for (;;) {
+          const int64_t q = p - lane;
+          unsigned long long sv = kScanInc + 0ull;
+          if (q >= 0) sv = *reinterpret_cast<volatile unsigned long long*>(&status[q]);
+          const unsigned long long flag = sv & ~kScanVal;
+          const uint32_t inc = __ballot_sync(0xffffffffu, flag == kScanInc);
+          const uint32_t empty = __ballot_sync(0xffffffffu, flag == 0);
+          // lanes up to and including the nearest inclusive prefix must all be published
+          const uint32_t need = inc ? (inc & (0u - inc)) * 2u - 1u : 0xffffffffu;
+          if (empty & need) continue;
+          unsigned long long part_sum = (need >> lane) & 1u ? (sv & kScanVal) : 0ull;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) part_sum += __shfl_xor_sync(0xffffffffu, part_sum, o);
+          excl += part_sum;
+          if (inc) break;
+          p -= 32;
+        }
+        if (lane == 0) atomicExch(&status[part], kScanInc | (excl + agg));
+      }
+      if (lane == 0) s_excl = excl;
+    }
     __syncthreads();
-    if (threadIdx.x == 1023) carry = pre + x;
+    unsigned long long o = s_excl + pre + x - sum;
+#pragma unroll
+    for (int k = 0; k < kScanPer; ++k) {
+      if (r0 + k < n) offsets[r0 + k] = o;
+      o += v[k];
+    }
+    if (part + 1 == nparts && t == kScanThreads - 1) {
+      const unsigned long long total = o;  // the last thread ends at the grand total
+      ctr->n_bin = total;
+      ctr->capacity = cap;
+      ctr->overflow = total > cap ? 1ull : 0ull;
+      ctr->n_sort = (uint32_t)(total < cap ? total : cap);
+    }
     __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    unsigned long long total = carry;
-    ctr->n_bin = total;
-    ctr->capacity = cap;
-    ctr->overflow = total > cap ? 1ull : 0ull;
-    ctr->n_sort = (uint32_t)(total < cap ? total : cap);
-  }
-}
-
-__global__ void __launch_bounds__(256) scan_down(const uint32_t* __restrict__ tt, const uint32_t* __restrict__ perm,
-                                                 uint32_t n, const unsigned long long* __restrict__ block_sums,
-                                                 unsigned long long* __restrict__ offsets) {
-  __shared__ unsigned long long warp_tot[8];
-  const uint32_t b0 = blockIdx.x * kScanItems;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  // each thread owns 8 consecutive items
-  uint32_t v[8];
-  unsigned long long s = 0;
-  for (int k = 0; k < 8; ++k) {
-    uint32_t r = b0 + threadIdx.x * 8 + k;
-    v[k] = r < n ? scan_load(tt, perm, r) : 0u;
-    s += v[k];
-  }
-  unsigned long long x = s;
-  for (int o = 1; o < 32; o <<= 1) {
-    unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) warp_tot[w] = x;
-  __syncthreads();
-  unsigned long long pre = block_sums[blockIdx.x];
-  for (int k = 0; k < w; ++k) pre += warp_tot[k];
-  pre += x - s;
-  for (int k = 0; k < 8; ++k) {
-    uint32_t r = b0 + threadIdx.x * 8 + k;
-    if (r < n) offsets[r] = pre;
-    pre += v[k];
   }
 }
 
 __global__ void set_count(uint32_t* p, uint32_t v) { *p = v; }
 
 static int launch_scan(const uint32_t* tt, const uint32_t* perm, uint32_t n, uint32_t cap,
-                       unsigned long long* block_sums,
-                       unsigned long long* offsets, Counters* ctr, cudaStream_t st) {
-  uint32_t nb = (n + kScanItems - 1) / kScanItems;
-  if (nb == 0) nb = 1;
-  scan_reduce<<<nb, 256, 0, st>>>(tt, perm, n, block_sums);
-  SGS_LAUNCH_CHECK("scan_reduce");
-  scan_blocks<<<1, 1024, 0, st>>>(block_sums, nb, cap, ctr);
-  SGS_LAUNCH_CHECK("scan_blocks");
-  scan_down<<<nb, 256, 0, st>>>(tt, perm, n, block_sums, offsets);
-  SGS_LAUNCH_CHECK("scan_down");
+                       unsigned long long* status, unsigned long long* offsets, Counters* ctr, cudaStream_t st) {
+  const uint32_t nparts = (n + kScanItems - 1) / kScanItems;
+  if (nparts == 0) {
+    SGS_CUDA(cudaMemsetAsync(&ctr->n_bin, 0, sizeof(ctr->n_bin), st));
+    SGS_CUDA(cudaMemsetAsync(&ctr->n_sort, 0, sizeof(ctr->n_sort), st));
+    return SGS_OK;
+  }
+  SGS_CUDA(cudaMemsetAsync(status, 0, (size_t)nparts * 8, st));
+  SGS_CUDA(cudaMemsetAsync(&ctr->part_counter[kScanTicket], 0, 4, st));
+  scan_onepass<<<persistent_grid(nparts, 1, 8), kScanThreads, 0, st>>>(tt, perm, n, cap, status,
+                                                                        &ctr->part_counter[kScanTicket], offsets,
+                                                                        ctr);
+  SGS_LAUNCH_CHECK("scan_onepass");
   return SGS_OK;
 }
 
@@ -346,7 +356,7 @@ int launch_bin(const SgsCam& cam, const sgs_workspace* ws, const Layout& lo, cud
   const uint32_t n = (uint32_t)lo.n;
   const uint32_t cap = (uint32_t)lo.cap;
   unsigned long long* offsets = at<unsigned long long>(ws, lo.offsets);
-  unsigned long long* block_sums = at<unsigned long long>(ws, lo.scan_blocks);
+  unsigned long long* status64 = at<unsigned long long>(ws, lo.scan_blocks);  // scan look-back status
   if (lo.sort_mode == SGS_SORT_DEPTH_FIRST) {
     uint32_t* dkey = at<uint32_t>(ws, lo.depth_key);
     uint32_t* ka = at<uint32_t>(ws, lo.dkey_alt);
@@ -365,14 +375,14 @@ int launch_bin(const SgsCam& cam, const sgs_workspace* ws, const Layout& lo, cud
                                                         true, RsRangeOut{nullptr, 0}, 0, false, true);
     if (rc) return rc;
     const uint32_t* perm = alt ? ib : ia;
-    rc = launch_scan(at<uint32_t>(ws, lo.super_touched), perm, n, cap, block_sums, offsets, ctr, st);
+    rc = launch_scan(at<uint32_t>(ws, lo.super_touched), perm, n, cap, status64, offsets, ctr, st);
     if (rc) return rc;
     // keys (super_id << 16 | 16-bit tile mask), sorted on the super id bits only
     const int sbits = tile_sort_bits(lo.n_super);
     if (sbits <= 9) return bin_entries<uint32_t, kTileSortIPT, 9, true>(cam, ws, lo, perm, sbits, 16, st);
     return bin_entries<uint32_t, kTileSortIPT, 8, true>(cam, ws, lo, perm, sbits, 16, st);
   }
-  int rc = launch_scan(at<uint32_t>(ws, lo.tiles_touched), nullptr, n, cap, block_sums, offsets, ctr, st);
+  int rc = launch_scan(at<uint32_t>(ws, lo.tiles_touched), nullptr, n, cap, status64, offsets, ctr, st);
   if (rc) return rc;
   return bin_entries<unsigned long long, kKey64SortIPT, 8, false>(cam, ws, lo, nullptr,
                                                                   32 + tile_sort_bits(lo.n_tiles), 32, st);

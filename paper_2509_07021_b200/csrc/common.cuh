@@ -28,6 +28,7 @@ constexpr int kDepthSortIPT = SGS_DEPTH_SORT_IPT;
 // which leave room for co-resident rasters, measured no faster)
 constexpr int kDepthSortThreads = SGS_DEPTH_SORT_THREADS;
 constexpr int kKey64SortIPT = 6;
+constexpr int kScanTicket = 15;       // Counters::part_counter slot of the offsets scan
 constexpr int kRowSpansPerPrim = 8;   // row-span store capacity, u16 entries per primitive
 constexpr uint32_t kNoRows = 0xffffffffu;  // row_off of a primitive whose spans are not stored
 constexpr uint32_t kMaxEntries = (1u << 30) - 1;  // look-back status packs 30-bit counts
@@ -65,7 +66,7 @@ struct Counters {
   unsigned long long n_bin;          // entries the binning sorts (super-tile entries in depth-first mode)
   uint32_t n_sort;                   // min(E, capacity): items the tile sort processes
   uint32_t n_depth;                  // primitives entering the depth sort
-  uint32_t part_counter[16];         // onesweep partition tickets, one per pass
+  uint32_t part_counter[16];         // onesweep partition tickets, one per pass; [kScanTicket] the offsets scan
   uint32_t row_alloc;                // row-span store: entries handed out by the preprocess
   uint32_t pad1[13];
 };
