@@ -38,10 +38,10 @@ UNIT = "frames/s"
 WORKLOAD = "configs[2]: 1,000,000 Gaussians (64 clusters), 3 SG lobes, 1920x1080, FoV 60"
 # libsgs kernels per forward frame (depth-first mode, 1080p): preprocess (also
 # accumulates the depth-digit histograms); set_count, histogram scan, 4 onesweep
-# passes (depth sort); 3 offsets-scan kernels; ranges_init, emit_entries (also the
-# cell histogram); histogram scan + 1 onesweep pass (super-tile sort + ranges);
-# ranges_fix; cell_order, raster_fwd
-KERNELS_PER_FRAME = 17
+# passes (depth sort); the one-pass offsets scan; ranges_init, emit_entries (also
+# the cell histogram); histogram scan + 1 onesweep pass (super-tile sort +
+# ranges); ranges_fix; cell_order, raster_fwd (profiles/r01_launches_v7.csv)
+KERNELS_PER_FRAME = 15
 
 
 def parse():
