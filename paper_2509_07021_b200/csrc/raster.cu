@@ -42,6 +42,28 @@ __device__ __forceinline__ float rcp_approx(float x) {
   return y;
 }
 
+// Eight per-lane values summed over the warp by recursive halving (4 + 2 +
+// 1 + 1 + 1 = 9 shuffles instead of 8 x 5).  Lane l ends with the total of
+// value reduce8_index(l) (the four lanes l & ~3 .. l | 3 hold the same one).
+__device__ __forceinline__ float warp_reduce8(const float v[8], int lane) {
+  const bool u16 = lane & 16, u8 = lane & 8, u4 = lane & 4;
+  float a[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    a[j] = (u16 ? v[j + 4] : v[j]) + __shfl_xor_sync(0xffffffffu, u16 ? v[j] : v[j + 4], 16);
+  float b[2];
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
+    b[j] = (u8 ? a[j + 2] : a[j]) + __shfl_xor_sync(0xffffffffu, u8 ? a[j] : a[j + 2], 8);
+  float c = (u4 ? b[1] : b[0]) + __shfl_xor_sync(0xffffffffu, u4 ? b[0] : b[1], 4);
+  c += __shfl_xor_sync(0xffffffffu, c, 2);
+  return c + __shfl_xor_sync(0xffffffffu, c, 1);
+}
+
+__device__ __forceinline__ int reduce8_index(int lane) {
+  return ((lane & 16) ? 4 : 0) + ((lane & 8) ? 2 : 0) + ((lane & 4) ? 1 : 0);
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -372,6 +394,8 @@ __global__ void __launch_bounds__(kFwdThreads, SGS_FWD_MIN_BLOCKS) raster_fwd_ke
                                                                  float* __restrict__ weight_sums,
                                                                  unsigned long long* __restrict__ pair_count) {
   __shared__ std::conditional_t<kImportance || kTrack, Stage<kFwdBuf>, StageNoIds<kFwdBuf>> s;
+  __shared__ float s_wp[kImportance ? kFwdThreads / 32 : 1][kImportance ? kFwdBuf : 1];
+  static_assert(!kImportance || kVoteEvery == 8, "importance sums reduce one 8-record vote group at a time");
   __shared__ uint32_t s_kend;
 
   int tx, ty;
@@ -434,6 +458,7 @@ __global__ void __launch_bounds__(kFwdThreads, SGS_FWD_MIN_BLOCKS) raster_fwd_ke
     constexpr bool kClamp = decltype(clamp_tag)::value;
     for (int k = 0; k < nb_pad; k += kVoteEvery) {
       if (!warp_any(T2.x > 0.0f || T2.y > 0.0f)) break;
+      float wv[kImportance ? kVoteEvery : 1];  // importance: this thread's weight per group record
 #pragma unroll
       for (int j = 0; j < kVoteEvery; ++j) {
         const int kk = k + j;
@@ -455,21 +480,31 @@ __global__ void __launch_bounds__(kFwdThreads, SGS_FWD_MIN_BLOCKS) raster_fwd_ke
             nc0 += (uint32_t)k0;
             nc1 += (uint32_t)k1;
           }
-          if constexpr (kImportance) {
-            const float w0 = w.x, w1 = w.y;
-            if (warp_any(w0 != 0.0f || w1 != 0.0f)) {
-              const float ws = warp_sum(w0 + w1);
-              if (lane == 0 && ws != 0.0f) atomicAdd(&weight_sums[s.id[kk]], ws);
-            }
-          }
+          if constexpr (kImportance) wv[j] = w.x + w.y;
         }
+      }
+      if constexpr (kImportance) {
+        // the group's per-record weight sums over the warp, all eight at once
+        const float tot = warp_reduce8(wv, lane);
+        if ((lane & 3) == 0) s_wp[wq][k + reduce8_index(lane)] = tot;
       }
     }
     };
+    if constexpr (kImportance) {  // this warp's per-record weight sums of the batch
+      for (int i = lq; i < nb_pad; i += 32) s_wp[wq][i] = 0.0f;
+      __syncwarp();
+    }
     if (batch_clamp)
       run_batch(std::true_type{});
     else
       run_batch(std::false_type{});
+    if constexpr (kImportance) {  // one atomic per (record, tile): the four warps' sums
+      __syncthreads();
+      for (int i = t; i < nb; i += kFwdThreads) {
+        const float x = (s_wp[0][i] + s_wp[1][i]) + (s_wp[2][i] + s_wp[3][i]);
+        if (x != 0.0f) atomicAdd(&weight_sums[s.id[i]], x);
+      }
+    }
     if constexpr (kTrack) {
       // the zero-opacity padding records count as kept for pixels still alive
       const uint32_t lim = hits_before + (uint32_t)nb;
