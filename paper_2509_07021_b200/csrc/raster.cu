@@ -64,11 +64,6 @@ __device__ __forceinline__ int reduce8_index(int lane) {
   return ((lane & 16) ? 4 : 0) + ((lane & 8) ? 2 : 0) + ((lane & 4) ? 1 : 0);
 }
 
-__device__ __forceinline__ float warp_sum(float v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
 
 struct ListArgs {
   const uint2* ranges;      // per cell [start, end) into vals
