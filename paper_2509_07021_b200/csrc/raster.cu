@@ -241,10 +241,16 @@ __device__ __forceinline__ void load_chunk(ChunkRegs<CPT>& r, uint32_t lo, uint3
   }
 }
 
-// stage_append on a register chunk (same result).
+// stage_append on a register chunk (same records), each staged in the
+// forward raster's tile-local form: geo = (c1, c2, log2 o_eff, -) with the
+// eigen-form offsets c1 = -(e1 mx' + e2 my'), c2 = e4 mx' - e3 my' of the
+// mean relative to the tile origin (mx' = mx - ox exactly), so a pixel at
+// tile-local (lx, ly) has t1 = e1 lx + e2 ly + c1, t2 = e3 ly - e4 lx + c2.
+// A listed record reaches the tile, so |t| stays small there and the offsets
+// cost no precision (|c| <~ |t| + |e| 16).
 template <int THREADS, int CPT, bool kFilter, class S>
 __device__ __forceinline__ int stage_append_regs(const ChunkRegs<CPT>& r, uint32_t local_bit, const ListArgs& a,
-                                                 int base, S& s) {
+                                                 int base, S& s, float ox, float oy) {
   constexpr int W = THREADS / 32;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const uint32_t lt = (1u << lane) - 1u;
@@ -270,8 +276,10 @@ __device__ __forceinline__ int stage_append_regs(const ChunkRegs<CPT>& r, uint32
     if ((bal[h] >> lane) & 1u) {
       const int pos = base + pre + __popc(bal[h] & lt);
       const uint32_t g = r.val[h];
-      s.geo[pos] = a.geo[g];
-      s.con[pos] = a.eig[g];
+      const float4 G = a.geo[g], E = a.eig[g];
+      const float mx = G.x - ox, my = G.y - oy;
+      s.geo[pos] = make_float4(fmaf(-E.x, mx, -(E.y * my)), fmaf(E.w, mx, -(E.z * my)), G.z, 0.0f);
+      s.con[pos] = E;
       s.col[pos] = a.col[g];
       if constexpr (S::kIds) {
         s.id[pos] = g;
@@ -405,7 +413,9 @@ __global__ void __launch_bounds__(kFwdThreads, SGS_FWD_MIN_BLOCKS) raster_fwd_ke
   const int py0 = ty * SGS_TILE + (wq >> 1) * 8 + 2 * (lq >> 3);  // rows py0 and py0 + 1
   const bool in0 = px < cam.width && py0 < cam.height;
   const bool in1 = px < cam.width && py0 + 1 < cam.height;
-  const float fx = (float)px + 0.5f, fy0 = (float)py0 + 0.5f;
+  // pixel centres relative to the tile origin (records are staged in that frame)
+  const float ox = (float)(tx * SGS_TILE), oy = (float)(ty * SGS_TILE);
+  const float lx = (float)(px - tx * SGS_TILE) + 0.5f, ly0 = (float)(py0 - ty * SGS_TILE) + 0.5f;
   const uint2 rg = la.ranges[list_cell(kFilter, tx, ty, tile, la.super_x)];
   const uint32_t cs = rg.x, ce = rg.y > rg.x ? rg.y : rg.x;
 
@@ -413,7 +423,7 @@ __global__ void __launch_bounds__(kFwdThreads, SGS_FWD_MIN_BLOCKS) raster_fwd_ke
   // image start terminated)
   float2 T2 = make_float2(in0 ? 1.0f : -1.0f, in1 ? 1.0f : -1.0f);
   float2 Cr = make_float2(0.0f, 0.0f), Cg = Cr, Cb = Cr;
-  const float2 fyv = make_float2(fy0, fy0 + 1.0f);  // the two pixels' row centres
+  const float2 lyv = make_float2(ly0, ly0 + 1.0f);  // the two pixels' tile-local row centres
   uint32_t nc0 = 0, nc1 = 0, reached = 0, kend = 0, hits_before = 0;
   if (kTrack && t == 0) s_kend = 0;
 
@@ -428,7 +438,7 @@ __global__ void __launch_bounds__(kFwdThreads, SGS_FWD_MIN_BLOCKS) raster_fwd_ke
       const uint32_t chi = cb + kFwdChunk < ce ? cb + kFwdChunk : ce;
       if (!have_pf) load_chunk<kFwdThreads, kFwdCPT, kFilter>(pf, cb, chi, la);
       have_pf = false;
-      nb += stage_append_regs<kFwdThreads, kFwdCPT, kFilter>(pf, lbit, la, nb, s);
+      nb += stage_append_regs<kFwdThreads, kFwdCPT, kFilter>(pf, lbit, la, nb, s, ox, oy);
       cb = chi;
     }
     if (nb == 0) break;
@@ -457,13 +467,10 @@ __global__ void __launch_bounds__(kFwdThreads, SGS_FWD_MIN_BLOCKS) raster_fwd_ke
 #pragma unroll
       for (int j = 0; j < kVoteEvery; ++j) {
         const int kk = k + j;
-        const float4 G = s.geo[kk];  // (mx, my, log2 o_eff, -)
+        const float4 G = s.geo[kk];  // (c1, c2, log2 o_eff, -): tile-local form
         const float4 E = s.con[kk];  // scaled eigen form (s1 ux, s1 uy, s2 ux, s2 uy)
-        const float dx = fx - G.x;
-        const float2 dy = __fadd2_rn(fyv, f2(-G.y));
-        const float e1dx = E.x * dx, e3dx = E.w * dx;
-        const float2 t1 = __ffma2_rn(f2(E.y), dy, f2(e1dx));
-        const float2 t2 = __ffma2_rn(f2(E.z), dy, f2(-e3dx));
+        const float2 t1 = __ffma2_rn(f2(E.y), lyv, f2(fmaf(E.x, lx, G.x)));
+        const float2 t2 = __ffma2_rn(f2(E.z), lyv, f2(fmaf(-E.w, lx, G.y)));
         const float2 p = __ffma2_rn(neg2(t1), t1, __ffma2_rn(neg2(t2), t2, f2(G.z)));
         if (kCount && kk < nb) reached += (uint32_t)(T2.x > 0.0f) + (uint32_t)(T2.y > 0.0f);
         {
