@@ -24,7 +24,10 @@ __device__ __forceinline__ void warp_count(unsigned long long* ctr, bool pred) {
 // slot.  The spans are sgs_super_row_spans -- the definition the emission and
 // the CPU restatement use -- so the counts agree bit for bit.
 template <int kL>
-__global__ void __launch_bounds__(256, 3) preprocess_kernel(sgs_params P, SgsCam cam, float4* __restrict__ rec_geo,
+#ifndef SGS_PRE_CTAS
+#define SGS_PRE_CTAS 3
+#endif
+__global__ void __launch_bounds__(256, SGS_PRE_CTAS) preprocess_kernel(sgs_params P, SgsCam cam, float4* __restrict__ rec_geo,
                                                          float4* __restrict__ rec_con, float4* __restrict__ rec_col,
                                                          float4* __restrict__ rec_span,
                                                          float4* __restrict__ rec_eig,
@@ -264,7 +267,7 @@ int launch_project_records(const sgs_params& P, const SgsCam& cam, float* out, c
 int launch_preprocess(const sgs_params& P, const SgsCam& cam, const sgs_workspace* ws, const Layout& lo,
                       cudaStream_t st) {
   Counters* ctr = at<Counters>(ws, lo.counters);
-  int grid = persistent_grid((uint64_t)P.n, 256, 3);  // one wave at 3 resident CTAs per SM
+  int grid = persistent_grid((uint64_t)P.n, 256, SGS_PRE_CTAS);  // one wave of resident CTAs
 #define SGS_PRE(KL)                                                                                             \
   preprocess_kernel<KL><<<grid, 256, 0, st>>>(P, cam, at<float4>(ws, lo.rec_geo), at<float4>(ws, lo.rec_con),    \
                                               at<float4>(ws, lo.rec_col), at<float4>(ws, lo.rec_span),           \

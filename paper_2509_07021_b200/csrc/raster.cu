@@ -463,7 +463,7 @@ __global__ void __launch_bounds__(kFwdThreads, SGS_FWD_MIN_BLOCKS) raster_fwd_ke
     constexpr bool kClamp = decltype(clamp_tag)::value;
     for (int k = 0; k < nb_pad; k += kVoteEvery) {
       if (!warp_any(T2.x > 0.0f || T2.y > 0.0f)) break;
-      float wv[kImportance ? kVoteEvery : 1];  // importance: this thread's weight per group record
+      [[maybe_unused]] float wv[kImportance ? kVoteEvery : 1];  // importance: this thread's weight per group record
 #pragma unroll
       for (int j = 0; j < kVoteEvery; ++j) {
         const int kk = k + j;
