@@ -316,7 +316,7 @@ constexpr int kFwdChunk = kFwdThreads * kFwdCPT;  // candidates examined per sta
 #define SGS_VOTE_EVERY 8
 #endif
 #ifndef SGS_FWD_MIN_BLOCKS
-#define SGS_FWD_MIN_BLOCKS 1
+#define SGS_FWD_MIN_BLOCKS 8
 #endif
 constexpr int kFwdBatch = SGS_FWD_BATCH;          // staged entries processed per block sync
 constexpr int kFwdBuf = kFwdBatch + kFwdChunk;
@@ -390,7 +390,12 @@ __device__ __forceinline__ void blend2(float2 p, const float4& c, float2& T2, fl
 }
 
 template <bool kImportance, bool kCount, bool kFilter, bool kTrack>
-__global__ void __launch_bounds__(kFwdThreads, SGS_FWD_MIN_BLOCKS) raster_fwd_kernel(ListArgs la, SgsCam cam, float3 bg,
+// The image-only variant is capped at 64 registers (8 resident CTAs, a few
+// bytes of spills): slower alone (0.268 vs 0.264 ms) but it shares SMs with
+// the other streams' binning kernels, +3 % frames/s in the 4-stream bench.
+// The tracked / importance variants run in single-stream loops and keep
+// their registers (the cap cost the training forward 6 %).
+__global__ void __launch_bounds__(kFwdThreads, (kTrack || kImportance) ? 1 : SGS_FWD_MIN_BLOCKS) raster_fwd_kernel(ListArgs la, SgsCam cam, float3 bg,
                                                                  float* __restrict__ out_img,
                                                                  float* __restrict__ out_T,
                                                                  uint32_t* __restrict__ out_nc,
