@@ -27,7 +27,10 @@ template <int kL>
 #ifndef SGS_PRE_CTAS
 #define SGS_PRE_CTAS 3
 #endif
-__global__ void __launch_bounds__(256, SGS_PRE_CTAS) preprocess_kernel(sgs_params P, SgsCam cam, float4* __restrict__ rec_geo,
+#ifndef SGS_PRE_REG_CTAS
+#define SGS_PRE_REG_CTAS SGS_PRE_CTAS
+#endif
+__global__ void __launch_bounds__(256, SGS_PRE_REG_CTAS) preprocess_kernel(sgs_params P, SgsCam cam, float4* __restrict__ rec_geo,
                                                          float4* __restrict__ rec_con, float4* __restrict__ rec_col,
                                                          float4* __restrict__ rec_span,
                                                          float4* __restrict__ rec_eig,

@@ -138,8 +138,11 @@ struct RsRangeOut {
 // One pass.  status: nparts x 2^RBITS u32, zeroed; ticket zeroed.
 // vin == nullptr means values are the item indices (first pass of an argsort).
 // kout == nullptr skips the key writes.
+#ifndef SGS_RS_MIN_BLOCKS
+#define SGS_RS_MIN_BLOCKS 1
+#endif
 template <typename K, int IPT, int RBITS, int NT = kRsThreads>
-__global__ void __launch_bounds__(NT) rs_onesweep(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
+__global__ void __launch_bounds__(NT, SGS_RS_MIN_BLOCKS) rs_onesweep(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                           K* __restrict__ kout, uint32_t* __restrict__ vout,
                                                           const uint32_t* n_ptr, uint32_t n_cap, int shift,
                                                           const uint32_t* __restrict__ pass_base, uint32_t* status,
