@@ -331,17 +331,31 @@ class Rasterizer:
         aligned); with ``accumulate`` the gradients are added into them, and
         with ``mask_logit`` the mask gradients are taken with respect to the
         logits whose sigmoids are the masks (x m (1 - m))."""
+        grad2d = self.backward_raster(g, frame, dimg)
+        out = self.backward_params(g, frame.cam, grad2d, mask_grads=mask_grads, out=out,
+                                   accumulate=accumulate, mask_logit=mask_logit)
+        out["grad2d"] = grad2d
+        return out
+
+    def backward_raster(self, g: GaussianTensors, frame: Frame, dimg: torch.Tensor) -> torch.Tensor:
+        """K6 alone: the (N, 9) per-primitive image-space partials for dL/dimg."""
         dimg = dimg.to(device=self.device, dtype=torch.float32).contiguous()
         if frame.ncontrib is None:
             raise ValueError("frame was rendered with track=False; the backward needs track=True")
         if tuple(dimg.shape) != tuple(frame.img.shape):
             raise ValueError(f"dimg shape {tuple(dimg.shape)} != image {tuple(frame.img.shape)}")
-        stream = C.c_void_p(_stream_ptr())
         c_bg = (C.c_float * 3)(*frame.bg)
         grad2d = torch.empty((g.n, 9), dtype=torch.float32, device=self.device)
         _ffi.call("sgs_raster_backward", C.byref(frame.cam), c_bg, C.byref(frame.ws.desc),
                   _ptr(frame.img), _ptr(frame.final_T), _ptr(frame.ncontrib), _ptr(dimg),
-                  _ptr(grad2d), stream)
+                  _ptr(grad2d), C.c_void_p(_stream_ptr()))
+        return grad2d
+
+    def backward_params(self, g: GaussianTensors, c_cam, grad2d: torch.Tensor, mask_grads: bool = True,
+                        out: dict | None = None, accumulate: bool = False,
+                        mask_logit: bool = False) -> dict:
+        """K7 alone: parameter (and mask) gradients from K6's partials, on the
+        current stream (``c_cam`` = the frame's sgs_camera)."""
         if out is None:
             if accumulate:
                 raise ValueError("accumulate=True needs the output tensors")
@@ -364,9 +378,8 @@ class Rasterizer:
         cg.lobe_mask = _ptr(out.get("lobe_mask")) if mask_grads else None
         cg.prim_mask = _ptr(out.get("prim_mask")) if mask_grads else None
         params = g.c_params()
-        _ffi.call("sgs_preprocess_backward", C.byref(params), C.byref(frame.cam), _ptr(grad2d),
-                  C.byref(cg), stream)
-        out["grad2d"] = grad2d
+        _ffi.call("sgs_preprocess_backward", C.byref(params), C.byref(c_cam), _ptr(grad2d),
+                  C.byref(cg), C.c_void_p(_stream_ptr()))
         return out
 
     # ----------------------------------------------------------------- exports

@@ -42,7 +42,11 @@ class SoftPruneTrainer:
     data-parallel training step over this rank's share of the views."""
 
     def __init__(self, arrays, prim_logit, lobe_logit, cfg: TrainConfig = TrainConfig(),
-                 device="cuda", group=None, grad_fn=None):
+                 device="cuda", group=None, grad_fn=None, streams: int = 3):
+        """``streams``: views of a step in flight at once on this many CUDA
+        streams (each with its own workspace); their parameter backwards
+        (K7, which add into the shared gradient bucket) run in view order on
+        one more stream."""
         self.device = torch.device(device)
         self.cfg = cfg
         self.group = group
@@ -56,6 +60,9 @@ class SoftPruneTrainer:
         self.bucket = GradBucket(shapes, self.device)
         self.grad_fn = grad_fn
         self.rast = None if grad_fn is not None else Rasterizer(device=self.device)
+        self.n_streams = max(1, int(streams)) if grad_fn is None else 1
+        self._streams = ([torch.cuda.Stream(self.device) for _ in range(self.n_streams)],
+                         torch.cuda.Stream(self.device)) if self.n_streams > 1 else None
 
     def masks(self):
         return torch.sigmoid(self.prim_logit), torch.sigmoid(self.lobe_logit)
@@ -92,6 +99,42 @@ class SoftPruneTrainer:
                                        grads_out=self._bucket_out(), accumulate=True, mask_logit=True)
         return val
 
+    def _views_pipelined(self, g: GaussianTensors, cams, targets, mine, ovf):
+        """The step's views on ``n_streams`` streams: forward, loss and raster
+        backward of view j on stream j mod S, then its K7 into the bucket on
+        the accumulation stream in view order (one writer: the bucket update
+        is a plain read-modify-write).  Returns the summed loss (device)."""
+        from .loss import image_loss
+        from .render import LossConfig
+        main = torch.cuda.current_stream(self.device)
+        views, acc = self._streams
+        start = torch.cuda.Event()
+        start.record(main)  # bucket zeroed, masks and overflow slots ready
+        acc.wait_event(start)
+        cfg = LossConfig(lambda_ssim=self.cfg.lambda_ssim)
+        out = self._bucket_out()
+        losses = []
+        for j, v in enumerate(mine):
+            st = views[j % len(views)]
+            st.wait_event(start)
+            with torch.cuda.stream(st):
+                frame = self.rast.forward(g, cams[v], check=False)
+                frame.record_overflow(ovf[j])
+                lo, dimg, _ = image_loss(frame.img, targets[v], cfg, grad="f32")
+                grad2d = self.rast.backward_raster(g, frame, dimg)
+                done = torch.cuda.Event()
+                done.record(st)
+            acc.wait_event(done)
+            grad2d.record_stream(acc)
+            with torch.cuda.stream(acc):
+                self.rast.backward_params(g, frame.cam, grad2d, mask_grads=True, out=out, accumulate=True,
+                                          mask_logit=True)
+            lo.record_stream(main)
+            losses.append(lo[0])
+        for st in views + [acc]:
+            main.wait_stream(st)
+        return torch.stack(losses).sum() if losses else torch.zeros((), dtype=torch.float64, device=self.device)
+
     def step(self, cams, targets, rank: int = 0, world: int = 1, apply: bool = True) -> float:
         """One step over all views (this rank renders its round-robin share);
         returns the global mean loss."""
@@ -104,8 +147,11 @@ class SoftPruneTrainer:
         # tile-entry overflow is checked once per step (no host round trip per view)
         ovf = None if self.grad_fn is not None else torch.zeros((len(mine), 2), dtype=torch.int64,
                                                                 device=self.device)
-        for j, v in enumerate(mine):
-            loss_sum += self._view_grads(g, cams[v], targets[v], None if ovf is None else ovf[j])
+        if self._streams is not None and len(mine) > 1:
+            loss_sum += self._views_pipelined(g, cams, targets, mine, ovf)
+        else:
+            for j, v in enumerate(mine):
+                loss_sum += self._view_grads(g, cams[v], targets[v], None if ovf is None else ovf[j])
         if ovf is not None:
             # some view outgrew its capacity: size it and redo the step (on every
             # rank together, so the collectives below stay matched)
