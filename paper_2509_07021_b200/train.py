@@ -42,7 +42,7 @@ class SoftPruneTrainer:
     data-parallel training step over this rank's share of the views."""
 
     def __init__(self, arrays, prim_logit, lobe_logit, cfg: TrainConfig = TrainConfig(),
-                 device="cuda", group=None, grad_fn=None, streams: int = 3):
+                 device="cuda", group=None, grad_fn=None, streams: int = 4):
         """``streams``: views of a step in flight at once on this many CUDA
         streams (each with its own workspace); their parameter backwards
         (K7, which add into the shared gradient bucket) run in view order on
