@@ -229,13 +229,46 @@ def accumulate_importance(scene, cams, background=(0.0, 0.0, 0.0)) -> np.ndarray
     return accumulate_importance_params(SceneParams.from_scene(scene), cams, background)
 
 
-def accumulate_importance_params(p, cams, background=(0.0, 0.0, 0.0)) -> np.ndarray:
+_SIDE_STREAMS: dict = {}
+
+
+def _side_streams(device, n: int) -> list:
+    key = str(device)
+    have = _SIDE_STREAMS.setdefault(key, [])
+    while len(have) < n:
+        have.append(torch.cuda.Stream(device))
+    return have[:n]
+
+
+def accumulate_importance_params(p, cams, background=(0.0, 0.0, 0.0), streams: int = 4) -> np.ndarray:
+    """render.py:416-428.  The views render concurrently on ``streams`` CUDA
+    streams (the weight sums are atomic adds into one array); tile-entry
+    capacity is checked once for all views, and a pass in which any view
+    outgrew its capacity is redone from zero with the capacity grown."""
     rast = rasterizer()
     g = _upload(p)
-    ws = torch.zeros(g.n, dtype=torch.float32, device=rast.device)
-    for cam in cams:
-        rast.forward(g, cam, _bg(background), weight_sums=ws, track=False)
-    return _to_np64(ws)
+    bg = _bg(background)
+    cams = list(cams)
+    main = torch.cuda.current_stream(rast.device)
+    side = _side_streams(rast.device, max(1, min(int(streams), len(cams))))
+    while True:
+        ws = torch.zeros(g.n, dtype=torch.float32, device=rast.device)
+        ovf = torch.zeros((max(len(cams), 1), 2), dtype=torch.int64, device=rast.device)
+        ready = torch.cuda.Event()
+        ready.record(main)
+        for j, cam in enumerate(cams):
+            st = side[j % len(side)]
+            st.wait_event(ready)
+            with torch.cuda.stream(st):
+                rast.forward(g, cam, bg, weight_sums=ws, track=False, check=False).record_overflow(ovf[j])
+        for st in side:
+            main.wait_stream(st)
+        o = ovf.cpu().numpy()
+        if not o[:, 0].any():
+            return _to_np64(ws)
+        for j, cam in enumerate(cams):
+            if o[j, 0]:
+                rast.grow_capacity(g, cam, int(o[j, 1]))
 
 
 # --------------------------------------------------------------------- loss
