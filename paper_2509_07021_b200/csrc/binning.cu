@@ -180,7 +180,12 @@ __global__ void __launch_bounds__(256) emit_entries(const uint32_t* __restrict__
                                                     KT* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
                                                     uint32_t* __restrict__ cell_hist,
                                                     const uint32_t* __restrict__ row_off,
-                                                    const uint16_t* __restrict__ row_spans) {
+                                                    const uint16_t* __restrict__ row_spans,
+                                                    uint2* __restrict__ ranges, int n_cells) {
+  // the sort after this kernel accumulates [start, end) per cell with
+  // atomicMin / atomicMax: start every cell empty (start > end)
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_cells; i += gridDim.x * blockDim.x)
+    ranges[i] = make_uint2(0xffffffffu, 0u);
   // cell_hist (single-pass super-tile sort): counts of the 9-bit cell digit
   // of every written entry, accumulated per CTA in shared memory
   __shared__ uint32_t s_hist[512];
@@ -297,17 +302,6 @@ __global__ void __launch_bounds__(256) emit_entries(const uint32_t* __restrict__
   }
 }
 
-__global__ void ranges_init(uint2* __restrict__ ranges, int n_tiles) {
-  for (int i = blockIdx.x * 256 + threadIdx.x; i < n_tiles; i += gridDim.x * 256) ranges[i] = make_uint2(0xffffffffu, 0u);
-}
-
-__global__ void ranges_fix(uint2* __restrict__ ranges, int n_tiles) {
-  for (int i = blockIdx.x * 256 + threadIdx.x; i < n_tiles; i += gridDim.x * 256) {
-    uint2 r = ranges[i];
-    if (r.x == 0xffffffffu) ranges[i] = make_uint2(0u, 0u);
-  }
-}
-
 // Final location of the sorted values (which ping-pong buffer).
 bool final_in_alt(const Layout& lo) {
   int passes = lo.sort_mode == SGS_SORT_KEY64 ? (32 + tile_sort_bits(lo.n_tiles) + 7) / 8
@@ -329,26 +323,23 @@ static int bin_entries(const SgsCam& cam, const sgs_workspace* ws, const Layout&
   uint32_t* v1 = at<uint32_t>(ws, lo.ent_val_alt);
   uint2* ranges = at<uint2>(ws, lo.ranges);
   const int n_cells = kSuper ? lo.n_super : lo.n_tiles;
-  const int rgrid = persistent_grid((uint64_t)n_cells, 256, 4);
-  ranges_init<<<rgrid, 256, 0, st>>>(ranges, n_cells);
-  SGS_LAUNCH_CHECK("ranges_init");
   emit_entries<KT, kSuper><<<persistent_grid(n, 256, 8), 256, 0, st>>>(
       perm, n, at<uint32_t>(ws, kSuper ? lo.super_touched : lo.tiles_touched), at<uint2>(ws, lo.rect),
       at<float4>(ws, lo.rec_geo), at<float4>(ws, lo.rec_con), at<float4>(ws, lo.rec_span),
       at<uint32_t>(ws, lo.depth_key),
       at<unsigned long long>(ws, lo.offsets), cam, lo.super_x, cap, &ctr->n_bin, k0, v0,
       fused_hist ? at<uint32_t>(ws, lo.hist) + kSuperHistOff : nullptr,
-      lo.row_cap ? at<uint32_t>(ws, lo.row_off) : nullptr, lo.row_cap ? at<uint16_t>(ws, lo.row_spans) : nullptr);
+      lo.row_cap ? at<uint32_t>(ws, lo.row_off) : nullptr, lo.row_cap ? at<uint16_t>(ws, lo.row_spans) : nullptr,
+      ranges, n_cells);
   SGS_LAUNCH_CHECK("emit_entries");
   bool alt = false;
   uint32_t* hist = at<uint32_t>(ws, lo.hist) + (fused_hist ? kSuperHistOff : 0);
   int rc = radix_sort_pairs<KT, IPT, RBITS>(k0, v0, k1, v1, &ctr->n_sort, cap, key_bits, hist,
                                      at<uint32_t>(ws, lo.status), &ctr->part_counter[8], &alt, st, false,
                                      RsRangeOut{ranges, tile_shift}, kSuper ? 16 : 0, kSuper, fused_hist);
-  if (rc) return rc;
-  ranges_fix<<<rgrid, 256, 0, st>>>(ranges, n_cells);
-  SGS_LAUNCH_CHECK("ranges_fix");
-  return SGS_OK;
+  // cells without entries keep (0xffffffff, 0): every consumer reads a range
+  // as [start, max(start, end)), i.e. empty
+  return rc;
 }
 
 int launch_bin(const SgsCam& cam, const sgs_workspace* ws, const Layout& lo, cudaStream_t st) {
@@ -363,16 +354,15 @@ int launch_bin(const SgsCam& cam, const sgs_workspace* ws, const Layout& lo, cud
     uint32_t* kb = at<uint32_t>(ws, lo.dkey_tmp);
     uint32_t* ia = at<uint32_t>(ws, lo.didx);
     uint32_t* ib = at<uint32_t>(ws, lo.didx_alt);
-    SGS_CUDA(cudaMemcpyAsync(ka, dkey, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
-    set_count<<<1, 1, 0, st>>>(&ctr->n_depth, n);
-    SGS_LAUNCH_CHECK("set_count");
     bool alt = false;
-    // depth keys are 31-bit (0x7fffffff = not emitting): 4 passes over N
-    // the preprocess accumulated the four depth-digit histograms
+    // depth keys are 31-bit (0x7fffffff = not emitting): 4 passes over N; the
+    // preprocess accumulated the four depth-digit histograms and set n_depth.
+    // The first pass reads the preprocess's keys in place (left intact, so
+    // sgs_bin may be repeated after one sgs_preprocess).
     int rc = radix_sort_pairs<uint32_t, kDepthSortIPT, 8, kDepthSortThreads>(ka, ia, kb, ib, &ctr->n_depth, n, 31,
                                                         at<uint32_t>(ws, lo.hist) + kDepthHistOff,
                                                         at<uint32_t>(ws, lo.status), &ctr->part_counter[0], &alt, st,
-                                                        true, RsRangeOut{nullptr, 0}, 0, false, true);
+                                                        true, RsRangeOut{nullptr, 0}, 0, false, true, dkey);
     if (rc) return rc;
     const uint32_t* perm = alt ? ib : ia;
     rc = launch_scan(at<uint32_t>(ws, lo.super_touched), perm, n, cap, status64, offsets, ctr, st);

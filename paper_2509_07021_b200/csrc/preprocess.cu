@@ -49,6 +49,7 @@ __global__ void __launch_bounds__(256, SGS_PRE_REG_CTAS) preprocess_kernel(sgs_p
   const int64_t n = P.n;
   const int L = kL > 0 ? kL : P.n_lobes;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  if (depth_hist && blockIdx.x == 0 && threadIdx.x == 0) ctr->n_depth = (uint32_t)n;  // the depth sort's count
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // iterate whole warps so the ballots and the cooperative row loop see converged warps
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
