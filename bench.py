@@ -37,11 +37,11 @@ METRIC = "frames/s & Mpix/s at 1080p, 1M Gaussians, 3 SG lobes (1/2/4/8 B200); p
 UNIT = "frames/s"
 WORKLOAD = "configs[2]: 1,000,000 Gaussians (64 clusters), 3 SG lobes, 1920x1080, FoV 60"
 # libsgs kernels per forward frame (depth-first mode, 1080p): preprocess (also
-# accumulates the depth-digit histograms); histogram scan, 4 onesweep passes
+# accumulates the depth-digit histograms); 4 onesweep passes
 # (depth sort); the one-pass offsets scan; emit_entries (also the cell
-# histogram and the range reset); histogram scan + 1 onesweep pass (super-tile
-# sort + ranges); cell_order, raster_fwd (profiles/r01_launches_v9.csv)
-KERNELS_PER_FRAME = 12
+# histogram and the range reset); 1 onesweep pass (super-tile
+# sort + ranges); cell_order, raster_fwd (profiles/r01_launches_v10.csv)
+KERNELS_PER_FRAME = 10
 
 
 def parse():

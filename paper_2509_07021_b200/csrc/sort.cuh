@@ -96,26 +96,6 @@ __global__ void __launch_bounds__(256) rs_histogram(const K* __restrict__ keys, 
   }
 }
 
-// In-place exclusive scan of each pass's 2^RBITS bins (one CTA per pass).
-template <int RBITS>
-__global__ void __launch_bounds__(1 << RBITS) rs_scan_hist(uint32_t* hist) {
-  constexpr int R = 1 << RBITS;
-  __shared__ uint32_t warp_tot[R / 32];
-  uint32_t* h = hist + blockIdx.x * R;
-  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  uint32_t v = h[t], x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) warp_tot[w] = x;
-  __syncthreads();
-  uint32_t pre = 0;
-  for (int i = 0; i < w; ++i) pre += warp_tot[i];
-  h[t] = pre + x - v;
-}
-
 template <typename K, int IPT, int RBITS, int NT = kRsThreads>
 struct RsSmem {
   static constexpr int kTile = NT * IPT;
@@ -124,6 +104,7 @@ struct RsSmem {
   uint32_t warp_hist[kWarps][R];
   uint32_t digit_start[R];
   uint32_t global_base[R];
+  uint32_t pass_base[R];  // exclusive scan of the pass's digit counts
   uint32_t warp_tot[kWarps];
   uint32_t part;
   uint32_t vals[kTile];
@@ -135,7 +116,8 @@ struct RsRangeOut {
   int tile_shift;  // cell id = key >> tile_shift
 };
 
-// One pass.  status: nparts x 2^RBITS u32, zeroed; ticket zeroed.
+// One pass.  pass_count: the pass's digit counts (every CTA scans them);
+// status: nparts x 2^RBITS u32, zeroed; ticket zeroed.
 // vin == nullptr means values are the item indices (first pass of an argsort).
 // kout == nullptr skips the key writes.
 #ifndef SGS_RS_MIN_BLOCKS
@@ -145,7 +127,7 @@ template <typename K, int IPT, int RBITS, int NT = kRsThreads>
 __global__ void __launch_bounds__(NT, SGS_RS_MIN_BLOCKS) rs_onesweep(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                           K* __restrict__ kout, uint32_t* __restrict__ vout,
                                                           const uint32_t* n_ptr, uint32_t n_cap, int shift,
-                                                          const uint32_t* __restrict__ pass_base, uint32_t* status,
+                                                          const uint32_t* __restrict__ pass_count, uint32_t* status,
                                                           uint32_t* ticket, RsRangeOut rout) {
   static_assert((1 << RBITS) <= NT, "one thread per digit");
   using S = RsSmem<K, IPT, RBITS, NT>;
@@ -158,6 +140,23 @@ __global__ void __launch_bounds__(NT, SGS_RS_MIN_BLOCKS) rs_onesweep(const K* __
   const uint32_t n = min(*n_ptr, n_cap);
   const uint32_t nparts = (n + kTile - 1) / kTile;
   const uint32_t lt = lanemask_lt();
+
+  // each CTA scans the pass's digit counts itself (no separate scan kernel)
+  {
+    const uint32_t c = t < R ? pass_count[t] : 0u;
+    uint32_t x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s.warp_tot[w] = x;
+    __syncthreads();
+    uint32_t pre = 0;
+    for (int i = 0; i < w; ++i) pre += s.warp_tot[i];
+    if (t < R) s.pass_base[t] = pre + x - c;
+    __syncthreads();
+  }
 
   for (;;) {
     if (t == 0) s.part = atomicAdd(ticket, 1u);
@@ -249,7 +248,7 @@ __global__ void __launch_bounds__(NT, SGS_RS_MIN_BLOCKS) rs_onesweep(const K* __
         }
         atomicExch(status + (size_t)part * R + t, kFlagInc | (excl + run));
       }
-      s.global_base[t] = pass_base[t] + excl;
+      s.global_base[t] = s.pass_base[t] + excl;
     }
     __syncthreads();
 
@@ -328,8 +327,6 @@ int radix_sort_pairs(K* k0, uint32_t* v0, K* k1, uint32_t* v1, const uint32_t* n
     rs_histogram<K, RBITS><<<hgrid, 256, hsmem, st>>>(k_first ? k_first : k0, n_ptr, n_cap, begin_bit, passes, hist);
     SGS_LAUNCH_CHECK("rs_histogram");
   }
-  rs_scan_hist<RBITS><<<passes, R, 0, st>>>(hist);
-  SGS_LAUNCH_CHECK("rs_scan_hist");
   const size_t smem = sizeof(RsSmem<K, IPT, RBITS, NT>);
   static bool attr_set = false;
   if (!attr_set) {
