@@ -213,3 +213,18 @@ def test_large_splats_overflow_row_span_store():
     _check_projected(rast, frame, ref)
     _check_bins(rast, frame, ref)
     _img_ok(frame, ref)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_bin_is_repeatable_after_one_preprocess(mode):
+    """sgs_bin leaves the preprocess outputs intact (the depth sort reads the
+    preprocess's keys in place): binning twice gives the same lists."""
+    import ctypes as C
+    scene, cams = scenes.config0(n=5000)
+    cam = cams[0]
+    rast, g, frame = _gpu_frame(scene, cam, mode)
+    k1, v1, r1 = (t.cpu().numpy().copy() for t in rast.export_bins(frame))
+    _ffi.call("sgs_bin", C.byref(frame.cam), C.byref(frame.ws.desc),
+              C.c_void_p(torch.cuda.current_stream().cuda_stream))
+    k2, v2, r2 = (t.cpu().numpy() for t in rast.export_bins(frame))
+    assert np.array_equal(k1, k2) and np.array_equal(v1, v2) and np.array_equal(r1, r2)
