@@ -25,11 +25,13 @@ __device__ __forceinline__ void warp_count(unsigned long long* ctr, bool pred) {
 // The exact tile counts are the expensive part: one ellipse-row span (two
 // quadratic roots) per tile row the support rectangle covers, and the row
 // count varies 1..>10 across a warp.  They are computed warp-cooperatively:
-// the warp's primitives' super-tile rows (4 tile rows each) are flattened
-// into one list and processed 32 at a time, lane = super row, and each row's
-// tile and super-tile counts are summed into its primitive's shared-memory
-// slot.  The spans are sgs_super_row_spans -- the definition the emission and
-// the CPU restatement use -- so the counts agree bit for bit.
+// the warp's primitives' tile rows are flattened into one list and processed
+// 32 at a time, lane = tile row; each row's tile count is summed into its
+// primitive's shared-memory slot and its super-tile columns are merged into
+// the (primitive, super row) slot, from which each primitive then sums its
+// super-tile count.  The spans are sgs_row_span -- the definition the
+// emission and the CPU restatement use -- so the counts agree bit for bit.
+// (SGS_PRE_TILE_ROWS=0: super-row items, four rows per lane.)
 template <int kL>
 #ifndef SGS_PRE_CTAS
 #define SGS_PRE_CTAS 3
