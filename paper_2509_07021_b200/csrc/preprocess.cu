@@ -10,12 +10,7 @@
 
 namespace sgs {
 
-// Exact counts over tile-row items (one tile row per lane) or super-row items
-// (four rows per lane, rows outside the rectangle evaluated and masked).
-#ifndef SGS_PRE_TILE_ROWS
-#define SGS_PRE_TILE_ROWS 1
-#endif
-constexpr int kPreSlots = 128;  // (primitive, super row) union slots per warp
+constexpr int kPreSlots = 256;  // (primitive, super row) union slots per warp
 
 __device__ __forceinline__ void warp_count(unsigned long long* ctr, bool pred) {
   unsigned m = __ballot_sync(0xffffffffu, pred);
@@ -31,7 +26,9 @@ __device__ __forceinline__ void warp_count(unsigned long long* ctr, bool pred) {
 // the (primitive, super row) slot, from which each primitive then sums its
 // super-tile count.  The spans are sgs_row_span -- the definition the
 // emission and the CPU restatement use -- so the counts agree bit for bit.
-// (SGS_PRE_TILE_ROWS=0: super-row items, four rows per lane.)
+// Warps whose rectangles are tall use super-row items instead (four rows per
+// lane; rows outside the rectangle evaluated and masked), which need fewer
+// item iterations when little is masked.
 template <int kL>
 #ifndef SGS_PRE_CTAS
 #define SGS_PRE_CTAS 3
@@ -50,10 +47,8 @@ __global__ void __launch_bounds__(256, SGS_PRE_REG_CTAS) preprocess_kernel(sgs_p
                                                          uint32_t* __restrict__ row_off, uint16_t* __restrict__ row_spans,
                                                          uint32_t row_cap, Counters* ctr) {
   __shared__ uint32_t s_cnt[8][32], s_sup[8][32];
-#if SGS_PRE_TILE_ROWS
   // per warp: (primitive, super row) slots of the super-tile column union
   __shared__ int s_lo[8][kPreSlots], s_hi[8][kPreSlots];
-#endif
   __shared__ uint32_t s_hist[4][256];  // depth-key digit counts of this CTA's primitives
   if (depth_hist) {
     for (int j = threadIdx.x; j < 4 * 256; j += blockDim.x) (&s_hist[0][0])[j] = 0;
@@ -92,135 +87,166 @@ __global__ void __launch_bounds__(256, SGS_PRE_REG_CTAS) preprocess_kernel(sgs_p
         sp = sgs_span(g, k);
       }
     }
-#if SGS_PRE_TILE_ROWS
-    // ---- exact counts, one tile row per lane (the rows of the warp's
-    // primitives flattened: no masked rows, full lanes); each row's span is
-    // stored, and its super-tile columns are merged into its (primitive,
-    // super row) slot with shared-memory min / max
-    const uint32_t nrows_all = pr.emits ? (uint32_t)(pr.ty1 - pr.ty0 + 1) : 0u;
-    const uint32_t nsr = pr.emits ? (uint32_t)(pr.ty1 / SGS_SUPER - pr.ty0 / SGS_SUPER + 1) : 0u;
-    const uint32_t sincl = warp_incl_scan(nsr, lane);
-    const uint32_t sbase = sincl - nsr;
-    const bool slots_ok = __shfl_sync(0xffffffffu, sincl, 31) <= (uint32_t)kPreSlots;  // warp-uniform
-    s_cnt[warp][lane] = 0;
-    if (slots_ok)
-      for (uint32_t j = lane; j < (uint32_t)kPreSlots; j += 32) {
-        s_lo[warp][j] = 0x7fffffff;
-        s_hi[warp][j] = -1;
-      }
-    __syncwarp();
-    const uint32_t incl = warp_incl_scan(nrows_all, lane);
-    const uint32_t start = incl - nrows_all;
-    const uint32_t R = __shfl_sync(0xffffffffu, incl, 31);
-    // row-span store: one u16 (first column - tx0 | count << 8) per tile row of
-    // the support rectangle, space handed out per warp; primitives that do not
-    // fit (store full, or wider than 255 tiles) are re-solved by the emission
-    uint32_t my_off = kNoRows;
-    if (row_spans) {
-      const uint32_t nrows = pr.tx1 - pr.tx0 < 255 ? nrows_all : 0u;
-      const uint32_t rincl = warp_incl_scan(nrows, lane);
-      const uint32_t rtot = __shfl_sync(0xffffffffu, rincl, 31);
-      uint32_t rbase = 0;
-      if (lane == 31 && rtot) rbase = atomicAdd(&ctr->row_alloc, rtot);
-      rbase = __shfl_sync(0xffffffffu, rbase, 31);
-      if (nrows && (uint64_t)rbase + rincl <= row_cap) my_off = rbase + rincl - nrows;
+    // tile-row items (no masked rows) unless the warp's rectangles are tall
+    // enough that four-row super-row items waste little (<= 20 % masked rows)
+    // and need fewer item iterations
+    uint32_t my_off, cnt, nsup;
+    bool tile_rows;
+    {
+      const uint32_t rows_w = __reduce_add_sync(0xffffffffu, pr.emits ? (uint32_t)(pr.ty1 - pr.ty0 + 1) : 0u);
+      const uint32_t srows_w =
+          __reduce_add_sync(0xffffffffu, pr.emits ? (uint32_t)(pr.ty1 / SGS_SUPER - pr.ty0 / SGS_SUPER + 1) : 0u);
+      tile_rows = 4ull * SGS_SUPER * srows_w > 5ull * rows_w;
     }
-    for (uint32_t k0 = 0; k0 < R; k0 += 32) {
-      const uint32_t kk = k0 + lane;
-      const int owner = lane_search(start, kk < R ? kk : R - 1);
-      const SgsSpan os = shfl_span(sp, owner);
-      const int otx0 = __shfl_sync(0xffffffffu, pr.tx0, owner);
-      const int oty0 = __shfl_sync(0xffffffffu, pr.ty0, owner);
-      const int otx1 = __shfl_sync(0xffffffffu, pr.tx1, owner);
-      const uint32_t ostart = __shfl_sync(0xffffffffu, start, owner);
-      const uint32_t ooff = __shfl_sync(0xffffffffu, my_off, owner);
-      const uint32_t osb = __shfl_sync(0xffffffffu, sbase, owner);
-      if (kk < R) {
-        const int ty = oty0 + (int)(kk - ostart);
-        int f;
-        const int c = sgs_row_span(&os, &cam, ty, otx0, otx1, &f);
-        if (c) {
-          atomicAdd(&s_cnt[warp][owner], (uint32_t)c);
-          if (slots_ok) {
-            const uint32_t slot = osb + (uint32_t)(ty / SGS_SUPER - oty0 / SGS_SUPER);
-            atomicMin(&s_lo[warp][slot], f / SGS_SUPER);
-            atomicMax(&s_hi[warp][slot], (f + c - 1) / SGS_SUPER);
+    if (tile_rows) {
+      // ---- exact counts, one tile row per lane (the rows of the warp's
+      // primitives flattened: no masked rows, full lanes); each row's span is
+      // stored, and its super-tile columns are merged into its (primitive,
+      // super row) slot with shared-memory min / max
+      const uint32_t nrows_all = pr.emits ? (uint32_t)(pr.ty1 - pr.ty0 + 1) : 0u;
+      const uint32_t nsr = pr.emits ? (uint32_t)(pr.ty1 / SGS_SUPER - pr.ty0 / SGS_SUPER + 1) : 0u;
+      const uint32_t sincl = warp_incl_scan(nsr, lane);
+      const uint32_t sbase = sincl - nsr;
+      const bool slots_ok = __shfl_sync(0xffffffffu, sincl, 31) <= (uint32_t)kPreSlots;  // warp-uniform
+      s_cnt[warp][lane] = 0;
+      if (slots_ok)
+        for (uint32_t j = lane; j < (uint32_t)kPreSlots; j += 32) {
+          s_lo[warp][j] = 0x7fffffff;
+          s_hi[warp][j] = -1;
+        }
+      __syncwarp();
+      const uint32_t incl = warp_incl_scan(nrows_all, lane);
+      const uint32_t start = incl - nrows_all;
+      const uint32_t R = __shfl_sync(0xffffffffu, incl, 31);
+      // row-span store: one u16 (first column - tx0 | count << 8) per tile row of
+      // the support rectangle, space handed out per warp; primitives that do not
+      // fit (store full, or wider than 255 tiles) are re-solved by the emission
+      my_off = kNoRows;
+      if (row_spans) {
+        const uint32_t nrows = pr.tx1 - pr.tx0 < 255 ? nrows_all : 0u;
+        const uint32_t rincl = warp_incl_scan(nrows, lane);
+        const uint32_t rtot = __shfl_sync(0xffffffffu, rincl, 31);
+        uint32_t rbase = 0;
+        if (lane == 31 && rtot) rbase = atomicAdd(&ctr->row_alloc, rtot);
+        rbase = __shfl_sync(0xffffffffu, rbase, 31);
+        if (nrows && (uint64_t)rbase + rincl <= row_cap) my_off = rbase + rincl - nrows;
+      }
+      for (uint32_t k0 = 0; k0 < R; k0 += 32) {
+        const uint32_t kk = k0 + lane;
+        const int owner = lane_search(start, kk < R ? kk : R - 1);
+        const SgsSpan os = shfl_span(sp, owner);
+        const int otx0 = __shfl_sync(0xffffffffu, pr.tx0, owner);
+        const int oty0 = __shfl_sync(0xffffffffu, pr.ty0, owner);
+        const int otx1 = __shfl_sync(0xffffffffu, pr.tx1, owner);
+        const uint32_t ostart = __shfl_sync(0xffffffffu, start, owner);
+        const uint32_t ooff = __shfl_sync(0xffffffffu, my_off, owner);
+        const uint32_t osb = __shfl_sync(0xffffffffu, sbase, owner);
+        if (kk < R) {
+          const int ty = oty0 + (int)(kk - ostart);
+          int f;
+          const int c = sgs_row_span(&os, &cam, ty, otx0, otx1, &f);
+          if (c) {
+            atomicAdd(&s_cnt[warp][owner], (uint32_t)c);
+            if (slots_ok) {
+              const uint32_t slot = osb + (uint32_t)(ty / SGS_SUPER - oty0 / SGS_SUPER);
+              atomicMin(&s_lo[warp][slot], f / SGS_SUPER);
+              atomicMax(&s_hi[warp][slot], (f + c - 1) / SGS_SUPER);
+            }
+          }
+          if (ooff != kNoRows)
+            row_spans[ooff + (kk - ostart)] = (uint16_t)(c > 0 ? (((f - otx0) & 0xff) | (c << 8)) : 0);
+        }
+      }
+      __syncwarp();
+      cnt = s_cnt[warp][lane];
+      nsup = 0;
+      if (cnt) {
+        if (slots_ok) {
+          for (uint32_t j = 0; j < nsr; ++j) {
+            const int lo = s_lo[warp][sbase + j], hi = s_hi[warp][sbase + j];
+            if (hi >= lo) nsup += (uint32_t)(hi - lo + 1);
+          }
+        } else {
+          // more super rows in this warp than slots: each primitive reads its
+          // stored row spans back (the __syncwarp above orders the stores), or
+          // re-solves them when they were not stored
+          for (int sr = pr.ty0 / SGS_SUPER; sr <= pr.ty1 / SGS_SUPER; ++sr) {
+            if (my_off != kNoRows) {
+              int lo = 0x7fffffff, hi = -1;
+  #pragma unroll
+              for (int q = 0; q < SGS_SUPER; ++q) {
+                const int ty = sr * SGS_SUPER + q;
+                if (ty < pr.ty0 || ty > pr.ty1) continue;
+                const uint32_t e = row_spans[my_off + (uint32_t)(ty - pr.ty0)];
+                const int c = (int)(e >> 8);
+                if (c > 0) {
+                  const int f = pr.tx0 + (int)(e & 0xffu);
+                  lo = min(lo, f / SGS_SUPER);
+                  hi = max(hi, (f + c - 1) / SGS_SUPER);
+                }
+              }
+              if (hi >= lo) nsup += (uint32_t)(hi - lo + 1);
+            } else {
+              int rf[SGS_SUPER], rc[SGS_SUPER], fsc;
+              nsup += (uint32_t)sgs_super_row_spans(&sp, &cam, pr.tx0, pr.ty0, pr.tx1, pr.ty1, sr, rf, rc, &fsc);
+            }
           }
         }
-        if (ooff != kNoRows)
-          row_spans[ooff + (kk - ostart)] = (uint16_t)(c > 0 ? (((f - otx0) & 0xff) | (c << 8)) : 0);
       }
-    }
-    __syncwarp();
-    const uint32_t cnt = s_cnt[warp][lane];
-    uint32_t nsup = 0;
-    if (cnt) {
-      if (slots_ok) {
-        for (uint32_t j = 0; j < nsr; ++j) {
-          const int lo = s_lo[warp][sbase + j], hi = s_hi[warp][sbase + j];
-          if (hi >= lo) nsup += (uint32_t)(hi - lo + 1);
-        }
-      } else {  // more super rows in this warp than slots: re-solve them per primitive
-        for (int sr = pr.ty0 / SGS_SUPER; sr <= pr.ty1 / SGS_SUPER; ++sr) {
+    } else {
+      // ---- exact counts, one super-tile row per lane
+      const uint32_t nitems = pr.emits ? (uint32_t)(pr.ty1 / SGS_SUPER - pr.ty0 / SGS_SUPER + 1) : 0u;
+      s_cnt[warp][lane] = 0;
+      s_sup[warp][lane] = 0;
+      __syncwarp();
+      const uint32_t incl = warp_incl_scan(nitems, lane);
+      const uint32_t start = incl - nitems;
+      const uint32_t R = __shfl_sync(0xffffffffu, incl, 31);
+      // row-span store: one u16 (first column - tx0 | count << 8) per tile row of
+      // the support rectangle, space handed out per warp; primitives that do not
+      // fit (store full, or wider than 255 tiles) are re-solved by the emission
+      my_off = kNoRows;
+      if (row_spans) {
+        const uint32_t nrows = pr.emits && pr.tx1 - pr.tx0 < 255 ? (uint32_t)(pr.ty1 - pr.ty0 + 1) : 0u;
+        const uint32_t rincl = warp_incl_scan(nrows, lane);
+        const uint32_t rtot = __shfl_sync(0xffffffffu, rincl, 31);
+        uint32_t rbase = 0;
+        if (lane == 31 && rtot) rbase = atomicAdd(&ctr->row_alloc, rtot);
+        rbase = __shfl_sync(0xffffffffu, rbase, 31);
+        if (nrows && (uint64_t)rbase + rincl <= row_cap) my_off = rbase + rincl - nrows;
+      }
+      for (uint32_t k0 = 0; k0 < R; k0 += 32) {
+        const uint32_t kk = k0 + lane;
+        const int owner = lane_search(start, kk < R ? kk : R - 1);
+        const SgsSpan os = shfl_span(sp, owner);
+        const int otx0 = __shfl_sync(0xffffffffu, pr.tx0, owner);
+        const int oty0 = __shfl_sync(0xffffffffu, pr.ty0, owner);
+        const int otx1 = __shfl_sync(0xffffffffu, pr.tx1, owner);
+        const int oty1 = __shfl_sync(0xffffffffu, pr.ty1, owner);
+        const uint32_t ostart = __shfl_sync(0xffffffffu, start, owner);
+        const uint32_t ooff = __shfl_sync(0xffffffffu, my_off, owner);
+        if (kk < R) {
+          const int sr = oty0 / SGS_SUPER + (int)(kk - ostart);
           int rf[SGS_SUPER], rc[SGS_SUPER], fsc;
-          nsup += (uint32_t)sgs_super_row_spans(&sp, &cam, pr.tx0, pr.ty0, pr.tx1, pr.ty1, sr, rf, rc, &fsc);
-        }
-      }
-    }
-#else
-    // ---- exact counts, one super-tile row per lane
-    const uint32_t nitems = pr.emits ? (uint32_t)(pr.ty1 / SGS_SUPER - pr.ty0 / SGS_SUPER + 1) : 0u;
-    s_cnt[warp][lane] = 0;
-    s_sup[warp][lane] = 0;
-    __syncwarp();
-    const uint32_t incl = warp_incl_scan(nitems, lane);
-    const uint32_t start = incl - nitems;
-    const uint32_t R = __shfl_sync(0xffffffffu, incl, 31);
-    // row-span store: one u16 (first column - tx0 | count << 8) per tile row of
-    // the support rectangle, space handed out per warp; primitives that do not
-    // fit (store full, or wider than 255 tiles) are re-solved by the emission
-    uint32_t my_off = kNoRows;
-    if (row_spans) {
-      const uint32_t nrows = pr.emits && pr.tx1 - pr.tx0 < 255 ? (uint32_t)(pr.ty1 - pr.ty0 + 1) : 0u;
-      const uint32_t rincl = warp_incl_scan(nrows, lane);
-      const uint32_t rtot = __shfl_sync(0xffffffffu, rincl, 31);
-      uint32_t rbase = 0;
-      if (lane == 31 && rtot) rbase = atomicAdd(&ctr->row_alloc, rtot);
-      rbase = __shfl_sync(0xffffffffu, rbase, 31);
-      if (nrows && (uint64_t)rbase + rincl <= row_cap) my_off = rbase + rincl - nrows;
-    }
-    for (uint32_t k0 = 0; k0 < R; k0 += 32) {
-      const uint32_t kk = k0 + lane;
-      const int owner = lane_search(start, kk < R ? kk : R - 1);
-      const SgsSpan os = shfl_span(sp, owner);
-      const int otx0 = __shfl_sync(0xffffffffu, pr.tx0, owner);
-      const int oty0 = __shfl_sync(0xffffffffu, pr.ty0, owner);
-      const int otx1 = __shfl_sync(0xffffffffu, pr.tx1, owner);
-      const int oty1 = __shfl_sync(0xffffffffu, pr.ty1, owner);
-      const uint32_t ostart = __shfl_sync(0xffffffffu, start, owner);
-      const uint32_t ooff = __shfl_sync(0xffffffffu, my_off, owner);
-      if (kk < R) {
-        const int sr = oty0 / SGS_SUPER + (int)(kk - ostart);
-        int rf[SGS_SUPER], rc[SGS_SUPER], fsc;
-        const int nsc = sgs_super_row_spans(&os, &cam, otx0, oty0, otx1, oty1, sr, rf, rc, &fsc);
-        const uint32_t nt = (uint32_t)(rc[0] + rc[1] + rc[2] + rc[3]);
-        if (nt) atomicAdd(&s_cnt[warp][owner], nt);
-        if (nsc) atomicAdd(&s_sup[warp][owner], (uint32_t)nsc);
-        if (ooff != kNoRows) {
-#pragma unroll
-          for (int j = 0; j < SGS_SUPER; ++j) {
-            const int ty = sr * SGS_SUPER + j;
-            if (ty >= oty0 && ty <= oty1)
-              row_spans[ooff + (uint32_t)(ty - oty0)] =
-                  (uint16_t)(rc[j] > 0 ? (((rf[j] - otx0) & 0xff) | (rc[j] << 8)) : 0);
+          const int nsc = sgs_super_row_spans(&os, &cam, otx0, oty0, otx1, oty1, sr, rf, rc, &fsc);
+          const uint32_t nt = (uint32_t)(rc[0] + rc[1] + rc[2] + rc[3]);
+          if (nt) atomicAdd(&s_cnt[warp][owner], nt);
+          if (nsc) atomicAdd(&s_sup[warp][owner], (uint32_t)nsc);
+          if (ooff != kNoRows) {
+  #pragma unroll
+            for (int j = 0; j < SGS_SUPER; ++j) {
+              const int ty = sr * SGS_SUPER + j;
+              if (ty >= oty0 && ty <= oty1)
+                row_spans[ooff + (uint32_t)(ty - oty0)] =
+                    (uint16_t)(rc[j] > 0 ? (((rf[j] - otx0) & 0xff) | (rc[j] << 8)) : 0);
+            }
           }
         }
       }
+      __syncwarp();
+      cnt = s_cnt[warp][lane];
+      nsup = s_sup[warp][lane];
     }
-    __syncwarp();
-    const uint32_t cnt = s_cnt[warp][lane];
-    const uint32_t nsup = s_sup[warp][lane];
-#endif
     const bool emitting = cnt > 0;
     if (live) {
       tiles_touched[i] = cnt;
