@@ -232,20 +232,25 @@ __global__ void __launch_bounds__(256) emit_entries(const uint32_t* __restrict__
       int rf[SGS_SUPER] = {0, 0, 0, 0}, rc[SGS_SUPER] = {0, 0, 0, 0};
       if (k < R) {
         if (kSuper && ooff != kNoRows) {
-          // the preprocess's stored row spans (the values sgs_super_row_spans gives)
+          // the preprocess's stored row spans (the values sgs_super_row_spans
+          // gives): the four loads are issued together (rows outside the
+          // rectangle read a clamped row and are masked), columns are >= 0
+          uint32_t e[SGS_SUPER];
+#pragma unroll
+          for (int q = 0; q < SGS_SUPER; ++q) {
+            const int ty = min(max(row * SGS_SUPER + q, oty0), oty1);
+            e[q] = row_spans[ooff + (uint32_t)(ty - oty0)];
+          }
           int lo = 0x7fffffff, hi = -1;
 #pragma unroll
           for (int q = 0; q < SGS_SUPER; ++q) {
             const int ty = row * SGS_SUPER + q;
             const bool in = ty >= oty0 && ty <= oty1;
-            const uint32_t e = in ? (uint32_t)row_spans[ooff + (uint32_t)(ty - oty0)] : 0u;
-            rc[q] = (int)(e >> 8);
-            rf[q] = rc[q] > 0 ? otx0 + (int)(e & 0xffu) : 0;
-            if (rc[q] > 0) {
-              const int a = rf[q] / SGS_SUPER, b = (rf[q] + rc[q] - 1) / SGS_SUPER;
-              lo = a < lo ? a : lo;
-              hi = b > hi ? b : hi;
-            }
+            rc[q] = in ? (int)(e[q] >> 8) : 0;
+            rf[q] = rc[q] > 0 ? otx0 + (int)(e[q] & 0xffu) : 0;
+            const int a = (int)((uint32_t)rf[q] >> 2), b = (int)((uint32_t)(rf[q] + rc[q] - 1) >> 2);
+            lo = rc[q] > 0 && a < lo ? a : lo;
+            hi = rc[q] > 0 && b > hi ? b : hi;
           }
           first = hi >= lo ? lo : 0;
           c = hi >= lo ? (uint32_t)(hi - lo + 1) : 0u;
