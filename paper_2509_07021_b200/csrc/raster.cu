@@ -248,7 +248,7 @@ __device__ __forceinline__ void load_chunk(ChunkRegs<CPT>& r, uint32_t lo, uint3
 // tile-local (lx, ly) has t1 = e1 lx + e2 ly + c1, t2 = e3 ly - e4 lx + c2.
 // A listed record reaches the tile, so |t| stays small there and the offsets
 // cost no precision (|c| <~ |t| + |e| 16).
-template <int THREADS, int CPT, bool kFilter, class S>
+template <int THREADS, int CPT, bool kFilter, class S, bool kLocal = true>
 __device__ __forceinline__ int stage_append_regs(const ChunkRegs<CPT>& r, uint32_t local_bit, const ListArgs& a,
                                                  int base, S& s, float ox, float oy) {
   constexpr int W = THREADS / 32;
@@ -277,8 +277,12 @@ __device__ __forceinline__ int stage_append_regs(const ChunkRegs<CPT>& r, uint32
       const int pos = base + pre + __popc(bal[h] & lt);
       const uint32_t g = r.val[h];
       const float4 G = a.geo[g], E = a.eig[g];
-      const float mx = G.x - ox, my = G.y - oy;
-      s.geo[pos] = make_float4(fmaf(-E.x, mx, -(E.y * my)), fmaf(E.w, mx, -(E.z * my)), G.z, 0.0f);
+      if constexpr (kLocal) {
+        const float mx = G.x - ox, my = G.y - oy;
+        s.geo[pos] = make_float4(fmaf(-E.x, mx, -(E.y * my)), fmaf(E.w, mx, -(E.z * my)), G.z, 0.0f);
+      } else {
+        s.geo[pos] = G;  // (mx, my, log2 o_eff, -) as stored
+      }
       s.con[pos] = E;
       s.col[pos] = a.col[g];
       if constexpr (S::kIds) {
@@ -667,10 +671,18 @@ __global__ void __launch_bounds__(kBwdThreads) raster_bwd_kernel(ListArgs la, Sg
   const int vidx = reduce9_index(lane);
   uint32_t hits_after = 0;
 
+  // the list keys / indices of the next (earlier) chunk load while this one
+  // is processed
+  ChunkRegs<kBwdCPT> pf;
+  if (cend > cs) load_chunk<kBwdThreads, kBwdCPT, kFilter>(pf, cend - cs > (uint32_t)kBwdChunk ? cend - kBwdChunk : cs,
+                                                           cend, la);
   for (uint32_t hi = cend; hi > cs;) {
     const uint32_t lo = hi - cs > (uint32_t)kBwdChunk ? hi - kBwdChunk : cs;
     __syncthreads();  // previous batch fully flushed
-    const int nb = stage_append<kBwdThreads, kBwdCPT, kFilter, true>(lo, hi, lbit, la, 0, s);
+    const int nb = stage_append_regs<kBwdThreads, kBwdCPT, kFilter, decltype(s), false>(pf, lbit, la, 0, s,
+                                                                                      0.0f, 0.0f);
+    if (lo > cs) load_chunk<kBwdThreads, kBwdCPT, kFilter>(pf, lo - cs > (uint32_t)kBwdChunk ? lo - kBwdChunk : cs,
+                                                           lo, la);
     const uint32_t base = max_nc - hits_after - (uint32_t)nb;  // per-tile list index of staged entry 0
     for (int k = nb - 1; k >= 0; --k) {
       const uint32_t idx = base + (uint32_t)k;
