@@ -228,3 +228,21 @@ def test_bin_is_repeatable_after_one_preprocess(mode):
               C.c_void_p(torch.cuda.current_stream().cuda_stream))
     k2, v2, r2 = (t.cpu().numpy() for t in rast.export_bins(frame))
     assert np.array_equal(k1, k2) and np.array_equal(v1, v2) and np.array_equal(r1, r2)
+
+
+@pytest.mark.parametrize("w,h", [(1, 1), (37, 23), (17, 250), (130, 9)])
+def test_odd_image_sizes(w, h):
+    """Partial tiles and super-tiles at the right / bottom edges (image sizes
+    that are no multiple of 16 or 64): lists bit-exact, image and backward
+    partials as the oracle's."""
+    scene, cams = scenes.config0(n=3000)
+    cam = cams[0].crop(100, 90, w, h)
+    ref = tiled.render(scene, cam)
+    rast, g, frame = _gpu_frame(scene, cam)
+    _check_projected(rast, frame, ref)
+    _check_bins(rast, frame, ref)
+    _img_ok(frame, ref)
+    dimg = np.random.default_rng(3).normal(size=ref.img.shape)
+    tiled.raster_backward(ref, dimg)
+    gr = rast.backward_raster(g, frame, torch.as_tensor(dimg, dtype=torch.float32, device="cuda"))
+    assert _composite_ok(gr.cpu().numpy().reshape(ref.grad2d.shape), ref.grad2d, floor=1e-4).all()
