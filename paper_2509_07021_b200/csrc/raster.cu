@@ -322,6 +322,9 @@ constexpr int kFwdChunk = kFwdThreads * kFwdCPT;  // candidates examined per sta
 #ifndef SGS_FWD_MIN_BLOCKS
 #define SGS_FWD_MIN_BLOCKS 8
 #endif
+#ifndef SGS_FWD_TRACK_MIN_BLOCKS
+#define SGS_FWD_TRACK_MIN_BLOCKS 7
+#endif
 constexpr int kFwdBatch = SGS_FWD_BATCH;          // staged entries processed per block sync
 constexpr int kFwdBuf = kFwdBatch + kFwdChunk;
 constexpr int kVoteEvery = SGS_VOTE_EVERY;
@@ -397,9 +400,10 @@ template <bool kImportance, bool kCount, bool kFilter, bool kTrack>
 // The image-only variant is capped at 64 registers (8 resident CTAs, a few
 // bytes of spills): slower alone (0.268 vs 0.264 ms) but it shares SMs with
 // the other streams' binning kernels, +3 % frames/s in the 4-stream bench.
-// The tracked / importance variants run in single-stream loops and keep
-// their registers (the cap cost the training forward 6 %).
-__global__ void __launch_bounds__(kFwdThreads, (kTrack || kImportance) ? 1 : SGS_FWD_MIN_BLOCKS) raster_fwd_kernel(ListArgs la, SgsCam cam, float3 bg,
+// The tracked variant (training, 4 view streams) is capped at 72 registers
+// (7 CTAs/SM): +1.4 % training views/s although a lone view is slower; the
+// importance variant keeps its registers.
+__global__ void __launch_bounds__(kFwdThreads, kImportance ? 1 : (kTrack ? SGS_FWD_TRACK_MIN_BLOCKS : SGS_FWD_MIN_BLOCKS)) raster_fwd_kernel(ListArgs la, SgsCam cam, float3 bg,
                                                                  float* __restrict__ out_img,
                                                                  float* __restrict__ out_T,
                                                                  uint32_t* __restrict__ out_nc,
