@@ -30,6 +30,9 @@ namespace sgs {
 #ifndef SGS_LOSS_TH
 #define SGS_LOSS_TH 16
 #endif
+#ifndef SGS_LOSS_MIN_BLOCKS
+#define SGS_LOSS_MIN_BLOCKS 4
+#endif
 constexpr int kLossTW = 32, kLossTH = SGS_LOSS_TH, kLossThreads = kLossTW * kLossTH;
 constexpr int kMaxWindow = 31;
 
@@ -66,7 +69,7 @@ __host__ __device__ inline size_t loss_smem_doubles(int r, int nplanes_in, int n
 // window, R = 5: unrolled taps, weights as constant-bank immediates, halo
 // index arithmetic by constants); R = 0 reads it from P.
 template <typename TI, typename TT, int R>
-__global__ void __launch_bounds__(kLossThreads) ssim_fwd_kernel(const TI* __restrict__ img, const TT* __restrict__ tgt,
+__global__ void __launch_bounds__(kLossThreads, SGS_LOSS_MIN_BLOCKS) ssim_fwd_kernel(const TI* __restrict__ img, const TT* __restrict__ tgt,
                                                                 LossParams P, double* __restrict__ dmu,
                                                                 double* __restrict__ dxx, double* __restrict__ dxy,
                                                                 double* __restrict__ smap, double* __restrict__ sums) {
@@ -151,7 +154,7 @@ __global__ void __launch_bounds__(kLossThreads) ssim_fwd_kernel(const TI* __rest
 }
 
 template <typename TI, typename TT, int R>
-__global__ void __launch_bounds__(kLossThreads) ssim_bwd_kernel(const TI* __restrict__ img, const TT* __restrict__ tgt,
+__global__ void __launch_bounds__(kLossThreads, SGS_LOSS_MIN_BLOCKS) ssim_bwd_kernel(const TI* __restrict__ img, const TT* __restrict__ tgt,
                                                                 LossParams P, const double* __restrict__ dmu,
                                                                 const double* __restrict__ dxx,
                                                                 const double* __restrict__ dxy, float* __restrict__ dimg,
