@@ -25,12 +25,12 @@ __device__ __forceinline__ void put(float* p, int64_t i, float v) {
     p[i] = v;
 }
 
-template <bool kAcc>
+template <bool kAcc, int kL>
 __global__ void __launch_bounds__(128) preprocess_bwd_kernel(sgs_params P, SgsCam cam,
                                                              const float* __restrict__ grad2d, sgs_grads out) {
   const bool logit = (out.flags & SGS_GRADS_MASK_LOGIT) != 0;
   const int64_t n = P.n;
-  const int L = P.n_lobes;
+  const int L = kL > 0 ? kL : P.n_lobes;  // kL = 3: lobe loops unrolled, per-lobe arrays in registers
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     float gv[kG2];
     bool any = false;
@@ -146,7 +146,8 @@ __global__ void __launch_bounds__(128) preprocess_bwd_kernel(sgs_params P, SgsCa
     const float v0 = v0r / rd, v1 = v1r / rd, v2 = v2r / rd;
     float cpre[3] = {P.diffuse[3 * i], P.diffuse[3 * i + 1], P.diffuse[3 * i + 2]};
     float e[SGS_MAX_LOBES], dotv[SGS_MAX_LOBES];
-    for (int l = 0; l < L; ++l) {
+#pragma unroll
+    for (int l = 0; l < (kL > 0 ? kL : L); ++l) {
       const float* u = P.axis_raw + (i * L + l) * 3;
       const float un = sqrtf(u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
       dotv[l] = (u[0] * v0 + u[1] * v1 + u[2] * v2) / un;
@@ -161,7 +162,8 @@ __global__ void __launch_bounds__(128) preprocess_bwd_kernel(sgs_params P, SgsCa
       d_diff[c] = dcp[c];
     }
     float dv[3] = {0, 0, 0};
-    for (int l = 0; l < L; ++l) {
+#pragma unroll
+    for (int l = 0; l < (kL > 0 ? kL : L); ++l) {
       const float* u = P.axis_raw + (i * L + l) * 3;
       const float* a = P.amplitude + (i * L + l) * 3;
       const float m = P.lobe_mask[i * L + l];
@@ -209,10 +211,18 @@ __global__ void __launch_bounds__(128) preprocess_bwd_kernel(sgs_params P, SgsCa
 int launch_preprocess_bwd(const sgs_params& P, const SgsCam& cam, const float* grad2d, const sgs_grads& g,
                           cudaStream_t st) {
   int grid = persistent_grid((uint64_t)P.n, 128, 16);
-  if (g.flags & SGS_GRADS_ACCUMULATE)
-    preprocess_bwd_kernel<true><<<grid, 128, 0, st>>>(P, cam, grad2d, g);
-  else
-    preprocess_bwd_kernel<false><<<grid, 128, 0, st>>>(P, cam, grad2d, g);
+  const bool acc = (g.flags & SGS_GRADS_ACCUMULATE) != 0;
+  if (P.n_lobes == 3) {
+    if (acc)
+      preprocess_bwd_kernel<true, 3><<<grid, 128, 0, st>>>(P, cam, grad2d, g);
+    else
+      preprocess_bwd_kernel<false, 3><<<grid, 128, 0, st>>>(P, cam, grad2d, g);
+  } else {
+    if (acc)
+      preprocess_bwd_kernel<true, 0><<<grid, 128, 0, st>>>(P, cam, grad2d, g);
+    else
+      preprocess_bwd_kernel<false, 0><<<grid, 128, 0, st>>>(P, cam, grad2d, g);
+  }
   SGS_LAUNCH_CHECK("preprocess_bwd_kernel");
   return SGS_OK;
 }
