@@ -144,6 +144,9 @@ static int launch_scan(const uint32_t* tt, const uint32_t* perm, uint32_t n, uin
 }
 
 // ------------------------------------------------------------- entry emission
+#ifndef SGS_EMIT_CTAS
+#define SGS_EMIT_CTAS 4  // grid = SMs x this (one wave at 4 resident CTAs), grid-stride over the ranks
+#endif
 __device__ __forceinline__ void unpack_rect(uint2 r, int& tx0, int& ty0, int& tx1, int& ty1) {
   tx0 = (int)(r.x & 0xffff);
   tx1 = (int)(int16_t)(r.x >> 16);
@@ -328,7 +331,7 @@ static int bin_entries(const SgsCam& cam, const sgs_workspace* ws, const Layout&
   uint32_t* v1 = at<uint32_t>(ws, lo.ent_val_alt);
   uint2* ranges = at<uint2>(ws, lo.ranges);
   const int n_cells = kSuper ? lo.n_super : lo.n_tiles;
-  emit_entries<KT, kSuper><<<persistent_grid(n, 256, 8), 256, 0, st>>>(
+  emit_entries<KT, kSuper><<<persistent_grid(n, 256, SGS_EMIT_CTAS), 256, 0, st>>>(
       perm, n, at<uint32_t>(ws, kSuper ? lo.super_touched : lo.tiles_touched), at<uint2>(ws, lo.rect),
       at<float4>(ws, lo.rec_geo), at<float4>(ws, lo.rec_con), at<float4>(ws, lo.rec_span),
       at<uint32_t>(ws, lo.depth_key),
