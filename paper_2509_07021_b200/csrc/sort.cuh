@@ -32,7 +32,10 @@ enum : uint32_t { kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kCountMask = (1u << 
 constexpr int kRsThreads = 512;  // default CTA size: 16 warps
 
 constexpr int kRsMaxRadix = 512;
-constexpr int kLookback = 32;    // predecessors examined per look-back step
+#ifndef SGS_RS_LOOKBACK
+#define SGS_RS_LOOKBACK 32
+#endif
+constexpr int kLookback = SGS_RS_LOOKBACK;  // predecessors examined per look-back step
 
 template <typename K, int RBITS>
 __device__ __forceinline__ uint32_t rs_digit(K k, int shift) {
