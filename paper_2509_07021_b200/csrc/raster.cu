@@ -688,13 +688,13 @@ __global__ void __launch_bounds__(kBwdThreads) raster_bwd_kernel(ListArgs la, Sg
     if (lo > cs) load_chunk<kBwdThreads, kBwdCPT, kFilter>(pf, lo - cs > (uint32_t)kBwdChunk ? lo - kBwdChunk : cs,
                                                            lo, la);
     const uint32_t base = max_nc - hits_after - (uint32_t)nb;  // per-tile list index of staged entry 0
-    for (int k = nb - 1; k >= 0; --k) {
+    const int wq_ = t >> 5;
+    // staged records at or past the warp's last kept one (list index >=
+    // warp_nc) need no work: their partial slots are zeroed together
+    const int k_top = (int)max((int64_t)-1, min((int64_t)nb - 1, (int64_t)warp_nc - 1 - (int64_t)base));
+    for (int i = (k_top + 1) * kGrad + lane; i < nb * kGrad; i += 32) (&s_part[wq_][0][0])[i] = 0.0f;
+    for (int k = k_top; k >= 0; --k) {
       const uint32_t idx = base + (uint32_t)k;
-      const int wq_ = t >> 5;
-      if (idx >= warp_nc) {  // warp-uniform: no pixel of this warp kept the record
-        if (vidx < kGrad) s_part[wq_][k][vidx] = 0.0f;
-        continue;
-      }
       const float4 G = s.geo[k];  // (mx, my, log2 o_eff, -)
       const float4 E = s.con[k];  // scaled eigen form (s1 ux, s1 uy, s2 ux, s2 uy)
       const float4 col = s.col[k];
