@@ -411,7 +411,7 @@ __global__ void __launch_bounds__(kFwdThreads, kImportance ? 1 : (kTrack ? SGS_F
                                                                  unsigned long long* __restrict__ pair_count) {
   __shared__ std::conditional_t<kImportance || kTrack, Stage<kFwdBuf>, StageNoIds<kFwdBuf>> s;
   __shared__ float s_wp[kImportance ? kFwdThreads / 32 : 1][kImportance ? kFwdBuf : 1];
-  static_assert(!kImportance || kVoteEvery == 8, "importance sums reduce one 8-record vote group at a time");
+  static_assert(!kImportance || kVoteEvery % 8 == 0, "importance sums reduce eight records at a time");
   __shared__ uint32_t s_kend;
 
   int tx, ty;
@@ -499,9 +499,12 @@ __global__ void __launch_bounds__(kFwdThreads, kImportance ? 1 : (kTrack ? SGS_F
         }
       }
       if constexpr (kImportance) {
-        // the group's per-record weight sums over the warp, all eight at once
-        const float tot = warp_reduce8(wv, lane);
-        if ((lane & 3) == 0) s_wp[wq][k + reduce8_index(lane)] = tot;
+        // the group's per-record weight sums over the warp, eight at a time
+#pragma unroll
+        for (int h = 0; h < kVoteEvery / 8; ++h) {
+          const float tot = warp_reduce8(wv + 8 * h, lane);
+          if ((lane & 3) == 0) s_wp[wq][k + 8 * h + reduce8_index(lane)] = tot;
+        }
       }
     }
     };
