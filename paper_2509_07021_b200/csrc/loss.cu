@@ -31,7 +31,7 @@ namespace sgs {
 #define SGS_LOSS_TH 16
 #endif
 #ifndef SGS_LOSS_MIN_BLOCKS
-#define SGS_LOSS_MIN_BLOCKS 4
+#define SGS_LOSS_MIN_BLOCKS 3
 #endif
 constexpr int kLossTW = 32, kLossTH = SGS_LOSS_TH, kLossThreads = kLossTW * kLossTH;
 constexpr int kMaxWindow = 31;
@@ -94,25 +94,43 @@ __global__ void __launch_bounds__(kLossThreads, SGS_LOSS_MIN_BLOCKS) ssim_fwd_ke
       sy[i] = in ? ld(tgt, g) : 0.0;
     }
     __syncthreads();
-    for (int i = t; i < HH * kLossTW; i += kLossThreads) {
-      const int row = i / kLossTW, col = i % kLossTW;
-      double a = 0, b = 0, aa = 0, bb = 0, ab = 0;
+    // two adjacent output columns per item: each loaded input (and its
+    // products) feeds both windows
+    for (int i = t; i < HH * (kLossTW / 2); i += kLossThreads) {
+      const int row = i / (kLossTW / 2), col = 2 * (i % (kLossTW / 2));
+      double a0 = 0, b0 = 0, aa0 = 0, bb0 = 0, ab0 = 0, a1 = 0, b1 = 0, aa1 = 0, bb1 = 0, ab1 = 0;
       #pragma unroll
-        for (int k = 0; k <= 2 * r; ++k) {
-        const double wx = P.w[k];
+      for (int k = 0; k <= 2 * r + 1; ++k) {
         const double u = sx[row * HW + col + k], v = sy[row * HW + col + k];
-        a = fma(wx, u, a);
-        b = fma(wx, v, b);
-        aa = fma(wx, u * u, aa);
-        bb = fma(wx, v * v, bb);
-        ab = fma(wx, u * v, ab);
+        const double uu = u * u, vv = v * v, uv = u * v;
+        if (k <= 2 * r) {
+          const double wx = P.w[k];
+          a0 = fma(wx, u, a0);
+          b0 = fma(wx, v, b0);
+          aa0 = fma(wx, uu, aa0);
+          bb0 = fma(wx, vv, bb0);
+          ab0 = fma(wx, uv, ab0);
+        }
+        if (k >= 1) {
+          const double wx = P.w[k - 1];
+          a1 = fma(wx, u, a1);
+          b1 = fma(wx, v, b1);
+          aa1 = fma(wx, uu, aa1);
+          bb1 = fma(wx, vv, bb1);
+          ab1 = fma(wx, uv, ab1);
+        }
       }
       const int o = row * kLossTW + col;
-      hs[o] = a;
-      hs[HH * kLossTW + o] = b;
-      hs[2 * HH * kLossTW + o] = aa;
-      hs[3 * HH * kLossTW + o] = bb;
-      hs[4 * HH * kLossTW + o] = ab;
+      hs[o] = a0;
+      hs[o + 1] = a1;
+      hs[HH * kLossTW + o] = b0;
+      hs[HH * kLossTW + o + 1] = b1;
+      hs[2 * HH * kLossTW + o] = aa0;
+      hs[2 * HH * kLossTW + o + 1] = aa1;
+      hs[3 * HH * kLossTW + o] = bb0;
+      hs[3 * HH * kLossTW + o + 1] = bb1;
+      hs[4 * HH * kLossTW + o] = ab0;
+      hs[4 * HH * kLossTW + o + 1] = ab1;
     }
     __syncthreads();
     if (inside) {
@@ -181,21 +199,33 @@ __global__ void __launch_bounds__(kLossThreads, SGS_LOSS_MIN_BLOCKS) ssim_bwd_ke
         s2[i] = in ? dxy[g] : 0.0;
       }
       __syncthreads();
-      for (int i = t; i < HH * kLossTW; i += kLossThreads) {
-        const int row = i / kLossTW, col = i % kLossTW;
-        double a = 0, b = 0, d = 0;
+      for (int i = t; i < HH * (kLossTW / 2); i += kLossThreads) {  // two output columns per item
+        const int row = i / (kLossTW / 2), col = 2 * (i % (kLossTW / 2));
+        double a0 = 0, b0 = 0, d0 = 0, a1 = 0, b1 = 0, d1 = 0;
         #pragma unroll
-        for (int k = 0; k <= 2 * r; ++k) {
-          const double wx = P.w[k];
+        for (int k = 0; k <= 2 * r + 1; ++k) {
           const int o = row * HW + col + k;
-          a = fma(wx, s0[o], a);
-          b = fma(wx, s1[o], b);
-          d = fma(wx, s2[o], d);
+          const double x0 = s0[o], x1 = s1[o], x2 = s2[o];
+          if (k <= 2 * r) {
+            const double wx = P.w[k];
+            a0 = fma(wx, x0, a0);
+            b0 = fma(wx, x1, b0);
+            d0 = fma(wx, x2, d0);
+          }
+          if (k >= 1) {
+            const double wx = P.w[k - 1];
+            a1 = fma(wx, x0, a1);
+            b1 = fma(wx, x1, b1);
+            d1 = fma(wx, x2, d1);
+          }
         }
         const int o = row * kLossTW + col;
-        hs[o] = a;
-        hs[HH * kLossTW + o] = b;
-        hs[2 * HH * kLossTW + o] = d;
+        hs[o] = a0;
+        hs[o + 1] = a1;
+        hs[HH * kLossTW + o] = b0;
+        hs[HH * kLossTW + o + 1] = b1;
+        hs[2 * HH * kLossTW + o] = d0;
+        hs[2 * HH * kLossTW + o + 1] = d1;
       }
       __syncthreads();
     }
