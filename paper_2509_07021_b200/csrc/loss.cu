@@ -15,7 +15,10 @@
 // dmu = 2 mu_y dA1 + 2 mu_x dB1 - 2 mu_x dB2 - 2 mu_y dA2, and the L1 term
 // (1-l) sign(x - y) / size (np.sign: 0 at 0).
 //
-// Two tiled kernels, 32x8 output pixels per CTA, one channel at a time: the
+// Two tiled kernels, 32x32 output pixels per CTA (512 threads, two
+// vertically adjacent outputs each; the horizontal passes compute two
+// adjacent columns per item, so loaded values feed two windows), one channel
+// at a time: the
 // forward stages the (8+2r) x (32+2r) halo of x and y in shared memory as
 // float64, filters rows then columns (all five statistics at once), writes
 // the three per-pixel float64 derivative planes (dmu, dB2, 2 dA2) and reduces the L1
@@ -31,9 +34,11 @@ namespace sgs {
 #define SGS_LOSS_TH 16
 #endif
 #ifndef SGS_LOSS_MIN_BLOCKS
-#define SGS_LOSS_MIN_BLOCKS 3
+#define SGS_LOSS_MIN_BLOCKS 2
 #endif
-constexpr int kLossTW = 32, kLossTH = SGS_LOSS_TH, kLossThreads = kLossTW * kLossTH;
+// each thread owns kLossRows vertically adjacent outputs of a column
+constexpr int kLossRows = 2;
+constexpr int kLossTW = 32, kLossTH = SGS_LOSS_TH * kLossRows, kLossThreads = kLossTW * SGS_LOSS_TH;
 constexpr int kMaxWindow = 31;
 
 struct LossParams {
@@ -81,9 +86,8 @@ __global__ void __launch_bounds__(kLossThreads, SGS_LOSS_MIN_BLOCKS) ssim_fwd_ke
   double* hs = sy + HH * HW;  // 5 planes of HH x TW
   const int x0 = blockIdx.x * kLossTW, y0 = blockIdx.y * kLossTH;
   const int t = threadIdx.x;
-  const int ox = t % kLossTW, oy = t / kLossTW;
-  const int px = x0 + ox, py = y0 + oy;
-  const bool inside = px < P.W && py < P.H;
+  const int ox = t % kLossTW, oy0 = (t / kLossTW) * kLossRows;
+  const int px = x0 + ox;
   double l1 = 0.0, ss = 0.0;
   for (int c = 0; c < 3; ++c) {
     for (int i = t; i < HH * HW; i += kLossThreads) {
@@ -133,33 +137,46 @@ __global__ void __launch_bounds__(kLossThreads, SGS_LOSS_MIN_BLOCKS) ssim_fwd_ke
       hs[4 * HH * kLossTW + o + 1] = ab1;
     }
     __syncthreads();
-    if (inside) {
-      double mx = 0, my = 0, mxx = 0, myy = 0, mxy = 0;
+    {
+      // the thread's kLossRows outputs share their column's loads
+      double m[kLossRows][5] = {};
       #pragma unroll
-        for (int k = 0; k <= 2 * r; ++k) {
-        const double wy = P.w[k];
-        const int o = (oy + k) * kLossTW + ox;
-        mx = fma(wy, hs[o], mx);
-        my = fma(wy, hs[HH * kLossTW + o], my);
-        mxx = fma(wy, hs[2 * HH * kLossTW + o], mxx);
-        myy = fma(wy, hs[3 * HH * kLossTW + o], myy);
-        mxy = fma(wy, hs[4 * HH * kLossTW + o], mxy);
+      for (int k = 0; k < 2 * r + kLossRows; ++k) {
+        const int o = (oy0 + k) * kLossTW + ox;
+        const double h0 = hs[o], h1 = hs[HH * kLossTW + o], h2 = hs[2 * HH * kLossTW + o],
+                     h3 = hs[3 * HH * kLossTW + o], h4 = hs[4 * HH * kLossTW + o];
+        #pragma unroll
+        for (int q = 0; q < kLossRows; ++q) {
+          if (k - q < 0 || k - q > 2 * r) continue;
+          const double wy = P.w[k - q];
+          m[q][0] = fma(wy, h0, m[q][0]);
+          m[q][1] = fma(wy, h1, m[q][1]);
+          m[q][2] = fma(wy, h2, m[q][2]);
+          m[q][3] = fma(wy, h3, m[q][3]);
+          m[q][4] = fma(wy, h4, m[q][4]);
+        }
       }
-      const double sxv = mxx - mx * mx, syv = myy - my * my, sxy = mxy - mx * my;
-      const double A1 = 2.0 * mx * my + P.c1, A2 = 2.0 * sxy + P.c2;
-      const double B1 = mx * mx + my * my + P.c1, B2 = sxv + syv + P.c2;
-      const double inv = 1.0 / (B1 * B2);
-      const double S = A1 * A2 * inv;
-      // 1 / B1 = B2 inv, 1 / B2 = B1 inv: one division
-      const double dA1 = A2 * inv, dA2 = A1 * inv, dB1 = -S * (B2 * inv), dB2 = -S * (B1 * inv);
-      const size_t g = ((size_t)py * P.W + px) * 3 + c;
-      dmu[g] = 2.0 * my * dA1 + 2.0 * mx * dB1 - 2.0 * mx * dB2 - 2.0 * my * dA2;
-      dxx[g] = dB2;
-      dxy[g] = 2.0 * dA2;
-      if (smap) smap[g] = S;
-      const double xv = sx[(oy + r) * HW + ox + r], yv = sy[(oy + r) * HW + ox + r];
-      l1 += fabs(xv - yv);
-      ss += S;
+      #pragma unroll
+      for (int q = 0; q < kLossRows; ++q) {
+        const int oy = oy0 + q, py = y0 + oy;
+        if (px >= P.W || py >= P.H) continue;
+        const double mx = m[q][0], my = m[q][1], mxx = m[q][2], myy = m[q][3], mxy = m[q][4];
+        const double sxv = mxx - mx * mx, syv = myy - my * my, sxy = mxy - mx * my;
+        const double A1 = 2.0 * mx * my + P.c1, A2 = 2.0 * sxy + P.c2;
+        const double B1 = mx * mx + my * my + P.c1, B2 = sxv + syv + P.c2;
+        const double inv = 1.0 / (B1 * B2);
+        const double S = A1 * A2 * inv;
+        // 1 / B1 = B2 inv, 1 / B2 = B1 inv: one division
+        const double dA1 = A2 * inv, dA2 = A1 * inv, dB1 = -S * (B2 * inv), dB2 = -S * (B1 * inv);
+        const size_t g = ((size_t)py * P.W + px) * 3 + c;
+        dmu[g] = 2.0 * my * dA1 + 2.0 * mx * dB1 - 2.0 * mx * dB2 - 2.0 * my * dA2;
+        dxx[g] = dB2;
+        dxy[g] = 2.0 * dA2;
+        if (smap) smap[g] = S;
+        const double xv = sx[(oy + r) * HW + ox + r], yv = sy[(oy + r) * HW + ox + r];
+        l1 += fabs(xv - yv);
+        ss += S;
+      }
     }
     __syncthreads();
   }
@@ -185,9 +202,8 @@ __global__ void __launch_bounds__(kLossThreads, SGS_LOSS_MIN_BLOCKS) ssim_bwd_ke
   double* hs = s2 + HH * HW;  // 3 planes of HH x TW
   const int x0 = blockIdx.x * kLossTW, y0 = blockIdx.y * kLossTH;
   const int t = threadIdx.x;
-  const int ox = t % kLossTW, oy = t / kLossTW;
-  const int px = x0 + ox, py = y0 + oy;
-  const bool inside = px < P.W && py < P.H;
+  const int ox = t % kLossTW, oy0 = (t / kLossTW) * kLossRows;
+  const int px = x0 + ox;
   for (int c = 0; c < 3; ++c) {
     if (P.lam != 0.0) {
       for (int i = t; i < HH * HW; i += kLossThreads) {
@@ -229,25 +245,36 @@ __global__ void __launch_bounds__(kLossThreads, SGS_LOSS_MIN_BLOCKS) ssim_bwd_ke
       }
       __syncthreads();
     }
-    if (inside) {
-      const size_t g = ((size_t)py * P.W + px) * 3 + c;
-      const double xv = ld(img, g), yv = ld(tgt, g);
-      const double diff = xv - yv;
-      double out = (1.0 - P.lam) * (double)((diff > 0.0) - (diff < 0.0)) * P.inv_size;
+    {
+      // the thread's kLossRows outputs share their column's loads
+      double f[kLossRows][3] = {};
       if (P.lam != 0.0) {
-        double fa = 0, fb = 0, fd = 0;
         #pragma unroll
-        for (int k = 0; k <= 2 * r; ++k) {
-          const double wy = P.w[k];
-          const int o = (oy + k) * kLossTW + ox;
-          fa = fma(wy, hs[o], fa);
-          fb = fma(wy, hs[HH * kLossTW + o], fb);
-          fd = fma(wy, hs[2 * HH * kLossTW + o], fd);
+        for (int k = 0; k < 2 * r + kLossRows; ++k) {
+          const int o = (oy0 + k) * kLossTW + ox;
+          const double h0 = hs[o], h1 = hs[HH * kLossTW + o], h2 = hs[2 * HH * kLossTW + o];
+          #pragma unroll
+          for (int q = 0; q < kLossRows; ++q) {
+            if (k - q < 0 || k - q > 2 * r) continue;
+            const double wy = P.w[k - q];
+            f[q][0] = fma(wy, h0, f[q][0]);
+            f[q][1] = fma(wy, h1, f[q][1]);
+            f[q][2] = fma(wy, h2, f[q][2]);
+          }
         }
-        out -= P.lam * (fa + 2.0 * xv * fb + yv * fd) * P.inv_size;
       }
-      if (dimg) dimg[g] = (float)out;
-      if (dimg64) dimg64[g] = out;
+      #pragma unroll
+      for (int q = 0; q < kLossRows; ++q) {
+        const int py = y0 + oy0 + q;
+        if (px >= P.W || py >= P.H) continue;
+        const size_t g = ((size_t)py * P.W + px) * 3 + c;
+        const double xv = ld(img, g), yv = ld(tgt, g);
+        const double diff = xv - yv;
+        double out = (1.0 - P.lam) * (double)((diff > 0.0) - (diff < 0.0)) * P.inv_size;
+        if (P.lam != 0.0) out -= P.lam * (f[q][0] + 2.0 * xv * f[q][1] + yv * f[q][2]) * P.inv_size;
+        if (dimg) dimg[g] = (float)out;
+        if (dimg64) dimg64[g] = out;
+      }
     }
     if (P.lam != 0.0) __syncthreads();
   }
