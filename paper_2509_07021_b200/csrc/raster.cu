@@ -567,6 +567,9 @@ __global__ void __launch_bounds__(kFwdThreads, kImportance ? 1 : (kTrack ? SGS_F
 }
 
 constexpr int kGrad = 9;
+#ifndef SGS_BWD_MIN_BLOCKS
+#define SGS_BWD_MIN_BLOCKS 7
+#endif
 constexpr int kBwdThreads = 128;
 constexpr int kBwdCPT = 1;
 constexpr int kBwdChunk = kBwdThreads * kBwdCPT;  // candidates staged per batch
@@ -619,7 +622,7 @@ __device__ __forceinline__ int reduce9_index(int lane) {
 // partials with one global atomic per (record, partial).  T is recovered with one hardware reciprocal
 // per pixel-record, T_i = T_{i+1} rcp(1 - alpha_i) (~1 ulp per record).
 template <bool kFilter>
-__global__ void __launch_bounds__(kBwdThreads) raster_bwd_kernel(ListArgs la, SgsCam cam, float3 bg,
+__global__ void __launch_bounds__(kBwdThreads, SGS_BWD_MIN_BLOCKS) raster_bwd_kernel(ListArgs la, SgsCam cam, float3 bg,
                                                                  const float* __restrict__ final_T,
                                                                  const uint32_t* __restrict__ ncontrib,
                                                                  const float* __restrict__ dimg,
