@@ -1,0 +1,45 @@
+"""bench.py keeps the driver's JSON-line contract: the reference arm on the
+host (CPU) and our arm on a B200 (gpu marker)."""
+
+import json
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+BASE_KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+             "scaling", "vs_baseline", "dtype", "data", "config", "e2e"}
+
+
+def _run(args, timeout):
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), *args], cwd=ROOT, capture_output=True,
+                         text=True, timeout=timeout)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    return json.loads(lines[0])
+
+
+def test_reference_arm_line():
+    d = _run(["--impl", "reference", "--steps", "1", "--warmup", "0"], timeout=600)
+    assert BASE_KEYS <= d.keys()
+    assert d["impl"] == "reference" and d["value"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+    assert {"value", "unit", "cores", "kind", "sample"} <= d["cpu_baseline"].keys()
+    assert d["cpu_baseline"]["kind"] in ("port", "reference")
+
+
+@pytest.mark.gpu
+def test_our_arm_line():
+    d = _run(["--steps", "2", "--warmup", "3", "--views", "2", "--no-cpu-baseline"], timeout=900)
+    assert BASE_KEYS <= d.keys()
+    assert d["value"] > 0 and d["n_gpus"] == 1 and d["steps"] == 2 and d["warmup"] == 3
+    assert {"bound", "achieved", "peak", "unit", "frac", "traffic"} <= d["roofline"].keys()
+    assert 0 < d["roofline"]["frac"] < 2
+    assert {"value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"} <= d["e2e"].keys()
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    assert d["gpu_launches"] > 0
+    assert {"sm_mhz", "sm_max_mhz", "reasons"} <= d["clocks"].keys()
+    assert "workload" in d["config"]
