@@ -51,7 +51,15 @@ class BatchRenderer:
     host-to-device stream, so with ``wait=False`` the upload of the next
     call's scene overlaps the renders and image read-backs of this one (the
     copy engines run both directions at once).  Every call still moves its
-    whole scene host -> device and every image device -> host."""
+    whole scene host -> device and every image device -> host.
+
+    Images are never silently truncated: every view's tile-entry overflow
+    counter is gathered on the device and read once per call.  A view that
+    outgrew its capacity grows it (dropping the graphs captured against the
+    smaller workspace) and is re-rendered with the checked forward into the
+    same host buffer -- at the end of the call with ``wait=True``, or, with
+    ``wait=False``, when the call's slot is next used (the call after next)
+    or at ``finish()``."""
 
     def __init__(self, rast: Rasterizer | None = None, device="cuda", streams: int = 4,
                  graphs: bool = True):
@@ -62,10 +70,14 @@ class BatchRenderer:
         self.streams = [torch.cuda.Stream(device=self.device) for _ in range(max(streams, 1))]
         self._host = {}
         self._dev = [None, None]      # two device copies of the scene
-        self._free = [None, None]     # event: renders of the copy's last use finished
+        self._free = [None, None]     # event: renders AND read-backs of the copy's last use finished
+        self._pending = [None, None]  # per slot: the unchecked overflow state of its last call
+        self._ovf_dev = {}
+        self._ovf_host = {}
         self._calls = 0
         self.graphs = graphs          # replay each (copy, view) render from a CUDA graph
         self._dev_out = {}
+        self.rerendered = 0           # views re-rendered after an overflow (diagnostics)
 
     def _host_buf(self, k, shape):
         buf = self._host.get(k)
@@ -74,11 +86,22 @@ class BatchRenderer:
             self._host[k] = buf
         return buf
 
+    def _ovf_bufs(self, slot: int, n: int):
+        d = self._ovf_dev.get(slot)
+        if d is None or d.shape[0] < n:
+            d = torch.zeros((max(n, 1), 2), dtype=torch.int64, device=self.device)
+            self._ovf_dev[slot] = d
+            self._ovf_host[slot] = torch.zeros((max(n, 1), 2), dtype=torch.int64, pin_memory=True)
+        return self._ovf_dev[slot], self._ovf_host[slot]
+
     def _upload(self, scene: PinnedScene, slot: int) -> GaussianTensors:
         dev = self._dev[slot]
         if dev is None or any(tuple(getattr(dev, f).shape) != tuple(t.shape)
-                              for f, t in scene.arrays.items()):
+                              for f, t in scene.arrays.items()) or \
+                (dev.prim_mask is None) != (scene.prim_mask is None):
             with torch.cuda.stream(self.h2d_stream):
+                if self._free[slot] is not None:
+                    self.h2d_stream.wait_event(self._free[slot])
                 arrs = {f: torch.empty(t.shape, dtype=torch.float32, device=self.device)
                         for f, t in scene.arrays.items()}
                 pm = None if scene.prim_mask is None else torch.empty(
@@ -94,20 +117,54 @@ class BatchRenderer:
                 dev.prim_mask.copy_(scene.prim_mask, non_blocking=True)
         return dev
 
+    def _resolve(self, slot: int) -> None:
+        """Check the overflow counters of the slot's last call (its device
+        scene copy is still intact) and re-render every view that outgrew
+        its capacity into that call's host buffer."""
+        pend = self._pending[slot]
+        if pend is None:
+            return
+        self._pending[slot] = None
+        done, ovf_host, cams, outs, background = pend
+        done.synchronize()
+        o = ovf_host[:len(cams)].numpy()
+        bad = [k for k in range(len(cams)) if o[k, 0]]
+        if not bad:
+            return
+        g = self._dev[slot]
+        for k in bad:
+            self.rast.grow_capacity(g, cams[k], int(o[k, 1]))
+        main = torch.cuda.current_stream(self.device)
+        for k in bad:
+            img = self.rast.forward(g, cams[k], background, check=True, track=False).img
+            outs[k].copy_(img)
+            self.rerendered += 1
+        main.synchronize()
+
+    def finish(self) -> None:
+        """Wait for every call in flight and resolve its overflow checks:
+        after this, every image a ``wait=False`` call returned is final."""
+        torch.cuda.synchronize(self.device)
+        for slot in (0, 1):
+            self._resolve(slot)
+
     def render_views(self, scene: PinnedScene, cams, background=(0.0, 0.0, 0.0), check=False,
                      wait: bool = True):
         """Upload the scene, render every view (spread over the render streams
         so binning of one view overlaps the raster of another), copy each
         image back as soon as it is done; returns the pinned host images.
         With ``wait=False`` the call returns once everything is enqueued: the
-        images are complete after the next device synchronisation, and the
-        host buffers are reused by the call after next."""
+        images are complete after ``finish()`` or once the call after next
+        returns (the host buffers are then reused by the call after that)."""
+        cams = list(cams)
         slot = self._calls % 2
         self._calls += 1
+        self._resolve(slot)  # the slot's last call: overflow checked before its copy is reused
         main = torch.cuda.current_stream(self.device)
-        g = self._upload(scene, slot)  # waits only for the renders that last used this copy
+        g = self._upload(scene, slot)  # waits for the renders and read-backs of the copy's last use
         up = torch.cuda.Event()
         up.record(self.h2d_stream)
+        ovf_dev, ovf_host = self._ovf_bufs(slot, len(cams))
         outs = []
         for k, cam in enumerate(cams):
             s = self.streams[k % len(self.streams)]
@@ -120,10 +177,12 @@ class BatchRenderer:
                         buf = (torch.empty((H, W, 3), dtype=torch.float32, device=self.device),
                                torch.empty((H, W), dtype=torch.float32, device=self.device))
                         self._dev_out[(slot, k)] = buf
-                    self.rast.graph_forward(g, cam, buf, background)
+                    ovf_dev[k].copy_(self.rast.graph_forward(g, cam, buf, background))
                     img = buf[0]
                 else:
-                    img = self.rast.forward(g, cam, background, check=check, track=False).img
+                    fr = self.rast.forward(g, cam, background, check=check, track=False)
+                    fr.record_overflow(ovf_dev[k])
+                    img = fr.img
                 done = torch.cuda.Event()
                 done.record(s)
             host = self._host_buf((slot, k), tuple(img.shape))
@@ -132,15 +191,21 @@ class BatchRenderer:
                 host.copy_(img, non_blocking=True)
                 img.record_stream(self.copy_stream)
             outs.append(host)
-        # the device copy may be overwritten once this call's renders are done
-        freed = torch.cuda.Event()
         for s in self.streams:
-            main.wait_stream(s)
+            self.copy_stream.wait_stream(s)
+        with torch.cuda.stream(self.copy_stream):
+            ovf_host[:len(cams)].copy_(ovf_dev[:len(cams)], non_blocking=True)
+        ready = torch.cuda.Event()
+        ready.record(self.copy_stream)
+        # the device copy and the device image buffers may be overwritten once
+        # this call's renders AND its read-backs are done
+        main.wait_stream(self.copy_stream)
+        freed = torch.cuda.Event()
         freed.record(main)
         self._free[slot] = freed
-        main.wait_stream(self.copy_stream)
+        self._pending[slot] = (ready, ovf_host, cams, outs, background)
         if wait:
-            main.synchronize()
+            self._resolve(slot)
         return outs
 
     @staticmethod

@@ -12,6 +12,7 @@ GradientSet / VramEstimate types when those exist.
 
 from __future__ import annotations
 
+import importlib
 import sys
 
 from . import postprocess as _post
@@ -30,6 +31,13 @@ def _wrap_grads(ref_mod, gs):
 def install(package: str = "sgsplat") -> list[str]:
     """Route sgsplat's render hot path through libsgs.so; returns what was patched."""
     __import__(package)
+    # every module that binds a hot-path name (prune.py:20, postprocess.py:17,
+    # toy.py:15, cli.py:29); the package __init__ imports all but cli
+    for sub in ("render", "prune", "postprocess", "toy", "cli"):
+        try:
+            importlib.import_module(f"{package}.{sub}")
+        except ImportError:  # pragma: no cover - optional entry points (cli needs pillow)
+            pass
     ref_render = sys.modules[f"{package}.render"]
     patched = []
 

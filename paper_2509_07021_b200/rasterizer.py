@@ -168,6 +168,17 @@ class Frame:
 MAX_CAPACITY = (1 << 30) - 1
 
 
+@dataclass
+class _GraphEntry:
+    """A captured image-only forward and everything its raw pointers refer to."""
+
+    graph: "torch.cuda.CUDAGraph"
+    ws: Workspace
+    key: tuple                 # (n, lobes, W, H): the capacity-hint key
+    ovf: torch.Tensor          # int64 (overflow, binned entries), written by each replay
+    keep: tuple                # scene and output tensors the graph reads / writes
+
+
 class Rasterizer:
     """Reusable render context (workspace cache + capacity policy)."""
 
@@ -195,7 +206,9 @@ class Rasterizer:
     def workspace(self, g, cam, private=False, capacity=None) -> Workspace:
         """The shared workspace for this (scene size, image size) on the
         current stream (one per stream, so views on different streams render
-        concurrently), or a private one."""
+        concurrently), or a private one.  A shared workspace that is too small
+        is replaced; CUDA graphs captured against it are dropped first (they
+        hold its raw pointers), see _retire."""
         key = self._key(g, cam)
         cap = capacity if capacity is not None else self._capacity(key, g)
         if private:
@@ -203,19 +216,47 @@ class Rasterizer:
         skey = key + (_stream_ptr(),)
         ws = self._shared.get(skey)
         if ws is None or ws.capacity < cap:
+            if ws is not None:
+                self._retire(ws)
             self._shared.pop(skey, None)
             ws = Workspace(*key[:4], cap, self.sort_mode, self.device)
             self._shared[skey] = ws
         return ws
 
+    def _retire(self, ws: Workspace) -> None:
+        """Drop every captured graph bound to ``ws`` before the workspace can
+        be freed.  Graph workspaces are allocated on a capture stream but
+        replayed on the caller's, so the device is synchronised first: no
+        replay may still be writing into the buffer the allocator is about
+        to hand out again."""
+        graphs = self.__dict__.get("_graphs", {})
+        dead = [k for k, e in graphs.items() if e.ws is ws]
+        if dead:
+            torch.cuda.synchronize(self.device)
+            for k in dead:
+                del graphs[k]
+
+    def _set_hint(self, key, need: int) -> None:
+        """Raise (never lower) the capacity hint for ``key``; captured graphs
+        whose workspace is now too small are dropped and recaptured on their
+        next use."""
+        cap = max(self._cap_hint.get(key, 0), min(MAX_CAPACITY, int(need)))
+        self._cap_hint[key] = cap
+        graphs = self.__dict__.get("_graphs", {})
+        small = [k for k, e in graphs.items() if e.key == key and e.ws.capacity < cap]
+        if small:
+            torch.cuda.synchronize(self.device)
+            for k in small:
+                del graphs[k]
+
     def grow_capacity(self, g, cam, n_entries: int) -> None:
         """Size the tile-entry capacity for ``n_entries`` binned entries (the
-        deferred form of forward(check=True)'s retry)."""
+        deferred form of forward(check=True)'s retry).  The hint only grows:
+        several views overflowing in one pass keep the largest need."""
         if n_entries > MAX_CAPACITY:
             raise _ffi.CapacityError("sgs_bin", _ffi.SGS_E_CAPACITY,
                                      f"{n_entries} entries exceed one bin call's limit {MAX_CAPACITY}")
-        key = self._key(g, cam)
-        self._cap_hint[key] = min(MAX_CAPACITY, int(n_entries * self.headroom) + 1024)
+        self._set_hint(self._key(g, cam), int(n_entries * self.headroom) + 1024)
 
     def release(self):
         self.release_graphs()
@@ -267,7 +308,7 @@ class Rasterizer:
                             "sgs_bin", _ffi.SGS_E_CAPACITY,
                             f"{st['n_bin_entries']} entries exceed one bin call's limit "
                             f"{MAX_CAPACITY}; render in tile-row strips")
-                    self._cap_hint[key] = min(MAX_CAPACITY, need)
+                    self._set_hint(key, need)
                     continue
             break
         if _events is not None:
@@ -280,22 +321,29 @@ class Rasterizer:
 
     # ------------------------------------------------------- graph forward
     def graph_forward(self, g: GaussianTensors, cam, out, background=(0.0, 0.0, 0.0),
-                      tile_rows=None) -> None:
+                      tile_rows=None) -> torch.Tensor:
         """Image-only forward of one view replayed from a CUDA graph on the
         current stream (one graph launch instead of ~20 kernel launches and
         ~3 FFI calls of host work per view).  The graph is captured on first
         use for this (scene buffers, camera, output buffers, stream) and
         re-reads the scene tensors at every replay, so in-place parameter
-        updates are seen.  ``out`` = (img, T) device tensors.  The tile-entry
-        capacity is sized before capture; a later frame that outgrows it
-        sets the overflow counter (Frame.stats / ensure via forward(check=True))."""
+        updates are seen.  ``out`` = (img, T) device tensors.
+
+        The entry keeps references to everything the graph writes or reads
+        (workspace, scene and output tensors), so none of them can be freed
+        and reused under it; a capacity growth drops the graphs bound to the
+        smaller workspace (_retire / _set_hint).  Returns the entry's int64
+        (overflow, binned entries) device pair, written by the replay: a
+        frame denser than the capacity the graph was captured with sets it,
+        and the caller must check it (BatchRenderer does, once per call)."""
         c = to_sgs(cam, tile_rows)
         stream = torch.cuda.current_stream(self.device)
-        key = (bytes(c), g.position.data_ptr(), g.n, g.n_lobes, out[0].data_ptr(), out[1].data_ptr(),
-               stream.cuda_stream, tuple(float(v) for v in background))
+        scene_t = tuple(getattr(g, f) for f in GRAD_FIELDS + ("lobe_mask",)) + (g.prim_mask,)
+        key = (bytes(c), tuple(_ptr(t) for t in scene_t), g.n, g.n_lobes, out[0].data_ptr(),
+               out[1].data_ptr(), stream.cuda_stream, tuple(float(v) for v in background))
         graphs = self.__dict__.setdefault("_graphs", {})
-        gr = graphs.get(key)
-        if gr is None:
+        e = graphs.get(key)
+        if e is None:
             # capture on a private (non-default) stream paired with the caller's
             # stream; its workspace belongs to that pairing, so graphs replayed
             # concurrently on different streams never share scratch
@@ -305,19 +353,25 @@ class Rasterizer:
                 cap = torch.cuda.Stream(device=self.device)
                 caps[stream.cuda_stream] = cap
             cap.wait_stream(stream)
+            ovf = torch.zeros(2, dtype=torch.int64, device=self.device)
             with torch.cuda.stream(cap):
                 self.forward(g, cam, background, check=True, tile_rows=tile_rows,
                              out=(out[0], out[1], None), track=False)
             cap.synchronize()
             gr = torch.cuda.CUDAGraph()
             with torch.cuda.graph(gr, stream=cap):
-                self.forward(g, cam, background, check=False, tile_rows=tile_rows,
-                             out=(out[0], out[1], None), track=False)
+                fr = self.forward(g, cam, background, check=False, tile_rows=tile_rows,
+                                  out=(out[0], out[1], None), track=False)
+                fr.record_overflow(ovf)
             stream.wait_stream(cap)
-            graphs[key] = gr
-        gr.replay()
+            e = _GraphEntry(gr, fr.ws, self._key(g, cam), ovf, scene_t + tuple(out))
+            graphs[key] = e
+        e.graph.replay()
+        return e.ovf
 
     def release_graphs(self):
+        if self.__dict__.get("_graphs"):
+            torch.cuda.synchronize(self.device)
         self.__dict__.pop("_graphs", None)
 
     # ----------------------------------------------------------------- backward

@@ -38,7 +38,20 @@ def rng():
 
 
 REFERENCE_SRC = Path("/root/reference/pkg/src")
+# the reference package installed unmodified by `pip install --target
+# baseline/_ref` (git-ignored; it travels to the GPU box with the repo)
+REFERENCE_INSTALL = ROOT / "baseline" / "_ref"
 
 
 def reference_available() -> bool:
     return (REFERENCE_SRC / "sgsplat" / "render.py").exists()
+
+
+def reference_package_path():
+    """Directory to put on sys.path to import the reference package
+    ``sgsplat`` (the unmodified install under baseline/_ref, else the
+    read-only source tree in the build container), or None."""
+    for p in (REFERENCE_INSTALL, REFERENCE_SRC):
+        if (p / "sgsplat" / "render.py").exists():
+            return p
+    return None

@@ -182,6 +182,33 @@ def gen_crop(name, cfg, cam_index, x0, y0, w, h):
          cam_index=np.array(cam_index), crop=np.array([x0, y0, w, h]), **cam_dict(cam))
 
 
+def gen_aniso_grads():
+    """Anisotropic gradients (configs[4] scale distribution: one log-scale axis
+    N(-2.5, 0.5), two N(-5, 0.5)): loss_and_grads (default L1 + 0.2 SSIM) on a
+    32x24 crop of the 4K camera, for the primitives of config4(n=500k) whose
+    opacity-aware support box (q <= 2 ln(o/1e-7)) meets the crop.  Checks the
+    backward's projection chain on elongated splats."""
+    from oracle import ref_dense
+    s, (cam0,) = scenes.config4(n=500_000)
+    x0, y0, w, h = 1200, 700, 32, 24
+    pr = ref_dense.project(s, cam0)
+    o = np.asarray(s.opacity, np.float64)[pr.idx]
+    qmax = np.maximum(2 * np.log(np.maximum(o, 1e-30) / 1e-7), 0.0)
+    hx, hy = np.sqrt(qmax * pr.cov[:, 0, 0]) + 1, np.sqrt(qmax * pr.cov[:, 1, 1]) + 1
+    mx, my = pr.mean[:, 0], pr.mean[:, 1]
+    m = (qmax > 0) & (mx + hx > x0) & (mx - hx < x0 + w) & (my + hy > y0) & (my - hy < y0 + h)
+    idx = np.sort(pr.idx[m]).astype(np.int64)
+    sub = s.subset(idx)
+    cam = cam0.crop(x0, y0, w, h)
+    tgt = scenes.target_image(4, cam.height, cam.width)
+    p = ref_params(sub)
+    val, g = R.loss_and_grads(p, ref_cam(cam), tgt.astype(np.float64), R.LossConfig())
+    img = R._render_params(p, ref_cam(cam), (0.0, 0.0, 0.0))
+    out = {f"g_{f}": getattr(g, f) for f in FIELDS}
+    save("aniso_grads", idx=idx, img=img, target=tgt, loss=np.array(val), digest=np.array(digest(s)),
+         crop=np.array([x0, y0, w, h]), **out, **cam_dict(cam))
+
+
 def gen_vram():
     """estimate_vram (postprocess.py:101-137) on seeded random scenes."""
     out = {}
@@ -288,6 +315,17 @@ GENERATORS = {
     "cfg3_crop": lambda: gen_crop("cfg3_crop", 3, 0, 632, 352, 16, 16),
     "cfg1_crop": lambda: gen_crop("cfg1_crop", 1, 0, 632, 352, 24, 16),
     "cfg4_crop": lambda: gen_crop("cfg4_crop", 4, 0, 1912, 1072, 8, 8),
+    # round 2: three reference crops per config, other
+    # cameras and positions, incl. the configs[4] cluster centre at 16x16
+    "cfg1_crop_b": lambda: gen_crop("cfg1_crop_b", 1, 0, 200, 150, 16, 16),
+    "cfg1_crop_c": lambda: gen_crop("cfg1_crop_c", 1, 0, 1000, 560, 16, 16),
+    "cfg2_crop_b": lambda: gen_crop("cfg2_crop_b", 2, 21, 400, 300, 16, 16),
+    "cfg2_crop_c": lambda: gen_crop("cfg2_crop_c", 2, 45, 1500, 800, 16, 16),
+    "cfg3_crop_b": lambda: gen_crop("cfg3_crop_b", 3, 3, 300, 200, 16, 16),
+    "cfg3_crop_c": lambda: gen_crop("cfg3_crop_c", 3, 6, 900, 500, 16, 16),
+    "cfg4_crop_b": lambda: gen_crop("cfg4_crop_b", 4, 0, 1904, 1064, 16, 16),
+    "cfg4_crop_c": lambda: gen_crop("cfg4_crop_c", 4, 0, 1200, 700, 16, 16),
+    "aniso_grads": gen_aniso_grads,
 }
 
 if __name__ == "__main__":
