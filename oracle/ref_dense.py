@@ -226,12 +226,20 @@ def backward(p, cam, pr, dimg, background=(0.0, 0.0, 0.0), block=1024):
         return out
     bg = _f64(background).reshape(3)
     g_all = _f64(dimg).reshape(-1, 3)
+    px, py = _pixels(cam)
+    acc = _backward_pixels(pr, g_all, px, py, bg, block)
+    _backward_chain(p, cam, pr, acc, out)
+    return out
+
+
+def _backward_pixels(pr, g_all, px, py, bg, block=1024):
+    """Per-primitive image-space partials (d colour, d o_eff, d mean, d conic)
+    accumulated over the given pixels (render.py:535-573)."""
     V = pr.idx.size
     d_col = np.zeros((V, 3))
     d_oe = np.zeros(V)
     d_mean = np.zeros((V, 2))
     d_con = np.zeros((V, 2, 2))
-    px, py = _pixels(cam)
     for s in range(0, px.size, block):
         b = _blend_block(pr, px[s:s + block], py[s:s + block])
         g = g_all[s:s + block]
@@ -252,7 +260,13 @@ def backward(p, cam, pr, dimg, background=(0.0, 0.0, 0.0), block=1024):
         d_con[:, 0, 1] += xy
         d_con[:, 1, 0] += xy
         d_con[:, 1, 1] += (dq * b["dy"] ** 2).sum(axis=1)
+    return d_col, d_oe, d_mean, d_con
 
+
+def _backward_chain(p, cam, pr, acc, out):
+    """Chain rule from the image-space partials to every parameter class
+    (render.py:575-637), scattered into ``out``."""
+    d_col, d_oe, d_mean, d_con = acc
     Wm = _f64(cam.rotation).reshape(3, 3)
     d_cov = -pr.conic @ d_con @ pr.conic
     MT = np.swapaxes(pr.M, 1, 2)
@@ -295,7 +309,75 @@ def backward(p, cam, pr, dimg, background=(0.0, 0.0, 0.0), block=1024):
     out["sharpness"][i] = d_sh
     out["amplitude"][i] = d_amp
     out["lobe_mask"][i] = da * pr.e
-    return out
+
+
+# ------------------------------------------- all host cores (CPU baseline)
+_POOL_STATE: dict = {}
+
+
+def _pool_render(job):
+    s, e = job
+    st = _POOL_STATE
+    px, py = st["px"][s:e], st["py"][s:e]
+    b = _blend_block(st["pr"], px, py)
+    return s, b["w"].T @ st["pr"].color + b["tbg"][:, None] * st["bg"]
+
+
+def _pool_backward(job):
+    s, e = job
+    st = _POOL_STATE
+    return _backward_pixels(st["pr"], st["g"][s:e], st["px"][s:e], st["py"][s:e], st["bg"], st["block"])
+
+
+def _jobs(npx, procs, block):
+    per = max(block, -(-npx // (4 * procs)) // block * block or block)
+    return [(s, min(s + per, npx)) for s in range(0, npx, per)]
+
+
+def render_parallel(p, cam, procs, background=(0.0, 0.0, 0.0), block=512):
+    """``render`` with the pixel blocks spread over ``procs`` forked host
+    processes (same arithmetic per pixel; used for CPU-baseline timing)."""
+    import multiprocessing as mp
+    bg = _f64(background).reshape(3)
+    pr = project(p, cam)
+    out = np.empty((cam.height * cam.width, 3))
+    if pr is None:
+        out[:] = bg
+        return out.reshape(cam.height, cam.width, 3)
+    px, py = _pixels(cam)
+    _POOL_STATE.update(pr=pr, px=px, py=py, bg=bg)
+    with mp.get_context("fork").Pool(procs) as pool:
+        for s, blk in pool.imap_unordered(_pool_render, _jobs(px.size, procs, block)):
+            out[s:s + blk.shape[0]] = blk
+    _POOL_STATE.clear()
+    return out.reshape(cam.height, cam.width, 3)
+
+
+def loss_and_grads_parallel(p, cam, target, procs, lambda_ssim=0.2, background=(0.0, 0.0, 0.0), block=512):
+    """``loss_and_grads`` with the forward and the per-pixel backward spread
+    over ``procs`` forked host processes; the partial sums are added and the
+    parameter chain runs once."""
+    import multiprocessing as mp
+    img = render_parallel(p, cam, procs, background, block)
+    val, dimg = loss_and_dimg(img, _f64(target), lambda_ssim)
+    n, L = _f64(p.position).shape[0], _f64(p.axis_raw).shape[1]
+    out = {"position": np.zeros((n, 3)), "quat": np.zeros((n, 4)), "log_scale": np.zeros((n, 3)),
+           "opacity": np.zeros(n), "diffuse": np.zeros((n, 3)), "axis_raw": np.zeros((n, L, 3)),
+           "sharpness": np.zeros((n, L)), "amplitude": np.zeros((n, L, 3)),
+           "lobe_mask": np.zeros((n, L)), "prim_mask": np.zeros(n)}
+    pr = project(p, cam)
+    if pr is None:
+        return val, out, img
+    px, py = _pixels(cam)
+    _POOL_STATE.update(pr=pr, px=px, py=py, bg=_f64(background).reshape(3), g=_f64(dimg).reshape(-1, 3),
+                       block=block)
+    acc = None
+    with mp.get_context("fork").Pool(procs) as pool:
+        for part in pool.imap_unordered(_pool_backward, _jobs(px.size, procs, block)):
+            acc = part if acc is None else tuple(a + b for a, b in zip(acc, part))
+    _POOL_STATE.clear()
+    _backward_chain(p, cam, pr, acc, out)
+    return val, out, img
 
 
 def loss_and_grads(p, cam, target, lambda_ssim=0.2, background=(0.0, 0.0, 0.0)):

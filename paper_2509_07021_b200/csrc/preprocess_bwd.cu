@@ -47,97 +47,111 @@ __global__ void __launch_bounds__(128) preprocess_bwd_kernel(sgs_params P, SgsCa
     const float pm = P.prim_mask ? P.prim_mask[i] : 1.0f;
 
     if (any) {
-      // ---------------- forward recompute
-      const float x = Wr[0] * pos[0] + Wr[1] * pos[1] + Wr[2] * pos[2] + cam.t[0];
-      const float y = Wr[3] * pos[0] + Wr[4] * pos[1] + Wr[5] * pos[2] + cam.t[1];
-      const float z = Wr[6] * pos[0] + Wr[7] * pos[1] + Wr[8] * pos[2] + cam.t[2];
+      // ---------------- forward recompute, float64 like K1's projection
+      // (sgs_geom.h sgs_project): for elongated splats cov2d is nearly
+      // singular before the low-pass floor, and the conic and the chain
+      // d cov = -K dK K amplify float32 cancellation far beyond rtol 1e-3.
+      const double p0 = pos[0], p1 = pos[1], p2 = pos[2];
+      const double x = (double)Wr[0] * p0 + (double)Wr[1] * p1 + (double)Wr[2] * p2 + (double)cam.t[0];
+      const double y = (double)Wr[3] * p0 + (double)Wr[4] * p1 + (double)Wr[5] * p2 + (double)cam.t[1];
+      const double z = (double)Wr[6] * p0 + (double)Wr[7] * p1 + (double)Wr[8] * p2 + (double)cam.t[2];
       const float4 q4 = reinterpret_cast<const float4*>(P.quat)[i];
-      const float qn = sqrtf(q4.x * q4.x + q4.y * q4.y + q4.z * q4.z + q4.w * q4.w);
-      const float qw = q4.x / qn, qx = q4.y / qn, qy = q4.z / qn, qz = q4.w / qn;
-      float R[9];
-      sgs_quat_to_rot(qw, qx, qy, qz, R);
-      float D[3];
-      for (int k = 0; k < 3; ++k) D[k] = expf(2.0f * P.log_scale[3 * i + k]);
-      float S[9];
+      const double qn = sqrt((double)q4.x * q4.x + (double)q4.y * q4.y + (double)q4.z * q4.z + (double)q4.w * q4.w);
+      const double qw = q4.x / qn, qx = q4.y / qn, qy = q4.z / qn, qz = q4.w / qn;
+      double R[9];
+      R[0] = 1.0 - 2.0 * (qy * qy + qz * qz);
+      R[1] = 2.0 * (qx * qy - qw * qz);
+      R[2] = 2.0 * (qx * qz + qw * qy);
+      R[3] = 2.0 * (qx * qy + qw * qz);
+      R[4] = 1.0 - 2.0 * (qx * qx + qz * qz);
+      R[5] = 2.0 * (qy * qz - qw * qx);
+      R[6] = 2.0 * (qx * qz - qw * qy);
+      R[7] = 2.0 * (qy * qz + qw * qx);
+      R[8] = 1.0 - 2.0 * (qx * qx + qy * qy);
+      double D[3];
+      for (int k = 0; k < 3; ++k) D[k] = exp(2.0 * (double)P.log_scale[3 * i + k]);
+      double S[9];
       for (int a = 0; a < 3; ++a)
         for (int b = 0; b < 3; ++b)
           S[3 * a + b] = R[3 * a] * D[0] * R[3 * b] + R[3 * a + 1] * D[1] * R[3 * b + 1] + R[3 * a + 2] * D[2] * R[3 * b + 2];
-      const float iz = 1.0f / z, iz2 = iz * iz;
-      const float J00 = cam.fx * iz, J02 = -cam.fx * x * iz2, J11 = cam.fy * iz, J12 = -cam.fy * y * iz2;
-      float M[6];
+      const double iz = 1.0 / z, iz2 = iz * iz;
+      const double fxd = cam.fx, fyd = cam.fy;
+      const double J00 = fxd * iz, J02 = -fxd * x * iz2, J11 = fyd * iz, J12 = -fyd * y * iz2;
+      double M[6];
       for (int k = 0; k < 3; ++k) {
         M[k] = J00 * Wr[k] + J02 * Wr[6 + k];
         M[3 + k] = J11 * Wr[3 + k] + J12 * Wr[6 + k];
       }
-      float MS[6];  // M Sigma
+      double MS[6];  // M Sigma
       for (int r = 0; r < 2; ++r)
         for (int k = 0; k < 3; ++k)
           MS[3 * r + k] = M[3 * r] * S[k] + M[3 * r + 1] * S[3 + k] + M[3 * r + 2] * S[6 + k];
-      const float ca = MS[0] * M[0] + MS[1] * M[1] + MS[2] * M[2] + cam.lowpass;
-      const float cb = MS[0] * M[3] + MS[1] * M[4] + MS[2] * M[5];
-      const float cc = MS[3] * M[3] + MS[4] * M[4] + MS[5] * M[5] + cam.lowpass;
-      const float det = ca * cc - cb * cb;
-      const float k00 = cc / det, k01 = -cb / det, k11 = ca / det;
+      const double lp = cam.lowpass;
+      const double ca = MS[0] * M[0] + MS[1] * M[1] + MS[2] * M[2] + lp;
+      const double cb = MS[0] * M[3] + MS[1] * M[4] + MS[2] * M[5];
+      const double cc = MS[3] * M[3] + MS[4] * M[4] + MS[5] * M[5] + lp;
+      const double idet = 1.0 / (ca * cc - cb * cb);
+      const double k00 = cc * idet, k01 = -cb * idet, k11 = ca * idet;
 
       // ---------------- 2D partials
-      const float m0 = gv[3], m1x = gv[4], m1y = gv[5], m2xx = gv[6], m2xy = gv[7], m2yy = gv[8];
-      const float dmx = -2.0f * (k00 * m1x + k01 * m1y);
-      const float dmy = -2.0f * (k01 * m1x + k11 * m1y);
+      const double m0 = gv[3], m1x = gv[4], m1y = gv[5], m2xx = gv[6], m2xy = gv[7], m2yy = gv[8];
+      const double dmx = -2.0 * (k00 * m1x + k01 * m1y);
+      const double dmy = -2.0 * (k01 * m1x + k11 * m1y);
       const float oeff = op * pm;
-      const float d_oeff = oeff > 0.0f ? -2.0f * m0 / oeff : 0.0f;
+      const float d_oeff = oeff > 0.0f ? (float)(-2.0 * m0 / (double)oeff) : 0.0f;
       d_op = pm * d_oeff;
       d_pm = op * d_oeff;
       // d_cov = -K dK K (K = conic, dK symmetric with off-diagonals m2xy)
-      const float t00 = k00 * m2xx + k01 * m2xy, t01 = k00 * m2xy + k01 * m2yy;
-      const float t10 = k01 * m2xx + k11 * m2xy, t11 = k01 * m2xy + k11 * m2yy;
-      const float dc00 = -(t00 * k00 + t01 * k01), dc01 = -(t00 * k01 + t01 * k11);
-      const float dc10 = -(t10 * k00 + t11 * k01), dc11 = -(t10 * k01 + t11 * k11);
+      const double t00 = k00 * m2xx + k01 * m2xy, t01 = k00 * m2xy + k01 * m2yy;
+      const double t10 = k01 * m2xx + k11 * m2xy, t11 = k01 * m2xy + k11 * m2yy;
+      const double dc00 = -(t00 * k00 + t01 * k01), dc01 = -(t00 * k01 + t01 * k11);
+      const double dc10 = -(t10 * k00 + t11 * k01), dc11 = -(t10 * k01 + t11 * k11);
       // dSigma = M^T dcov M ; dM = 2 dcov M Sigma (dcov symmetric)
-      float dS[9];
+      double dS[9];
       for (int a = 0; a < 3; ++a)
         for (int b = 0; b < 3; ++b)
           dS[3 * a + b] = M[a] * (dc00 * M[b] + dc01 * M[3 + b]) + M[3 + a] * (dc10 * M[b] + dc11 * M[3 + b]);
-      float dM[6];
+      double dM[6];
       for (int k = 0; k < 3; ++k) {
-        dM[k] = 2.0f * (dc00 * MS[k] + dc01 * MS[3 + k]);
-        dM[3 + k] = 2.0f * (dc10 * MS[k] + dc11 * MS[3 + k]);
+        dM[k] = 2.0 * (dc00 * MS[k] + dc01 * MS[3 + k]);
+        dM[3 + k] = 2.0 * (dc10 * MS[k] + dc11 * MS[3 + k]);
       }
       // dJ = dM W^T (only J00, J02, J11, J12 are live)
-      const float dJ00 = dM[0] * Wr[0] + dM[1] * Wr[1] + dM[2] * Wr[2];
-      const float dJ02 = dM[0] * Wr[6] + dM[1] * Wr[7] + dM[2] * Wr[8];
-      const float dJ11 = dM[3] * Wr[3] + dM[4] * Wr[4] + dM[5] * Wr[5];
-      const float dJ12 = dM[3] * Wr[6] + dM[4] * Wr[7] + dM[5] * Wr[8];
-      const float iz3 = iz2 * iz;
-      float dpc0 = dJ02 * (-cam.fx * iz2) + dmx * cam.fx * iz;
-      float dpc1 = dJ12 * (-cam.fy * iz2) + dmy * cam.fy * iz;
-      float dpc2 = dJ00 * (-cam.fx * iz2) + dJ11 * (-cam.fy * iz2) + dJ02 * (2.0f * cam.fx * x * iz3) +
-                   dJ12 * (2.0f * cam.fy * y * iz3) - dmx * cam.fx * x * iz2 - dmy * cam.fy * y * iz2;
-      for (int k = 0; k < 3; ++k) d_pos[k] = Wr[k] * dpc0 + Wr[3 + k] * dpc1 + Wr[6 + k] * dpc2;
+      const double dJ00 = dM[0] * Wr[0] + dM[1] * Wr[1] + dM[2] * Wr[2];
+      const double dJ02 = dM[0] * Wr[6] + dM[1] * Wr[7] + dM[2] * Wr[8];
+      const double dJ11 = dM[3] * Wr[3] + dM[4] * Wr[4] + dM[5] * Wr[5];
+      const double dJ12 = dM[3] * Wr[6] + dM[4] * Wr[7] + dM[5] * Wr[8];
+      const double iz3 = iz2 * iz;
+      const double dpc0 = dJ02 * (-fxd * iz2) + dmx * fxd * iz;
+      const double dpc1 = dJ12 * (-fyd * iz2) + dmy * fyd * iz;
+      const double dpc2 = dJ00 * (-fxd * iz2) + dJ11 * (-fyd * iz2) + dJ02 * (2.0 * fxd * x * iz3) +
+                          dJ12 * (2.0 * fyd * y * iz3) - dmx * fxd * x * iz2 - dmy * fyd * y * iz2;
+      for (int k = 0; k < 3; ++k) d_pos[k] = (float)(Wr[k] * dpc0 + Wr[3 + k] * dpc1 + Wr[6 + k] * dpc2);
 
       // Sigma = R D R^T
-      float dR[9];
+      double dR[9];
       for (int a = 0; a < 3; ++a)
         for (int k = 0; k < 3; ++k)
-          dR[3 * a + k] = 2.0f * (dS[3 * a] * R[k] + dS[3 * a + 1] * R[3 + k] + dS[3 * a + 2] * R[6 + k]) * D[k];
+          dR[3 * a + k] = 2.0 * (dS[3 * a] * R[k] + dS[3 * a + 1] * R[3 + k] + dS[3 * a + 2] * R[6 + k]) * D[k];
       for (int k = 0; k < 3; ++k) {
-        float s = 0.0f;
+        double s = 0.0;
         for (int a = 0; a < 3; ++a)
           s += R[3 * a + k] * (dS[3 * a] * R[k] + dS[3 * a + 1] * R[3 + k] + dS[3 * a + 2] * R[6 + k]);
-        d_ls[k] = 2.0f * D[k] * s;
+        d_ls[k] = (float)(2.0 * D[k] * s);
       }
       // d qhat = sum_ij dR_ij dR_ij/dqhat (render.py:217-229)
-      const float gw = 2.0f * (-qz * dR[1] + qy * dR[2] + qz * dR[3] - qx * dR[5] - qy * dR[6] + qx * dR[7]);
-      const float gx = 2.0f * (qy * dR[1] + qz * dR[2] + qy * dR[3] - 2.0f * qx * dR[4] - qw * dR[5] + qz * dR[6] +
-                               qw * dR[7] - 2.0f * qx * dR[8]);
-      const float gy = 2.0f * (-2.0f * qy * dR[0] + qx * dR[1] + qw * dR[2] + qx * dR[3] + qz * dR[5] - qw * dR[6] +
-                               qz * dR[7] - 2.0f * qy * dR[8]);
-      const float gz = 2.0f * (-2.0f * qz * dR[0] - qw * dR[1] + qx * dR[2] + qw * dR[3] - 2.0f * qz * dR[4] +
+      const double gw = 2.0 * (-qz * dR[1] + qy * dR[2] + qz * dR[3] - qx * dR[5] - qy * dR[6] + qx * dR[7]);
+      const double gx = 2.0 * (qy * dR[1] + qz * dR[2] + qy * dR[3] - 2.0 * qx * dR[4] - qw * dR[5] + qz * dR[6] +
+                               qw * dR[7] - 2.0 * qx * dR[8]);
+      const double gy = 2.0 * (-2.0 * qy * dR[0] + qx * dR[1] + qw * dR[2] + qx * dR[3] + qz * dR[5] - qw * dR[6] +
+                               qz * dR[7] - 2.0 * qy * dR[8]);
+      const double gz = 2.0 * (-2.0 * qz * dR[0] - qw * dR[1] + qx * dR[2] + qw * dR[3] - 2.0 * qz * dR[4] +
                                qy * dR[5] + qx * dR[6] + qy * dR[7]);
-      const float qd = qw * gw + qx * gx + qy * gy + qz * gz;
-      d_q[0] = (gw - qw * qd) / qn;
-      d_q[1] = (gx - qx * qd) / qn;
-      d_q[2] = (gy - qy * qd) / qn;
-      d_q[3] = (gz - qz * qd) / qn;
+      const double qd = qw * gw + qx * gx + qy * gy + qz * gz;
+      d_q[0] = (float)((gw - qw * qd) / qn);
+      d_q[1] = (float)((gx - qx * qd) / qn);
+      d_q[2] = (float)((gy - qy * qd) / qn);
+      d_q[3] = (float)((gz - qz * qd) / qn);
     }
 
     // ---------------- color path (all lobes, masked ones too: dL/dm_l)

@@ -319,6 +319,19 @@ class Rasterizer:
             _events[1].record()
         return Frame(img=img, final_T=T, ncontrib=nc, ws=ws, cam=c_cam, bg=bg)
 
+    def preprocess_only(self, g: GaussianTensors, cam, tile_rows=None):
+        """K1 alone (no binning, no raster): per-primitive (depth bits, packed
+        tile rectangle, tile count) device tensors, e.g. for strip planning
+        (sharding.row_costs_from_rects).  Uses a private workspace of
+        capacity 1."""
+        c_cam = to_sgs(cam, tile_rows)
+        ws = self.workspace(g, cam, private=True, capacity=1)
+        _ffi.call("sgs_preprocess", C.byref(g.c_params()), C.byref(c_cam), C.byref(ws.desc),
+                  C.c_void_p(_stream_ptr()))
+        fr = Frame(img=None, final_T=None, ncontrib=None, ws=ws, cam=c_cam, bg=(0.0, 0.0, 0.0))
+        depth, rect, tt, _ = self.export_projected(fr)
+        return depth, rect, tt
+
     # ------------------------------------------------------- graph forward
     def graph_forward(self, g: GaussianTensors, cam, out, background=(0.0, 0.0, 0.0),
                       tile_rows=None) -> torch.Tensor:

@@ -29,11 +29,16 @@ def test_reference_arm_line():
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert {"value", "unit", "cores", "kind", "sample"} <= d["cpu_baseline"].keys()
     assert d["cpu_baseline"]["kind"] in ("port", "reference")
+    assert d["cpu_baseline"]["cpu_model"]
+    sys.path.insert(0, str(ROOT))
+    import bench
+    assert d["config"] == bench.headline_config(1)   # the driver compares the arms' configs
 
 
 @pytest.mark.gpu
 def test_our_arm_line():
-    d = _run(["--steps", "2", "--warmup", "3", "--views", "2", "--no-cpu-baseline"], timeout=900)
+    d = _run(["--steps", "2", "--warmup", "3", "--cams", "4", "--workload", "all", "--no-cpu-baseline"],
+             timeout=1200)
     assert BASE_KEYS <= d.keys()
     assert d["value"] > 0 and d["n_gpus"] == 1 and d["steps"] == 2 and d["warmup"] == 3
     assert {"bound", "achieved", "peak", "unit", "frac", "traffic"} <= d["roofline"].keys()
@@ -43,3 +48,8 @@ def test_our_arm_line():
     assert d["gpu_launches"] > 0
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= d["clocks"].keys()
     assert "workload" in d["config"]
+    w = d["workloads"]
+    assert {"cfg1", "cfg3", "cfg4", "cfg2_key64"} <= w.keys()
+    assert all(w[k]["value"] > 0 for k in w)
+    assert w["cfg1"]["vram"]["measured_peak_dynamic_bytes"] > 0
+    assert 0 < w["cfg3"]["roofline_backward"]["frac"] < 2

@@ -101,8 +101,7 @@ def test_config4_densest_strip_bit_exact():
     scene, (cam,) = scenes.config4()
     rast = Rasterizer()
     g = GaussianTensors.from_arrays(scene)
-    f0 = rast.forward(g, cam, tile_rows=(0, 1), track=False)
-    _, rect, tt, _ = rast.export_projected(f0)
+    _, rect, tt = rast.preprocess_only(g, cam)
     tiles_y = (cam.height + 15) // 16
     cost = row_costs_from_rects(rect.cpu().numpy().view(np.uint32), tt.cpu().numpy().view(np.uint32), tiles_y)
     y = int(np.argmax(cost))
