@@ -803,10 +803,10 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": h["t_ms"] / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded BASELINE configs[2] distributions, random-init scene)",
-            "config": dict(headline_config(ctx.world, args.cams),
-                           streams_per_gpu=args.streams,
-                           launch="host launches" if args.no_graphs else "one CUDA graph per view",
-                           sort_mode=["depth_first", "key64"][args.sort_mode]),
+            "config": headline_config(ctx.world, args.cams),
+            "setup": {"streams_per_gpu": args.streams,
+                      "launch": "host launches" if args.no_graphs else "one CUDA graph per view",
+                      "sort_mode": ["depth_first", "key64"][args.sort_mode]},
             "mpix_per_s": h["mpix_per_s"], "vram": h["vram"], "roofline": h["roofline"],
             "e2e": {"value": h["e2e"], "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "api": "batch.BatchRenderer.render_views (pinned host scene in, host images out, "

@@ -53,6 +53,15 @@ typedef struct sgs_camera {
   int32_t width, height;
   int32_t tile_y0, tile_y1;
   float lowpass; /* cov2d diagonal floor in px^2, render.py:26 (0.3) */
+  /* Depth in float64 (render.py:262-263, 307): the camera's third row and
+   * t_z as the caller's doubles, and the near plane.  The visibility test
+   * z > near and the depth ORDER use z = (w0 x + w1 y) + w2 z + t_z in
+   * float64, so primitives are ordered exactly like the reference's
+   * argsort of its float64 z (ties by lower index); the float32 depth key is
+   * that z rounded, and equal keys are ordered by the float64 residual.
+   * depth_row all zero = derive it from the float32 rotation/translation. */
+  double depth_row[4];
+  double near_z64;
 } sgs_camera;
 
 /* Packed parameter arrays, render.py:90-108 (SceneParams) + soft masks. */

@@ -57,7 +57,7 @@ def project(p, cam, lowpass=LOWPASS):
     Wm = _f64(cam.rotation).reshape(3, 3)
     tvec = _f64(cam.translation).reshape(3)
     pos = _f64(p.position)
-    pc_all = np.einsum("ij,nj->ni", Wm, pos) + tvec
+    pc_all = pos @ Wm.T + tvec          # exactly the reference's expression (render.py:262)
     keep = np.flatnonzero(pc_all[:, 2] > getattr(cam, "near", 0.1))
     if keep.size == 0:
         return None

@@ -35,9 +35,13 @@
 namespace {
 
 SgsCam make_cam(const float* R, const float* t, float fx, float fy, float cx, float cy, float near_z, int W, int H,
-                int tile_y0, int tile_y1, float lowpass) {
+                int tile_y0, int tile_y1, float lowpass, const double* cam_d) {
   SgsCam c;
   c.lowpass = lowpass;
+  // float64 depth row + near (sgs_camera.depth_row / near_z64): cam_d = (w0, w1, w2, tz, near)
+  for (int k = 0; k < 3; ++k) c.rz[k] = cam_d ? cam_d[k] : (double)R[6 + k];
+  c.tz = cam_d ? cam_d[3] : (double)t[2];
+  c.near64 = cam_d ? cam_d[4] : (double)near_z;
   for (int i = 0; i < 9; ++i) c.R[i] = R[i];
   for (int i = 0; i < 3; ++i) c.t[i] = t[i];
   for (int k = 0; k < 3; ++k) {
@@ -70,10 +74,10 @@ extern "C" {
 void oracle_preprocess(int64_t n, int L, const float* pos, const float* quat, const float* ls, const float* opac,
                        const float* diffuse, const float* axis, const float* sharp, const float* amp,
                        const float* lmask, const float* pmask, const float* cam_f, const int32_t* cam_i,
-                       uint32_t* depth_bits, uint32_t* rect, uint32_t* tiles_touched, float* records,
-                       int64_t* counts) {
+                       const double* cam_d, uint32_t* depth_bits, float* depth_res, uint32_t* rect,
+                       uint32_t* tiles_touched, float* records, int64_t* counts) {
   SgsCam cam = make_cam(cam_f, cam_f + 9, cam_f[12], cam_f[13], cam_f[14], cam_f[15], cam_f[16], cam_i[0], cam_i[1],
-                        cam_i[2], cam_i[3], cam_f[17]);
+                        cam_i[2], cam_i[3], cam_f[17], cam_d);
   int64_t vis = 0, emit = 0;
   for (int64_t i = 0; i < n; ++i) {
     SgsProj pr;
@@ -87,6 +91,7 @@ void oracle_preprocess(int64_t n, int L, const float* pos, const float* quat, co
     }
     tiles_touched[i] = cnt;
     depth_bits[i] = cnt ? sgs_float_to_bits(pr.depth) : 0x7fffffffu;
+    depth_res[i] = cnt ? pr.depth_res : 0.0f;
     rect[2 * i] = (uint32_t)(pr.tx0 & 0xffff) | ((uint32_t)(pr.tx1 & 0xffff) << 16);
     rect[2 * i + 1] = (uint32_t)(pr.ty0 & 0xffff) | ((uint32_t)(pr.ty1 & 0xffff) << 16);
     float* rec = records + 16 * i;
@@ -120,13 +125,15 @@ int64_t oracle_count_entries(int64_t n, const uint32_t* tiles_touched) {
   return e;
 }
 
-// Emit (tile<<32 | depth_bits, index) in index order, stable sort, ranges.
-// keys/vals have room for E entries; ranges has tiles_x*tiles_y*2 u32 (zeroed here).
-void oracle_bin(int64_t n, const uint32_t* depth_bits, const uint32_t* rect, const uint32_t* tiles_touched,
-                const float* records, const float* cam_f, const int32_t* cam_i, uint64_t* keys, uint32_t* vals,
-                uint32_t* ranges) {
+// Emit (tile<<32 | depth_bits, index) in index order, stable sort on the key
+// and, for equal keys, the float64 depth residual: the per-tile order is the
+// reference's stable argsort of float64 z (render.py:307).  keys/vals have
+// room for E entries; ranges has tiles_x*tiles_y*2 u32 (zeroed here).
+void oracle_bin(int64_t n, const uint32_t* depth_bits, const float* depth_res, const uint32_t* rect,
+                const uint32_t* tiles_touched, const float* records, const float* cam_f, const int32_t* cam_i,
+                uint64_t* keys, uint32_t* vals, uint32_t* ranges) {
   SgsCam cam = make_cam(cam_f, cam_f + 9, cam_f[12], cam_f[13], cam_f[14], cam_f[15], cam_f[16], cam_i[0], cam_i[1],
-                        cam_i[2], cam_i[3], cam_f[17]);
+                        cam_i[2], cam_i[3], cam_f[17], nullptr);
   std::vector<std::pair<uint64_t, uint32_t>> ent;
   for (int64_t i = 0; i < n; ++i) {
     if (!tiles_touched[i]) continue;
@@ -143,8 +150,9 @@ void oracle_bin(int64_t n, const uint32_t* depth_bits, const uint32_t* rect, con
     }
   }
   std::stable_sort(ent.begin(), ent.end(),
-                   [](const std::pair<uint64_t, uint32_t>& a, const std::pair<uint64_t, uint32_t>& b) {
-                     return a.first < b.first;
+                   [depth_res](const std::pair<uint64_t, uint32_t>& a, const std::pair<uint64_t, uint32_t>& b) {
+                     if (a.first != b.first) return a.first < b.first;
+                     return depth_res[a.second] < depth_res[b.second];
                    });
   const size_t T = (size_t)cam.tiles_x * cam.tiles_y;
   memset(ranges, 0, T * 2 * sizeof(uint32_t));
@@ -162,7 +170,7 @@ void oracle_raster_forward(const uint32_t* ranges, const uint32_t* vals, const f
                            const int32_t* cam_i, const float* bg, float* img, float* Tout, uint32_t* nc_out,
                            double* weight_sums) {
   SgsCam cam = make_cam(cam_f, cam_f + 9, cam_f[12], cam_f[13], cam_f[14], cam_f[15], cam_f[16], cam_i[0], cam_i[1],
-                        cam_i[2], cam_i[3], cam_f[17]);
+                        cam_i[2], cam_i[3], cam_f[17], nullptr);
   for (int py = cam.tile_y0 * SGS_TILE; py < std::min(cam.height, cam.tile_y1 * SGS_TILE); ++py)
     for (int px = 0; px < cam.width; ++px) {
       const int tile = (py / SGS_TILE) * cam.tiles_x + px / SGS_TILE;
@@ -201,7 +209,7 @@ void oracle_raster_forward(const uint32_t* ranges, const uint32_t* vals, const f
 void oracle_raster_backward(const uint32_t* ranges, const uint32_t* vals, const float* records, const float* cam_f,
                             const int32_t* cam_i, const float* bg, const float* dimg, double* grad2d) {
   SgsCam cam = make_cam(cam_f, cam_f + 9, cam_f[12], cam_f[13], cam_f[14], cam_f[15], cam_f[16], cam_i[0], cam_i[1],
-                        cam_i[2], cam_i[3], cam_f[17]);
+                        cam_i[2], cam_i[3], cam_f[17], nullptr);
   struct Item {
     uint32_t g;
     double G, a, alpha, T, dx, dy;

@@ -52,6 +52,13 @@ def cam_arrays(cam, tile_rows=(0, 0), lowpass=0.3):
     return f, i
 
 
+def cam_f64(cam):
+    """(w0, w1, w2, t_z, near) in float64: the depth row (sgs_camera.depth_row)."""
+    r = np.asarray(cam.rotation, dtype=np.float64).reshape(3, 3)
+    t = np.asarray(cam.translation, dtype=np.float64).reshape(3)
+    return np.array([r[2, 0], r[2, 1], r[2, 2], t[2], float(getattr(cam, "near", 0.1))], np.float64)
+
+
 def _arrays(s):
     f32 = lambda a: np.ascontiguousarray(np.asarray(a), dtype=np.float32)  # noqa: E731
     out = {k: f32(getattr(s, k)) for k in ("position", "quat", "log_scale", "opacity", "diffuse",
@@ -71,6 +78,7 @@ def preprocess(scene, cam, tile_rows=(0, 0), lowpass=0.3):
     cf, ci = cam_arrays(cam, tile_rows, lowpass)
     r = TiledResult()
     r.depth_bits = np.zeros(n, np.uint32)
+    r.depth_res = np.zeros(n, np.float32)
     r.rect = np.zeros((n, 2), np.uint32)
     r.tiles_touched = np.zeros(n, np.uint32)
     r.records = np.zeros((n, 16), np.float32)
@@ -78,8 +86,8 @@ def preprocess(scene, cam, tile_rows=(0, 0), lowpass=0.3):
     lib().oracle_preprocess(C.c_int64(n), C.c_int(L), _p(a["position"]), _p(a["quat"]),
                             _p(a["log_scale"]), _p(a["opacity"]), _p(a["diffuse"]),
                             _p(a["axis_raw"]), _p(a["sharpness"]), _p(a["amplitude"]),
-                            _p(a["lobe_mask"]), _p(a["prim_mask"]), _p(cf), _p(ci),
-                            _p(r.depth_bits), _p(r.rect), _p(r.tiles_touched), _p(r.records),
+                            _p(a["lobe_mask"]), _p(a["prim_mask"]), _p(cf), _p(ci), _p(cam_f64(cam)),
+                            _p(r.depth_bits), _p(r.depth_res), _p(r.rect), _p(r.tiles_touched), _p(r.records),
                             _p(counts))
     r.n_visible, r.n_emitting = int(counts[0]), int(counts[1])
     r.cam_f, r.cam_i, r.n, r.arrays = cf, ci, n, a
@@ -92,7 +100,7 @@ def bin(r):  # noqa: A001 - mirrors sgs_bin
     r.keys = np.zeros(max(E, 1), np.uint64)
     r.vals = np.zeros(max(E, 1), np.uint32)
     r.ranges = np.zeros((tiles, 2), np.uint32)
-    lib().oracle_bin(C.c_int64(r.n), _p(r.depth_bits), _p(r.rect), _p(r.tiles_touched),
+    lib().oracle_bin(C.c_int64(r.n), _p(r.depth_bits), _p(r.depth_res), _p(r.rect), _p(r.tiles_touched),
                      _p(r.records), _p(r.cam_f), _p(r.cam_i), _p(r.keys), _p(r.vals),
                      _p(r.ranges))
     r.keys, r.vals, r.n_entries = r.keys[:E], r.vals[:E], E

@@ -26,7 +26,8 @@ class SgsCamera(C.Structure):
     _fields_ = [("rotation", C.c_float * 9), ("translation", C.c_float * 3),
                 ("fx", C.c_float), ("fy", C.c_float), ("cx", C.c_float), ("cy", C.c_float),
                 ("near_z", C.c_float), ("width", C.c_int32), ("height", C.c_int32),
-                ("tile_y0", C.c_int32), ("tile_y1", C.c_int32), ("lowpass", C.c_float)]
+                ("tile_y0", C.c_int32), ("tile_y1", C.c_int32), ("lowpass", C.c_float),
+                ("depth_row", C.c_double * 4), ("near_z64", C.c_double)]
 
 
 class SgsParams(C.Structure):

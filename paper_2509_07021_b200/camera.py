@@ -84,4 +84,11 @@ def to_sgs(cam, tile_rows: tuple[int, int] | None = None, lowpass: float = 0.3) 
     else:
         c.tile_y0, c.tile_y1 = int(tile_rows[0]), int(tile_rows[1])
     c.lowpass = float(np.float32(lowpass))
+    # float64 depth row (render.py:262): z = p . R[2] + t[2] in the caller's doubles
+    r64 = np.asarray(cam.rotation, dtype=np.float64).reshape(3, 3)
+    t64 = np.asarray(cam.translation, dtype=np.float64).reshape(3)
+    for k in range(3):
+        c.depth_row[k] = float(r64[2, k])
+    c.depth_row[3] = float(t64[2])
+    c.near_z64 = float(getattr(cam, "near", 0.1))
     return c

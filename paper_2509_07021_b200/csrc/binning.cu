@@ -143,6 +143,42 @@ static int launch_scan(const uint32_t* tt, const uint32_t* perm, uint32_t n, uin
   return SGS_OK;
 }
 
+// ------------------------------------------------------ float64 depth ties
+// The radix sorts order by the float32 depth key (the float64 z rounded,
+// sgs_project) and keep equal keys in primitive-index order.  The reference
+// orders by its float64 z (render.py:307: argsort(z, kind="stable")), so
+// within a run of equal keys the primitives are re-ordered by the float64
+// residual z64 - key (sgs_project's depth_res; equal residuals keep index
+// order).  Runs are rare and short (configs[2]: ~3 % of the primitives, 2-4
+// long), so the thread at a run's first element insertion-sorts it.
+// keys: the sort's final (sorted) keys; vals: the sorted primitive indices,
+// fixed in place.  `skip`: the not-emitting key (sorted last) or ~0.
+template <typename K>
+__global__ void __launch_bounds__(256) depth_tie_fixup(const K* __restrict__ keys, uint32_t* __restrict__ vals,
+                                                       const float* __restrict__ res, const uint32_t* n_ptr,
+                                                       uint32_t n_cap, K skip) {
+  const uint32_t n = min(*n_ptr, n_cap);
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i + 1 < n; i += stride) {
+    const K k = keys[i];
+    if (k == skip || keys[i + 1] != k || (i > 0 && keys[i - 1] == k)) continue;
+    uint32_t j = i + 2;
+    while (j < n && keys[j] == k) ++j;
+    for (uint32_t a = i + 1; a < j; ++a) {
+      const uint32_t v = vals[a];
+      const float r = res[v];
+      uint32_t b = a;
+      while (b > i) {
+        const uint32_t u = vals[b - 1];
+        if (!(res[u] > r)) break;
+        vals[b] = u;
+        --b;
+      }
+      vals[b] = v;
+    }
+  }
+}
+
 // ------------------------------------------------------------- entry emission
 #ifndef SGS_EMIT_CTAS
 #define SGS_EMIT_CTAS 4  // grid = SMs x this (one wave at 4 resident CTAs), grid-stride over the ranks
@@ -344,7 +380,16 @@ static int bin_entries(const SgsCam& cam, const sgs_workspace* ws, const Layout&
   uint32_t* hist = at<uint32_t>(ws, lo.hist) + (fused_hist ? kSuperHistOff : 0);
   int rc = radix_sort_pairs<KT, IPT, RBITS>(k0, v0, k1, v1, &ctr->n_sort, cap, key_bits, hist,
                                      at<uint32_t>(ws, lo.status), &ctr->part_counter[8], &alt, st, false,
-                                     RsRangeOut{ranges, tile_shift}, kSuper ? 16 : 0, kSuper, fused_hist);
+                                     RsRangeOut{ranges, tile_shift}, kSuper ? 16 : 0, true, fused_hist);
+  if (rc) return rc;
+  if (!kSuper) {
+    // 64-bit keys: entries were emitted in primitive-index order, so equal
+    // (tile, depth) keys need the float64 residual order too
+    depth_tie_fixup<KT><<<persistent_grid(cap, 256, 8), 256, 0, st>>>(alt ? k1 : k0, alt ? v1 : v0,
+                                                                    at<float>(ws, lo.depth_res), &ctr->n_sort, cap,
+                                                                    ~KT(0));
+    SGS_LAUNCH_CHECK("depth_tie_fixup");
+  }
   // cells without entries keep (0xffffffff, 0): every consumer reads a range
   // as [start, max(start, end)), i.e. empty
   return rc;
@@ -372,7 +417,10 @@ int launch_bin(const SgsCam& cam, const sgs_workspace* ws, const Layout& lo, cud
                                                         at<uint32_t>(ws, lo.status), &ctr->part_counter[0], &alt, st,
                                                         true, RsRangeOut{nullptr, 0}, 0, false, true, dkey);
     if (rc) return rc;
-    const uint32_t* perm = alt ? ib : ia;
+    uint32_t* perm = alt ? ib : ia;
+    depth_tie_fixup<uint32_t><<<persistent_grid(n, 256, 8), 256, 0, st>>>(
+        alt ? kb : ka, perm, at<float>(ws, lo.depth_res), &ctr->n_depth, n, 0x7fffffffu);
+    SGS_LAUNCH_CHECK("depth_tie_fixup");
     rc = launch_scan(at<uint32_t>(ws, lo.super_touched), perm, n, cap, status64, offsets, ctr, st);
     if (rc) return rc;
     // keys (super_id << 16 | 16-bit tile mask), sorted on the super id bits only

@@ -79,7 +79,8 @@ struct Layout {
   int32_t sort_mode;
   int64_t cap;
   // offsets into the workspace
-  uint64_t counters, rec_geo, rec_con, rec_col, rec_span, rec_eig, depth_key, rect, tiles_touched, super_touched, cand_end;
+  uint64_t counters, rec_geo, rec_con, rec_col, rec_span, rec_eig, depth_key, depth_res, rect, tiles_touched,
+      super_touched, cand_end;
   uint64_t cell_order, row_off, row_spans;
   uint64_t row_cap;
   uint64_t dkey_alt, dkey_tmp, didx, didx_alt, offsets, scan_blocks;
@@ -142,6 +143,7 @@ inline int make_layout(const sgs_workspace* ws, Layout* lo) {
   lo->rec_span = take(n * 16);
   lo->rec_eig = take(n * 16);
   lo->depth_key = take(n * 4);
+  lo->depth_res = take(n * 4);
   lo->rect = take(n * 8);
   lo->tiles_touched = take(n * 4);
   lo->super_touched = take(n * 4);
@@ -231,6 +233,11 @@ inline int make_cam(const sgs_camera* c, const Layout& lo, SgsCam* out) {
     return SGS_E_ARG;
   }
   out->lowpass = c->lowpass;
+  const bool have64 = c->depth_row[0] != 0.0 || c->depth_row[1] != 0.0 || c->depth_row[2] != 0.0 ||
+                      c->depth_row[3] != 0.0;
+  for (int k = 0; k < 3; ++k) out->rz[k] = have64 ? c->depth_row[k] : (double)c->rotation[6 + k];
+  out->tz = have64 ? c->depth_row[3] : (double)c->translation[2];
+  out->near64 = c->near_z64 > 0.0 ? c->near_z64 : (double)c->near_z;
   return SGS_OK;
 }
 

@@ -40,7 +40,8 @@ __global__ void __launch_bounds__(256, SGS_PRE_REG_CTAS) preprocess_kernel(sgs_p
                                                          float4* __restrict__ rec_con, float4* __restrict__ rec_col,
                                                          float4* __restrict__ rec_span,
                                                          float4* __restrict__ rec_eig,
-                                                         uint32_t* __restrict__ depth_key, uint2* __restrict__ rect,
+                                                         uint32_t* __restrict__ depth_key,
+                                                         float* __restrict__ depth_res, uint2* __restrict__ rect,
                                                          uint32_t* __restrict__ tiles_touched,
                                                          uint32_t* __restrict__ super_touched,
                                                          uint32_t* __restrict__ depth_hist,
@@ -254,6 +255,7 @@ __global__ void __launch_bounds__(256, SGS_PRE_REG_CTAS) preprocess_kernel(sgs_p
       if (row_off) row_off[i] = cnt ? my_off : kNoRows;
       const uint32_t dk = emitting ? sgs_float_to_bits(pr.depth) : 0x7fffffffu;
       depth_key[i] = dk;
+      depth_res[i] = emitting ? pr.depth_res : 0.0f;
       if (depth_hist) {
 #pragma unroll
         for (int d = 0; d < 4; ++d) atomicAdd(&s_hist[d][(dk >> (8 * d)) & 0xffu], 1u);
@@ -392,6 +394,7 @@ int launch_preprocess(const sgs_params& P, const SgsCam& cam, const sgs_workspac
   preprocess_kernel<KL><<<grid, 256, 0, st>>>(P, cam, at<float4>(ws, lo.rec_geo), at<float4>(ws, lo.rec_con),    \
                                               at<float4>(ws, lo.rec_col), at<float4>(ws, lo.rec_span),           \
                                               at<float4>(ws, lo.rec_eig), at<uint32_t>(ws, lo.depth_key),        \
+                                              at<float>(ws, lo.depth_res),                                        \
                                               at<uint2>(ws, lo.rect), at<uint32_t>(ws, lo.tiles_touched),        \
                                               at<uint32_t>(ws, lo.super_touched),                                 \
                                               lo.sort_mode == SGS_SORT_DEPTH_FIRST                                 \

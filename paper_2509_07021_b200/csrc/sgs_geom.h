@@ -188,12 +188,15 @@ typedef struct SgsCam {
   int32_t tiles_x, tiles_y;
   int32_t tile_y0, tile_y1;  // tile-row window [y0, y1) for strip renders
   float lowpass;             // px^2 added to the cov2d diagonal (render.py:26, 285-286)
+  double rz[3], tz;          // float64 depth row: z64 = (rz0 x + rz1 y) + rz2 z + tz (render.py:262)
+  double near64;             // visible iff z64 > near64 (render.py:263)
 } SgsCam;
 
 // Projected primitive: everything the binning stage and the forward raster
 // read.  conic/cov are the symmetric 2x2 (00, 01, 11) entries.
 typedef struct SgsProj {
-  float depth;
+  float depth;       // float32 rounding of z64: the depth key (monotone in z64)
+  float depth_res;   // z64 - depth, rounded: orders equal keys like z64 does
   float mx, my;
   float cov00, cov01, cov11;
   float con00, con01, con11;
@@ -235,8 +238,15 @@ SGS_HD void sgs_project(const float pos[3], const float quat[4], const float ls[
   float x = F_ADD(sgs_dot3(W[0], W[1], W[2], pos[0], pos[1], pos[2]), cam->t[0]);
   float y = F_ADD(sgs_dot3(W[3], W[4], W[5], pos[0], pos[1], pos[2]), cam->t[1]);
   float z = F_ADD(sgs_dot3(W[6], W[7], W[8], pos[0], pos[1], pos[2]), cam->t[2]);
-  o->depth = z;
-  o->visible = z > cam->near_z;
+  // depth and visibility in float64 from the caller's float64 camera row:
+  // the reference orders by its float64 z (render.py:307), which the
+  // float32 z above (float32 camera) does not reproduce for near-ties
+  const double z64 = D_ADD(D_ADD(D_ADD(D_MUL(cam->rz[0], (double)pos[0]), D_MUL(cam->rz[1], (double)pos[1])),
+                                 D_MUL(cam->rz[2], (double)pos[2])),
+                           cam->tz);
+  o->depth = (float)z64;
+  o->depth_res = (float)D_SUB(z64, (double)o->depth);
+  o->visible = z64 > cam->near64 && z > 0.0f;
   o->emits = 0;
   o->tx0 = o->ty0 = 0;
   o->tx1 = o->ty1 = -1;

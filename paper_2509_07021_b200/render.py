@@ -387,11 +387,14 @@ def _prepare(p, cam, lowpass: float = LOWPASS_FLOOR) -> Projection | None:
     vis = np.flatnonzero(rec[:, 0] > 0)
     if vis.size == 0:
         return None
-    order = vis[np.argsort(rec[vis, 1].astype(np.float32), kind="stable")]
+    # the reference's order: stable argsort of its float64 z (render.py:262, 307)
+    z64 = (np.asarray(p.position, dtype=np.float64)[vis] @ np.asarray(cam.rotation, dtype=np.float64).T
+           + np.asarray(cam.translation, dtype=np.float64))[:, 2]
+    order = vis[np.argsort(z64, kind="stable")]
     r = rec[order]
     pr = Projection()
     pr.orig_idx = order
-    pr.depth = r[:, 1]
+    pr.depth = z64[np.argsort(z64, kind="stable")]
     pr.mean2d = r[:, 2:4].copy()
     pr.cov2d = np.stack([np.stack([r[:, 4], r[:, 5]], -1), np.stack([r[:, 5], r[:, 6]], -1)], 1)
     pr.conic = np.stack([np.stack([r[:, 7], r[:, 8]], -1), np.stack([r[:, 8], r[:, 9]], -1)], 1)

@@ -33,7 +33,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_struct_layouts_match_header():
     # sizes of the ABI structs as C sees them (x86-64 SysV)
-    assert C.sizeof(_ffi.SgsCamera) == 4 * 9 + 4 * 3 + 4 * 5 + 4 * 4 + 4
+    assert C.sizeof(_ffi.SgsCamera) == 4 * 9 + 4 * 3 + 4 * 5 + 4 * 4 + 4 + 8 * 4 + 8
     assert C.sizeof(_ffi.SgsParams) == 10 * 8 + 8 + 8
     assert C.sizeof(_ffi.SgsWorkspace) == 8 + 8 + 8 + 4 * 4 + 8
     assert C.sizeof(_ffi.SgsStats) == 8 * 8
