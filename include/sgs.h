@@ -159,19 +159,27 @@ int sgs_bin(const sgs_camera* cam, const sgs_workspace* ws, void* stream);
  * out_ncontrib (H,W) number of per-tile entries consumed by each pixel.
  * out_T and out_ncontrib may be NULL for an image-only render (render.py:411);
  * sgs_raster_backward needs both from the same frame.
- * weight_sums (N) is ACCUMULATED (like the reference's in-place np.add.at,
- * render.py:406-407) when non-NULL.  pair_count (one device uint64), when
- * non-NULL, is incremented by the number of (pixel, entry) pairs evaluated
- * before each pixel terminated -- the raster's algorithmic work unit. */
+ * weight_sums_fx (N uint64, two's-complement fixed point in units of 2^-32)
+ * is ACCUMULATED with the composited blending weights (the reference's
+ * in-place np.add.at, render.py:406-407) when non-NULL: integer addition
+ * makes the sums independent of the order tiles and views land in, so the
+ * importance scores are bitwise reproducible; sgs_fixed_to_float(.., 32, ..)
+ * converts.  pair_count (one device uint64), when non-NULL, is incremented by
+ * the number of (pixel, entry) pairs evaluated before each pixel terminated
+ * -- the raster's algorithmic work unit. */
 int sgs_raster_forward(const sgs_camera* cam, const float background[3],
                        const sgs_workspace* ws, float* out_img, float* out_T,
-                       uint32_t* out_ncontrib, float* weight_sums, uint64_t* pair_count,
+                       uint32_t* out_ncontrib, uint64_t* weight_sums_fx, uint64_t* pair_count,
+                       void* stream);
+
+/* out[i] (+)= (int64)fx[i] * 2^-frac_bits for i < n (accumulate != 0: add). */
+int sgs_fixed_to_float(const uint64_t* fx, int64_t n, int32_t frac_bits, float* out, int32_t accumulate,
                        void* stream);
 
 /* Convenience: preprocess + bin + raster_forward in one call (graph-capturable). */
 int sgs_render_forward(const sgs_params* params, const sgs_camera* cam, const float background[3],
                        const sgs_workspace* ws, float* out_img, float* out_T, uint32_t* out_ncontrib,
-                       float* weight_sums, uint64_t* pair_count, void* stream);
+                       uint64_t* weight_sums_fx, uint64_t* pair_count, void* stream);
 
 /* K6 backward raster -- replaces the pixel loop of _backward_from_blend
  * (render.py:535-573).  dimg (H,W,3) = dL/dimage.  grad2d (N,9) is
@@ -180,6 +188,16 @@ int sgs_render_forward(const sgs_params* params, const sgs_camera* cam, const fl
 int sgs_raster_backward(const sgs_camera* cam, const float background[3],
                         const sgs_workspace* ws, const float* img, const float* final_T,
                         const uint32_t* ncontrib, const float* dimg, float* grad2d, void* stream);
+
+/* sgs_raster_backward with bitwise-reproducible sums: the raster runs twice
+ * (per-(primitive, partial) max |partial|, then 64-bit fixed-point sums
+ * scaled to it), so grad2d does not depend on the order tiles finish in.
+ * scratch: device bytes >= sgs_raster_backward_det_scratch_bytes(N). */
+uint64_t sgs_raster_backward_det_scratch_bytes(int64_t n);
+int sgs_raster_backward_det(const sgs_camera* cam, const float background[3],
+                            const sgs_workspace* ws, const float* img, const float* final_T,
+                            const uint32_t* ncontrib, const float* dimg, float* grad2d,
+                            void* scratch, uint64_t scratch_bytes, void* stream);
 
 /* K7 preprocess backward -- replaces render.py:575-636 (conic -> cov2d ->
  * Sigma/J -> quat/log_scale/position, SG color path, scatter) and adds the

@@ -44,6 +44,7 @@ class SgsGrads(C.Structure):
                 ("prim_mask", C.c_void_p), ("flags", C.c_int32)]
 
 
+WEIGHT_FRAC_BITS = 32  # sgs_raster_forward's weight_sums_fx fixed point
 GRADS_ACCUMULATE = 1   # SGS_GRADS_ACCUMULATE
 GRADS_MASK_LOGIT = 2   # SGS_GRADS_MASK_LOGIT
 
@@ -86,6 +87,11 @@ SIGNATURES = {
                                      C.c_void_p]),
     "sgs_raster_backward": (C.c_int, [_P(SgsCamera), _P(C.c_float), _P(SgsWorkspace), C.c_void_p,
                                       C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "sgs_raster_backward_det_scratch_bytes": (C.c_uint64, [C.c_int64]),
+    "sgs_raster_backward_det": (C.c_int, [_P(SgsCamera), _P(C.c_float), _P(SgsWorkspace), C.c_void_p,
+                                          C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                          C.c_uint64, C.c_void_p]),
+    "sgs_fixed_to_float": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p]),
     "sgs_preprocess_backward": (C.c_int, [_P(SgsParams), _P(SgsCamera), C.c_void_p, _P(SgsGrads),
                                           C.c_void_p]),
     "sgs_project_records": (C.c_int, [_P(SgsParams), _P(SgsCamera), C.c_void_p, C.c_void_p]),

@@ -216,21 +216,64 @@ class DevicePrunerState:
         return {f: t.detach().to(torch.float64).cpu().numpy() for f, t in self.params.items()}
 
 
-def _check_finite(grads: dict, n: int):
-    """prune.py:151-159: NumericalFailure naming the first bad primitive."""
-    bad = torch.zeros(n, dtype=torch.bool, device=grads["position"].device)
-    for name in GRAD_FIELDS:
-        bad |= ~torch.isfinite(grads[name].reshape(n, -1)).all(dim=1)
-    if bool(bad.any()):
-        i = int(torch.nonzero(bad)[0])
-        for name in GRAD_FIELDS:
-            if not bool(torch.isfinite(grads[name].reshape(n, -1)[i]).all()):
-                raise NumericalFailure(f"non-finite gradient in {name} at primitive {i}", index=i)
+class _Failure:
+    """A non-finite gradient found on the device, reported at the next host
+    synchronisation (prune.py:151-159 raises at once; the device loop defers
+    the check so a step costs no host round trip).  From the failing step on
+    every update is masked off, so the state is the one the reference leaves
+    behind when it raises."""
+
+    def __init__(self, device):
+        self.flag = torch.zeros((), dtype=torch.bool, device=device)      # any failure so far
+        self.index = torch.zeros((), dtype=torch.int64, device=device)    # first bad primitive
+        self.field = torch.zeros((), dtype=torch.int64, device=device)    # its first bad class
+        self.iteration = torch.zeros((), dtype=torch.int64, device=device)
+
+    def observe(self, grads: dict, n: int, iteration: int) -> torch.Tensor:
+        """Record the step's failure (if it is the first); returns the device
+        bool 'this step may update'."""
+        rows = torch.stack([~torch.isfinite(grads[f].reshape(n, -1)).all(dim=1) for f in GRAD_FIELDS])
+        bad_row = rows.any(dim=0)
+        bad = bad_row.any()
+        i = torch.argmax(bad_row.to(torch.int8))                  # first bad primitive
+        code = torch.argmax(rows[:, i].to(torch.int8))            # first bad class there
+        new = bad & ~self.flag
+        self.index = torch.where(new, i, self.index)
+        self.field = torch.where(new, code, self.field)
+        self.iteration = torch.where(new, torch.full_like(self.iteration, iteration), self.iteration)
+        self.flag = self.flag | bad
+        return ~self.flag
+
+    def raise_if_failed(self, state=None) -> None:
+        if bool(self.flag):
+            i, f = int(self.index), GRAD_FIELDS[int(self.field)]
+            if state is not None:
+                state.iteration = int(self.iteration)
+            raise NumericalFailure(f"non-finite gradient in {f} at primitive {i}", index=i)
 
 
-def gradient_step(state: DevicePrunerState, view, cfg, rast: Rasterizer | None = None) -> float:
+def _failure(state: DevicePrunerState) -> _Failure:
+    f = getattr(state, "_failure", None)
+    if f is None:
+        f = _Failure(state.params["opacity"].device)
+        state._failure = f
+    return f
+
+
+def _masked_sub_(t: torch.Tensor, delta: torch.Tensor, ok: torch.Tensor) -> None:
+    t.copy_(torch.where(ok, t - delta, t))
+
+
+def gradient_step(state: DevicePrunerState, view, cfg, rast: Rasterizer | None = None, sync: bool = True,
+                  deterministic: bool = True):
     """One penalized descent step on one view; returns the data loss
-    (prune.py:162-201, same update order)."""
+    (prune.py:162-201, same update order).
+
+    No host synchronisation with ``sync=False``: the loss is returned as a
+    0-dim float64 device tensor and a non-finite gradient is reported at the
+    next synchronisation (run_state's trace rows), with the state as the
+    reference leaves it.  ``deterministic``: bitwise-reproducible gradient
+    sums (Rasterizer.backward), so repeated runs take identical steps."""
     cam, target = view
     p = state.params
     r = cfg.group_rates
@@ -238,28 +281,32 @@ def gradient_step(state: DevicePrunerState, view, cfg, rast: Rasterizer | None =
     tgt = _t(target)
     g = state.gaussians()
     n = g.n
+    fail = _failure(state)
     loss_val, g1 = loss_and_grads_device(g, cam, tgt, cfg.loss_cfg, cfg.background, rast=rast,
-                                         sync=False)
-    _check_finite(g1, n)
+                                         sync=False, deterministic=deterministic)
+    ok = fail.observe(g1, n, state.iteration)
     with torch.no_grad():
         if cfg.delta == 0.0:
-            p["opacity"].sub_(eta * r.opacity * g1["opacity"])
-            p["sharpness"].sub_(eta * r.sharpness * g1["sharpness"])
+            _masked_sub_(p["opacity"], eta * r.opacity * g1["opacity"], ok)
+            _masked_sub_(p["sharpness"], eta * r.sharpness * g1["sharpness"], ok)
         else:
-            p["opacity"].sub_(eta * r.opacity * (g1["opacity"] + _delta_o(cfg) * (
-                p["opacity"] - state.proxy_o + state.dual_o)))
+            _masked_sub_(p["opacity"], eta * r.opacity * (g1["opacity"] + _delta_o(cfg) * (
+                p["opacity"] - state.proxy_o + state.dual_o)), ok)
             p["opacity"].clamp_(0.0, 1.0)
             _, g2 = loss_and_grads_device(g, cam, tgt, cfg.loss_cfg, cfg.background, rast=rast,
-                                          sync=False)
-            _check_finite(g2, n)
-            p["sharpness"].sub_(eta * r.sharpness * (g2["sharpness"] + _delta_s(cfg) * (
-                p["sharpness"] - state.proxy_s + state.dual_s)))
+                                          sync=False, deterministic=deterministic)
+            ok = fail.observe(g2, n, state.iteration)
+            _masked_sub_(p["sharpness"], eta * r.sharpness * (g2["sharpness"] + _delta_s(cfg) * (
+                p["sharpness"] - state.proxy_s + state.dual_s)), ok)
         for name in ("position", "quat", "log_scale", "diffuse", "axis_raw", "amplitude"):
-            p[name].sub_(eta * getattr(r, name) * g1[name])
+            _masked_sub_(p[name], eta * getattr(r, name) * g1[name], ok)
         p["opacity"].clamp_(0.0, 1.0)
         p["sharpness"].clamp_(min=0.0)
     state.iteration += 1
-    return float(loss_val)
+    if sync:
+        fail.raise_if_failed(state)
+        return float(loss_val)
+    return loss_val
 
 
 def dual_update(state: DevicePrunerState) -> DevicePrunerState:
@@ -271,16 +318,19 @@ def dual_update(state: DevicePrunerState) -> DevicePrunerState:
 
 
 def _prox_inputs(state: DevicePrunerState, cfg, views, rast: Rasterizer):
+    """Importance scores (prune.py:281-290 -> render.py:416-428): every view's
+    composited weights added as exact fixed point, then float64 -- the same
+    bits whatever order the views' tiles finish in."""
     if cfg.opacity_operator != "importance":
         return None
     if not views:
         raise ConfigError("importance operator needs training views")
     g = state.gaussians()
-    ws = torch.zeros(g.n, dtype=torch.float32, device=g.device)
+    fx = torch.zeros(g.n, dtype=torch.int64, device=g.device)
     bg = tuple(float(v) for v in np.asarray(cfg.background, dtype=np.float64).reshape(3))
     for cam, _ in views:
-        rast.forward(g, cam, bg, weight_sums=ws, track=False)
-    return ws
+        rast.forward(g, cam, bg, weight_fx=fx, track=False)
+    return fx.to(torch.float64) * 2.0 ** -_ffi.WEIGHT_FRAC_BITS
 
 
 def _proximal_event(state: DevicePrunerState, cfg, importance):
@@ -307,11 +357,14 @@ class TraceRow:
     budget_units: int
 
 
-def run_state(state: DevicePrunerState, views, cfg, rast: Rasterizer | None = None) -> list[TraceRow]:
+def run_state(state: DevicePrunerState, views, cfg, rast: Rasterizer | None = None,
+              deterministic: bool = True) -> list[TraceRow]:
     """The full schedule (prune.py:312-354): view order from
     default_rng(seed) permutations, a proximal event + dual update every
     prox_every iterations, a terminal projection, then zeroing of primal
-    entries outside the kept support."""
+    entries outside the kept support.  The gradient steps between proximal
+    events run without host synchronisation; ``deterministic`` (default)
+    makes the whole run bitwise reproducible."""
     if not views:
         raise ConfigError("need at least one training view")
     rast = rast or Rasterizer(device=_dev())
@@ -322,9 +375,12 @@ def run_state(state: DevicePrunerState, views, cfg, rast: Rasterizer | None = No
     pos = 0
     loss_val = float("nan")
 
+    fail = _failure(state)
+
     def record(iteration, active_o, active_s, units):
+        fail.raise_if_failed(state)
         trace.append(TraceRow(
-            iteration=iteration, loss=loss_val,
+            iteration=iteration, loss=float(loss_val),
             residual_o=float(torch.linalg.vector_norm((p["opacity"] - state.proxy_o).double())),
             residual_s=float(torch.linalg.vector_norm((p["sharpness"] - state.proxy_s).double())),
             active_primitives=active_o, active_lobes=active_s, budget_units=units))
@@ -334,7 +390,7 @@ def run_state(state: DevicePrunerState, views, cfg, rast: Rasterizer | None = No
         if pos == len(order):
             order = rng.permutation(len(views))
             pos = 0
-        loss_val = gradient_step(state, views[order[pos]], cfg, rast)
+        loss_val = gradient_step(state, views[order[pos]], cfg, rast, sync=False, deterministic=deterministic)
         pos += 1
         ended_with_event = False
         if cfg.prox_every is not None and (k + 1) % cfg.prox_every == 0:
@@ -350,4 +406,5 @@ def run_state(state: DevicePrunerState, views, cfg, rast: Rasterizer | None = No
             p["opacity"].copy_(torch.where(state.proxy_o != 0.0, p["opacity"], torch.zeros_like(p["opacity"])))
             p["sharpness"].copy_(torch.where(state.proxy_s != 0.0, p["sharpness"],
                                              torch.zeros_like(p["sharpness"])))
+    fail.raise_if_failed(state)
     return trace

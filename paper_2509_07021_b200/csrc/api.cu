@@ -46,10 +46,13 @@ int launch_vram3s(const sgs_params& P, const SgsCam& cam, int tile_px, Counters*
 int launch_bin(const SgsCam& cam, const sgs_workspace* ws, const Layout& lo, cudaStream_t st);
 bool final_in_alt(const Layout& lo);
 int launch_raster_fwd(const SgsCam& cam, float3 bg, const sgs_workspace* ws, const Layout& lo, const uint32_t* vals,
-                      float* img, float* T, uint32_t* nc, float* weight_sums, unsigned long long* pairs,
+                      float* img, float* T, uint32_t* nc, unsigned long long* weight_fx, unsigned long long* pairs,
                       cudaStream_t st);
 int launch_raster_bwd(const SgsCam& cam, float3 bg, const sgs_workspace* ws, const Layout& lo, const uint32_t* vals,
-                      const float* T, const uint32_t* nc, const float* dimg, float* grad2d, cudaStream_t st);
+                      const float* T, const uint32_t* nc, const float* dimg, float* grad2d, void* det_scratch,
+                      cudaStream_t st);
+uint64_t raster_bwd_det_scratch_bytes(int64_t n);
+int launch_fixed_to_float(const unsigned long long* fx, int64_t n, int frac_bits, float* out, int acc, cudaStream_t st);
 int launch_preprocess_bwd(const sgs_params& P, const SgsCam& cam, const float* grad2d, const sgs_grads& g,
                           cudaStream_t st);
 int launch_export_lists(const SgsCam& cam, const sgs_workspace* ws, const Layout& lo, const uint32_t* vals,
@@ -100,7 +103,7 @@ using namespace sgs;
 
 extern "C" {
 
-int32_t sgs_version(void) { return 100; }
+int32_t sgs_version(void) { return 200; }
 
 const char* sgs_last_error(void) { return g_err; }
 
@@ -138,7 +141,7 @@ int sgs_bin(const sgs_camera* cam, const sgs_workspace* ws, void* stream) {
 }
 
 int sgs_raster_forward(const sgs_camera* cam, const float background[3], const sgs_workspace* ws, float* out_img,
-                       float* out_T, uint32_t* out_ncontrib, float* weight_sums, uint64_t* pair_count,
+                       float* out_T, uint32_t* out_ncontrib, uint64_t* weight_sums_fx, uint64_t* pair_count,
                        void* stream) {
   Layout lo;
   SgsCam c;
@@ -150,17 +153,18 @@ int sgs_raster_forward(const sgs_camera* cam, const float background[3], const s
     return SGS_E_ARG;
   }
   float3 bg = make_float3(background[0], background[1], background[2]);
-  return launch_raster_fwd(c, bg, ws, lo, final_vals(ws, lo), out_img, out_T, out_ncontrib, weight_sums,
+  return launch_raster_fwd(c, bg, ws, lo, final_vals(ws, lo), out_img, out_T, out_ncontrib,
+                           reinterpret_cast<unsigned long long*>(weight_sums_fx),
                            reinterpret_cast<unsigned long long*>(pair_count), as_stream(stream));
 }
 
 int sgs_render_forward(const sgs_params* params, const sgs_camera* cam, const float background[3],
                        const sgs_workspace* ws, float* out_img, float* out_T, uint32_t* out_ncontrib,
-                       float* weight_sums, uint64_t* pair_count, void* stream) {
+                       uint64_t* weight_sums_fx, uint64_t* pair_count, void* stream) {
   int rc = sgs_preprocess(params, cam, ws, stream);
   if (!rc) rc = sgs_bin(cam, ws, stream);
   if (!rc)
-    rc = sgs_raster_forward(cam, background, ws, out_img, out_T, out_ncontrib, weight_sums, pair_count, stream);
+    rc = sgs_raster_forward(cam, background, ws, out_img, out_T, out_ncontrib, weight_sums_fx, pair_count, stream);
   return rc;
 }
 
@@ -178,7 +182,43 @@ int sgs_raster_backward(const sgs_camera* cam, const float background[3], const 
   }
   (void)img;
   float3 bg = make_float3(background[0], background[1], background[2]);
-  return launch_raster_bwd(c, bg, ws, lo, final_vals(ws, lo), final_T, ncontrib, dimg, grad2d, as_stream(stream));
+  return launch_raster_bwd(c, bg, ws, lo, final_vals(ws, lo), final_T, ncontrib, dimg, grad2d, nullptr,
+                           as_stream(stream));
+}
+
+uint64_t sgs_raster_backward_det_scratch_bytes(int64_t n) { return raster_bwd_det_scratch_bytes(n); }
+
+int sgs_raster_backward_det(const sgs_camera* cam, const float background[3], const sgs_workspace* ws,
+                            const float* img, const float* final_T, const uint32_t* ncontrib, const float* dimg,
+                            float* grad2d, void* scratch, uint64_t scratch_bytes, void* stream) {
+  Layout lo;
+  SgsCam c;
+  int rc = check_ws(ws, &lo);
+  if (!rc) rc = make_cam(cam, lo, &c);
+  if (rc) return rc;
+  if (!final_T || !ncontrib || !dimg || !grad2d || !background || !scratch) {
+    set_error("null buffer");
+    return SGS_E_ARG;
+  }
+  if (scratch_bytes < raster_bwd_det_scratch_bytes(lo.n)) {
+    set_error("deterministic backward scratch too small: need %llu bytes",
+              (unsigned long long)raster_bwd_det_scratch_bytes(lo.n));
+    return SGS_E_WORKSPACE;
+  }
+  (void)img;
+  float3 bg = make_float3(background[0], background[1], background[2]);
+  return launch_raster_bwd(c, bg, ws, lo, final_vals(ws, lo), final_T, ncontrib, dimg, grad2d, scratch,
+                           as_stream(stream));
+}
+
+int sgs_fixed_to_float(const uint64_t* fx, int64_t n, int32_t frac_bits, float* out, int32_t accumulate,
+                       void* stream) {
+  if (n < 0 || (n > 0 && (!fx || !out)) || frac_bits < 0 || frac_bits > 62) {
+    set_error("invalid fixed-point conversion arguments");
+    return SGS_E_ARG;
+  }
+  return launch_fixed_to_float(reinterpret_cast<const unsigned long long*>(fx), n, frac_bits, out, accumulate,
+                               as_stream(stream));
 }
 
 int sgs_preprocess_backward(const sgs_params* params, const sgs_camera* cam, const float* grad2d, sgs_grads* grads,

@@ -164,6 +164,34 @@ __global__ void __launch_bounds__(256) depth_tie_fixup(const K* __restrict__ key
     if (k == skip || keys[i + 1] != k || (i > 0 && keys[i - 1] == k)) continue;
     uint32_t j = i + 2;
     while (j < n && keys[j] == k) ++j;
+    constexpr int kRegRun = 8;
+    if (j - i <= (uint32_t)kRegRun) {
+      // short run (nearly all): every load issued at once, sorted in registers
+      const int len = (int)(j - i);
+      uint32_t v[kRegRun];
+      float r[kRegRun];
+#pragma unroll
+      for (int a = 0; a < kRegRun; ++a) v[a] = a < len ? vals[i + a] : 0u;
+#pragma unroll
+      for (int a = 0; a < kRegRun; ++a) r[a] = a < len ? res[v[a]] : INFINITY;
+      // stable odd-even transposition sort on (r, original position)
+#pragma unroll
+      for (int round = 0; round < kRegRun; ++round)
+#pragma unroll
+        for (int a = round & 1; a + 1 < kRegRun; a += 2)
+          if (r[a + 1] < r[a]) {
+            const float tr = r[a];
+            r[a] = r[a + 1];
+            r[a + 1] = tr;
+            const uint32_t tv = v[a];
+            v[a] = v[a + 1];
+            v[a + 1] = tv;
+          }
+#pragma unroll
+      for (int a = 0; a < kRegRun; ++a)
+        if (a < len) vals[i + a] = v[a];
+      continue;
+    }
     for (uint32_t a = i + 1; a < j; ++a) {
       const uint32_t v = vals[a];
       const float r = res[v];

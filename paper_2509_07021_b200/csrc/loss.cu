@@ -65,6 +65,19 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   return s;
 }
 
+// The per-block sums of the loss terms are added as 64-bit fixed point
+// (2^-36 units, in the double's bits): integer addition is exact in any
+// order, so the loss value is bitwise reproducible (a float atomicAdd
+// would depend on which block lands first).  |sum| < 2^27 for any frame up
+// to 4K x 3 channels with |term| <= 2.
+constexpr double kLossFixed = 68719476736.0;  // 2^36
+__device__ __forceinline__ void fixed_add(double* slot, double v) {
+  atomicAdd(reinterpret_cast<unsigned long long*>(slot), (unsigned long long)__double2ll_rn(v * kLossFixed));
+}
+__device__ __forceinline__ double fixed_value(double slot) {
+  return (double)__double_as_longlong(slot) / kLossFixed;
+}
+
 // Shared layout (doubles): sx, sy [(TH+2r) x (TW+2r)], then hs[5][(TH+2r) x TW].
 __host__ __device__ inline size_t loss_smem_doubles(int r, int nplanes_in, int nplanes_h) {
   return (size_t)nplanes_in * (kLossTH + 2 * r) * (kLossTW + 2 * r) + (size_t)nplanes_h * (kLossTH + 2 * r) * kLossTW;
@@ -183,8 +196,8 @@ __global__ void __launch_bounds__(kLossThreads, SGS_LOSS_MIN_BLOCKS) ssim_fwd_ke
   const double tl1 = block_sum(l1, red);
   const double tss = block_sum(ss, red);
   if (t == 0) {
-    atomicAdd(&sums[0], tl1);
-    atomicAdd(&sums[1], tss);
+    fixed_add(&sums[0], tl1);
+    fixed_add(&sums[1], tss);
   }
 }
 
@@ -289,11 +302,11 @@ __global__ void __launch_bounds__(kLossThreads) l1_sum_kernel(const TI* __restri
   for (size_t i = (size_t)blockIdx.x * kLossThreads + threadIdx.x; i < n; i += (size_t)gridDim.x * kLossThreads)
     s += fabs(ld(img, i) - ld(tgt, i));
   const double tot = block_sum(s, red);
-  if (threadIdx.x == 0) atomicAdd(&sums[0], tot);
+  if (threadIdx.x == 0) fixed_add(&sums[0], tot);
 }
 
 __global__ void loss_finish_kernel(double* out, double lam, double inv_size) {
-  const double l1 = out[3] * inv_size, sm = out[4] * inv_size;
+  const double l1 = fixed_value(out[3]) * inv_size, sm = fixed_value(out[4]) * inv_size;
   out[0] = lam == 0.0 ? (1.0 - lam) * l1 : (1.0 - lam) * l1 + lam * (1.0 - sm);
   out[1] = l1;
   out[2] = lam == 0.0 ? 0.0 : sm;

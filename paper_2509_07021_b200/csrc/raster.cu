@@ -310,6 +310,7 @@ __device__ __forceinline__ uint32_t tile_local_bit(int tx, int ty) {
 // only bounds the work a finished warp wastes.
 // kTrack: record per-pixel contributor counts and the per-tile candidate end
 // the backward pass walks from; a render that only returns the image skips it.
+constexpr double kWeightScale = 4294967296.0;  // importance fixed point: 2^32 units
 constexpr int kFwdThreads = 128;
 constexpr int kFwdCPT = 2;
 constexpr int kFwdChunk = kFwdThreads * kFwdCPT;  // candidates examined per staging step
@@ -407,7 +408,7 @@ __global__ void __launch_bounds__(kFwdThreads, kImportance ? 1 : (kTrack ? SGS_F
                                                                  float* __restrict__ out_img,
                                                                  float* __restrict__ out_T,
                                                                  uint32_t* __restrict__ out_nc,
-                                                                 float* __restrict__ weight_sums,
+                                                                 unsigned long long* __restrict__ weight_fx,
                                                                  unsigned long long* __restrict__ pair_count) {
   __shared__ std::conditional_t<kImportance || kTrack, Stage<kFwdBuf>, StageNoIds<kFwdBuf>> s;
   __shared__ float s_wp[kImportance ? kFwdThreads / 32 : 1][kImportance ? kFwdBuf : 1];
@@ -520,7 +521,10 @@ __global__ void __launch_bounds__(kFwdThreads, kImportance ? 1 : (kTrack ? SGS_F
       __syncthreads();
       for (int i = t; i < nb; i += kFwdThreads) {
         const float x = (s_wp[0][i] + s_wp[1][i]) + (s_wp[2][i] + s_wp[3][i]);
-        if (x != 0.0f) atomicAdd(&weight_sums[s.id[i]], x);
+        // fixed point (2^-32 units): integer sums do not depend on the order
+        // the tiles' atomics land in, so the importance -- and the top-k
+        // selection ties it feeds (prune.py:204) -- is bitwise reproducible
+        if (x != 0.0f) atomicAdd(&weight_fx[s.id[i]], (unsigned long long)__double2ll_rn((double)x * kWeightScale));
       }
     }
     if constexpr (kTrack) {
@@ -621,12 +625,27 @@ __device__ __forceinline__ int reduce9_index(int lane) {
 // batch's shared partials; each batch is flushed by summing the 4 warps'
 // partials with one global atomic per (record, partial).  T is recovered with one hardware reciprocal
 // per pixel-record, T_i = T_{i+1} rcp(1 - alpha_i) (~1 ulp per record).
-template <bool kFilter>
+// Deterministic mode (kMode 1 + 2, sgs_raster_backward_det): the float
+// atomics below add the (record, tile) partials in whatever order the tiles
+// finish, so sums are reproducible only to rounding.  Pass 1 (kMode 1)
+// records each (primitive, partial)'s largest |partial| (an order-free
+// atomicMax on the float bits); pass 2 (kMode 2) recomputes the identical
+// partials and adds them as 64-bit fixed point scaled to that maximum
+// (fx_scale: every term < 2^42, < 2^20 tiles per primitive), which integer
+// addition sums exactly in any order; bwd_fixed_finalize converts back.
+__device__ __forceinline__ double fx_scale(uint32_t max_bits) {
+  const int e = (int)((max_bits >> 23) & 0xffu) - 127;  // |partial| < 2^(e + 1)
+  return __longlong_as_double((long long)(1023 + 41 - e) << 52);  // 2^(41 - e)
+}
+
+template <bool kFilter, int kMode>
 __global__ void __launch_bounds__(kBwdThreads, SGS_BWD_MIN_BLOCKS) raster_bwd_kernel(ListArgs la, SgsCam cam, float3 bg,
                                                                  const float* __restrict__ final_T,
                                                                  const uint32_t* __restrict__ ncontrib,
                                                                  const float* __restrict__ dimg,
-                                                                 float* __restrict__ grad2d) {
+                                                                 float* __restrict__ grad2d,
+                                                                 uint32_t* __restrict__ gmax,
+                                                                 unsigned long long* __restrict__ gfx) {
   __shared__ Stage<kBwdChunk> s;
   // per-warp partial totals (plain stores; shared-memory float atomics are CAS
   // loops on sm_100), summed over the 4 warps when the batch is flushed
@@ -750,7 +769,15 @@ __global__ void __launch_bounds__(kBwdThreads, SGS_BWD_MIN_BLOCKS) raster_bwd_ke
       float x = 0.0f;
 #pragma unroll
       for (int w = 0; w < kBwdThreads / 32; ++w) x += s_part[w][k][c];
-      if (x != 0.0f) atomicAdd(grad2d + (size_t)s.id[k] * kGrad + c, x);
+      if (x != 0.0f) {
+        const size_t o = (size_t)s.id[k] * kGrad + c;
+        if constexpr (kMode == 0)
+          atomicAdd(grad2d + o, x);
+        else if constexpr (kMode == 1)
+          atomicMax(gmax + o, __float_as_uint(fabsf(x)));
+        else
+          atomicAdd(gfx + o, (unsigned long long)__double2ll_rn((double)x * fx_scale(gmax[o])));
+      }
     }
     hits_after += (uint32_t)nb;
     hi = lo;
@@ -835,7 +862,7 @@ static ListArgs list_args(const sgs_workspace* ws, const Layout& lo, const uint3
 }
 
 int launch_raster_fwd(const SgsCam& cam, float3 bg, const sgs_workspace* ws, const Layout& lo, const uint32_t* vals,
-                      float* img, float* T, uint32_t* nc, float* weight_sums, unsigned long long* pairs,
+                      float* img, float* T, uint32_t* nc, unsigned long long* weight_fx, unsigned long long* pairs,
                       cudaStream_t st) {
   ListArgs a = list_args(ws, lo, vals);
   const bool filt = lo.sort_mode == SGS_SORT_DEPTH_FIRST;
@@ -856,17 +883,17 @@ int launch_raster_fwd(const SgsCam& cam, float3 bg, const sgs_workspace* ws, con
     SGS_LAUNCH_CHECK("cell_order_kernel");
   }
 #define SGS_FWD(I, C, F, K) \
-  raster_fwd_kernel<I, C, F, K><<<grid, kFwdThreads, 0, st>>>(a, cam, bg, img, T, nc, weight_sums, pairs)
+  raster_fwd_kernel<I, C, F, K><<<grid, kFwdThreads, 0, st>>>(a, cam, bg, img, T, nc, weight_fx, pairs)
 #define SGS_FWD_TRACK(I, C, F) \
   if (nc) SGS_FWD(I, C, F, true); else SGS_FWD(I, C, F, false)
   if (filt) {
-    if (weight_sums && pairs) SGS_FWD_TRACK(true, true, true);
-    else if (weight_sums) SGS_FWD_TRACK(true, false, true);
+    if (weight_fx && pairs) SGS_FWD_TRACK(true, true, true);
+    else if (weight_fx) SGS_FWD_TRACK(true, false, true);
     else if (pairs) SGS_FWD_TRACK(false, true, true);
     else SGS_FWD_TRACK(false, false, true);
   } else {
-    if (weight_sums && pairs) SGS_FWD_TRACK(true, true, false);
-    else if (weight_sums) SGS_FWD_TRACK(true, false, false);
+    if (weight_fx && pairs) SGS_FWD_TRACK(true, true, false);
+    else if (weight_fx) SGS_FWD_TRACK(true, false, false);
     else if (pairs) SGS_FWD_TRACK(false, true, false);
     else SGS_FWD_TRACK(false, false, false);
   }
@@ -876,16 +903,63 @@ int launch_raster_fwd(const SgsCam& cam, float3 bg, const sgs_workspace* ws, con
   return SGS_OK;
 }
 
+__global__ void __launch_bounds__(256) bwd_fixed_finalize(const uint32_t* __restrict__ gmax,
+                                                          const unsigned long long* __restrict__ gfx,
+                                                          float* __restrict__ grad2d, size_t n) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const uint32_t m = gmax[i];
+    grad2d[i] = m ? (float)((double)(long long)gfx[i] / fx_scale(m)) : 0.0f;
+  }
+}
+
+uint64_t raster_bwd_det_scratch_bytes(int64_t n) { return (uint64_t)(n > 0 ? n : 1) * kGrad * (4 + 8) + 256; }
+
 int launch_raster_bwd(const SgsCam& cam, float3 bg, const sgs_workspace* ws, const Layout& lo, const uint32_t* vals,
-                      const float* T, const uint32_t* nc, const float* dimg, float* grad2d, cudaStream_t st) {
+                      const float* T, const uint32_t* nc, const float* dimg, float* grad2d, void* det_scratch,
+                      cudaStream_t st) {
   const int grid = (cam.tile_y1 - cam.tile_y0) * cam.tiles_x;
-  SGS_CUDA(cudaMemsetAsync(grad2d, 0, (size_t)lo.n * kGrad * sizeof(float), st));
+  const size_t nv = (size_t)lo.n * kGrad;
   const ListArgs a = list_args(ws, lo, vals);
-  if (lo.sort_mode == SGS_SORT_DEPTH_FIRST)
-    raster_bwd_kernel<true><<<grid, kBwdThreads, 0, st>>>(a, cam, bg, T, nc, dimg, grad2d);
-  else
-    raster_bwd_kernel<false><<<grid, kBwdThreads, 0, st>>>(a, cam, bg, T, nc, dimg, grad2d);
-  SGS_LAUNCH_CHECK("raster_bwd_kernel");
+  const bool filt = lo.sort_mode == SGS_SORT_DEPTH_FIRST;
+  if (!det_scratch) {
+    SGS_CUDA(cudaMemsetAsync(grad2d, 0, nv * sizeof(float), st));
+    if (filt)
+      raster_bwd_kernel<true, 0><<<grid, kBwdThreads, 0, st>>>(a, cam, bg, T, nc, dimg, grad2d, nullptr, nullptr);
+    else
+      raster_bwd_kernel<false, 0><<<grid, kBwdThreads, 0, st>>>(a, cam, bg, T, nc, dimg, grad2d, nullptr, nullptr);
+    SGS_LAUNCH_CHECK("raster_bwd_kernel");
+    return SGS_OK;
+  }
+  unsigned long long* gfx = reinterpret_cast<unsigned long long*>(
+      (reinterpret_cast<uintptr_t>(det_scratch) + 255) & ~uintptr_t(255));
+  uint32_t* gmax = reinterpret_cast<uint32_t*>(gfx + nv);
+  SGS_CUDA(cudaMemsetAsync(gfx, 0, nv * (8 + 4), st));
+  if (filt) {
+    raster_bwd_kernel<true, 1><<<grid, kBwdThreads, 0, st>>>(a, cam, bg, T, nc, dimg, grad2d, gmax, gfx);
+    raster_bwd_kernel<true, 2><<<grid, kBwdThreads, 0, st>>>(a, cam, bg, T, nc, dimg, grad2d, gmax, gfx);
+  } else {
+    raster_bwd_kernel<false, 1><<<grid, kBwdThreads, 0, st>>>(a, cam, bg, T, nc, dimg, grad2d, gmax, gfx);
+    raster_bwd_kernel<false, 2><<<grid, kBwdThreads, 0, st>>>(a, cam, bg, T, nc, dimg, grad2d, gmax, gfx);
+  }
+  SGS_LAUNCH_CHECK("raster_bwd_kernel (deterministic)");
+  bwd_fixed_finalize<<<persistent_grid(nv, 256, 8), 256, 0, st>>>(gmax, gfx, grad2d, nv);
+  SGS_LAUNCH_CHECK("bwd_fixed_finalize");
+  return SGS_OK;
+}
+
+__global__ void __launch_bounds__(256) fixed_to_float_kernel(const unsigned long long* __restrict__ fx, size_t n,
+                                                             double inv_scale, float* __restrict__ out, int acc) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const float v = (float)((double)(long long)fx[i] * inv_scale);
+    out[i] = acc ? out[i] + v : v;
+  }
+}
+
+int launch_fixed_to_float(const unsigned long long* fx, int64_t n, int frac_bits, float* out, int acc, cudaStream_t st) {
+  if (n <= 0) return SGS_OK;
+  fixed_to_float_kernel<<<persistent_grid((uint64_t)n, 256, 8), 256, 0, st>>>(fx, (size_t)n, ldexp(1.0, -frac_bits),
+                                                                           out, acc);
+  SGS_LAUNCH_CHECK("fixed_to_float_kernel");
   return SGS_OK;
 }
 

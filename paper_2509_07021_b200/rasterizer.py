@@ -265,11 +265,14 @@ class Rasterizer:
     # ------------------------------------------------------------------ forward
     def forward(self, g: GaussianTensors, cam, background=(0.0, 0.0, 0.0), weight_sums=None,
                 check=True, private=False, tile_rows=None, out=None, pair_count=None,
-                track=True, _events=None) -> Frame:
+                track=True, weight_fx=None, _events=None) -> Frame:
         # _events (timing hooks): (raster start, raster end[, preprocess start,
         # preprocess end]) CUDA events recorded on the current stream
         """Render one view.  ``weight_sums`` (N float32 device tensor) is
-        accumulated in place (render.py:406-407).  ``out`` may supply
+        accumulated in place (render.py:406-407); ``weight_fx`` (N int64,
+        fixed point in 2^-32 units) instead accumulates the exact integer
+        sums, for several views to be added order-independently and
+        converted once (``fixed_to_float``).  ``out`` may supply
         preallocated (img, T, nc) tensors.  ``track=False`` renders the image
         (and T) only, skipping the per-pixel contributor counts the backward
         needs (an image-only render, render.py:411)."""
@@ -288,6 +291,14 @@ class Rasterizer:
         if weight_sums is not None:
             if weight_sums.dtype != torch.float32 or tuple(weight_sums.shape) != (g.n,):
                 raise ValueError("weight_sums must be a float32 (N,) tensor")
+            if weight_fx is not None:
+                raise ValueError("pass weight_sums or weight_fx, not both")
+            weight_fx = torch.zeros(g.n, dtype=torch.int64, device=self.device)
+            to_float = weight_sums
+        else:
+            to_float = None
+        if weight_fx is not None and (weight_fx.dtype != torch.int64 or tuple(weight_fx.shape) != (g.n,)):
+            raise ValueError("weight_fx must be an int64 (N,) tensor")
         params = g.c_params()
         stream = C.c_void_p(_stream_ptr())
         key = self._key(g, cam)
@@ -314,9 +325,11 @@ class Rasterizer:
         if _events is not None:
             _events[0].record()
         _ffi.call("sgs_raster_forward", C.byref(c_cam), c_bg, C.byref(ws.desc), _ptr(img), _ptr(T),
-                  _ptr(nc), _ptr(weight_sums), _ptr(pair_count), stream)
+                  _ptr(nc), _ptr(weight_fx), _ptr(pair_count), stream)
         if _events is not None:
             _events[1].record()
+        if to_float is not None:
+            fixed_to_float(weight_fx, to_float, accumulate=True)
         return Frame(img=img, final_T=T, ncontrib=nc, ws=ws, cam=c_cam, bg=bg)
 
     def preprocess_only(self, g: GaussianTensors, cam, tile_rows=None):
@@ -390,22 +403,25 @@ class Rasterizer:
     # ----------------------------------------------------------------- backward
     def backward(self, g: GaussianTensors, frame: Frame, dimg: torch.Tensor,
                  mask_grads: bool = True, out: dict | None = None, accumulate: bool = False,
-                 mask_logit: bool = False) -> dict:
+                 mask_logit: bool = False, deterministic: bool = False) -> dict:
         """dL/dparams for dL/dimg (H,W,3).  Returns a dict of float32 tensors
         shaped like the parameters (+ 'lobe_mask' / 'prim_mask' when
         ``mask_grads``) and 'grad2d' (N,9).  ``out`` supplies the output
         tensors (contiguous float32, parameter-shaped, 'quat' 16-byte
         aligned); with ``accumulate`` the gradients are added into them, and
         with ``mask_logit`` the mask gradients are taken with respect to the
-        logits whose sigmoids are the masks (x m (1 - m))."""
-        grad2d = self.backward_raster(g, frame, dimg)
+        logits whose sigmoids are the masks (x m (1 - m)).  ``deterministic``:
+        bitwise-reproducible raster sums (sgs_raster_backward_det, ~2x K6)."""
+        grad2d = self.backward_raster(g, frame, dimg, deterministic=deterministic)
         out = self.backward_params(g, frame.cam, grad2d, mask_grads=mask_grads, out=out,
                                    accumulate=accumulate, mask_logit=mask_logit)
         out["grad2d"] = grad2d
         return out
 
-    def backward_raster(self, g: GaussianTensors, frame: Frame, dimg: torch.Tensor) -> torch.Tensor:
-        """K6 alone: the (N, 9) per-primitive image-space partials for dL/dimg."""
+    def backward_raster(self, g: GaussianTensors, frame: Frame, dimg: torch.Tensor,
+                        deterministic: bool = False) -> torch.Tensor:
+        """K6 alone: the (N, 9) per-primitive image-space partials for dL/dimg
+        (``deterministic``: order-independent fixed-point sums)."""
         dimg = dimg.to(device=self.device, dtype=torch.float32).contiguous()
         if frame.ncontrib is None:
             raise ValueError("frame was rendered with track=False; the backward needs track=True")
@@ -413,6 +429,13 @@ class Rasterizer:
             raise ValueError(f"dimg shape {tuple(dimg.shape)} != image {tuple(frame.img.shape)}")
         c_bg = (C.c_float * 3)(*frame.bg)
         grad2d = torch.empty((g.n, 9), dtype=torch.float32, device=self.device)
+        if deterministic:
+            nb = int(_ffi.load().sgs_raster_backward_det_scratch_bytes(g.n))
+            scratch = torch.empty(nb, dtype=torch.uint8, device=self.device)
+            _ffi.call("sgs_raster_backward_det", C.byref(frame.cam), c_bg, C.byref(frame.ws.desc),
+                      _ptr(frame.img), _ptr(frame.final_T), _ptr(frame.ncontrib), _ptr(dimg),
+                      _ptr(grad2d), _ptr(scratch), nb, C.c_void_p(_stream_ptr()))
+            return grad2d
         _ffi.call("sgs_raster_backward", C.byref(frame.cam), c_bg, C.byref(frame.ws.desc),
                   _ptr(frame.img), _ptr(frame.final_T), _ptr(frame.ncontrib), _ptr(dimg),
                   _ptr(grad2d), C.c_void_p(_stream_ptr()))
@@ -486,6 +509,16 @@ class Rasterizer:
         _ffi.call("sgs_export_projected", C.byref(frame.ws.desc), _ptr(depth), _ptr(rect),
                   _ptr(tt), _ptr(rec), C.c_void_p(_stream_ptr()))
         return depth[:n], rect[:n], tt[:n], rec[:n]
+
+
+def fixed_to_float(fx: torch.Tensor, out: torch.Tensor, accumulate: bool = False,
+                   frac_bits: int = _ffi.WEIGHT_FRAC_BITS) -> torch.Tensor:
+    """out (+)= fx * 2^-frac_bits (int64 fixed point -> float32), on the device."""
+    if fx.dtype != torch.int64 or out.dtype != torch.float32 or fx.numel() != out.numel():
+        raise ValueError("fixed_to_float needs an int64 source and a float32 output of equal size")
+    _ffi.call("sgs_fixed_to_float", _ptr(fx), fx.numel(), int(frac_bits), _ptr(out), int(accumulate),
+              C.c_void_p(_stream_ptr()))
+    return out
 
 
 def sort_pairs_u64(keys: torch.Tensor, vals: torch.Tensor, key_bits: int) -> None:

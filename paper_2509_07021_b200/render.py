@@ -209,14 +209,20 @@ def _render_params(p, cam, background, weight_sums: np.ndarray | None = None) ->
     with the composited blending weights (render.py:393-408)."""
     rast = rasterizer()
     g = _upload(p)
-    ws = None
+    fx = None
     if weight_sums is not None:
-        ws = torch.zeros(g.n, dtype=torch.float32, device=rast.device)
-    frame = rast.forward(g, cam, _bg(background), weight_sums=ws, track=False)
+        fx = torch.zeros(g.n, dtype=torch.int64, device=rast.device)
+    frame = rast.forward(g, cam, _bg(background), weight_fx=fx, track=False)
     img = _to_np64(frame.img)
     if weight_sums is not None:
-        weight_sums += _to_np64(ws)
+        weight_sums += _fx_to_np64(fx)
     return img
+
+
+def _fx_to_np64(fx: torch.Tensor) -> np.ndarray:
+    """Exact integer weight sums (2^-32 units) -> float64, as the reference
+    accumulates its weights in float64 (render.py:406-407)."""
+    return (fx.to(torch.float64) * 2.0 ** -_ffi.WEIGHT_FRAC_BITS).cpu().numpy()
 
 
 def render(scene, cam, background=(0.0, 0.0, 0.0)) -> np.ndarray:
@@ -242,9 +248,12 @@ def _side_streams(device, n: int) -> list:
 
 def accumulate_importance_params(p, cams, background=(0.0, 0.0, 0.0), streams: int = 4) -> np.ndarray:
     """render.py:416-428.  The views render concurrently on ``streams`` CUDA
-    streams (the weight sums are atomic adds into one array); tile-entry
-    capacity is checked once for all views, and a pass in which any view
-    outgrew its capacity is redone from zero with the capacity grown."""
+    streams; their weights are added as exact 64-bit fixed point into one
+    array (so the result does not depend on the order the views and tiles
+    land in: bitwise reproducible, ties stay ties for the top-k of
+    prune.py:204).  Tile-entry capacity is checked once for all views, and a
+    pass in which any view outgrew its capacity is redone from zero with the
+    capacity grown."""
     rast = rasterizer()
     g = _upload(p)
     bg = _bg(background)
@@ -252,7 +261,7 @@ def accumulate_importance_params(p, cams, background=(0.0, 0.0, 0.0), streams: i
     main = torch.cuda.current_stream(rast.device)
     side = _side_streams(rast.device, max(1, min(int(streams), len(cams))))
     while True:
-        ws = torch.zeros(g.n, dtype=torch.float32, device=rast.device)
+        fx = torch.zeros(g.n, dtype=torch.int64, device=rast.device)
         ovf = torch.zeros((max(len(cams), 1), 2), dtype=torch.int64, device=rast.device)
         ready = torch.cuda.Event()
         ready.record(main)
@@ -260,12 +269,12 @@ def accumulate_importance_params(p, cams, background=(0.0, 0.0, 0.0), streams: i
             st = side[j % len(side)]
             st.wait_event(ready)
             with torch.cuda.stream(st):
-                rast.forward(g, cam, bg, weight_sums=ws, track=False, check=False).record_overflow(ovf[j])
+                rast.forward(g, cam, bg, weight_fx=fx, track=False, check=False).record_overflow(ovf[j])
         for st in side:
             main.wait_stream(st)
         o = ovf.cpu().numpy()
         if not o[:, 0].any():
-            return _to_np64(ws)
+            return _fx_to_np64(fx)
         for j, cam in enumerate(cams):
             if o[j, 0]:
                 rast.grow_capacity(g, cam, int(o[j, 1]))
@@ -334,21 +343,23 @@ def _grads_to_set(gr: dict) -> GradientSet:
 def loss_and_grads_device(g: GaussianTensors, cam, target: torch.Tensor, cfg: LossConfig = LossConfig(),
                           background=(0.0, 0.0, 0.0), rast: Rasterizer | None = None,
                           mask_grads: bool = False, sync: bool = True, overflow_out=None,
-                          grads_out: dict | None = None, accumulate: bool = False, mask_logit: bool = False):
+                          grads_out: dict | None = None, accumulate: bool = False, mask_logit: bool = False,
+                          deterministic: bool = False):
     """Device-resident variant: (loss, dict of float32 gradient tensors).  The
     loss is a float, or a 0-dim float64 device tensor with ``sync=False`` (no
     host round trip).  With ``overflow_out`` (int64 device tensor of 2) the
     tile-entry capacity is not checked here: the frame's (overflow, entries)
     counters land in it and the caller checks them later (Frame.record_overflow).
-    ``grads_out`` / ``accumulate`` / ``mask_logit``: see Rasterizer.backward
-    (a training step sums its views straight into one gradient bucket)."""
+    ``grads_out`` / ``accumulate`` / ``mask_logit`` / ``deterministic``: see
+    Rasterizer.backward (a training step sums its views straight into one
+    gradient bucket; the ADMM loop asks for bitwise-reproducible sums)."""
     rast = rast or rasterizer()
     frame = rast.forward(g, cam, _bg(background), check=overflow_out is None)
     if overflow_out is not None:
         frame.record_overflow(overflow_out)
     out, dimg, _ = image_loss(frame.img, target, cfg, grad="f32")
     grads = rast.backward(g, frame, dimg, mask_grads=mask_grads, out=grads_out, accumulate=accumulate,
-                          mask_logit=mask_logit)
+                          mask_logit=mask_logit, deterministic=deterministic)
     return (float(out[0]) if sync else out[0]), grads
 
 
