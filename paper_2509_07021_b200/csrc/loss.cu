@@ -65,18 +65,10 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   return s;
 }
 
-// The per-block sums of the loss terms are added as 64-bit fixed point
-// (2^-36 units, in the double's bits): integer addition is exact in any
-// order, so the loss value is bitwise reproducible (a float atomicAdd
-// would depend on which block lands first).  |sum| < 2^27 for any frame up
-// to 4K x 3 channels with |term| <= 2.
-constexpr double kLossFixed = 68719476736.0;  // 2^36
-__device__ __forceinline__ void fixed_add(double* slot, double v) {
-  atomicAdd(reinterpret_cast<unsigned long long*>(slot), (unsigned long long)__double2ll_rn(v * kLossFixed));
-}
-__device__ __forceinline__ double fixed_value(double slot) {
-  return (double)__double_as_longlong(slot) / kLossFixed;
-}
+// Each block writes its sums of the loss terms to its own slot (part[2 b],
+// part[2 b + 1]); loss_finish_kernel adds the slots in a fixed order, so the
+// loss value is bitwise reproducible (a float atomicAdd per block would
+// depend on which block lands first).
 
 // Shared layout (doubles): sx, sy [(TH+2r) x (TW+2r)], then hs[5][(TH+2r) x TW].
 __host__ __device__ inline size_t loss_smem_doubles(int r, int nplanes_in, int nplanes_h) {
@@ -196,8 +188,9 @@ __global__ void __launch_bounds__(kLossThreads, SGS_LOSS_MIN_BLOCKS) ssim_fwd_ke
   const double tl1 = block_sum(l1, red);
   const double tss = block_sum(ss, red);
   if (t == 0) {
-    fixed_add(&sums[0], tl1);
-    fixed_add(&sums[1], tss);
+    const size_t b = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
+    sums[2 * b] = tl1;
+    sums[2 * b + 1] = tss;
   }
 }
 
@@ -302,11 +295,35 @@ __global__ void __launch_bounds__(kLossThreads) l1_sum_kernel(const TI* __restri
   for (size_t i = (size_t)blockIdx.x * kLossThreads + threadIdx.x; i < n; i += (size_t)gridDim.x * kLossThreads)
     s += fabs(ld(img, i) - ld(tgt, i));
   const double tot = block_sum(s, red);
-  if (threadIdx.x == 0) fixed_add(&sums[0], tot);
+  if (threadIdx.x == 0) {
+    sums[2 * blockIdx.x] = tot;
+    sums[2 * blockIdx.x + 1] = 0.0;
+  }
 }
 
-__global__ void loss_finish_kernel(double* out, double lam, double inv_size) {
-  const double l1 = fixed_value(out[3]) * inv_size, sm = fixed_value(out[4]) * inv_size;
+// One CTA: thread t sums slots t, t + 256, ... in order, then a fixed tree.
+__global__ void __launch_bounds__(256) loss_finish_kernel(double* out, const double* __restrict__ part, int nparts,
+                                                          double lam, double inv_size) {
+  __shared__ double r0[256], r1[256];
+  double a = 0.0, b = 0.0;
+  for (int i = threadIdx.x; i < nparts; i += 256) {
+    a += part[2 * i];
+    b += part[2 * i + 1];
+  }
+  r0[threadIdx.x] = a;
+  r1[threadIdx.x] = b;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) {
+      r0[threadIdx.x] += r0[threadIdx.x + w];
+      r1[threadIdx.x] += r1[threadIdx.x + w];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x != 0) return;
+  out[3] = r0[0];
+  out[4] = r1[0];
+  const double l1 = out[3] * inv_size, sm = out[4] * inv_size;
   out[0] = lam == 0.0 ? (1.0 - lam) * l1 : (1.0 - lam) * l1 + lam * (1.0 - sm);
   out[1] = l1;
   out[2] = lam == 0.0 ? 0.0 : sm;
@@ -320,23 +337,26 @@ static int run_loss(const TI* img, const TT* tgt, const LossParams& P, float* di
   double* dmu = planes;
   double* dxx = planes + n;
   double* dxy = planes + 2 * n;
+  double* part = planes + 3 * n;  // per-block partial sums (loss_workspace_bytes)
   const dim3 grid((P.W + kLossTW - 1) / kLossTW, (P.H + kLossTH - 1) / kLossTH);
+  int nparts = (int)(grid.x * grid.y);
   if (P.lam != 0.0) {
     const size_t smem = loss_smem_doubles(P.r, 2, 5) * sizeof(double);
     if (P.r == 5) {
       SGS_CUDA(cudaFuncSetAttribute(ssim_fwd_kernel<TI, TT, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      ssim_fwd_kernel<TI, TT, 5><<<grid, kLossThreads, smem, st>>>(img, tgt, P, dmu, dxx, dxy, smap, out + 3);
+      ssim_fwd_kernel<TI, TT, 5><<<grid, kLossThreads, smem, st>>>(img, tgt, P, dmu, dxx, dxy, smap, part);
     } else {
       SGS_CUDA(cudaFuncSetAttribute(ssim_fwd_kernel<TI, TT, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      ssim_fwd_kernel<TI, TT, 0><<<grid, kLossThreads, smem, st>>>(img, tgt, P, dmu, dxx, dxy, smap, out + 3);
+      ssim_fwd_kernel<TI, TT, 0><<<grid, kLossThreads, smem, st>>>(img, tgt, P, dmu, dxx, dxy, smap, part);
     }
     SGS_LAUNCH_CHECK("ssim_fwd_kernel");
   } else {
     const int g = persistent_grid(n, kLossThreads * 8, 4);
-    l1_sum_kernel<TI, TT><<<g, kLossThreads, 0, st>>>(img, tgt, n, out + 3);
+    nparts = g;
+    l1_sum_kernel<TI, TT><<<g, kLossThreads, 0, st>>>(img, tgt, n, part);
     SGS_LAUNCH_CHECK("l1_sum_kernel");
   }
-  loss_finish_kernel<<<1, 1, 0, st>>>(out, P.lam, P.inv_size);
+  loss_finish_kernel<<<1, 256, 0, st>>>(out, part, nparts, P.lam, P.inv_size);
   SGS_LAUNCH_CHECK("loss_finish_kernel");
   if (dimg || dimg64) {
     const size_t smem = P.lam != 0.0 ? loss_smem_doubles(P.r, 3, 3) * sizeof(double) : 0;
@@ -352,7 +372,11 @@ static int run_loss(const TI* img, const TT* tgt, const LossParams& P, float* di
   return SGS_OK;
 }
 
-uint64_t loss_workspace_bytes(int H, int W) { return (uint64_t)3 * H * W * 3 * sizeof(double); }
+uint64_t loss_workspace_bytes(int H, int W) {
+  const uint64_t blocks = (uint64_t)((W + kLossTW - 1) / kLossTW) * ((H + kLossTH - 1) / kLossTH);
+  const uint64_t parts = blocks > (uint64_t)kNumSMs * 4 ? blocks : (uint64_t)kNumSMs * 4;
+  return (uint64_t)3 * H * W * 3 * sizeof(double) + 2 * parts * sizeof(double);
+}
 
 int launch_image_loss(const void* img, int img_f64, const void* tgt, int tgt_f64, int H, int W,
                       const sgs_loss_config* cfg, float* dimg, double* dimg64, double* smap, double* out,
