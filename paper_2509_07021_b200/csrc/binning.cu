@@ -159,11 +159,27 @@ __global__ void __launch_bounds__(256) depth_tie_fixup(const K* __restrict__ key
                                                        uint32_t n_cap, K skip) {
   const uint32_t n = min(*n_ptr, n_cap);
   const uint32_t stride = gridDim.x * blockDim.x;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i + 1 < n; i += stride) {
-    const K k = keys[i];
-    if (k == skip || keys[i + 1] != k || (i > 0 && keys[i - 1] == k)) continue;
+  const int lane = threadIdx.x & 31;
+  for (uint32_t base = blockIdx.x * blockDim.x; base < n; base += stride) {
+    // neighbours by shuffle: one key load per element
+    const uint32_t i = base + threadIdx.x;
+    const K k = i < n ? keys[i] : skip;
+    K up = (K)__shfl_down_sync(0xffffffffu, (unsigned long long)k, 1);
+    K dn = (K)__shfl_up_sync(0xffffffffu, (unsigned long long)k, 1);
+    if (lane == 31) up = i + 1 < n ? keys[i + 1] : skip;
+    if (lane == 0) dn = i > 0 && i < n ? keys[i - 1] : skip;
+    const bool start = i + 1 < n && k != skip && up == k && dn != k;
+    if (!__any_sync(0xffffffffu, start) || !start) continue;
     uint32_t j = i + 2;
     while (j < n && keys[j] == k) ++j;
+    if (j - i == 2) {  // the common case: a pair
+      const uint32_t a = vals[i], b = vals[i + 1];
+      if (res[b] < res[a]) {
+        vals[i] = b;
+        vals[i + 1] = a;
+      }
+      continue;
+    }
     constexpr int kRegRun = 8;
     if (j - i <= (uint32_t)kRegRun) {
       // short run (nearly all): every load issued at once, sorted in registers

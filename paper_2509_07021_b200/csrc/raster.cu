@@ -696,6 +696,9 @@ __global__ void __launch_bounds__(kBwdThreads, SGS_BWD_MIN_BLOCKS) raster_bwd_ke
   __syncthreads();
   const uint32_t max_nc = s_max_nc;
   const uint32_t warp_nc = __reduce_max_sync(0xffffffffu, ncm);
+  // (a pixel off the image has nc 0, so its warp never takes the all-active
+  // body, which would advance its unused transmittance)
+  const uint32_t warp_min_nc = __reduce_min_sync(0xffffffffu, min(nc0, nc1));
   const uint32_t lbit = tile_local_bit(tx, ty);
   const int vidx = reduce9_index(lane);
   uint32_t hits_after = 0;
@@ -718,7 +721,13 @@ __global__ void __launch_bounds__(kBwdThreads, SGS_BWD_MIN_BLOCKS) raster_bwd_ke
     // warp_nc) need no work: their partial slots are zeroed together
     const int k_top = (int)max((int64_t)-1, min((int64_t)nb - 1, (int64_t)warp_nc - 1 - (int64_t)base));
     for (int i = (k_top + 1) * kGrad + lane; i < nb * kGrad; i += 32) (&s_part[wq_][0][0])[i] = 0.0f;
-    for (int k = k_top; k >= 0; --k) {
+    // Records whose per-tile index is below every pixel's kept count in this
+    // warp (warp_min_nc: ~82 % of the records processed at configs[3]) are
+    // active for all 64 pixels -- the loop body drops the per-pixel activity
+    // selects for them (kAll); the records between the warp's smallest and
+    // largest kept count take the general body.
+    auto record = [&](int k, auto all_tag) {
+      constexpr bool kAll = decltype(all_tag)::value;
       const uint32_t idx = base + (uint32_t)k;
       const float4 G = s.geo[k];  // (mx, my, log2 o_eff, -)
       const float4 E = s.con[k];  // scaled eigen form (s1 ux, s1 uy, s2 ux, s2 uy)
@@ -730,13 +739,13 @@ __global__ void __launch_bounds__(kBwdThreads, SGS_BWD_MIN_BLOCKS) raster_bwd_ke
       const float2 t1 = __ffma2_rn(f2(E.y), dy, f2(e1dx));
       const float2 t2 = __ffma2_rn(f2(E.z), dy, f2(-e3dx));
       const float2 p = __ffma2_rn(neg2(t1), t1, __ffma2_rn(neg2(t2), t2, f2(G.z)));
-      const bool act0 = idx < nc0, act1 = idx < nc1;
+      const bool act0 = kAll || idx < nc0, act1 = kAll || idx < nc1;
       // A record outside the support of every active pixel of the warp
       // (alpha < 1e-7 for all of them) contributes < 1e-7 of any partial and
       // changes T by a factor within 1e-7 of 1: skip it whole.
       if (!warp_any((act0 && p.x >= SGS_LOG2_EPS) || (act1 && p.y >= SGS_LOG2_EPS))) {
         if (vidx < kGrad) s_part[wq_][k][vidx] = 0.0f;
-        continue;
+        return;
       }
       const float2 a = make_float2(ex2_approx(p.x), ex2_approx(p.y));
       const float2 alpha = make_float2(fminf(a.x, SGS_ALPHA_MAX), fminf(a.y, SGS_ALPHA_MAX));
@@ -751,10 +760,16 @@ __global__ void __launch_bounds__(kBwdThreads, SGS_BWD_MIN_BLOCKS) raster_bwd_ke
       const float2 Sn = __ffma2_rn(w, cg, S2);
       const bool l0 = act0 && a.x < SGS_ALPHA_MAX, l1 = act1 && a.y < SGS_ALPHA_MAX;
       const float2 dqa = make_float2(l0 ? dq.x : 0.0f, l1 ? dq.y : 0.0f);
-      const float ww0 = act0 ? w.x : 0.0f, ww1 = act1 ? w.y : 0.0f;
-      S2 = make_float2(act0 ? Sn.x : S2.x, act1 ? Sn.y : S2.y);
-      T2 = make_float2(act0 ? Ti.x : T2.x, act1 ? Ti.y : T2.y);
-      const float2 ww = make_float2(ww0, ww1);
+      float2 ww;
+      if constexpr (kAll) {
+        S2 = Sn;
+        T2 = Ti;
+        ww = w;
+      } else {
+        ww = make_float2(act0 ? w.x : 0.0f, act1 ? w.y : 0.0f);
+        S2 = make_float2(act0 ? Sn.x : S2.x, act1 ? Sn.y : S2.y);
+        T2 = make_float2(act0 ? Ti.x : T2.x, act1 ? Ti.y : T2.y);
+      }
       const float2 wgx = __fmul2_rn(ww, gx2), wgy = __fmul2_rn(ww, gy2), wgz = __fmul2_rn(ww, gz2);
       // the column's pixels share dx: the dq moments are summed in dy only and
       // the dx factors applied to the column sums inside the reduction
@@ -762,7 +777,10 @@ __global__ void __launch_bounds__(kBwdThreads, SGS_BWD_MIN_BLOCKS) raster_bwd_ke
       const float tot = warp_reduce9(wgx.x + wgx.y, wgy.x + wgy.y, wgz.x + wgz.y, dqa.x + dqa.y, qy.x + qy.y,
                                      fmaf(qy.y, dy.y, qy.x * dy.x), dx, lane);
       if (vidx < kGrad) s_part[wq_][k][vidx] = tot;
-    }
+    };
+    const int k_all = (int)max((int64_t)0, min((int64_t)k_top + 1, (int64_t)warp_min_nc - (int64_t)base));
+    for (int k = k_top; k >= k_all; --k) record(k, std::false_type{});
+    for (int k = k_all - 1; k >= 0; --k) record(k, std::true_type{});
     __syncthreads();
     for (int i = t; i < nb * kGrad; i += kBwdThreads) {
       const int k = i / kGrad, c = i - k * kGrad;
@@ -921,6 +939,12 @@ int launch_raster_bwd(const SgsCam& cam, float3 bg, const sgs_workspace* ws, con
   const size_t nv = (size_t)lo.n * kGrad;
   const ListArgs a = list_args(ws, lo, vals);
   const bool filt = lo.sort_mode == SGS_SORT_DEPTH_FIRST;
+  static bool carve = false;
+  if (!carve) {  // all of the SM's shared memory for the CTAs' partial slots
+    SGS_CUDA(cudaFuncSetAttribute(raster_bwd_kernel<true, 0>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    SGS_CUDA(cudaFuncSetAttribute(raster_bwd_kernel<false, 0>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    carve = true;
+  }
   if (!det_scratch) {
     SGS_CUDA(cudaMemsetAsync(grad2d, 0, nv * sizeof(float), st));
     if (filt)
