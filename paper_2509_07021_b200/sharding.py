@@ -69,32 +69,69 @@ def row_costs_from_rects(rects: np.ndarray, tiles_touched: np.ndarray, tiles_y: 
 
 
 class GradBucket:
-    """Flatten a dict of gradient tensors into one contiguous buffer (one
-    NCCL all-reduce per step) and scatter it back."""
+    """Flatten a dict of gradient tensors into one contiguous buffer and
+    scatter it back.
 
-    def __init__(self, shapes: dict, device, dtype=torch.float32):
+    ``chunks == 1``: field-major (every field contiguous; one all-reduce).
+    ``chunks > 1`` (``n`` = the shared leading dimension, the primitive
+    count): chunk-major -- primitive range c holds every field's rows of that
+    range contiguously -- so chunk c can be all-reduced as soon as the
+    parameter backward of its rows is done, while later chunks are still
+    being accumulated (the overlapped, bucketed reduction of SURVEY §8(e)).
+    Every field row block starts on a 16-byte boundary (float4 rows)."""
+
+    def __init__(self, shapes: dict, device, dtype=torch.float32, chunks: int = 1, n: int | None = None):
         self.keys = list(shapes)
         self.shapes = {k: tuple(shapes[k]) for k in self.keys}
         self.sizes = {k: int(np.prod(self.shapes[k])) for k in self.keys}
+        self.chunks = max(1, int(chunks))
+        if self.chunks > 1:
+            n = int(n if n is not None else self.shapes[self.keys[0]][0])
+            if any(self.shapes[k][0] != n for k in self.keys):
+                raise ValueError("chunked buckets need a common leading dimension")
+            per = -(-n // self.chunks)
+            per = (per + 3) // 4 * 4
+            self.bounds = [(min(c * per, n), min((c + 1) * per, n)) for c in range(self.chunks)]
+        else:
+            self.bounds = [(0, None)]
         self.offsets = {}
+        self.chunk_off = []
         off = 0
-        for k in self.keys:
-            self.offsets[k] = off
-            off += (self.sizes[k] + 3) // 4 * 4  # 16-byte aligned views (float4 rows)
+        for c, (p0, p1) in enumerate(self.bounds):
+            self.chunk_off.append(off)
+            for k in self.keys:
+                rows = self.shapes[k][0] if self.chunks == 1 else p1 - p0
+                size = self.sizes[k] if self.chunks == 1 else rows * int(np.prod(self.shapes[k][1:]))
+                self.offsets[(k, c)] = (off, size)
+                off += (size + 3) // 4 * 4
+        self.chunk_off.append(off)
         self.numel = off
         self.flat = torch.zeros(off, device=device, dtype=dtype)
 
     def zero(self):
         self.flat.zero_()
 
+    def chunk_view(self, k, c: int = 0) -> torch.Tensor:
+        o, size = self.offsets[(k, c)]
+        if self.chunks == 1:
+            return self.flat[o:o + size].view(self.shapes[k])
+        p0, p1 = self.bounds[c]
+        return self.flat[o:o + size].view((p1 - p0,) + self.shapes[k][1:])
+
+    def chunk_flat(self, c: int) -> torch.Tensor:
+        return self.flat[self.chunk_off[c]:self.chunk_off[c + 1]]
+
     def view(self, k) -> torch.Tensor:
-        o = self.offsets[k]
-        return self.flat[o:o + self.sizes[k]].view(self.shapes[k])
+        if self.chunks != 1:
+            raise ValueError("a chunked bucket has no single view per field; use chunk_view / as_dict")
+        return self.chunk_view(k, 0)
 
     def add_(self, grads: dict):
         for k in self.keys:
             if k in grads and grads[k] is not None:
-                self.view(k).add_(grads[k].to(self.flat.dtype))
+                for c, (p0, p1) in enumerate(self.bounds):
+                    src = grads[k] if self.chunks == 1 else grads[k][p0:p1]
+                    self.chunk_view(k, c).add_(src.to(self.flat.dtype))
 
     def allreduce_(self, group=None, average_over: float | None = None):
         if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
@@ -104,4 +141,6 @@ class GradBucket:
         return self
 
     def as_dict(self) -> dict:
-        return {k: self.view(k) for k in self.keys}
+        if self.chunks == 1:
+            return {k: self.chunk_view(k, 0) for k in self.keys}
+        return {k: torch.cat([self.chunk_view(k, c) for c in range(self.chunks)]) for k in self.keys}

@@ -37,16 +37,28 @@ class TrainConfig:
         "lobe_logit": 1e-1})
 
 
+def _world(group) -> int:
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_world_size(group)
+    return 1
+
+
 class SoftPruneTrainer:
     """Holds device parameters + mask logits; ``step(cams, targets)`` runs one
     data-parallel training step over this rank's share of the views."""
 
     def __init__(self, arrays, prim_logit, lobe_logit, cfg: TrainConfig = TrainConfig(),
-                 device="cuda", group=None, grad_fn=None, streams: int = 4):
+                 device="cuda", group=None, grad_fn=None, streams: int = 4, comm_chunks: int = 4,
+                 chunk_single_rank: bool = False):
         """``streams``: views of a step in flight at once on this many CUDA
         streams (each with its own workspace); their parameter backwards
         (K7, which add into the shared gradient bucket) run in view order on
-        one more stream."""
+        one more stream.  ``comm_chunks``: with more than one rank the
+        gradient bucket is split into this many primitive ranges, each
+        all-reduced as soon as the last view's K7 has added its rows, so the
+        collective overlaps the rest of the parameter backward
+        (``chunk_single_rank``: chunk on one rank too -- tests)."""
         self.device = torch.device(device)
         self.cfg = cfg
         self.group = group
@@ -57,7 +69,9 @@ class SoftPruneTrainer:
         shapes = {f: t.shape for f, t in self.params.items()}
         shapes["prim_logit"] = self.prim_logit.shape
         shapes["lobe_logit"] = self.lobe_logit.shape
-        self.bucket = GradBucket(shapes, self.device)
+        n = int(self.prim_logit.shape[0])
+        self.chunks = max(1, int(comm_chunks)) if (_world(group) > 1 or chunk_single_rank) else 1
+        self.bucket = GradBucket(shapes, self.device, chunks=self.chunks, n=n)
         self.grad_fn = grad_fn
         self.rast = None if grad_fn is not None else Rasterizer(device=self.device)
         self.n_streams = max(1, int(streams)) if grad_fn is None else 1
@@ -74,13 +88,24 @@ class SoftPruneTrainer:
             return SimpleNamespace(**self.params, lobe_mask=m_l.contiguous(), prim_mask=m_p.contiguous())
         return GaussianTensors(**self.params, lobe_mask=m_l.contiguous(), prim_mask=m_p.contiguous())
 
-    def _bucket_out(self) -> dict:
-        out = {f: self.bucket.view(f) for f in GRAD_FIELDS}
-        out["prim_mask"] = self.bucket.view("prim_logit")
-        out["lobe_mask"] = self.bucket.view("lobe_logit")
+    def _bucket_out(self, c: int = 0) -> dict:
+        out = {f: self.bucket.chunk_view(f, c) for f in GRAD_FIELDS}
+        out["prim_mask"] = self.bucket.chunk_view("prim_logit", c)
+        out["lobe_mask"] = self.bucket.chunk_view("lobe_logit", c)
         return out
 
-    def _view_grads(self, g: GaussianTensors, cam, target, overflow=None):
+    def _rows(self, c: int) -> slice:
+        p0, p1 = self.bucket.bounds[c]
+        return slice(p0, p1)
+
+    def _chunk_gaussians(self, g: GaussianTensors, c: int) -> GaussianTensors:
+        if self.chunks == 1:
+            return g
+        r = self._rows(c)
+        return GaussianTensors(*(getattr(g, f)[r] for f in GRAD_FIELDS), lobe_mask=g.lobe_mask[r],
+                               prim_mask=g.prim_mask[r])
+
+    def _view_grads(self, g, cam, target, overflow=None):
         """Loss of one view; its gradients are added to the bucket (mask
         gradients through the sigmoid, i.e. with respect to the logits)."""
         if self.grad_fn is not None:
@@ -89,21 +114,30 @@ class SoftPruneTrainer:
             d_mp = gr.pop("prim_mask")
             d_ml = gr.pop("lobe_mask")
             gr.pop("grad2d", None)
+            gr["prim_logit"] = d_mp * m_p * (1 - m_p)
+            gr["lobe_logit"] = d_ml * m_l * (1 - m_l)
             self.bucket.add_(gr)
-            self.bucket.view("prim_logit").add_(d_mp * m_p * (1 - m_p))
-            self.bucket.view("lobe_logit").add_(d_ml * m_l * (1 - m_l))
             return val
-        from .render import LossConfig, loss_and_grads_device
-        val, _ = loss_and_grads_device(g, cam, target, LossConfig(lambda_ssim=self.cfg.lambda_ssim),
-                                       rast=self.rast, mask_grads=True, sync=False, overflow_out=overflow,
-                                       grads_out=self._bucket_out(), accumulate=True, mask_logit=True)
-        return val
+        from .loss import image_loss
+        from .render import LossConfig
+        frame = self.rast.forward(g, cam, check=overflow is None)
+        if overflow is not None:
+            frame.record_overflow(overflow)
+        lo, dimg, _ = image_loss(frame.img, target, LossConfig(lambda_ssim=self.cfg.lambda_ssim), grad="f32")
+        grad2d = self.rast.backward_raster(g, frame, dimg)
+        for c in range(self.chunks):
+            self.rast.backward_params(self._chunk_gaussians(g, c), frame.cam, grad2d[self._rows(c)],
+                                      mask_grads=True, out=self._bucket_out(c), accumulate=True, mask_logit=True)
+        return lo[0]
 
     def _views_pipelined(self, g: GaussianTensors, cams, targets, mine, ovf):
         """The step's views on ``n_streams`` streams: forward, loss and raster
         backward of view j on stream j mod S, then its K7 into the bucket on
-        the accumulation stream in view order (one writer: the bucket update
-        is a plain read-modify-write).  Returns the summed loss (device)."""
+        the accumulation stream in view order, chunk by chunk (one writer:
+        the bucket update is a plain read-modify-write).  Returns the summed
+        loss (device) and one event per chunk, recorded on the accumulation
+        stream when the last view's K7 has added that chunk's rows.  The
+        current stream waits for the views' streams only, not for K7."""
         from .loss import image_loss
         from .render import LossConfig
         main = torch.cuda.current_stream(self.device)
@@ -112,8 +146,10 @@ class SoftPruneTrainer:
         start.record(main)  # bucket zeroed, masks and overflow slots ready
         acc.wait_event(start)
         cfg = LossConfig(lambda_ssim=self.cfg.lambda_ssim)
-        out = self._bucket_out()
         losses = []
+        chunk_done = [torch.cuda.Event() for _ in range(self.chunks)]
+        gc = [self._chunk_gaussians(g, c) for c in range(self.chunks)]
+        outs = [self._bucket_out(c) for c in range(self.chunks)]
         for j, v in enumerate(mine):
             st = views[j % len(views)]
             st.wait_event(start)
@@ -127,19 +163,28 @@ class SoftPruneTrainer:
             acc.wait_event(done)
             grad2d.record_stream(acc)
             with torch.cuda.stream(acc):
-                self.rast.backward_params(g, frame.cam, grad2d, mask_grads=True, out=out, accumulate=True,
-                                          mask_logit=True)
+                for c in range(self.chunks):
+                    self.rast.backward_params(gc[c], frame.cam, grad2d[self._rows(c)], mask_grads=True,
+                                              out=outs[c], accumulate=True, mask_logit=True)
+                    if j == len(mine) - 1:
+                        chunk_done[c].record(acc)
             lo.record_stream(main)
             losses.append(lo[0])
-        for st in views + [acc]:
+        if not mine:
+            for c in range(self.chunks):
+                chunk_done[c].record(acc)
+        for st in views:
             main.wait_stream(st)
-        return torch.stack(losses).sum() if losses else torch.zeros((), dtype=torch.float64, device=self.device)
+        loss = torch.stack(losses).sum() if losses else torch.zeros((), dtype=torch.float64, device=self.device)
+        return loss, chunk_done
 
     def step(self, cams, targets, rank: int = 0, world: int = 1, apply: bool = True) -> float:
         """One step over all views (this rank renders its round-robin share);
         returns the global mean loss."""
+        import torch.distributed as dist
         n_views = len(cams)
         mine = shard_views(n_views, rank, world)
+        multi = dist.is_available() and dist.is_initialized() and dist.get_world_size(self.group) > 1
         self.bucket.zero()
         g = self.gaussians()
         m_p, m_l = g.prim_mask, g.lobe_mask
@@ -147,52 +192,75 @@ class SoftPruneTrainer:
         # tile-entry overflow is checked once per step (no host round trip per view)
         ovf = None if self.grad_fn is not None else torch.zeros((len(mine), 2), dtype=torch.int64,
                                                                 device=self.device)
+        chunk_done = None
         if self._streams is not None and len(mine) > 1:
-            loss_sum += self._views_pipelined(g, cams, targets, mine, ovf)
+            ls, chunk_done = self._views_pipelined(g, cams, targets, mine, ovf)
+            loss_sum += ls
         else:
             for j, v in enumerate(mine):
                 loss_sum += self._view_grads(g, cams[v], targets[v], None if ovf is None else ovf[j])
         if ovf is not None:
             # some view outgrew its capacity: size it and redo the step (on every
             # rank together, so the collectives below stay matched)
-            import torch.distributed as dist
             need = (ovf[:, 0].max() if len(mine) else torch.zeros((), dtype=torch.int64,
                                                                    device=self.device)).reshape(1)
-            if dist.is_available() and dist.is_initialized() and dist.get_world_size(self.group) > 1:
+            if multi:
                 dist.all_reduce(need, op=dist.ReduceOp.MAX, group=self.group)
             if int(need.item()):
+                if self._streams is not None:
+                    torch.cuda.current_stream(self.device).wait_stream(self._streams[1])
                 o = ovf.cpu()
                 for j, v in enumerate(mine):
                     if o[j, 0]:
                         self.rast.grow_capacity(g, cams[v], int(o[j, 1]))
                 return self.step(cams, targets, rank, world, apply)
-        # all-reduce the summed view gradients and the loss, then average
+        # bucketed all-reduce: chunk c leaves as soon as its rows are complete,
+        # while the accumulation stream still adds the later chunks
+        works = []
+        main = torch.cuda.current_stream(self.device) if self.device.type == "cuda" else None
+        for c in range(self.chunks):
+            if chunk_done is not None:
+                main.wait_event(chunk_done[c])
+            if multi:
+                works.append(dist.all_reduce(self.bucket.chunk_flat(c), op=dist.ReduceOp.SUM, group=self.group,
+                                             async_op=True))
         stats = torch.stack([loss_sum, torch.tensor(float(len(mine)), dtype=torch.float64,
                                                     device=self.device)])
-        self.bucket.allreduce_(self.group, average_over=n_views)
-        import torch.distributed as dist
-        if dist.is_available() and dist.is_initialized() and dist.get_world_size(self.group) > 1:
+        if multi:
             dist.all_reduce(stats, group=self.group)
         loss = float(stats[0]) / n_views
-        # sparsity penalty lambda_m (11 mean m_p + 7 mean m_l), through the sigmoid
         lam = self.cfg.lambda_mask
-        if lam:
+        if lam:  # sparsity penalty lambda_m (11 mean m_p + 7 mean m_l), through the sigmoid
             loss += lam * (11.0 * float(m_p.mean()) + 7.0 * float(m_l.mean()))
-            self.bucket.view("prim_logit").add_(lam * 11.0 / m_p.numel() * m_p * (1 - m_p))
-            self.bucket.view("lobe_logit").add_(lam * 7.0 / m_l.numel() * m_l * (1 - m_l))
-        if apply:
-            self.apply()
+        for c in range(self.chunks):
+            if works:
+                works[c].wait()
+            self.bucket.chunk_flat(c).div_(n_views)
+            r = self._rows(c)
+            if lam:
+                mp, ml = m_p[r], m_l[r]
+                self.bucket.chunk_view("prim_logit", c).add_(lam * 11.0 / m_p.numel() * mp * (1 - mp))
+                self.bucket.chunk_view("lobe_logit", c).add_(lam * 7.0 / m_l.numel() * ml * (1 - ml))
+            if apply:
+                self._apply_chunk(c)
+        if self._streams is not None:
+            torch.cuda.current_stream(self.device).wait_stream(self._streams[1])
         return loss
 
-    def apply(self):
+    def _apply_chunk(self, c: int):
         lr = self.cfg.lr
+        r = self._rows(c)
         with torch.no_grad():
             for f, t in self.params.items():
-                t.sub_(lr[f] * self.bucket.view(f))
-            self.params["opacity"].clamp_(0.0, 1.0)      # prune.py:185 keeps opacity in [0, 1]
-            self.params["sharpness"].clamp_(min=0.0)
-            self.prim_logit.sub_(lr["prim_logit"] * self.bucket.view("prim_logit"))
-            self.lobe_logit.sub_(lr["lobe_logit"] * self.bucket.view("lobe_logit"))
+                t[r].sub_(lr[f] * self.bucket.chunk_view(f, c))
+            self.params["opacity"][r].clamp_(0.0, 1.0)      # prune.py:185 keeps opacity in [0, 1]
+            self.params["sharpness"][r].clamp_(min=0.0)
+            self.prim_logit[r].sub_(lr["prim_logit"] * self.bucket.chunk_view("prim_logit", c))
+            self.lobe_logit[r].sub_(lr["lobe_logit"] * self.bucket.chunk_view("lobe_logit", c))
+
+    def apply(self):
+        for c in range(self.chunks):
+            self._apply_chunk(c)
 
     def grads(self) -> dict:
         return self.bucket.as_dict()

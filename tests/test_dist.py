@@ -50,8 +50,13 @@ def _worker(rank, world, port, q):
     scene, cams, targets = _setup()
     tr = SoftPruneTrainer(scene, scene.extra["prim_logit"], scene.extra["lobe_logit"],
                           TrainConfig(), device="cpu", grad_fn=_oracle_grad_fn)
+    assert tr.chunks == 4 and tr.bucket.chunks == 4   # bucketed, per-chunk async all-reduce
     loss = tr.step(cams, targets, rank=rank, world=world, apply=False)
-    q.put((rank, loss, {k: v.clone().numpy() for k, v in tr.grads().items()}))
+    grads = {k: v.clone().numpy() for k, v in tr.grads().items()}
+    tr.step(cams, targets, rank=rank, world=world, apply=True)
+    params = {k: v.clone().numpy() for k, v in tr.params.items()}
+    params["prim_logit"] = tr.prim_logit.clone().numpy()
+    q.put((rank, loss, grads, params))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -62,6 +67,9 @@ def test_grad_allreduce_matches_single_process():
                               TrainConfig(), device="cpu", grad_fn=_oracle_grad_fn)
     loss1 = single.step(cams, targets, apply=False)
     ref = {k: v.clone().numpy() for k, v in single.grads().items()}
+    single.step(cams, targets, apply=True)
+    ref_params = {k: v.clone().numpy() for k, v in single.params.items()}
+    ref_params["prim_logit"] = single.prim_logit.clone().numpy()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -72,10 +80,12 @@ def test_grad_allreduce_matches_single_process():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    for rank, loss, grads in res:
+    for rank, loss, grads, params in res:
         assert loss == pytest.approx(loss1, rel=1e-6)
         for k, v in ref.items():
             np.testing.assert_allclose(grads[k], v, rtol=1e-5, atol=1e-9 * max(1.0, np.abs(v).max()))
+        for k, v in ref_params.items():   # the chunk-by-chunk update equals the one-bucket update
+            np.testing.assert_allclose(params[k], v, rtol=1e-6, atol=1e-7)
     assert np.abs(ref["position"]).max() > 0 and np.abs(ref["prim_logit"]).max() > 0
 
 
@@ -87,6 +97,26 @@ def test_bucket_roundtrip_and_average():
     assert torch.equal(b.view("a"), torch.ones(3, 2))
     assert torch.equal(b.view("b"), torch.arange(4.0) / 2)
     assert b.numel == 12  # each view starts on a 16-byte boundary: 6 -> 8, + 4
+
+
+def test_chunked_bucket_layout():
+    """Chunk-major bucket: every chunk is one contiguous all-reduce unit and
+    holds every field's rows of its primitive range, 16-byte aligned."""
+    shapes = {"position": (10, 3), "quat": (10, 4), "opacity": (10,), "lobe": (10, 3)}
+    b = GradBucket(shapes, "cpu", chunks=3, n=10)
+    assert b.bounds == [(0, 4), (4, 8), (8, 10)]
+    g = {k: torch.randn(shp) for k, shp in shapes.items()}
+    b.add_(g)
+    back = b.as_dict()
+    assert all(torch.equal(back[k], g[k]) for k in shapes)
+    for c in range(3):
+        flat = b.chunk_flat(c)
+        assert flat.numel() == b.chunk_off[c + 1] - b.chunk_off[c]
+        for k in shapes:
+            v = b.chunk_view(k, c)
+            assert v.data_ptr() % 16 == 0 and flat.data_ptr() <= v.data_ptr() < flat.data_ptr() + 4 * flat.numel()
+    with pytest.raises(ValueError):
+        b.view("position")
 
 
 def test_strip_sharding_reassembles_the_frame_cpu_oracle():

@@ -100,3 +100,25 @@ def test_backward_accumulate_and_mask_logit_flags():
         assert torch.allclose(acc[f], want, rtol=1e-4, atol=1e-5 * float(ref[f].abs().max())), f
     with pytest.raises(ValueError):
         rast.backward(g, fr, dimg, accumulate=True)
+
+
+def test_chunked_bucket_step_equals_single_bucket():
+    """The bucketed step (K7 per primitive range into a chunk-major bucket,
+    chunk-by-chunk reduction and update -- the multi-rank path, forced on one
+    rank) gives the single-bucket step's gradients and parameters."""
+    scene, cams, targets = _setup(n=3001, views=4)
+    a = SoftPruneTrainer(scene, scene.extra["prim_logit"], scene.extra["lobe_logit"], TrainConfig())
+    b = SoftPruneTrainer(scene, scene.extra["prim_logit"], scene.extra["lobe_logit"], TrainConfig(),
+                         comm_chunks=3, chunk_single_rank=True)
+    assert b.chunks == 3
+    la = a.step(cams, targets, apply=False)
+    lb = b.step(cams, targets, apply=False)
+    assert la == pytest.approx(lb, rel=1e-9)
+    ga, gb = a.grads(), b.grads()
+    for k in ga:
+        ref = ga[k].double()
+        assert torch.allclose(gb[k].double(), ref, rtol=1e-5, atol=1e-6 * float(ref.abs().max())), k
+    a.step(cams, targets)
+    b.step(cams, targets)
+    for k in a.params:
+        assert torch.allclose(a.params[k], b.params[k], rtol=1e-5, atol=1e-6), k
