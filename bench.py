@@ -668,18 +668,28 @@ def run_cfg4(ctx) -> dict:
     from paper_2509_07021_b200 import scenes
     from paper_2509_07021_b200._ffi import CapacityError
     from paper_2509_07021_b200.rasterizer import GaussianTensors, Rasterizer
-    from paper_2509_07021_b200.sharding import balanced_strips, row_costs_from_rects
+    from paper_2509_07021_b200.sharding import balanced_strips, row_costs_from_rects, row_costs_measured
     args, dev = ctx.args, ctx.dev
     n = args.n if (args.n and args.workload == "stress") else 5_000_000
     scene, (cam,) = scenes.config4(n=n)
     rast = Rasterizer(device=dev)
     g = GaussianTensors.from_arrays(scene, device=dev)
     tiles_y = (cam.height + 15) // 16
-    # cost estimate from one preprocess pass (host-side strip planning)
+    # strip planning from one measured full frame: raster cost per tile row
+    # from the kept pairs (contributor counts), binning cost from the tile
+    # entries (sharding.row_costs_measured)
     _, rect, tt = rast.preprocess_only(g, cam)
-    cost = row_costs_from_rects(rect.cpu().numpy().view(np.uint32), tt.cpu().numpy().view(np.uint32), tiles_y)
+    entry_rows = row_costs_from_rects(rect.cpu().numpy().view(np.uint32), tt.cpu().numpy().view(np.uint32),
+                                      tiles_y)
     img = torch.empty((cam.height, cam.width, 3), device=dev)
     T = torch.empty((cam.height, cam.width), device=dev)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    full = rast.forward(g, cam, check=True, _events=ev)
+    full = rast.forward(g, cam, check=True, _events=ev)
+    torch.cuda.synchronize(dev)
+    cost = row_costs_measured(full.ncontrib.cpu().numpy(), entry_rows, ev[0].elapsed_time(ev[1]),
+                              ev[3].elapsed_time(ev[0]))
+    full = None
     per_rank = 1
     while True:
         strips = balanced_strips(cost, ctx.world * per_rank)[ctx.rank * per_rank:(ctx.rank + 1) * per_rank]

@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(256, SGS_PRE_REG_CTAS) preprocess_kernel(sgs_p
       const uint32_t dk = emitting ? sgs_float_to_bits(pr.depth) : 0x7fffffffu;
       depth_key[i] = dk;
       depth_res[i] = emitting ? pr.depth_res : 0.0f;
-      if (depth_hist) {
+      if (depth_hist && emitting) {
 #pragma unroll
         for (int d = 0; d < 4; ++d) atomicAdd(&s_hist[d][(dk >> (8 * d)) & 0xffu], 1u);
       }
@@ -287,6 +287,19 @@ __global__ void __launch_bounds__(256, SGS_PRE_REG_CTAS) preprocess_kernel(sgs_p
         sgs_pack_eig(&pr, e4);
         rec_eig[i] = make_float4(e4[0], e4[1], e4[2], e4[3]);
         rec_col[i] = make_float4(c[0], c[1], c[2], 0.0f);
+      }
+    }
+    if (depth_hist) {
+      // the not-emitting key 0x7fffffff: one count per warp (32 lanes on the
+      // same four shared counters would serialise -- most of a strip's
+      // primitives are not emitting)
+      const uint32_t m = __ballot_sync(0xffffffffu, live && !emitting);
+      if (lane == 0 && m) {
+        const uint32_t c = (uint32_t)__popc(m);
+        atomicAdd(&s_hist[0][0xffu], c);
+        atomicAdd(&s_hist[1][0xffu], c);
+        atomicAdd(&s_hist[2][0xffu], c);
+        atomicAdd(&s_hist[3][0x7fu], c);
       }
     }
     warp_count(&ctr->n_visible, visible);

@@ -231,22 +231,30 @@ SGS_HD float sgs_dot3(float a0, float a1, float a2, float b0, float b1, float b2
   return F_ADD(F_ADD(F_MUL(a0, b0), F_MUL(a1, b1)), F_MUL(a2, b2));
 }
 
+// Camera-space depth: float32 z (float32 camera, for the projection) and
+// float64 z64 from the caller's float64 camera row -- the reference orders by
+// its float64 z (render.py:307), which the float32 z does not reproduce for
+// near-ties.  Returns visibility, z64 > near (render.py:263).
+SGS_HD int sgs_depth(const float pos[3], const SgsCam* cam, float* z, double* z64) {
+  const float* W = cam->R;
+  *z = F_ADD(sgs_dot3(W[6], W[7], W[8], pos[0], pos[1], pos[2]), cam->t[2]);
+  *z64 = D_ADD(D_ADD(D_ADD(D_MUL(cam->rz[0], (double)pos[0]), D_MUL(cam->rz[1], (double)pos[1])),
+                     D_MUL(cam->rz[2], (double)pos[2])),
+               cam->tz);
+  return *z64 > cam->near64 && *z > 0.0f;
+}
+
 // Geometry of one primitive (render.py:262-292 plus the support rectangle).
 SGS_HD void sgs_project(const float pos[3], const float quat[4], const float ls[3],
                         float opacity, float pmask, const SgsCam* cam, SgsProj* o) {
   const float* W = cam->R;
   float x = F_ADD(sgs_dot3(W[0], W[1], W[2], pos[0], pos[1], pos[2]), cam->t[0]);
   float y = F_ADD(sgs_dot3(W[3], W[4], W[5], pos[0], pos[1], pos[2]), cam->t[1]);
-  float z = F_ADD(sgs_dot3(W[6], W[7], W[8], pos[0], pos[1], pos[2]), cam->t[2]);
-  // depth and visibility in float64 from the caller's float64 camera row:
-  // the reference orders by its float64 z (render.py:307), which the
-  // float32 z above (float32 camera) does not reproduce for near-ties
-  const double z64 = D_ADD(D_ADD(D_ADD(D_MUL(cam->rz[0], (double)pos[0]), D_MUL(cam->rz[1], (double)pos[1])),
-                                 D_MUL(cam->rz[2], (double)pos[2])),
-                           cam->tz);
+  float z;
+  double z64;
+  o->visible = sgs_depth(pos, cam, &z, &z64);
   o->depth = (float)z64;
   o->depth_res = (float)D_SUB(z64, (double)o->depth);
-  o->visible = z64 > cam->near64 && z > 0.0f;
   o->emits = 0;
   o->tx0 = o->ty0 = 0;
   o->tx1 = o->ty1 = -1;
