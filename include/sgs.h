@@ -62,6 +62,13 @@ typedef struct sgs_camera {
    * depth_row all zero = derive it from the float32 rotation/translation. */
   double depth_row[4];
   double near_z64;
+  /* Gradient renders: bin every primitive with at least this opacity's
+   * support (o_eff below it still blends with its true opacity, 0 included).
+   * The reference blends every primitive into every pixel, so dL/do of a
+   * primitive at o_eff = 0 is sum dL/dalpha G, not 0 (render.py:538-560);
+   * with grad_floor > 0 such primitives get that gradient (and can recover
+   * in the pruning loop).  0 = plain opacity-aware support. */
+  float grad_floor;
 } sgs_camera;
 
 /* Packed parameter arrays, render.py:90-108 (SceneParams) + soft masks. */
@@ -131,6 +138,10 @@ typedef struct sgs_stats {
 
 /* Library / ABI version and last error message (thread-local). */
 int32_t sgs_version(void);
+
+/* sizeof of the ABI structs as this library was compiled: out[0..3] =
+ * sgs_camera, sgs_params, sgs_workspace, sgs_stats (bindings check theirs). */
+int sgs_abi_sizes(uint64_t out[4]);
 const char* sgs_last_error(void);
 
 /* Bytes of device workspace for N primitives, an image of width x height

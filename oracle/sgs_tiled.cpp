@@ -42,6 +42,7 @@ SgsCam make_cam(const float* R, const float* t, float fx, float fy, float cx, fl
   for (int k = 0; k < 3; ++k) c.rz[k] = cam_d ? cam_d[k] : (double)R[6 + k];
   c.tz = cam_d ? cam_d[3] : (double)t[2];
   c.near64 = cam_d ? cam_d[4] : (double)near_z;
+  c.grad_floor = cam_d ? (float)cam_d[5] : 0.0f;
   for (int i = 0; i < 9; ++i) c.R[i] = R[i];
   for (int i = 0; i < 3; ++i) c.t[i] = t[i];
   for (int k = 0; k < 3; ++k) {
@@ -228,7 +229,10 @@ void oracle_raster_backward(const uint32_t* ranges, const uint32_t* vals, const 
         const double t1 = (double)r[8] * dx + (double)r[9] * dy, t2 = (double)r[10] * dy - (double)r[11] * dx;
         const double p = (double)r[2] - t1 * t1 - t2 * t2;  // log2(o_eff G)
         const double a = exp2(p);
-        const double G = a;  // o_eff G: dq below is -1/2 o G dalpha
+        // o_eff G: dq below is -1/2 o G dalpha; a record at o_eff = 0 (binned
+        // by the gradient floor) carries G itself, the opacity partial per
+        // unit opacity (its geometry partials are zero: alpha = 0 G)
+        const double G = std::isinf(r[2]) ? exp2(-t1 * t1 - t2 * t2) : a;
         const double alpha = std::min(a, 0.99);
         const double Tn = T * (1.0 - alpha);
         if (Tn < (double)SGS_T_KEEP) break;
@@ -330,11 +334,14 @@ void oracle_preprocess_backward(int64_t n, int L, const float* pos, const float*
       cov[3] += (double)cam_f[17];
       const double det = cov[0] * cov[3] - cov[1] * cov[2];
       const double K[4] = {cov[3] / det, -cov[1] / det, -cov[2] / det, cov[0] / det};
-      const double dK[4] = {gv[6], gv[7], gv[7], gv[8]};
-      const double dmx = -2.0 * (K[0] * gv[4] + K[1] * gv[5]);
-      const double dmy = -2.0 * (K[2] * gv[4] + K[3] * gv[5]);
+      const double zg0 = ((double)opac[i] * (pmask ? pmask[i] : 1.0f)) > 0 ? 1.0 : 0.0;
+      const double dK[4] = {zg0 * gv[6], zg0 * gv[7], zg0 * gv[7], zg0 * gv[8]};
+      const double dmx = -2.0 * zg0 * (K[0] * gv[4] + K[1] * gv[5]);
+      const double dmy = -2.0 * zg0 * (K[2] * gv[4] + K[3] * gv[5]);
       const double oe = (double)opac[i] * (pmask ? pmask[i] : 1.0f);
-      const double doe = oe > 0 ? -2.0 * gv[3] / oe : 0.0;
+      // o_eff = 0: the raster stored -1/2 sum G dalpha (per unit opacity) and
+      // the mean / conic partials of alpha = 0 G are zero
+      const double doe = oe > 0 ? -2.0 * gv[3] / oe : -2.0 * gv[3];
       dop = (pmask ? pmask[i] : 1.0f) * doe;
       dpm = opac[i] * doe;
       double KdK[4], dcov[4];

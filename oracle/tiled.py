@@ -52,11 +52,12 @@ def cam_arrays(cam, tile_rows=(0, 0), lowpass=0.3):
     return f, i
 
 
-def cam_f64(cam):
+def cam_f64(cam, grad_floor: float = 0.0):
     """(w0, w1, w2, t_z, near) in float64: the depth row (sgs_camera.depth_row)."""
     r = np.asarray(cam.rotation, dtype=np.float64).reshape(3, 3)
     t = np.asarray(cam.translation, dtype=np.float64).reshape(3)
-    return np.array([r[2, 0], r[2, 1], r[2, 2], t[2], float(getattr(cam, "near", 0.1))], np.float64)
+    return np.array([r[2, 0], r[2, 1], r[2, 2], t[2], float(getattr(cam, "near", 0.1)),
+                     float(np.float32(grad_floor))], np.float64)
 
 
 def _arrays(s):
@@ -72,7 +73,7 @@ class TiledResult:
     pass
 
 
-def preprocess(scene, cam, tile_rows=(0, 0), lowpass=0.3):
+def preprocess(scene, cam, tile_rows=(0, 0), lowpass=0.3, grad_floor=0.0):
     a = _arrays(scene)
     n, L = a["position"].shape[0], a["axis_raw"].shape[1]
     cf, ci = cam_arrays(cam, tile_rows, lowpass)
@@ -86,7 +87,7 @@ def preprocess(scene, cam, tile_rows=(0, 0), lowpass=0.3):
     lib().oracle_preprocess(C.c_int64(n), C.c_int(L), _p(a["position"]), _p(a["quat"]),
                             _p(a["log_scale"]), _p(a["opacity"]), _p(a["diffuse"]),
                             _p(a["axis_raw"]), _p(a["sharpness"]), _p(a["amplitude"]),
-                            _p(a["lobe_mask"]), _p(a["prim_mask"]), _p(cf), _p(ci), _p(cam_f64(cam)),
+                            _p(a["lobe_mask"]), _p(a["prim_mask"]), _p(cf), _p(ci), _p(cam_f64(cam, grad_floor)),
                             _p(r.depth_bits), _p(r.depth_res), _p(r.rect), _p(r.tiles_touched), _p(r.records),
                             _p(counts))
     r.n_visible, r.n_emitting = int(counts[0]), int(counts[1])
@@ -148,8 +149,8 @@ def preprocess_backward(r, grad2d=None):
     return out
 
 
-def render(scene, cam, background=(0.0, 0.0, 0.0), tile_rows=(0, 0), importance=False):
-    r = preprocess(scene, cam, tile_rows)
+def render(scene, cam, background=(0.0, 0.0, 0.0), tile_rows=(0, 0), importance=False, grad_floor=0.0):
+    r = preprocess(scene, cam, tile_rows, grad_floor=grad_floor)
     bin(r)
     return raster_forward(r, background, importance)
 

@@ -27,7 +27,7 @@ class SgsCamera(C.Structure):
                 ("fx", C.c_float), ("fy", C.c_float), ("cx", C.c_float), ("cy", C.c_float),
                 ("near_z", C.c_float), ("width", C.c_int32), ("height", C.c_int32),
                 ("tile_y0", C.c_int32), ("tile_y1", C.c_int32), ("lowpass", C.c_float),
-                ("depth_row", C.c_double * 4), ("near_z64", C.c_double)]
+                ("depth_row", C.c_double * 4), ("near_z64", C.c_double), ("grad_floor", C.c_float)]
 
 
 class SgsParams(C.Structure):
@@ -76,6 +76,7 @@ class SgsLossConfig(C.Structure):
 _P = C.POINTER
 SIGNATURES = {
     "sgs_version": (C.c_int32, []),
+    "sgs_abi_sizes": (C.c_int, [_P(C.c_uint64)]),
     "sgs_last_error": (C.c_char_p, []),
     "sgs_workspace_size": (C.c_int, [_P(SgsWorkspace), _P(C.c_uint64)]),
     "sgs_preprocess": (C.c_int, [_P(SgsParams), _P(SgsCamera), _P(SgsWorkspace), C.c_void_p]),

@@ -67,7 +67,8 @@ class Camera:
                       near=self.near)
 
 
-def to_sgs(cam, tile_rows: tuple[int, int] | None = None, lowpass: float = 0.3) -> _ffi.SgsCamera:
+def to_sgs(cam, tile_rows: tuple[int, int] | None = None, lowpass: float = 0.3,
+           grad_floor: float = 0.0) -> _ffi.SgsCamera:
     """Duck-typed camera -> C struct (float32, as the GPU computes)."""
     c = _ffi.SgsCamera()
     rot = np.asarray(cam.rotation, dtype=np.float64).reshape(9).astype(np.float32)
@@ -91,4 +92,5 @@ def to_sgs(cam, tile_rows: tuple[int, int] | None = None, lowpass: float = 0.3) 
         c.depth_row[k] = float(r64[2, k])
     c.depth_row[3] = float(t64[2])
     c.near_z64 = float(getattr(cam, "near", 0.1))
+    c.grad_floor = float(np.float32(grad_floor))
     return c

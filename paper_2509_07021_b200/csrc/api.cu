@@ -105,6 +105,15 @@ extern "C" {
 
 int32_t sgs_version(void) { return 200; }
 
+int sgs_abi_sizes(uint64_t out[4]) {
+  if (!out) return SGS_E_ARG;
+  out[0] = sizeof(sgs_camera);
+  out[1] = sizeof(sgs_params);
+  out[2] = sizeof(sgs_workspace);
+  out[3] = sizeof(sgs_stats);
+  return SGS_OK;
+}
+
 const char* sgs_last_error(void) { return g_err; }
 
 int sgs_workspace_size(const sgs_workspace* ws, uint64_t* bytes_out) {

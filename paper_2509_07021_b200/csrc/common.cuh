@@ -238,6 +238,11 @@ inline int make_cam(const sgs_camera* c, const Layout& lo, SgsCam* out) {
   for (int k = 0; k < 3; ++k) out->rz[k] = have64 ? c->depth_row[k] : (double)c->rotation[6 + k];
   out->tz = have64 ? c->depth_row[3] : (double)c->translation[2];
   out->near64 = c->near_z64 > 0.0 ? c->near_z64 : (double)c->near_z;
+  if (!(c->grad_floor >= 0.0f) || c->grad_floor > 1.0f) {
+    set_error("grad_floor must be in [0, 1]");
+    return SGS_E_ARG;
+  }
+  out->grad_floor = c->grad_floor;
   return SGS_OK;
 }
 

@@ -94,11 +94,15 @@ __global__ void __launch_bounds__(128) preprocess_bwd_kernel(sgs_params P, SgsCa
       const double k00 = cc * idet, k01 = -cb * idet, k11 = ca * idet;
 
       // ---------------- 2D partials
-      const double m0 = gv[3], m1x = gv[4], m1y = gv[5], m2xx = gv[6], m2xy = gv[7], m2yy = gv[8];
+      // o_eff = 0 (binned by the gradient floor): K6 stored the dq partials
+      // per unit opacity, and alpha = 0 G has no mean / conic gradient
+      const float oeff = op * pm;
+      const double zg = oeff > 0.0f ? 1.0 : 0.0;
+      const double m0 = gv[3], m1x = zg * gv[4], m1y = zg * gv[5], m2xx = zg * gv[6], m2xy = zg * gv[7],
+                   m2yy = zg * gv[8];
       const double dmx = -2.0 * (k00 * m1x + k01 * m1y);
       const double dmy = -2.0 * (k01 * m1x + k11 * m1y);
-      const float oeff = op * pm;
-      const float d_oeff = oeff > 0.0f ? (float)(-2.0 * m0 / (double)oeff) : 0.0f;
+      const float d_oeff = (float)(oeff > 0.0f ? -2.0 * m0 / (double)oeff : -2.0 * m0);
       d_op = pm * d_oeff;
       d_pm = op * d_oeff;
       // d_cov = -K dK K (K = conic, dK symmetric with off-diagonals m2xy)

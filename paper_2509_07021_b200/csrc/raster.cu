@@ -740,10 +740,16 @@ __global__ void __launch_bounds__(kBwdThreads, SGS_BWD_MIN_BLOCKS) raster_bwd_ke
       const float2 t2 = __ffma2_rn(f2(E.z), dy, f2(-e3dx));
       const float2 p = __ffma2_rn(neg2(t1), t1, __ffma2_rn(neg2(t2), t2, f2(G.z)));
       const bool act0 = kAll || idx < nc0, act1 = kAll || idx < nc1;
+      // o_eff = 0 (binned by the gradient floor, sgs_camera.grad_floor): alpha
+      // is 0 everywhere, but dL/do_eff = sum G dL/dalpha is not; its dq
+      // partials are taken per unit opacity (G itself, K7 reads them so) and
+      // its support is the floor's, log2 o_bin = log2 eps - pmin (geo.w)
+      const bool zero_o = G.z == -INFINITY;  // warp-uniform: one record
+      const float2 ps = zero_o ? __ffma2_rn(neg2(t1), t1, __ffma2_rn(neg2(t2), t2, f2(SGS_LOG2_EPS - G.w))) : p;
       // A record outside the support of every active pixel of the warp
       // (alpha < 1e-7 for all of them) contributes < 1e-7 of any partial and
       // changes T by a factor within 1e-7 of 1: skip it whole.
-      if (!warp_any((act0 && p.x >= SGS_LOG2_EPS) || (act1 && p.y >= SGS_LOG2_EPS))) {
+      if (!warp_any((act0 && ps.x >= SGS_LOG2_EPS) || (act1 && ps.y >= SGS_LOG2_EPS))) {
         if (vidx < kGrad) s_part[wq_][k][vidx] = 0.0f;
         return;
       }
@@ -756,7 +762,12 @@ __global__ void __launch_bounds__(kBwdThreads, SGS_BWD_MIN_BLOCKS) raster_bwd_ke
       const float2 w = __fmul2_rn(alpha, Ti);
       const float2 cg = __ffma2_rn(f2(col.x), gx2, __ffma2_rn(f2(col.y), gy2, __fmul2_rn(f2(col.z), gz2)));
       const float2 dal = __ffma2_rn(Ti, cg, neg2(__fmul2_rn(S2, rom)));
-      const float2 dq = __fmul2_rn(__fmul2_rn(f2(-0.5f), a), dal);
+      float2 ag = a;
+      if (zero_o) {
+        const float2 pg = __ffma2_rn(neg2(t1), t1, __fmul2_rn(neg2(t2), t2));
+        ag = make_float2(ex2_approx(pg.x), ex2_approx(pg.y));
+      }
+      const float2 dq = __fmul2_rn(__fmul2_rn(f2(-0.5f), ag), dal);
       const float2 Sn = __ffma2_rn(w, cg, S2);
       const bool l0 = act0 && a.x < SGS_ALPHA_MAX, l1 = act1 && a.y < SGS_ALPHA_MAX;
       const float2 dqa = make_float2(l0 ? dq.x : 0.0f, l1 ? dq.y : 0.0f);

@@ -190,6 +190,7 @@ typedef struct SgsCam {
   float lowpass;             // px^2 added to the cov2d diagonal (render.py:26, 285-286)
   double rz[3], tz;          // float64 depth row: z64 = (rz0 x + rz1 y) + rz2 z + tz (render.py:262)
   double near64;             // visible iff z64 > near64 (render.py:263)
+  float grad_floor;          // binning opacity floor of gradient renders (sgs_camera.grad_floor)
 } SgsCam;
 
 // Projected primitive: everything the binning stage and the forward raster
@@ -204,7 +205,8 @@ typedef struct SgsProj {
   // t1 = u . d, t2 = u x d (u = unit major axis of cov2d)
   float ux, uy, ilmax, ilmin;
   float o_eff;
-  float ln_o;        // ln(o_eff) (sgs_logf), valid when emits
+  float ln_o;        // ln(max(o_eff, grad_floor)) (sgs_logf): the support, valid when emits
+  float ln_oe;       // ln(o_eff): the blend (-inf at o_eff = 0)
   float qmax;
   int32_t tx0, ty0, tx1, ty1;
   int32_t visible;   // z > near (render.py:263)
@@ -344,11 +346,13 @@ SGS_HD void sgs_project(const float pos[3], const float quat[4], const float ls[
   }
   float oe = F_MUL(opacity, pmask);
   o->o_eff = oe;
-  if (!(oe > SGS_EPS) || !(det > 0.0)) {
+  const float ob = oe > cam->grad_floor ? oe : cam->grad_floor;  // support opacity
+  if (!(ob > SGS_EPS) || !(det > 0.0)) {
     o->qmax = 0.0f;
     return;
   }
-  o->ln_o = sgs_logf(oe);
+  o->ln_o = sgs_logf(ob);
+  o->ln_oe = ob == oe ? o->ln_o : sgs_logf(oe);
   float qmax = F_MUL(2.0f, F_SUB(o->ln_o, SGS_LN_EPS));
   o->qmax = qmax;
   // exact bounding box of {d : d^T cov^-1 d <= qmax} is sqrt(qmax * cov_ii)
@@ -614,7 +618,7 @@ SGS_HD void sgs_pack_geo(const SgsProj* p, float geo[4], float con[4]) {
   const float k = -0.5f * SGS_LOG2E;
   geo[0] = p->mx;
   geo[1] = p->my;
-  geo[2] = F_MUL(p->ln_o, SGS_LOG2E);
+  geo[2] = F_MUL(p->ln_oe, SGS_LOG2E);  // blend: log2 o_eff (-inf at 0); geo[3] holds the support
   geo[3] = F_MUL(k, p->qmax);
   con[0] = F_MUL(k, p->con00);
   con[1] = F_MUL(2.0f * k, p->con01);

@@ -265,7 +265,7 @@ class Rasterizer:
     # ------------------------------------------------------------------ forward
     def forward(self, g: GaussianTensors, cam, background=(0.0, 0.0, 0.0), weight_sums=None,
                 check=True, private=False, tile_rows=None, out=None, pair_count=None,
-                track=True, weight_fx=None, _events=None) -> Frame:
+                track=True, weight_fx=None, grad_floor: float = 0.0, _events=None) -> Frame:
         # _events (timing hooks): (raster start, raster end[, preprocess start,
         # preprocess end]) CUDA events recorded on the current stream
         """Render one view.  ``weight_sums`` (N float32 device tensor) is
@@ -275,8 +275,10 @@ class Rasterizer:
         converted once (``fixed_to_float``).  ``out`` may supply
         preallocated (img, T, nc) tensors.  ``track=False`` renders the image
         (and T) only, skipping the per-pixel contributor counts the backward
-        needs (an image-only render, render.py:411)."""
-        c_cam = to_sgs(cam, tile_rows)
+        needs (an image-only render, render.py:411).  ``grad_floor``: bin
+        every primitive with at least this opacity's support (gradient
+        renders: primitives at o_eff = 0 still get dL/do, see sgs.h)."""
+        c_cam = to_sgs(cam, tile_rows, grad_floor=grad_floor)
         bg = tuple(float(v) for v in np.asarray(background, dtype=np.float64).reshape(3))
         c_bg = (C.c_float * 3)(*bg)
         H, W = int(cam.height), int(cam.width)

@@ -38,6 +38,12 @@ ALPHA_MAX = 0.99
 T_CUTOFF = 1e-4
 LOWPASS_FLOOR = 0.3
 _PIXEL_CHUNK = 4096
+# Gradient renders bin every primitive with at least this opacity's support:
+# the reference blends every primitive into every pixel, so a primitive at
+# opacity 0 (the pruning loop clamps there, prune.py:185) still has
+# dL/do = sum G dL/dalpha (render.py:538-560) and can recover.  The support
+# q <= 2 ln(1e-3 / 1e-7) (4.3 sigma) holds all but ~1e-4 of that sum.
+GRAD_OPACITY_FLOOR = 1e-3
 _CACHE_ELEMENTS = 32_000_000
 
 __all__ = ["Camera", "Splat2D", "SceneParams", "GradientSet", "LossConfig", "ColorModelError",
@@ -344,7 +350,7 @@ def loss_and_grads_device(g: GaussianTensors, cam, target: torch.Tensor, cfg: Lo
                           background=(0.0, 0.0, 0.0), rast: Rasterizer | None = None,
                           mask_grads: bool = False, sync: bool = True, overflow_out=None,
                           grads_out: dict | None = None, accumulate: bool = False, mask_logit: bool = False,
-                          deterministic: bool = False):
+                          deterministic: bool = False, grad_floor: float = GRAD_OPACITY_FLOOR):
     """Device-resident variant: (loss, dict of float32 gradient tensors).  The
     loss is a float, or a 0-dim float64 device tensor with ``sync=False`` (no
     host round trip).  With ``overflow_out`` (int64 device tensor of 2) the
@@ -354,7 +360,7 @@ def loss_and_grads_device(g: GaussianTensors, cam, target: torch.Tensor, cfg: Lo
     Rasterizer.backward (a training step sums its views straight into one
     gradient bucket; the ADMM loop asks for bitwise-reproducible sums)."""
     rast = rast or rasterizer()
-    frame = rast.forward(g, cam, _bg(background), check=overflow_out is None)
+    frame = rast.forward(g, cam, _bg(background), check=overflow_out is None, grad_floor=grad_floor)
     if overflow_out is not None:
         frame.record_overflow(overflow_out)
     out, dimg, _ = image_loss(frame.img, target, cfg, grad="f32")

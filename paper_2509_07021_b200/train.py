@@ -23,6 +23,7 @@ from dataclasses import dataclass, field
 
 import torch
 
+from .render import GRAD_OPACITY_FLOOR
 from .sharding import GradBucket, shard_views
 from .rasterizer import GRAD_FIELDS, GaussianTensors, Rasterizer
 
@@ -120,7 +121,7 @@ class SoftPruneTrainer:
             return val
         from .loss import image_loss
         from .render import LossConfig
-        frame = self.rast.forward(g, cam, check=overflow is None)
+        frame = self.rast.forward(g, cam, check=overflow is None, grad_floor=GRAD_OPACITY_FLOOR)
         if overflow is not None:
             frame.record_overflow(overflow)
         lo, dimg, _ = image_loss(frame.img, target, LossConfig(lambda_ssim=self.cfg.lambda_ssim), grad="f32")
@@ -154,7 +155,7 @@ class SoftPruneTrainer:
             st = views[j % len(views)]
             st.wait_event(start)
             with torch.cuda.stream(st):
-                frame = self.rast.forward(g, cams[v], check=False)
+                frame = self.rast.forward(g, cams[v], check=False, grad_floor=GRAD_OPACITY_FLOOR)
                 frame.record_overflow(ovf[j])
                 lo, dimg, _ = image_loss(frame.img, targets[v], cfg, grad="f32")
                 grad2d = self.rast.backward_raster(g, frame, dimg)

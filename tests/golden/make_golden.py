@@ -209,6 +209,21 @@ def gen_aniso_grads():
          crop=np.array([x0, y0, w, h]), **out, **cam_dict(cam))
 
 
+def gen_zero_opacity():
+    """Primitives at opacity exactly 0 (the pruning loop clamps there,
+    prune.py:185): the reference's dense blend still gives them
+    dL/do = sum G dL/dalpha (render.py:538-560).  configs[0] distributions,
+    2000 primitives, every fifth one at opacity 0, a 64x48 crop."""
+    s, cams = scenes.config0(n=2000, seed=5)
+    s.opacity[::5] = np.float32(0.0)
+    cam = cams[0].crop(96, 100, 64, 48)
+    tgt = scenes.target_image(5, cam.height, cam.width)
+    p = ref_params(s)
+    val, g = R.loss_and_grads(p, ref_cam(cam), tgt.astype(np.float64), R.LossConfig())
+    out = {f"g_{f}": getattr(g, f) for f in FIELDS}
+    save("zero_opacity", target=tgt, loss=np.array(val), **out, **scene_dict(s), **cam_dict(cam))
+
+
 def gen_vram():
     """estimate_vram (postprocess.py:101-137) on seeded random scenes."""
     out = {}
@@ -326,6 +341,7 @@ GENERATORS = {
     "cfg4_crop_b": lambda: gen_crop("cfg4_crop_b", 4, 0, 1904, 1064, 16, 16),
     "cfg4_crop_c": lambda: gen_crop("cfg4_crop_c", 4, 0, 1200, 700, 16, 16),
     "aniso_grads": gen_aniso_grads,
+    "zero_opacity": gen_zero_opacity,
 }
 
 if __name__ == "__main__":

@@ -33,7 +33,12 @@ def test_library_exports_every_declared_symbol():
 
 def test_struct_layouts_match_header():
     # sizes of the ABI structs as C sees them (x86-64 SysV)
-    assert C.sizeof(_ffi.SgsCamera) == 4 * 9 + 4 * 3 + 4 * 5 + 4 * 4 + 4 + 8 * 4 + 8
+    assert C.sizeof(_ffi.SgsCamera) == 4 * 9 + 4 * 3 + 4 * 5 + 4 * 4 + 4 + 8 * 4 + 8 + 8
+    # ... and as the library itself was compiled
+    sizes = (C.c_uint64 * 4)()
+    assert _ffi.load().sgs_abi_sizes(sizes) == _ffi.SGS_OK
+    assert list(sizes) == [C.sizeof(_ffi.SgsCamera), C.sizeof(_ffi.SgsParams), C.sizeof(_ffi.SgsWorkspace),
+                           C.sizeof(_ffi.SgsStats)]
     assert C.sizeof(_ffi.SgsParams) == 10 * 8 + 8 + 8
     assert C.sizeof(_ffi.SgsWorkspace) == 8 + 8 + 8 + 4 * 4 + 8
     assert C.sizeof(_ffi.SgsStats) == 8 * 8
