@@ -738,18 +738,14 @@ __global__ void __launch_bounds__(kBwdThreads, SGS_BWD_MIN_BLOCKS) raster_bwd_ke
       const float e1dx = E.x * dx, e3dx = E.w * dx;
       const float2 t1 = __ffma2_rn(f2(E.y), dy, f2(e1dx));
       const float2 t2 = __ffma2_rn(f2(E.z), dy, f2(-e3dx));
-      const float2 p = __ffma2_rn(neg2(t1), t1, __ffma2_rn(neg2(t2), t2, f2(G.z)));
+      const float2 pq = __ffma2_rn(neg2(t1), t1, __fmul2_rn(neg2(t2), t2));  // log2 G = -(t1^2 + t2^2)
+      const float2 p = __fadd2_rn(pq, f2(G.z));                                // log2 (o_eff G)
       const bool act0 = kAll || idx < nc0, act1 = kAll || idx < nc1;
-      // o_eff = 0 (binned by the gradient floor, sgs_camera.grad_floor): alpha
-      // is 0 everywhere, but dL/do_eff = sum G dL/dalpha is not; its dq
-      // partials are taken per unit opacity (G itself, K7 reads them so) and
-      // its support is the floor's, log2 o_bin = log2 eps - pmin (geo.w)
-      const bool zero_o = G.z == -INFINITY;  // warp-uniform: one record
-      const float2 ps = zero_o ? __ffma2_rn(neg2(t1), t1, __ffma2_rn(neg2(t2), t2, f2(SGS_LOG2_EPS - G.w))) : p;
-      // A record outside the support of every active pixel of the warp
-      // (alpha < 1e-7 for all of them) contributes < 1e-7 of any partial and
-      // changes T by a factor within 1e-7 of 1: skip it whole.
-      if (!warp_any((act0 && ps.x >= SGS_LOG2_EPS) || (act1 && ps.y >= SGS_LOG2_EPS))) {
+      // A record outside the support every active pixel of the warp was
+      // binned with (log2 G >= pmin, geo.w: o_bin G >= 1e-7) contributes
+      // < 1e-7 of any partial and changes T by a factor within 1e-7 of 1:
+      // skip it whole.  o_bin = max(o_eff, grad_floor) (sgs_camera).
+      if (!warp_any((act0 && pq.x >= G.w) || (act1 && pq.y >= G.w))) {
         if (vidx < kGrad) s_part[wq_][k][vidx] = 0.0f;
         return;
       }
@@ -762,11 +758,11 @@ __global__ void __launch_bounds__(kBwdThreads, SGS_BWD_MIN_BLOCKS) raster_bwd_ke
       const float2 w = __fmul2_rn(alpha, Ti);
       const float2 cg = __ffma2_rn(f2(col.x), gx2, __ffma2_rn(f2(col.y), gy2, __fmul2_rn(f2(col.z), gz2)));
       const float2 dal = __ffma2_rn(Ti, cg, neg2(__fmul2_rn(S2, rom)));
+      // o_eff = 0 (binned by the gradient floor): alpha is 0 everywhere, but
+      // dL/do_eff = sum G dL/dalpha is not; its dq partials are taken per
+      // unit opacity (G itself; K7 reads them so)
       float2 ag = a;
-      if (zero_o) {
-        const float2 pg = __ffma2_rn(neg2(t1), t1, __fmul2_rn(neg2(t2), t2));
-        ag = make_float2(ex2_approx(pg.x), ex2_approx(pg.y));
-      }
+      if (G.z == -INFINITY) ag = make_float2(ex2_approx(pq.x), ex2_approx(pq.y));  // warp-uniform
       const float2 dq = __fmul2_rn(__fmul2_rn(f2(-0.5f), ag), dal);
       const float2 Sn = __ffma2_rn(w, cg, S2);
       const bool l0 = act0 && a.x < SGS_ALPHA_MAX, l1 = act1 && a.y < SGS_ALPHA_MAX;
