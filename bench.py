@@ -457,9 +457,18 @@ def run_headline(ctx, timed_clocks: bool = True) -> dict:
     ctx.barrier()
     t_e2e = e0.elapsed_time(e1)
     assert br.rerendered == 0, "e2e views re-rendered after an overflow inside the timed region"
+    # release the pinned host buffers now (cudaFreeHost synchronises the
+    # device; a later garbage collection would stall another workload's
+    # event-timed region)
     pinned = None
     br = None
+    import gc
+    gc.collect()
+    torch.cuda.synchronize(dev)
 
+    # the e2e path's own roofline: pinned host <-> device copy bandwidth,
+    # measured here (both directions at once, as the batch API overlaps them)
+    link = measure_link(dev)
     t_ms, t_e2e = ctx.max_over_ranks(t_ms, t_e2e)
     frames = len(cams64) * args.steps
     value = frames / (t_ms / 1e3)
@@ -513,10 +522,43 @@ def run_headline(ctx, timed_clocks: bool = True) -> dict:
                              f"memory-bound",
                      "raster_ms_per_view": raster_mean},
         "e2e_bytes": (int(pinned_bytes(scene)), int(sum(c.width * c.height * 12 + 16 for c in my_cams))),
+        "link": link,
         "stages": stages, "super_tile_entries_per_view": Es,
         "clocks": clk, "gpu_launches": int(args.steps * V * (KERNELS_PER_FRAME if args.sort_mode == 0 else 12)),
         "scene": scene, "cams": cams64,
     }
+
+
+def measure_link(dev, nbytes: int = 1 << 30) -> dict:
+    """Pinned host <-> device copy bandwidth (GB/s): D2H alone, H2D alone,
+    and both at once on two streams (CUDA events, best of 3)."""
+    import torch
+    h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    h2 = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    d2 = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    out = {}
+    for name in ("d2h", "h2d", "both"):
+        best = 0.0
+        for _ in range(3):
+            torch.cuda.synchronize(dev)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(s1)
+            s2.wait_event(a)
+            if name in ("d2h", "both"):
+                with torch.cuda.stream(s1):
+                    h.copy_(d, non_blocking=True)
+            if name in ("h2d", "both"):
+                with torch.cuda.stream(s2):
+                    d2.copy_(h2, non_blocking=True)
+            s1.wait_stream(s2)
+            b.record(s1)
+            torch.cuda.synchronize(dev)
+            moved = nbytes * (2 if name == "both" else 1)
+            best = max(best, moved / (a.elapsed_time(b) / 1e3) / 1e9)
+        out[name + "_GBs"] = best
+    return out
 
 
 def pinned_bytes(scene) -> int:
@@ -620,10 +662,13 @@ def run_cfg3(ctx) -> dict:
     rast = tr.rast
     phases = {"forward": [], "loss": [], "backward_raster": [], "backward_params": []}
     pairs = []
+    for cam in cams:  # size every view's workspace first: no host sync inside the timed phases
+        rast.forward(g, cam, check=True)
+    torch.cuda.synchronize(dev)
     for v, cam in enumerate(cams):
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
         ev[0].record(stream)
-        fr = rast.forward(g, cam, check=True)
+        fr = rast.forward(g, cam, check=False)
         ev[1].record(stream)
         _, dimg, _ = image_loss(fr.img, targets[v], LossConfig())
         ev[2].record(stream)
@@ -786,6 +831,21 @@ def run_key64(ctx, scene, cams) -> dict:
             "tile_entries_per_view": E}
 
 
+def e2e_roofline(h, h2d, d2h, steps) -> dict:
+    """The batch API moves every image D2H (fp32 RGB, 24.9 MB at 1080p) and
+    the scene H2D each step; the copies overlap the renders, so the step is
+    bounded by the link: max(D2H bytes / D2H bandwidth, device step time)."""
+    link = h["link"]
+    t_link = d2h / (link["d2h_GBs"] * 1e9)
+    t_dev = h["t_ms"] / 1e3 / steps
+    bound = max(t_link, t_dev)
+    achieved_ms = h["frames"] / h["e2e"] / steps * 1e3
+    return {"bound": "pcie_d2h" if t_link >= t_dev else "device",
+            "link_GBs": link, "d2h_GB_per_step": d2h / 1e9,
+            "bound_ms_per_step": bound * 1e3, "achieved_ms_per_step": achieved_ms,
+            "frac": bound * 1e3 / achieved_ms}
+
+
 def run_ours(args):
     """Our arm: the configs[2] headline (+ the sub-workloads with --workload all)."""
     ctx = Ctx(args)
@@ -820,7 +880,8 @@ def run_ours(args):
             "mpix_per_s": h["mpix_per_s"], "vram": h["vram"], "roofline": h["roofline"],
             "e2e": {"value": h["e2e"], "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "api": "batch.BatchRenderer.render_views (pinned host scene in, host images out, "
-                           "overflow-checked)"},
+                           "overflow-checked)",
+                    "roofline": e2e_roofline(h, h2d, d2h, args.steps)},
             "stages": h["stages"], "super_tile_entries_per_view": h["super_tile_entries_per_view"],
             "gpu_launches": h["gpu_launches"], "clocks": h["clocks"],
         }
