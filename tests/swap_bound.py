@@ -49,8 +49,10 @@ def _alpha(rec, px, py):
 
 
 def swap_bound(z64, depth_bits, rect, tiles_touched, records, width, height, window=8, floor=1e-6,
-               half=3, max_eval=10**7):
-    """Returns a dict of counts and the largest swap effect found."""
+               half=3, max_eval=10**7, depth_res=None):
+    """Returns a dict of counts and the largest swap effect found.  The order
+    analysed is the float32 key order with ties by index or, with
+    ``depth_res``, ties by the float64 residual first (the build's order)."""
     emit = np.flatnonzero(np.asarray(tiles_touched) > 0)
     out = {"emitting": int(emit.size), "inverted_pairs": 0, "overlapping_pairs": 0,
            "pairs_above_floor": 0, "pixels_evaluated": 0, "max_bound": 0.0, "max_effect": 0.0,
@@ -60,7 +62,10 @@ def swap_bound(z64, depth_bits, rect, tiles_touched, records, width, height, win
     z64 = np.asarray(z64, np.float64)
     db = np.asarray(depth_bits).view(np.uint32).astype(np.int64)
     ref = emit[np.argsort(z64[emit], kind="stable")]
-    gpu = emit[np.lexsort((emit, db[emit]))]          # float bits, ties by lower index
+    if depth_res is None:
+        gpu = emit[np.lexsort((emit, db[emit]))]      # float bits, ties by lower index
+    else:                                             # float bits, then the float64 residual, then index
+        gpu = emit[np.lexsort((emit, np.asarray(depth_res)[emit], db[emit]))]
     rank = np.empty(int(emit.max()) + 1, np.int64)
     rank[gpu] = np.arange(gpu.size)
     r32 = np.asarray(rect).view(np.uint32)

@@ -8,11 +8,14 @@
   within the composite criterion -- the same bar the GPU is held to.
 """
 
+from pathlib import Path
+
 import numpy as np
 import pytest
 
 from helpers import composite_ok, crop_fixture, golden, golden_camera, golden_scene
 from oracle import ref_dense, tiled
+from paper_2509_07021_b200 import scenes
 
 
 def test_dense_matches_reference_crop_grads():
@@ -147,3 +150,23 @@ def test_tiled_bins_are_a_stable_key_sort():
     nz = r.ranges[:, 1] > r.ranges[:, 0]
     assert r.ranges[nz, 1].sum() - r.ranges[nz, 0].sum() == r.n_entries
     assert np.all((k >> np.uint64(32)).astype(np.int64)[r.ranges[nz, 0]] == np.flatnonzero(nz))
+
+
+@pytest.mark.parametrize("cfg", [1, 3])
+def test_float32_key_order_inverts_pairs_and_the_residual_order_does_not(cfg):
+    """SURVEY App. B depth-swap bound on the CPU restatement (bit-identical to
+    the GPU preprocess): the float32 depth key alone inverts hundreds of
+    pairs relative to the reference's float64 argsort (render.py:307); the
+    build's order (ties by the float64 residual) inverts none."""
+    import sys
+    sys.path.insert(0, str(Path(__file__).resolve().parent))
+    from swap_bound import f64_depth, swap_bound
+    scene, cams = scenes.CONFIGS[cfg]()
+    cam = cams[0]
+    r = tiled.preprocess(scene, cam)
+    z = f64_depth(scene.position, cam)
+    args = (z, r.depth_bits, r.rect, r.tiles_touched, r.records, cam.width, cam.height)
+    f32 = swap_bound(*args, floor=1.0)   # counts only
+    exact = swap_bound(*args, floor=1.0, depth_res=r.depth_res)
+    assert f32["inverted_pairs"] > 100 and f32["overlapping_pairs"] > 10
+    assert exact["inverted_pairs"] == 0
