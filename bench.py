@@ -695,6 +695,7 @@ def run_cfg3(ctx) -> dict:
             "roofline_backward": {
                 "bound": "fp32_issue", "kernel": "raster_bwd_kernel", "achieved": achieved / 1e9,
                 "peak": peak / 1e9, "unit": "Gpair/s", "frac": achieved / peak,
+                "traffic": profiled_traffic("raster_bwd_kernel"),
                 "pairs_per_view": float(np.mean(pairs)), "ms_per_view": k6_ms,
                 "note": f"pairs = sum over pixels of the kept contributor count; peak = {ctx.n_sm} SMs x "
                         f"{ctx.sm_mhz:.0f} MHz x 128/45 (SURVEY §8(d): 2.5x the forward's 18 FP32 "
