@@ -40,7 +40,8 @@ __device__ __forceinline__ uint32_t scan_load(const uint32_t* tt, const uint32_t
 }
 
 __global__ void __launch_bounds__(kScanThreads) scan_onepass(const uint32_t* __restrict__ tt,
-                                                            const uint32_t* __restrict__ perm, uint32_t n,
+                                                            const uint32_t* __restrict__ perm, uint32_t n_max,
+                                                            const uint32_t* __restrict__ n_ptr,
                                                             uint32_t cap, unsigned long long* status,
                                                             uint32_t* ticket,
                                                             unsigned long long* __restrict__ offsets,
@@ -49,7 +50,17 @@ __global__ void __launch_bounds__(kScanThreads) scan_onepass(const uint32_t* __r
   __shared__ unsigned long long s_excl;
   __shared__ uint32_t s_part;
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const uint32_t n = n_ptr ? min(*n_ptr, n_max) : n_max;  // ranks: the depth-sorted emitting primitives
   const uint32_t nparts = (n + kScanItems - 1) / kScanItems;
+  if (nparts == 0) {  // nothing emits
+    if (blockIdx.x == 0 && t == 0) {
+      ctr->n_bin = 0;
+      ctr->capacity = cap;
+      ctr->overflow = 0;
+      ctr->n_sort = 0;
+    }
+    return;
+  }
   for (;;) {
     if (t == 0) s_part = atomicAdd(ticket, 1u);
     __syncthreads();
@@ -126,9 +137,9 @@ __global__ void __launch_bounds__(kScanThreads) scan_onepass(const uint32_t* __r
 
 __global__ void set_count(uint32_t* p, uint32_t v) { *p = v; }
 
-static int launch_scan(const uint32_t* tt, const uint32_t* perm, uint32_t n, uint32_t cap,
+static int launch_scan(const uint32_t* tt, const uint32_t* perm, uint32_t n, const uint32_t* n_ptr, uint32_t cap,
                        unsigned long long* status, unsigned long long* offsets, Counters* ctr, cudaStream_t st) {
-  const uint32_t nparts = (n + kScanItems - 1) / kScanItems;
+  const uint32_t nparts = (n + kScanItems - 1) / kScanItems;  // upper bound when n_ptr is given
   if (nparts == 0) {
     SGS_CUDA(cudaMemsetAsync(&ctr->n_bin, 0, sizeof(ctr->n_bin), st));
     SGS_CUDA(cudaMemsetAsync(&ctr->n_sort, 0, sizeof(ctr->n_sort), st));
@@ -136,7 +147,7 @@ static int launch_scan(const uint32_t* tt, const uint32_t* perm, uint32_t n, uin
   }
   SGS_CUDA(cudaMemsetAsync(status, 0, (size_t)nparts * 8, st));
   SGS_CUDA(cudaMemsetAsync(&ctr->part_counter[kScanTicket], 0, 4, st));
-  scan_onepass<<<persistent_grid(nparts, 1, 8), kScanThreads, 0, st>>>(tt, perm, n, cap, status,
+  scan_onepass<<<persistent_grid(nparts, 1, 8), kScanThreads, 0, st>>>(tt, perm, n, n_ptr, cap, status,
                                                                         &ctr->part_counter[kScanTicket], offsets,
                                                                         ctr);
   SGS_LAUNCH_CHECK("scan_onepass");
@@ -145,14 +156,15 @@ static int launch_scan(const uint32_t* tt, const uint32_t* perm, uint32_t n, uin
 
 // ------------------------------------------------------ float64 depth ties
 // The radix sorts order by the float32 depth key (the float64 z rounded,
-// sgs_project) and keep equal keys in primitive-index order.  The reference
-// orders by its float64 z (render.py:307: argsort(z, kind="stable")), so
-// within a run of equal keys the primitives are re-ordered by the float64
-// residual z64 - key (sgs_project's depth_res; equal residuals keep index
-// order).  Runs are rare and short (configs[2]: ~3 % of the primitives, 2-4
-// long), so the thread at a run's first element insertion-sorts it.
-// keys: the sort's final (sorted) keys; vals: the sorted primitive indices,
-// fixed in place.  `skip`: the not-emitting key (sorted last) or ~0.
+// sgs_project); equal keys come out in input order, which is the
+// preprocess's compaction order (depth-first mode) or primitive order
+// (64-bit keys).  The reference orders by its float64 z (render.py:307:
+// argsort(z, kind="stable")), so every run of equal keys is re-ordered by
+// (float64 residual z64 - key, primitive index) -- sgs_project's depth_res;
+// equal residuals go by index like the stable argsort.  Runs are rare and
+// short (configs[2]: ~4 % of the primitives, 2-4 long), so the thread at a
+// run's first element sorts it.  keys: the sort's final (sorted) keys; vals:
+// the sorted primitive indices, fixed in place; `skip`: a key never sorted.
 template <typename K>
 __global__ void __launch_bounds__(256) depth_tie_fixup(const K* __restrict__ keys, uint32_t* __restrict__ vals,
                                                        const float* __restrict__ res, const uint32_t* n_ptr,
@@ -174,7 +186,8 @@ __global__ void __launch_bounds__(256) depth_tie_fixup(const K* __restrict__ key
     while (j < n && keys[j] == k) ++j;
     if (j - i == 2) {  // the common case: a pair
       const uint32_t a = vals[i], b = vals[i + 1];
-      if (res[b] < res[a]) {
+      const float ra = res[a], rb = res[b];
+      if (rb < ra || (rb == ra && b < a)) {
         vals[i] = b;
         vals[i + 1] = a;
       }
@@ -187,15 +200,16 @@ __global__ void __launch_bounds__(256) depth_tie_fixup(const K* __restrict__ key
       uint32_t v[kRegRun];
       float r[kRegRun];
 #pragma unroll
-      for (int a = 0; a < kRegRun; ++a) v[a] = a < len ? vals[i + a] : 0u;
+      for (int a = 0; a < kRegRun; ++a) v[a] = a < len ? vals[i + a] : 0xffffffffu;
 #pragma unroll
       for (int a = 0; a < kRegRun; ++a) r[a] = a < len ? res[v[a]] : INFINITY;
-      // stable odd-even transposition sort on (r, original position)
+      // padding (r = inf, v = ~0) sorts after every real element
+      // odd-even transposition sort on (residual, primitive index)
 #pragma unroll
       for (int round = 0; round < kRegRun; ++round)
 #pragma unroll
         for (int a = round & 1; a + 1 < kRegRun; a += 2)
-          if (r[a + 1] < r[a]) {
+          if (r[a + 1] < r[a] || (r[a + 1] == r[a] && v[a + 1] < v[a])) {
             const float tr = r[a];
             r[a] = r[a + 1];
             r[a + 1] = tr;
@@ -214,11 +228,38 @@ __global__ void __launch_bounds__(256) depth_tie_fixup(const K* __restrict__ key
       uint32_t b = a;
       while (b > i) {
         const uint32_t u = vals[b - 1];
-        if (!(res[u] > r)) break;
+        const float ru = res[u];
+        if (!(ru > r || (ru == r && u > v))) break;
         vals[b] = u;
         --b;
       }
       vals[b] = v;
+    }
+  }
+}
+
+// Strip renders (a tile-row window): most primitives do not emit, and
+// sorting their sentinel keys would make every rank sort all N.  Only the
+// emitting primitives' (key, index) enter the depth sort: compacted here,
+// one counter atomic per warp; their order does not matter (depth_tie_fixup
+// orders equal keys by residual and index).  A separate kernel: done inside
+// the preprocess, the returned atomic cost the full-frame path 26 %.
+__global__ void __launch_bounds__(256) compact_depth_keys(const uint32_t* __restrict__ depth_key, uint32_t n,
+                                                          uint32_t* __restrict__ dkey_c, uint32_t* __restrict__ didx_c,
+                                                          uint32_t* __restrict__ count) {
+  const int lane = threadIdx.x & 31;
+  for (uint32_t base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
+    const uint32_t i = base + threadIdx.x;
+    const uint32_t k = i < n ? depth_key[i] : 0x7fffffffu;
+    const bool e = k != 0x7fffffffu;
+    const uint32_t m = __ballot_sync(0xffffffffu, e);
+    uint32_t b = 0;
+    if (lane == 0 && m) b = atomicAdd(count, (uint32_t)__popc(m));
+    b = __shfl_sync(0xffffffffu, b, 0);
+    if (e) {
+      const uint32_t pos = b + __popc(m & ((1u << lane) - 1u));
+      dkey_c[pos] = k;
+      didx_c[pos] = i;
     }
   }
 }
@@ -250,7 +291,8 @@ __device__ __forceinline__ KT make_key(uint32_t tile, uint32_t dbits) {
 // kSuper: rows are super-tile rows and entries are (super-tile, primitive);
 // otherwise rows are tile rows and entries (tile, primitive).
 template <typename KT, bool kSuper>
-__global__ void __launch_bounds__(256) emit_entries(const uint32_t* __restrict__ perm, uint32_t n,
+__global__ void __launch_bounds__(256) emit_entries(const uint32_t* __restrict__ perm, uint32_t n_max,
+                                                    const uint32_t* __restrict__ n_ptr,
                                                     const uint32_t* __restrict__ counts,
                                                     const uint2* __restrict__ rect,
                                                     const float4* __restrict__ rec_geo,
@@ -277,6 +319,7 @@ __global__ void __launch_bounds__(256) emit_entries(const uint32_t* __restrict__
     __syncthreads();
   }
   const int lane = threadIdx.x & 31;
+  const uint32_t n = n_ptr ? min(*n_ptr, n_max) : n_max;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
   const unsigned long long total = *total_ptr;
@@ -399,7 +442,7 @@ bool final_in_alt(const Layout& lo) {
 
 template <typename KT, int IPT, int RBITS, bool kSuper>
 static int bin_entries(const SgsCam& cam, const sgs_workspace* ws, const Layout& lo, const uint32_t* perm,
-                       int key_bits, int tile_shift, cudaStream_t st) {
+                       const uint32_t* n_ptr, int key_bits, int tile_shift, cudaStream_t st) {
   // the emission accumulates the histogram when the cell sort is one 9-bit pass
   const bool fused_hist = kSuper && RBITS == 9 && key_bits <= 9;
   Counters* ctr = at<Counters>(ws, lo.counters);
@@ -412,7 +455,7 @@ static int bin_entries(const SgsCam& cam, const sgs_workspace* ws, const Layout&
   uint2* ranges = at<uint2>(ws, lo.ranges);
   const int n_cells = kSuper ? lo.n_super : lo.n_tiles;
   emit_entries<KT, kSuper><<<persistent_grid(n, 256, SGS_EMIT_CTAS), 256, 0, st>>>(
-      perm, n, at<uint32_t>(ws, kSuper ? lo.super_touched : lo.tiles_touched), at<uint2>(ws, lo.rect),
+      perm, n, n_ptr, at<uint32_t>(ws, kSuper ? lo.super_touched : lo.tiles_touched), at<uint2>(ws, lo.rect),
       at<float4>(ws, lo.rec_geo), at<float4>(ws, lo.rec_con), at<float4>(ws, lo.rec_span),
       at<uint32_t>(ws, lo.depth_key),
       at<unsigned long long>(ws, lo.offsets), cam, lo.super_x, cap, &ctr->n_bin, k0, v0,
@@ -446,35 +489,50 @@ int launch_bin(const SgsCam& cam, const sgs_workspace* ws, const Layout& lo, cud
   unsigned long long* offsets = at<unsigned long long>(ws, lo.offsets);
   unsigned long long* status64 = at<unsigned long long>(ws, lo.scan_blocks);  // scan look-back status
   if (lo.sort_mode == SGS_SORT_DEPTH_FIRST) {
-    uint32_t* dkey = at<uint32_t>(ws, lo.depth_key);
     uint32_t* ka = at<uint32_t>(ws, lo.dkey_alt);
     uint32_t* kb = at<uint32_t>(ws, lo.dkey_tmp);
     uint32_t* ia = at<uint32_t>(ws, lo.didx);
     uint32_t* ib = at<uint32_t>(ws, lo.didx_alt);
     bool alt = false;
     // depth keys are 31-bit (0x7fffffff = not emitting): 4 passes over N; the
-    // preprocess accumulated the four depth-digit histograms and set n_depth.
-    // The first pass reads the preprocess's keys in place (left intact, so
-    // sgs_bin may be repeated after one sgs_preprocess).
-    int rc = radix_sort_pairs<uint32_t, kDepthSortIPT, 8, kDepthSortThreads>(ka, ia, kb, ib, &ctr->n_depth, n, 31,
-                                                        at<uint32_t>(ws, lo.hist) + kDepthHistOff,
-                                                        at<uint32_t>(ws, lo.status), &ctr->part_counter[0], &alt, st,
-                                                        true, RsRangeOut{nullptr, 0}, 0, false, true, dkey);
+    // depth keys are 31-bit (0x7fffffff = not emitting): 4 passes; the
+    // preprocess accumulated the four depth-digit histograms.  Full frames
+    // sort all N primitives (n_depth = N), the first pass reading the
+    // preprocess's keys in place; strip renders sort only the emitting ones,
+    // compacted first.  Either input is left intact, so sgs_bin may be
+    // repeated after one sgs_preprocess.
+    const bool window = cam.tile_y0 > 0 || cam.tile_y1 < cam.tiles_y;
+    const uint32_t* k_first = at<uint32_t>(ws, lo.depth_key);
+    const uint32_t* v_first = nullptr;
+    if (window) {
+      SGS_CUDA(cudaMemsetAsync(&ctr->n_depth, 0, sizeof(uint32_t), st));
+      compact_depth_keys<<<persistent_grid(n, 256, 8), 256, 0, st>>>(at<uint32_t>(ws, lo.depth_key), n,
+                                                                   at<uint32_t>(ws, lo.dkey_c),
+                                                                   at<uint32_t>(ws, lo.didx_c), &ctr->n_depth);
+      SGS_LAUNCH_CHECK("compact_depth_keys");
+      k_first = at<uint32_t>(ws, lo.dkey_c);
+      v_first = at<uint32_t>(ws, lo.didx_c);
+    }
+    int rc = radix_sort_pairs<uint32_t, kDepthSortIPT, 8, kDepthSortThreads>(
+        ka, ia, kb, ib, &ctr->n_depth, n, 31, at<uint32_t>(ws, lo.hist) + kDepthHistOff,
+        at<uint32_t>(ws, lo.status), &ctr->part_counter[0], &alt, st, !window, RsRangeOut{nullptr, 0}, 0, false,
+        true, k_first, v_first);
     if (rc) return rc;
     uint32_t* perm = alt ? ib : ia;
     depth_tie_fixup<uint32_t><<<persistent_grid(n, 256, 8), 256, 0, st>>>(
         alt ? kb : ka, perm, at<float>(ws, lo.depth_res), &ctr->n_depth, n, 0x7fffffffu);
     SGS_LAUNCH_CHECK("depth_tie_fixup");
-    rc = launch_scan(at<uint32_t>(ws, lo.super_touched), perm, n, cap, status64, offsets, ctr, st);
+    rc = launch_scan(at<uint32_t>(ws, lo.super_touched), perm, n, &ctr->n_depth, cap, status64, offsets, ctr, st);
     if (rc) return rc;
     // keys (super_id << 16 | 16-bit tile mask), sorted on the super id bits only
     const int sbits = tile_sort_bits(lo.n_super);
-    if (sbits <= 9) return bin_entries<uint32_t, kTileSortIPT, 9, true>(cam, ws, lo, perm, sbits, 16, st);
-    return bin_entries<uint32_t, kTileSortIPT, 8, true>(cam, ws, lo, perm, sbits, 16, st);
+    if (sbits <= 9)
+      return bin_entries<uint32_t, kTileSortIPT, 9, true>(cam, ws, lo, perm, &ctr->n_depth, sbits, 16, st);
+    return bin_entries<uint32_t, kTileSortIPT, 8, true>(cam, ws, lo, perm, &ctr->n_depth, sbits, 16, st);
   }
-  int rc = launch_scan(at<uint32_t>(ws, lo.tiles_touched), nullptr, n, cap, status64, offsets, ctr, st);
+  int rc = launch_scan(at<uint32_t>(ws, lo.tiles_touched), nullptr, n, nullptr, cap, status64, offsets, ctr, st);
   if (rc) return rc;
-  return bin_entries<unsigned long long, kKey64SortIPT, 8, false>(cam, ws, lo, nullptr,
+  return bin_entries<unsigned long long, kKey64SortIPT, 8, false>(cam, ws, lo, nullptr, nullptr,
                                                                   32 + tile_sort_bits(lo.n_tiles), 32, st);
 }
 

@@ -83,7 +83,7 @@ struct Layout {
       super_touched, cand_end;
   uint64_t cell_order, row_off, row_spans;
   uint64_t row_cap;
-  uint64_t dkey_alt, dkey_tmp, didx, didx_alt, offsets, scan_blocks;
+  uint64_t dkey_alt, dkey_tmp, didx, didx_alt, dkey_c, didx_c, offsets, scan_blocks;
   uint64_t ent_key, ent_key_alt, ent_val, ent_val_alt, ranges;
   uint64_t hist, status;
   uint64_t status_bytes;
@@ -159,6 +159,10 @@ inline int make_layout(const sgs_workspace* ws, Layout* lo) {
   lo->dkey_tmp = take(n * 4);
   lo->didx = take(n * 4);
   lo->didx_alt = take(n * 4);
+  // depth-first mode: the emitting primitives' (depth key, index), compacted
+  // by the preprocess (the depth sort's read-only first-pass input)
+  lo->dkey_c = take(ws->sort_mode == SGS_SORT_DEPTH_FIRST ? n * 4 : 0);
+  lo->didx_c = take(ws->sort_mode == SGS_SORT_DEPTH_FIRST ? n * 4 : 0);
   lo->offsets = take(n * 8);
   lo->scan_blocks = take(((n + 2047) / 2048 + 1) * 8);
   const uint64_t key_bytes = k64 ? 8 : 4;  // depth-first: (super_id << 16 | tile mask)

@@ -58,8 +58,9 @@ __global__ void __launch_bounds__(256, SGS_PRE_REG_CTAS) preprocess_kernel(sgs_p
   const int64_t n = P.n;
   const int L = kL > 0 ? kL : P.n_lobes;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  if (depth_hist && blockIdx.x == 0 && threadIdx.x == 0) ctr->n_depth = (uint32_t)n;  // the depth sort's count
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool window = cam.tile_y0 > 0 || cam.tile_y1 < cam.tiles_y;  // strip render
+  if (depth_hist && !window && blockIdx.x == 0 && threadIdx.x == 0) ctr->n_depth = (uint32_t)n;
   // iterate whole warps so the ballots and the cooperative row loop see converged warps
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
     const int64_t i = base + threadIdx.x;
@@ -289,10 +290,11 @@ __global__ void __launch_bounds__(256, SGS_PRE_REG_CTAS) preprocess_kernel(sgs_p
         rec_col[i] = make_float4(c[0], c[1], c[2], 0.0f);
       }
     }
-    if (depth_hist) {
-      // the not-emitting key 0x7fffffff: one count per warp (32 lanes on the
-      // same four shared counters would serialise -- most of a strip's
-      // primitives are not emitting)
+    if (depth_hist && !window) {
+      // full frames sort every primitive: the not-emitting key 0x7fffffff
+      // counted once per warp (32 lanes on the same four shared counters
+      // would serialise).  Strip renders sort only the emitting primitives
+      // (compacted by compact_depth_keys), so they are not counted there.
       const uint32_t m = __ballot_sync(0xffffffffu, live && !emitting);
       if (lane == 0 && m) {
         const uint32_t c = (uint32_t)__popc(m);

@@ -305,7 +305,8 @@ template <typename K, int IPT, int RBITS, int NT = kRsThreads>
 int radix_sort_pairs(K* k0, uint32_t* v0, K* k1, uint32_t* v1, const uint32_t* n_ptr, uint32_t n_cap, int bits,
                      uint32_t* hist, uint32_t* status, uint32_t* tickets, bool* result_in_alt, cudaStream_t st,
                      bool iota_values = false, RsRangeOut rout = RsRangeOut{nullptr, 0}, int begin_bit = 0,
-                     bool keep_last_keys = false, bool hist_ready = false, const K* k_first = nullptr) {
+                     bool keep_last_keys = false, bool hist_ready = false, const K* k_first = nullptr,
+                     const uint32_t* v_first = nullptr) {
   constexpr int R = 1 << RBITS;
   const int passes = (bits + RBITS - 1) / RBITS;
   const uint64_t parts = rs_parts<K, IPT, NT>(n_cap);
@@ -344,8 +345,8 @@ int radix_sort_pairs(K* k0, uint32_t* v0, K* k1, uint32_t* v1, const uint32_t* n
     return SGS_E_CUDA;
   }
   const int grid = (int)std::min<uint64_t>(parts, (uint64_t)sms * per_sm);
-  // k_first: input keys of the first pass (read only); the passes then
-  // ping-pong between k1 and k0 as if the first had read k0
+  // k_first / v_first: input keys / values of the first pass (read only);
+  // the passes then ping-pong between k1 and k0 as if the first had read k0
   K* ka = k0;
   K* kb = k1;
   uint32_t* va = v0;
@@ -353,7 +354,9 @@ int radix_sort_pairs(K* k0, uint32_t* v0, K* k1, uint32_t* v1, const uint32_t* n
   for (int p = 0; p < passes; ++p) {
     const bool last = p + 1 == passes;
     rs_onesweep<K, IPT, RBITS, NT><<<grid, NT, smem, st>>>(
-        (p == 0 && k_first) ? k_first : ka, (p == 0 && iota_values) ? nullptr : va, (last && rout.ranges && !keep_last_keys) ? nullptr : kb, vb,
+        (p == 0 && k_first) ? k_first : ka,
+        (p == 0 && iota_values) ? nullptr : ((p == 0 && v_first) ? v_first : va),
+        (last && rout.ranges && !keep_last_keys) ? nullptr : kb, vb,
         n_ptr, n_cap, begin_bit + RBITS * p, hist + R * p, status + (size_t)parts * R * p, tickets + p,
         last ? rout : RsRangeOut{nullptr, 0});
     SGS_LAUNCH_CHECK("rs_onesweep");
