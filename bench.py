@@ -714,7 +714,8 @@ def run_cfg4(ctx) -> dict:
     from paper_2509_07021_b200 import scenes
     from paper_2509_07021_b200._ffi import CapacityError
     from paper_2509_07021_b200.rasterizer import GaussianTensors, Rasterizer
-    from paper_2509_07021_b200.sharding import balanced_strips, row_costs_from_rects, row_costs_measured
+    from paper_2509_07021_b200.sharding import (balanced_strips, refine_row_costs, row_costs_from_rects,
+                                                row_costs_measured)
     args, dev = ctx.args, ctx.dev
     n = args.n if (args.n and args.workload == "stress") else 5_000_000
     scene, (cam,) = scenes.config4(n=n)
@@ -752,6 +753,33 @@ def run_cfg4(ctx) -> dict:
         if ok:
             break
         per_rank *= 2
+
+    def strip_ms(y0, y1) -> float:
+        for _ in range(2):
+            rast.forward(g, cam, check=True, tile_rows=(y0, y1), out=(img, T, None), track=False)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        rast.forward(g, cam, check=False, tile_rows=(y0, y1), out=(img, T, None), track=False)
+        e1.record()
+        torch.cuda.synchronize(dev)
+        return e0.elapsed_time(e1)
+
+    # re-plan twice from the measured strip times (sharding.refine_row_costs):
+    # every strip also projects and depth-sorts each primitive overlapping it,
+    # which a per-row model cannot see (profiles/predict_strips.py)
+    n_strips = ctx.world * per_rank
+    if n_strips > 1:
+        for _ in range(2):
+            plan = balanced_strips(cost, n_strips)
+            t = torch.zeros(n_strips, dtype=torch.float64, device=dev)
+            for j in range(ctx.rank * per_rank, (ctx.rank + 1) * per_rank):
+                t[j] = strip_ms(*plan[j])
+            if ctx.world > 1:
+                dist.all_reduce(t)
+            cost = refine_row_costs(cost, plan, t.cpu().numpy())
+        strips = balanced_strips(cost, n_strips)[ctx.rank * per_rank:(ctx.rank + 1) * per_rank]
+        for y0, y1 in strips:  # size the refined strips' workspaces
+            rast.forward(g, cam, check=True, tile_rows=(y0, y1), out=(img, T, None), track=False)
 
     def frame():
         for y0, y1 in strips:

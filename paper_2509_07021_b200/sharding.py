@@ -90,6 +90,20 @@ def row_costs_measured(ncontrib, entry_rows, raster_ms: float, bin_ms: float, ti
     return cost
 
 
+def refine_row_costs(row_cost, strips, strip_ms) -> np.ndarray:
+    """One refinement step of a strip plan from measured strip times: the
+    rows of each strip are rescaled so they sum to that strip's measured
+    time (which includes what a per-row model misses -- each strip projects
+    and depth-sorts every primitive overlapping it), keeping the within-strip
+    shape.  balanced_strips on the result re-plans."""
+    cost = np.asarray(row_cost, dtype=np.float64).copy()
+    for (y0, y1), t in zip(strips, strip_ms):
+        s = cost[y0:y1].sum()
+        if y1 > y0:
+            cost[y0:y1] = cost[y0:y1] * (t / s) if s > 0 else t / (y1 - y0)
+    return cost
+
+
 class GradBucket:
     """Flatten a dict of gradient tensors into one contiguous buffer and
     scatter it back.

@@ -133,3 +133,27 @@ def test_strip_sharding_reassembles_the_frame_cpu_oracle():
         parts[y0 * 16:y1 * 16] = r.img[y0 * 16:y1 * 16]
     assert np.array_equal(full, parts)
     assert sorted(sum((shard_views(64, r, 8) for r in range(8)), [])) == list(range(64))
+
+
+def test_strip_plan_refinement_equalises_measured_times():
+    """sharding.refine_row_costs: a strip plan re-balanced from measured strip
+    times (each strip's rows rescaled to its time) equalises a cost the
+    per-row model did not see -- here a fixed cost per strip plus a
+    quadratic per-row term."""
+    from paper_2509_07021_b200.sharding import balanced_strips, refine_row_costs
+    rows = 135
+    model = np.ones(rows)                       # what the planner believes
+    truth = 0.2 + 4.0 * (np.arange(rows) / rows - 0.5) ** 2
+
+    def measure(plan):
+        return [0.3 + truth[y0:y1].sum() for y0, y1 in plan]   # + a per-strip constant
+    plan = balanced_strips(model, 8)
+    t0 = measure(plan)
+    cost = model
+    for _ in range(3):
+        cost = refine_row_costs(cost, plan, measure(plan))
+        plan = balanced_strips(cost, 8)
+    t1 = measure(plan)
+    assert max(t1) / min(t1) < max(t0) / min(t0)
+    assert max(t1) < max(t0)
+    assert plan[0][0] == 0 and plan[-1][1] == rows and all(a[1] == b[0] for a, b in zip(plan, plan[1:]))
