@@ -139,6 +139,36 @@ typedef struct sgs_stats {
 /* Library / ABI version and last error message (thread-local). */
 int32_t sgs_version(void);
 
+/* ADMM penalized descent step (prune.py:162-201), fused: every parameter
+ * class of every primitive updated in one pass per stage, no host sync.
+ * Parameter / gradient arrays in the SceneParams layout (float32). */
+typedef struct sgs_admm_fields {
+  float* position;
+  float* quat;
+  float* log_scale;
+  float* opacity;
+  float* diffuse;
+  float* axis_raw;
+  float* sharpness;
+  float* amplitude;
+} sgs_admm_fields;
+
+typedef struct sgs_admm_rates {
+  float position, quat, log_scale, opacity, diffuse, axis_raw, sharpness, amplitude; /* group rates */
+  float eta, delta_o, delta_s;                                                       /* step, penalties */
+} sgs_admm_rates;
+
+/* stage 1 (delta != 0, after the first gradient g1): the opacity step with
+ * its penalty and clip.  stage 2 (after g2 -- or after g1 when delta == 0,
+ * with update_o = 1 and delta_s = 0): the sharpness step with its penalty
+ * (gradient g_sharpness), the other classes from g1, the clips.  proxy /
+ * dual vectors z_o, u_o (N), z_s, u_s (N,L).  ok: device uint8, 0 = leave
+ * everything unchanged (a non-finite gradient was seen); NULL = always. */
+int sgs_admm_update(int64_t n, int32_t n_lobes, int32_t stage, int32_t update_o, const sgs_admm_fields* params,
+                    const sgs_admm_fields* g1, const float* g_sharpness, const float* z_o, const float* u_o,
+                    const float* z_s, const float* u_s, const sgs_admm_rates* rates, const uint8_t* ok,
+                    void* stream);
+
 /* sizeof of the ABI structs as this library was compiled: out[0..3] =
  * sgs_camera, sgs_params, sgs_workspace, sgs_stats (bindings check theirs). */
 int sgs_abi_sizes(uint64_t out[4]);

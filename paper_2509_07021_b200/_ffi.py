@@ -67,6 +67,16 @@ class SgsSceneSoa(C.Structure):
                                            "axis_raw", "sharpness", "amplitude", "lobe_mask")]
 
 
+class SgsAdmmFields(C.Structure):
+    _fields_ = [(f, C.c_void_p) for f in ("position", "quat", "log_scale", "opacity", "diffuse", "axis_raw",
+                                           "sharpness", "amplitude")]
+
+
+class SgsAdmmRates(C.Structure):
+    _fields_ = [(f, C.c_float) for f in ("position", "quat", "log_scale", "opacity", "diffuse", "axis_raw",
+                                         "sharpness", "amplitude", "eta", "delta_o", "delta_s")]
+
+
 class SgsLossConfig(C.Structure):
     _fields_ = [("lambda_ssim", C.c_double), ("window", C.c_int32), ("sigma", C.c_double),
                 ("c1", C.c_double), ("c2", C.c_double)]
@@ -77,6 +87,9 @@ _P = C.POINTER
 SIGNATURES = {
     "sgs_version": (C.c_int32, []),
     "sgs_abi_sizes": (C.c_int, [_P(C.c_uint64)]),
+    "sgs_admm_update": (C.c_int, [C.c_int64, C.c_int32, C.c_int32, C.c_int32, _P(SgsAdmmFields), _P(SgsAdmmFields),
+                                  C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, _P(SgsAdmmRates),
+                                  C.c_void_p, C.c_void_p]),
     "sgs_last_error": (C.c_char_p, []),
     "sgs_workspace_size": (C.c_int, [_P(SgsWorkspace), _P(C.c_uint64)]),
     "sgs_preprocess": (C.c_int, [_P(SgsParams), _P(SgsCamera), _P(SgsWorkspace), C.c_void_p]),

@@ -15,7 +15,8 @@ GPU:
 
 The renders, losses and gradients run in libsgs.so (loss_and_grads_device);
 the top-k keep masks run in libsgs.so's stable radix sort (sgs_topk_mask);
-the elementwise updates are PyTorch tensor ops on the device.  Parameters
+each stage of the penalized update is one fused kernel (sgs_admm_update);
+the proximal event's bookkeeping uses PyTorch tensor ops on the device.  Parameters
 are float32 (the renderer's precision); scores are float64.  Configs are
 duck-typed: the reference's PrunerConfig / GroupRates work as well as the
 mirrors below.
@@ -260,8 +261,31 @@ def _failure(state: DevicePrunerState) -> _Failure:
     return f
 
 
-def _masked_sub_(t: torch.Tensor, delta: torch.Tensor, ok: torch.Tensor) -> None:
-    t.copy_(torch.where(ok, t - delta, t))
+_CLASSES = ("position", "quat", "log_scale", "opacity", "diffuse", "axis_raw", "sharpness", "amplitude")
+
+
+def _fields(d: dict) -> _ffi.SgsAdmmFields:
+    f = _ffi.SgsAdmmFields()
+    for k in _CLASSES:
+        t = d[k]
+        if t.dtype != torch.float32 or not t.is_contiguous():
+            raise ValueError(f"{k} must be a contiguous float32 tensor")
+        setattr(f, k, t.data_ptr())
+    return f
+
+
+def _update(state, stage: int, g1: dict, g_sharp, cfg, ok: torch.Tensor, update_o: bool, delta_s: float):
+    """One fused device pass of the step (sgs_admm_update, select.cu)."""
+    r = cfg.group_rates
+    rates = _ffi.SgsAdmmRates(*(float(getattr(r, k)) for k in _CLASSES), float(cfg.eta),
+                              float(_delta_o(cfg)), float(delta_s))
+    p = state.params
+    okb = ok.to(torch.uint8)
+    ptr = lambda t: None if t is None else t.data_ptr()  # noqa: E731
+    _ffi.call("sgs_admm_update", int(p["opacity"].numel()), int(p["sharpness"].shape[1]) if p["sharpness"].dim() > 1
+              else 0, int(stage), int(update_o), C.byref(_fields(p)), C.byref(_fields(g1)), ptr(g_sharp),
+              ptr(state.proxy_o), ptr(state.dual_o), ptr(state.proxy_s), ptr(state.dual_s), C.byref(rates),
+              okb.data_ptr(), C.c_void_p(torch.cuda.current_stream(p["opacity"].device).cuda_stream))
 
 
 def gradient_step(state: DevicePrunerState, view, cfg, rast: Rasterizer | None = None, sync: bool = True,
@@ -275,9 +299,6 @@ def gradient_step(state: DevicePrunerState, view, cfg, rast: Rasterizer | None =
     reference leaves it.  ``deterministic``: bitwise-reproducible gradient
     sums (Rasterizer.backward), so repeated runs take identical steps."""
     cam, target = view
-    p = state.params
-    r = cfg.group_rates
-    eta = float(cfg.eta)
     tgt = _t(target)
     g = state.gaussians()
     n = g.n
@@ -287,21 +308,13 @@ def gradient_step(state: DevicePrunerState, view, cfg, rast: Rasterizer | None =
     ok = fail.observe(g1, n, state.iteration)
     with torch.no_grad():
         if cfg.delta == 0.0:
-            _masked_sub_(p["opacity"], eta * r.opacity * g1["opacity"], ok)
-            _masked_sub_(p["sharpness"], eta * r.sharpness * g1["sharpness"], ok)
+            _update(state, 2, g1, g1["sharpness"], cfg, ok, update_o=True, delta_s=0.0)
         else:
-            _masked_sub_(p["opacity"], eta * r.opacity * (g1["opacity"] + _delta_o(cfg) * (
-                p["opacity"] - state.proxy_o + state.dual_o)), ok)
-            p["opacity"].clamp_(0.0, 1.0)
+            _update(state, 1, g1, None, cfg, ok, update_o=False, delta_s=0.0)
             _, g2 = loss_and_grads_device(g, cam, tgt, cfg.loss_cfg, cfg.background, rast=rast,
                                           sync=False, deterministic=deterministic)
             ok = fail.observe(g2, n, state.iteration)
-            _masked_sub_(p["sharpness"], eta * r.sharpness * (g2["sharpness"] + _delta_s(cfg) * (
-                p["sharpness"] - state.proxy_s + state.dual_s)), ok)
-        for name in ("position", "quat", "log_scale", "diffuse", "axis_raw", "amplitude"):
-            _masked_sub_(p[name], eta * getattr(r, name) * g1[name], ok)
-        p["opacity"].clamp_(0.0, 1.0)
-        p["sharpness"].clamp_(min=0.0)
+            _update(state, 2, g1, g2["sharpness"], cfg, ok, update_o=False, delta_s=_delta_s(cfg))
     state.iteration += 1
     if sync:
         fail.raise_if_failed(state)

@@ -97,6 +97,10 @@ int compact_index(const uint8_t* data, uint64_t size, uint64_t* offsets, int64_t
 int launch_compact_decode(const uint8_t* data, const uint64_t* offsets, int64_t n, int L, const sgs_scene_soa* out,
                           cudaStream_t st);
 
+int launch_admm_update(int64_t n, int L, int stage, int update_o, const sgs_admm_fields& F, const sgs_admm_fields& G,
+                       const float* gs, const float* zo, const float* uo, const float* zs, const float* us,
+                       const sgs_admm_rates& R, const uint8_t* ok, cudaStream_t st);
+
 }  // namespace sgs
 
 using namespace sgs;
@@ -104,6 +108,27 @@ using namespace sgs;
 extern "C" {
 
 int32_t sgs_version(void) { return 200; }
+
+int sgs_admm_update(int64_t n, int32_t n_lobes, int32_t stage, int32_t update_o, const sgs_admm_fields* params,
+                    const sgs_admm_fields* g1, const float* g_sharpness, const float* z_o, const float* u_o,
+                    const float* z_s, const float* u_s, const sgs_admm_rates* rates, const uint8_t* ok,
+                    void* stream) {
+  if (n < 0 || n_lobes < 0 || n_lobes > SGS_MAX_LOBES || !params || !g1 || !rates || (stage != 1 && stage != 2)) {
+    set_error("invalid ADMM update arguments");
+    return SGS_E_ARG;
+  }
+  if (n > 0 && (!params->opacity || !g1->opacity || (stage == 1 && (!z_o || !u_o)) ||
+                (stage == 2 && (!params->position || !params->quat || !params->log_scale || !params->diffuse ||
+                                !g1->position || !g1->quat || !g1->log_scale || !g1->diffuse ||
+                                (n_lobes > 0 && (!params->axis_raw || !params->sharpness || !params->amplitude ||
+                                                 !g1->axis_raw || !g1->amplitude || !g_sharpness ||
+                                                 (rates->delta_s != 0.0f && (!z_s || !u_s)))))))) {
+    set_error("null ADMM buffer");
+    return SGS_E_ARG;
+  }
+  return sgs::launch_admm_update(n, n_lobes, stage, update_o, *params, *g1, g_sharpness, z_o, u_o, z_s, u_s, *rates,
+                                 ok, as_stream(stream));
+}
 
 int sgs_abi_sizes(uint64_t out[4]) {
   if (!out) return SGS_E_ARG;
