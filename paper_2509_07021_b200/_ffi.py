@@ -160,7 +160,12 @@ def load(path: Path | None = None) -> C.CDLL:
         from ._build import build_lib
         build_lib()
     lib = C.CDLL(str(p))
+    # SGS_ALLOW_MISSING=1: bind what an older build exports (A/B timing of
+    # earlier revisions, profiles/variant.py); the product never sets it
+    allow_missing = os.environ.get("SGS_ALLOW_MISSING") == "1"
     for name, (res, args) in SIGNATURES.items():
+        if allow_missing and not hasattr(lib, name):
+            continue
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
