@@ -15,6 +15,7 @@ read) when ``check=True`` or by ``Frame.ensure_ok()``.
 
 from __future__ import annotations
 
+import collections
 import ctypes as C
 from dataclasses import dataclass
 
@@ -183,13 +184,16 @@ class Rasterizer:
     """Reusable render context (workspace cache + capacity policy)."""
 
     def __init__(self, sort_mode: int = _ffi.SORT_DEPTH_FIRST, device="cuda", headroom=1.25,
-                 initial_capacity: int | None = None):
+                 initial_capacity: int | None = None, max_graphs: int = 256):
         _ffi.load()
         self.sort_mode = sort_mode
         self.device = torch.device(device)
         self.headroom = headroom
         self.initial_capacity = initial_capacity
         self._cap_hint: dict = {}
+        # captured view graphs kept (each holds its scene, output and
+        # workspace buffers alive); the least recently replayed go first
+        self.max_graphs = int(max_graphs)
         self._shared: dict = {}
 
     # --------------------------------------------------------------- workspace
@@ -369,9 +373,17 @@ class Rasterizer:
         scene_t = tuple(getattr(g, f) for f in GRAD_FIELDS + ("lobe_mask",)) + (g.prim_mask,)
         key = (bytes(c), tuple(_ptr(t) for t in scene_t), g.n, g.n_lobes, out[0].data_ptr(),
                out[1].data_ptr(), stream.cuda_stream, tuple(float(v) for v in background))
-        graphs = self.__dict__.setdefault("_graphs", {})
+        graphs = self.__dict__.setdefault("_graphs", collections.OrderedDict())
         e = graphs.get(key)
-        if e is None:
+        if e is not None:
+            graphs.move_to_end(key)
+        else:
+            if len(graphs) >= self.max_graphs:
+                # least recently replayed first; its buffers may still be in
+                # use by a replay in flight
+                torch.cuda.synchronize(self.device)
+                while len(graphs) >= self.max_graphs:
+                    graphs.popitem(last=False)
             # capture on a private (non-default) stream paired with the caller's
             # stream; its workspace belongs to that pairing, so graphs replayed
             # concurrently on different streams never share scratch

@@ -123,3 +123,20 @@ def test_graph_replay_reports_overflow_and_recaptures_after_growth():
     assert int(ovf[0]) == 0
     want = rast.forward(g, cam, track=False, check=True).img
     assert torch.equal(out[0], want)
+
+
+def test_graph_cache_is_bounded():
+    """Captured graphs hold their buffers alive; the cache keeps the most
+    recently replayed max_graphs and replays stay correct after eviction."""
+    scene, cams = scenes.config1(n=5_000)
+    views = [cams[0].crop(64 * k, 0, 64, 64) for k in range(6)]
+    rast = Rasterizer(max_graphs=4)
+    g = GaussianTensors.from_arrays(scene)
+    outs = [(torch.empty((64, 64, 3), device="cuda"), torch.empty((64, 64), device="cuda")) for _ in views]
+    for _ in range(2):
+        for v, o in zip(views, outs):
+            rast.graph_forward(g, v, o)
+    torch.cuda.synchronize()
+    assert len(rast._graphs) == 4
+    for v, o in zip(views, outs):
+        assert torch.equal(o[0], rast.forward(g, v, track=False).img)
