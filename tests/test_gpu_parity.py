@@ -281,3 +281,30 @@ def test_grad_floor_bins_and_backward_match_oracle(mode):
         assert ok.mean() == 1.0, f"{k}: {np.count_nonzero(~ok)} of {ok.size} outside tolerance"
     zo = og["opacity"][::4]
     assert np.count_nonzero(np.abs(zo) > 1e-3 * np.abs(og["opacity"]).max()) > 10
+
+
+def test_autograd_function_matches_explicit_backward():
+    """render_torch (torch.autograd.Function over K5/K6/K7, SURVEY §8(b)'s
+    fast path): gradients of a torch-composed L1 loss equal the explicit
+    Rasterizer.backward on the same dL/dimg, mask gradients included."""
+    from paper_2509_07021_b200.rasterizer import GRAD_FIELDS, render_torch
+    scene, cams = scenes.config1(n=3000)
+    cam = cams[0].crop(560, 300, 128, 96)
+    tgt = torch.from_numpy(scenes.target_image(2, cam.height, cam.width)).cuda()
+    rast = Rasterizer()
+    leaves = {f: torch.from_numpy(np.ascontiguousarray(getattr(scene, f))).cuda().requires_grad_(True)
+              for f in GRAD_FIELDS}
+    lm = torch.from_numpy(np.ascontiguousarray(scene.lobe_mask)).cuda().requires_grad_(True)
+    pm = torch.from_numpy(np.ascontiguousarray(scene.prim_mask)).cuda().requires_grad_(True)
+    img = render_torch(rast, cam, (0.0, 0.0, 0.0), *(leaves[f] for f in GRAD_FIELDS), lm, pm)
+    loss = (img - tgt).abs().mean()
+    loss.backward()
+    g = GaussianTensors.from_arrays(scene)
+    frame = rast.forward(g, cam)
+    assert torch.equal(frame.img, img.detach())
+    dimg = torch.sign(frame.img - tgt) / img.numel()
+    want = rast.backward(g, frame, dimg, mask_grads=True)
+    for f in GRAD_FIELDS:
+        assert torch.allclose(leaves[f].grad, want[f], rtol=1e-5, atol=1e-7 * float(want[f].abs().max())), f
+    assert torch.allclose(lm.grad, want["lobe_mask"], rtol=1e-5, atol=1e-7 * float(want["lobe_mask"].abs().max()))
+    assert torch.allclose(pm.grad, want["prim_mask"], rtol=1e-5, atol=1e-7 * float(want["prim_mask"].abs().max()))
