@@ -33,7 +33,7 @@ constexpr int kRsThreads = 512;  // default CTA size: 16 warps
 
 constexpr int kRsMaxRadix = 512;
 #ifndef SGS_RS_LOOKBACK
-#define SGS_RS_LOOKBACK 32
+#define SGS_RS_LOOKBACK 8
 #endif
 constexpr int kLookback = SGS_RS_LOOKBACK;  // predecessors examined per look-back step
 
