@@ -194,7 +194,7 @@ class SoftPruneTrainer:
         ovf = None if self.grad_fn is not None else torch.zeros((len(mine), 2), dtype=torch.int64,
                                                                 device=self.device)
         chunk_done = None
-        if self._streams is not None and len(mine) > 1:
+        if self._streams is not None and len(mine) >= 1:  # one view too: K7 chunks overlap the reduction
             ls, chunk_done = self._views_pipelined(g, cams, targets, mine, ovf)
             loss_sum += ls
         else:
