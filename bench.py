@@ -652,7 +652,7 @@ def run_cfg3(ctx) -> dict:
     torch.cuda.synchronize(dev)
     e0.record(stream)
     for _ in range(args.steps):
-        tr.step(cams, targets, ctx.rank, ctx.world, apply=True)
+        tr.step(cams, targets, ctx.rank, ctx.world, apply=True, sync=False)
     e1.record(stream)
     torch.cuda.synchronize(dev)
     clk = clocks.stop() if clocks else None

@@ -179,9 +179,11 @@ class SoftPruneTrainer:
         loss = torch.stack(losses).sum() if losses else torch.zeros((), dtype=torch.float64, device=self.device)
         return loss, chunk_done
 
-    def step(self, cams, targets, rank: int = 0, world: int = 1, apply: bool = True) -> float:
+    def step(self, cams, targets, rank: int = 0, world: int = 1, apply: bool = True, sync: bool = True):
         """One step over all views (this rank renders its round-robin share);
-        returns the global mean loss."""
+        returns the global mean loss -- a float, or with ``sync=False`` a
+        0-dim float64 device tensor (the step then synchronises the host only
+        once, for the tile-capacity check)."""
         import torch.distributed as dist
         n_views = len(cams)
         mine = shard_views(n_views, rank, world)
@@ -214,7 +216,7 @@ class SoftPruneTrainer:
                 for j, v in enumerate(mine):
                     if o[j, 0]:
                         self.rast.grow_capacity(g, cams[v], int(o[j, 1]))
-                return self.step(cams, targets, rank, world, apply)
+                return self.step(cams, targets, rank, world, apply, sync)
         # bucketed all-reduce: chunk c leaves as soon as its rows are complete,
         # while the accumulation stream still adds the later chunks
         works = []
@@ -229,10 +231,10 @@ class SoftPruneTrainer:
                                                     device=self.device)])
         if multi:
             dist.all_reduce(stats, group=self.group)
-        loss = float(stats[0]) / n_views
+        loss = stats[0] / n_views
         lam = self.cfg.lambda_mask
         if lam:  # sparsity penalty lambda_m (11 mean m_p + 7 mean m_l), through the sigmoid
-            loss += lam * (11.0 * float(m_p.mean()) + 7.0 * float(m_l.mean()))
+            loss = loss + lam * (11.0 * m_p.double().mean() + 7.0 * m_l.double().mean())
         for c in range(self.chunks):
             if works:
                 works[c].wait()
@@ -246,7 +248,7 @@ class SoftPruneTrainer:
                 self._apply_chunk(c)
         if self._streams is not None:
             torch.cuda.current_stream(self.device).wait_stream(self._streams[1])
-        return loss
+        return float(loss) if sync else loss
 
     def _apply_chunk(self, c: int):
         lr = self.cfg.lr
