@@ -572,7 +572,7 @@ __global__ void __launch_bounds__(kFwdThreads, kImportance ? 1 : (kTrack ? SGS_F
 
 constexpr int kGrad = 9;
 #ifndef SGS_BWD_MIN_BLOCKS
-#define SGS_BWD_MIN_BLOCKS 7
+#define SGS_BWD_MIN_BLOCKS 8
 #endif
 constexpr int kBwdThreads = 128;
 constexpr int kBwdCPT = 1;
