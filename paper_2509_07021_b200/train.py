@@ -202,21 +202,18 @@ class SoftPruneTrainer:
         else:
             for j, v in enumerate(mine):
                 loss_sum += self._view_grads(g, cams[v], targets[v], None if ovf is None else ovf[j])
+        # Everything below is enqueued before the host reads the overflow flag:
+        # the update is masked on the device by `ok` (no view outgrew its
+        # tile capacity, on any rank), so the GPU never waits for the host;
+        # the one host synchronisation of the step comes last.  On overflow
+        # nothing was applied: capacities grow and the step is redone.
+        need = None
         if ovf is not None:
-            # some view outgrew its capacity: size it and redo the step (on every
-            # rank together, so the collectives below stay matched)
             need = (ovf[:, 0].max() if len(mine) else torch.zeros((), dtype=torch.int64,
                                                                    device=self.device)).reshape(1)
-            if multi:
+            if multi:  # every rank redoes together, so the collectives stay matched
                 dist.all_reduce(need, op=dist.ReduceOp.MAX, group=self.group)
-            if int(need.item()):
-                if self._streams is not None:
-                    torch.cuda.current_stream(self.device).wait_stream(self._streams[1])
-                o = ovf.cpu()
-                for j, v in enumerate(mine):
-                    if o[j, 0]:
-                        self.rast.grow_capacity(g, cams[v], int(o[j, 1]))
-                return self.step(cams, targets, rank, world, apply, sync)
+        ok = None if need is None else (need[0] == 0)
         # bucketed all-reduce: chunk c leaves as soon as its rows are complete,
         # while the accumulation stream still adds the later chunks
         works = []
@@ -245,21 +242,47 @@ class SoftPruneTrainer:
                 self.bucket.chunk_view("prim_logit", c).add_(lam * 11.0 / m_p.numel() * mp * (1 - mp))
                 self.bucket.chunk_view("lobe_logit", c).add_(lam * 7.0 / m_l.numel() * ml * (1 - ml))
             if apply:
-                self._apply_chunk(c)
+                self._apply_chunk(c, ok)
         if self._streams is not None:
             torch.cuda.current_stream(self.device).wait_stream(self._streams[1])
+        if need is not None and int(need.item()):
+            o = ovf.cpu()
+            for j, v in enumerate(mine):
+                if o[j, 0]:
+                    self.rast.grow_capacity(g, cams[v], int(o[j, 1]))
+            return self.step(cams, targets, rank, world, apply, sync)
         return float(loss) if sync else loss
 
-    def _apply_chunk(self, c: int):
+    def _apply_chunk(self, c: int, ok=None):
+        """Plain gradient step on primitive range c (opacity kept in [0, 1],
+        prune.py:185; sharpness >= 0), masked by the device bool ``ok``.  On
+        the GPU one fused kernel updates every parameter class
+        (sgs_admm_update, stage 2 without penalties); the mask logits follow."""
         lr = self.cfg.lr
         r = self._rows(c)
         with torch.no_grad():
-            for f, t in self.params.items():
-                t[r].sub_(lr[f] * self.bucket.chunk_view(f, c))
-            self.params["opacity"][r].clamp_(0.0, 1.0)      # prune.py:185 keeps opacity in [0, 1]
-            self.params["sharpness"][r].clamp_(min=0.0)
-            self.prim_logit[r].sub_(lr["prim_logit"] * self.bucket.chunk_view("prim_logit", c))
-            self.lobe_logit[r].sub_(lr["lobe_logit"] * self.bucket.chunk_view("lobe_logit", c))
+            if self.device.type == "cuda":
+                import ctypes as C
+                from . import _ffi
+                from .admm import _CLASSES, _fields
+                p = {f: self.params[f][r] for f in _CLASSES}
+                gr = {f: self.bucket.chunk_view(f, c) for f in _CLASSES}
+                rates = _ffi.SgsAdmmRates(*(float(lr[f]) for f in _CLASSES), 1.0, 0.0, 0.0)
+                okb = None if ok is None else ok.to(torch.uint8)
+                L = int(p["sharpness"].shape[1]) if p["sharpness"].dim() > 1 else 0
+                _ffi.call("sgs_admm_update", int(p["opacity"].numel()), L, 2, 1, C.byref(_fields(p)),
+                          C.byref(_fields(gr)), gr["sharpness"].data_ptr(), None, None, None, None, C.byref(rates),
+                          None if okb is None else okb.data_ptr(),
+                          C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream))
+            else:
+                for f, t in self.params.items():
+                    upd = t[r] - lr[f] * self.bucket.chunk_view(f, c)
+                    t[r].copy_(upd if ok is None else torch.where(ok, upd, t[r]))
+                self.params["opacity"][r].clamp_(0.0, 1.0)
+                self.params["sharpness"][r].clamp_(min=0.0)
+            for name, t in (("prim_logit", self.prim_logit), ("lobe_logit", self.lobe_logit)):
+                upd = t[r] - lr[name] * self.bucket.chunk_view(name, c)
+                t[r].copy_(upd if ok is None else torch.where(ok, upd, t[r]))
 
     def apply(self):
         for c in range(self.chunks):
