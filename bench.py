@@ -643,7 +643,7 @@ def run_cfg3(ctx) -> dict:
     tr = SoftPruneTrainer(scene, scene.extra["prim_logit"], scene.extra["lobe_logit"], device=dev,
                           group=group)
     for _ in range(max(args.warmup, 3)):
-        tr.step(cams, targets, ctx.rank, ctx.world, apply=True)  # steady state: capacities sized
+        tr.step(cams, targets, ctx.rank, ctx.world, apply=True, graph=not args.no_graphs)  # sized, captured
     torch.cuda.synchronize(dev)
     stream = torch.cuda.current_stream(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -652,7 +652,8 @@ def run_cfg3(ctx) -> dict:
     torch.cuda.synchronize(dev)
     e0.record(stream)
     for _ in range(args.steps):
-        tr.step(cams, targets, ctx.rank, ctx.world, apply=True, sync=False)
+        tr.step(cams, targets, ctx.rank, ctx.world, apply=True, sync=False,
+                graph=not args.no_graphs)
     e1.record(stream)
     torch.cuda.synchronize(dev)
     clk = clocks.stop() if clocks else None

@@ -78,6 +78,10 @@ class SoftPruneTrainer:
         self.n_streams = max(1, int(streams)) if grad_fn is None else 1
         self._streams = ([torch.cuda.Stream(self.device) for _ in range(self.n_streams)],
                          torch.cuda.Stream(self.device)) if self.n_streams > 1 else None
+        # step(graph=True) without a collective captures the reduction and the
+        # update too; False keeps them eager, as a multi-rank step does
+        self.graph_tail = True
+        self._gstep = self._graph_warm = None
 
     def masks(self):
         return torch.sigmoid(self.prim_logit), torch.sigmoid(self.lobe_logit)
@@ -131,14 +135,16 @@ class SoftPruneTrainer:
                                       mask_grads=True, out=self._bucket_out(c), accumulate=True, mask_logit=True)
         return lo[0]
 
-    def _views_pipelined(self, g: GaussianTensors, cams, targets, mine, ovf):
+    def _views_pipelined(self, g: GaussianTensors, cams, targets, mine, ovf, capture: bool = False):
         """The step's views on ``n_streams`` streams: forward, loss and raster
         backward of view j on stream j mod S, then its K7 into the bucket on
         the accumulation stream in view order, chunk by chunk (one writer:
         the bucket update is a plain read-modify-write).  Returns the summed
         loss (device) and one event per chunk, recorded on the accumulation
         stream when the last view's K7 has added that chunk's rows.  The
-        current stream waits for the views' streams only, not for K7."""
+        current stream waits for the views' streams only, not for K7
+        (``capture``: inside a CUDA-graph capture -- no chunk events, every
+        stream joined back, see _capture_views)."""
         from .loss import image_loss
         from .render import LossConfig
         main = torch.cuda.current_stream(self.device)
@@ -167,46 +173,124 @@ class SoftPruneTrainer:
                 for c in range(self.chunks):
                     self.rast.backward_params(gc[c], frame.cam, grad2d[self._rows(c)], mask_grads=True,
                                               out=outs[c], accumulate=True, mask_logit=True)
-                    if j == len(mine) - 1:
+                    if j == len(mine) - 1 and not capture:
                         chunk_done[c].record(acc)
-            lo.record_stream(main)
+            if not capture:
+                lo.record_stream(main)
             losses.append(lo[0])
-        if not mine:
+        if not mine and not capture:
             for c in range(self.chunks):
                 chunk_done[c].record(acc)
-        for st in views:
+        # join only the streams this step used: under capture, waiting on a
+        # stream that never forked from the capture stream invalidates it
+        used = views[:len(mine)] if capture else views
+        for st in used + ([acc] if capture else []):
             main.wait_stream(st)
         loss = torch.stack(losses).sum() if losses else torch.zeros((), dtype=torch.float64, device=self.device)
-        return loss, chunk_done
+        return loss, (None if capture else chunk_done)
 
-    def step(self, cams, targets, rank: int = 0, world: int = 1, apply: bool = True, sync: bool = True):
+    def _capture_views(self, cams, targets, mine, tail=None):
+        """CUDA graph of the step's device work: bucket reset, masks, every
+        view's forward, loss, K6 and K7 (captured from the same streams and
+        workspaces an eager step just used) and, when the step has no
+        collective (``tail`` = (n_views, apply)), the reduction, penalty and
+        masked update too.  A one-view step launches ~80 kernels from Python:
+        replayed, its host cost is one launch and the GPU no longer waits for
+        it."""
+        dev = self.device
+        cur = torch.cuda.current_stream(dev)
+        torch.cuda.synchronize(dev)
+        if getattr(self, "_cap_stream", None) is None:
+            self._cap_stream = torch.cuda.Stream(dev)
+        cap = self._cap_stream
+        ovf = torch.zeros((max(len(mine), 1), 2), dtype=torch.int64, device=dev)
+        graph = torch.cuda.CUDAGraph()
+        cap.wait_stream(cur)
+        loss = need = None
+        with torch.cuda.graph(graph, stream=cap):
+            self.bucket.zero()
+            g = self.gaussians()
+            ovf.zero_()
+            loss_sum, _ = self._views_pipelined(g, cams, targets, mine, ovf[:len(mine)], capture=True)
+            if tail is not None:
+                loss, need = self._tail(g, ovf[:len(mine)], loss_sum, None, mine, tail[0], False, tail[1],
+                                        capture=True)
+        cur.wait_stream(cap)
+        return {"graph": graph, "ovf": ovf[:len(mine)], "loss": loss_sum, "g": g, "full": tail is not None,
+                "step_loss": loss, "need": need,
+                "key": self._graph_key(cams, targets, mine, tail), "hint": dict(self.rast._cap_hint)}
+
+    def _graph_key(self, cams, targets, mine, tail=None):
+        from .camera import to_sgs
+        cfg = (tuple(sorted(self.cfg.lr.items())), self.cfg.lambda_mask, self.cfg.lambda_ssim)
+        return (tuple(mine), tuple(bytes(to_sgs(cams[v], grad_floor=GRAD_OPACITY_FLOOR)) for v in mine),
+                tuple(targets[v].data_ptr() for v in mine), tail, cfg)
+
+    def step(self, cams, targets, rank: int = 0, world: int = 1, apply: bool = True, sync: bool = True,
+             graph: bool = False):
         """One step over all views (this rank renders its round-robin share);
         returns the global mean loss -- a float, or with ``sync=False`` a
         0-dim float64 device tensor (the step then synchronises the host only
-        once, for the tile-capacity check)."""
+        once, for the tile-capacity check).  ``graph``: replay the views'
+        device work from a CUDA graph, captured on the first step whose
+        capacities an eager step has already sized (recaptured when views,
+        targets or capacities change); the reductions stay eager."""
         import torch.distributed as dist
         n_views = len(cams)
         mine = shard_views(n_views, rank, world)
         multi = dist.is_available() and dist.is_initialized() and dist.get_world_size(self.group) > 1
-        self.bucket.zero()
-        g = self.gaussians()
-        m_p, m_l = g.prim_mask, g.lobe_mask
-        loss_sum = torch.zeros((), dtype=torch.float64, device=self.device)
-        # tile-entry overflow is checked once per step (no host round trip per view)
-        ovf = None if self.grad_fn is not None else torch.zeros((len(mine), 2), dtype=torch.int64,
-                                                                device=self.device)
         chunk_done = None
-        if self._streams is not None and len(mine) >= 1:  # one view too: K7 chunks overlap the reduction
-            ls, chunk_done = self._views_pipelined(g, cams, targets, mine, ovf)
-            loss_sum += ls
+        use_graph = graph and self._streams is not None and len(mine) >= 1
+        tail = None if (multi or not self.graph_tail) else (n_views, apply)  # no collective: one graph
+        gs = self._gstep
+        if use_graph:
+            key = self._graph_key(cams, targets, mine, tail)
+            if gs is not None and (gs["key"] != key or gs["hint"] != self.rast._cap_hint):
+                gs = self._gstep = None
+            if gs is None and self._graph_warm == key:
+                gs = self._gstep = self._capture_views(cams, targets, mine, tail)
+        if use_graph and gs is not None:
+            gs["graph"].replay()  # bucket reset, masks, views (and the tail): one launch
+            g, ovf = gs["g"], gs["ovf"]
+            if gs["full"]:
+                loss, need = gs["step_loss"].clone(), gs["need"]
+            else:
+                loss, need = self._tail(g, ovf, gs["loss"].clone(), None, mine, n_views, multi, apply)
         else:
+            self.bucket.zero()
+            g = self.gaussians()
+            loss_sum = torch.zeros((), dtype=torch.float64, device=self.device)
+            # tile-entry overflow is checked once per step (no host round trip per view)
+            ovf = None if self.grad_fn is not None else torch.zeros((len(mine), 2), dtype=torch.int64,
+                                                                    device=self.device)
+            if self._streams is not None and len(mine) >= 1:  # one view too: K7 chunks overlap the reduction
+                ls, chunk_done = self._views_pipelined(g, cams, targets, mine, ovf)
+                loss_sum += ls
+                if use_graph:  # an eager step sized this configuration: capture from the next one
+                    self._graph_warm = self._graph_key(cams, targets, mine, tail)
+            else:
+                for j, v in enumerate(mine):
+                    loss_sum += self._view_grads(g, cams[v], targets[v], None if ovf is None else ovf[j])
+            loss, need = self._tail(g, ovf, loss_sum, chunk_done, mine, n_views, multi, apply)
+        if need is not None and int(need.item()):  # the step's one host synchronisation
+            o = ovf.cpu()
+            self._gstep = None            # its workspaces are about to be replaced
+            self._graph_warm = None
+            torch.cuda.synchronize(self.device)
             for j, v in enumerate(mine):
-                loss_sum += self._view_grads(g, cams[v], targets[v], None if ovf is None else ovf[j])
-        # Everything below is enqueued before the host reads the overflow flag:
-        # the update is masked on the device by `ok` (no view outgrew its
-        # tile capacity, on any rank), so the GPU never waits for the host;
-        # the one host synchronisation of the step comes last.  On overflow
-        # nothing was applied: capacities grow and the step is redone.
+                if o[j, 0]:
+                    self.rast.grow_capacity(g, cams[v], int(o[j, 1]))
+            return self.step(cams, targets, rank, world, apply, sync, graph)
+        return float(loss) if sync else loss
+
+    def _tail(self, g, ovf, loss_sum, chunk_done, mine, n_views, multi, apply, capture=False):
+        """Everything after the views, enqueued before the host reads the
+        overflow flag: the update is masked on the device by `ok` (no view
+        outgrew its tile capacity, on any rank), so the GPU never waits for
+        the host.  On overflow nothing was applied: capacities grow and the
+        step is redone.  Returns (loss, need) as device tensors."""
+        import torch.distributed as dist
+        m_p, m_l = g.prim_mask, g.lobe_mask
         need = None
         if ovf is not None:
             need = (ovf[:, 0].max() if len(mine) else torch.zeros((), dtype=torch.int64,
@@ -224,8 +308,8 @@ class SoftPruneTrainer:
             if multi:
                 works.append(dist.all_reduce(self.bucket.chunk_flat(c), op=dist.ReduceOp.SUM, group=self.group,
                                              async_op=True))
-        stats = torch.stack([loss_sum, torch.tensor(float(len(mine)), dtype=torch.float64,
-                                                    device=self.device)])
+        stats = torch.stack([loss_sum, torch.full((), float(len(mine)), dtype=torch.float64,
+                                                  device=self.device)])
         if multi:
             dist.all_reduce(stats, group=self.group)
         loss = stats[0] / n_views
@@ -243,15 +327,9 @@ class SoftPruneTrainer:
                 self.bucket.chunk_view("lobe_logit", c).add_(lam * 7.0 / m_l.numel() * ml * (1 - ml))
             if apply:
                 self._apply_chunk(c, ok)
-        if self._streams is not None:
+        if self._streams is not None and not capture:
             torch.cuda.current_stream(self.device).wait_stream(self._streams[1])
-        if need is not None and int(need.item()):
-            o = ovf.cpu()
-            for j, v in enumerate(mine):
-                if o[j, 0]:
-                    self.rast.grow_capacity(g, cams[v], int(o[j, 1]))
-            return self.step(cams, targets, rank, world, apply, sync)
-        return float(loss) if sync else loss
+        return loss, need
 
     def _apply_chunk(self, c: int, ok=None):
         """Plain gradient step on primitive range c (opacity kept in [0, 1],

@@ -122,3 +122,30 @@ def test_chunked_bucket_step_equals_single_bucket():
     b.step(cams, targets)
     for k in a.params:
         assert torch.allclose(a.params[k], b.params[k], rtol=1e-5, atol=1e-6), k
+
+
+@pytest.mark.parametrize("views,tail", [(1, True), (3, True), (3, False)])
+def test_graph_step_equals_eager_step(views, tail):
+    """step(graph=True): the views' device work replayed from a CUDA graph
+    (captured after an eager step sized the workspaces) gives the eager
+    step's losses and parameters, and recaptures when the capacity grows."""
+    scene, cams, targets = _setup(n=3000, views=views)
+    a = SoftPruneTrainer(scene, scene.extra["prim_logit"], scene.extra["lobe_logit"], TrainConfig())
+    b = SoftPruneTrainer(scene, scene.extra["prim_logit"], scene.extra["lobe_logit"], TrainConfig())
+    b.graph_tail = tail                              # False: reduction and update eager (multi-rank form)
+    la = [a.step(cams, targets) for _ in range(4)]
+    lb = [b.step(cams, targets, graph=True) for _ in range(4)]
+    assert b._gstep is not None                      # steps 2-4 replayed the graph
+    np.testing.assert_allclose(lb, la, rtol=1e-6)
+    for k in a.params:
+        assert torch.allclose(a.params[k], b.params[k], rtol=1e-5, atol=1e-6), k
+    # a denser scene in the same buffers overflows the captured capacity: the
+    # step redoes itself eagerly, then recaptures
+    for f in ("log_scale",):
+        b.params[f].add_(1.0)
+        a.params[f].add_(1.0)
+    la2 = a.step(cams, targets)
+    lb2 = b.step(cams, targets, graph=True)
+    assert lb2 == pytest.approx(la2, rel=1e-6)
+    for k in a.params:
+        assert torch.allclose(a.params[k], b.params[k], rtol=1e-5, atol=1e-6), k
