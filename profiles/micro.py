@@ -55,11 +55,11 @@ if what in ("all", "train"):
     scene, cams = scenes.config3()
     targets = [torch.from_numpy(scenes.target_image(0, c.height, c.width, v)).to(dev) for v, c in enumerate(cams)]
     tr = SoftPruneTrainer(scene, scene.extra["prim_logit"], scene.extra["lobe_logit"], device=dev)
-    for _ in range(3): tr.step(cams, targets)
+    for _ in range(3): tr.step(cams, targets, graph=True)
     torch.cuda.synchronize()
     a, b = ev(), ev()
     a.record()
-    for _ in range(5): tr.step(cams, targets)
+    for _ in range(5): tr.step(cams, targets, sync=False, graph=True)
     b.record()
     torch.cuda.synchronize()
     out["train_vps"] = 40 / (a.elapsed_time(b) / 1e3)
