@@ -332,6 +332,35 @@ def bwd_pair_peak(ctx) -> float:
     return ctx.n_sm * ctx.sm_mhz * 1e6 * 128.0 / 45.0
 
 
+def run_dropin(scene, cams) -> dict:
+    """The reference-signature path a drop-in user calls per view:
+    render._render_params (render.py:393-408) with the reference's float64
+    SceneParams in and a float64 (H, W, 3) image out -- the scene crosses the
+    link on every call, as the signature requires (no cache can prove a
+    caller's arrays unchanged without reading them).  Wall clock per call
+    (the call is synchronous: it returns host memory)."""
+    import time
+
+    import torch
+
+    from paper_2509_07021_b200 import render as R
+    from paper_2509_07021_b200 import scenes
+    p = R.SceneParams(**{f: getattr(scene, f).astype(np.float64) for f in scenes.FIELDS},
+                      lobe_mask=scene.lobe_mask)
+    R._render_params(p, cams[0], (0.0, 0.0, 0.0))  # workspaces sized
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for cam in cams:
+        img = R._render_params(p, cam, (0.0, 0.0, 0.0))
+    dt = time.perf_counter() - t0
+    assert img.dtype == np.float64
+    h2d = sum(int(getattr(p, f).size) * 4 for f in scenes.FIELDS) + int(p.lobe_mask.size) * 4
+    return {"value": len(cams) / dt, "unit": UNIT, "views": len(cams),
+            "h2d_bytes_per_view": h2d, "d2h_bytes_per_view": int(img.size) * 4,
+            "api": "render._render_params (float64 SceneParams in, float64 image out, one call per view, "
+                   "scene uploaded every call), wall clock"}
+
+
 def run_headline(ctx, timed_clocks: bool = True) -> dict:
     """configs[2]: the 64-camera batch, sharded over the ranks."""
     import torch
@@ -466,6 +495,8 @@ def run_headline(ctx, timed_clocks: bool = True) -> dict:
     gc.collect()
     torch.cuda.synchronize(dev)
 
+    dropin = run_dropin(scene, my_cams[:min(V, 16)]) if V else None
+
     # the e2e path's own roofline: pinned host <-> device copy bandwidth,
     # measured here (both directions at once, as the batch API overlaps them)
     link = measure_link(dev)
@@ -505,7 +536,7 @@ def run_headline(ctx, timed_clocks: bool = True) -> dict:
     }
     traffic = profiled_traffic("raster_fwd_kernel")
     return {
-        "value": value, "t_ms": t_ms, "e2e": e2e, "frames": frames, "mine": V,
+        "value": value, "t_ms": t_ms, "e2e": e2e, "frames": frames, "mine": V, "dropin": dropin,
         "mpix_per_s": value * 1920 * 1080 / 1e6,
         "vram": {"peak_dynamic_bytes_per_frame": int(frame_vram["peak_dynamic_bytes"]),
                  "workspace_bytes_per_frame": int(frame_vram["workspace_bytes"]),
@@ -912,6 +943,7 @@ def run_ours(args):
                     "api": "batch.BatchRenderer.render_views (pinned host scene in, host images out, "
                            "overflow-checked)",
                     "roofline": e2e_roofline(h, h2d, d2h, args.steps)},
+            "e2e_dropin": h["dropin"],
             "stages": h["stages"], "super_tile_entries_per_view": h["super_tile_entries_per_view"],
             "gpu_launches": h["gpu_launches"], "clocks": h["clocks"],
         }

@@ -17,6 +17,7 @@ from __future__ import annotations
 
 import collections
 import ctypes as C
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -41,6 +42,69 @@ def _dev_f32(a, device) -> torch.Tensor:
     if isinstance(a, torch.Tensor):
         return a.detach().to(device=device, dtype=torch.float32).contiguous()
     return torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.float32))).to(device)
+
+
+class _PinnedArena:
+    """One growing page-locked float32 host buffer.  Host arrays (the drop-in
+    API's float64 SceneParams, bool lobe masks, ...) are narrowed into it by
+    torch's multithreaded copy and cross the link in one copy at the full
+    pinned bandwidth; numpy's single-threaded astype plus a pageable copy
+    took 1.6x as long for configs[2] (1M Gaussians)."""
+
+    def __init__(self):
+        self.buf = None
+        self.lock = threading.Lock()
+
+    def upload(self, arrays, device) -> list:
+        arrays = [np.ascontiguousarray(np.asarray(a)) for a in arrays]
+        sizes = [a.size for a in arrays]
+        # each array starts on a 256-byte boundary (the kernels' float4 loads
+        # need 16, coalescing likes 256)
+        offs = np.concatenate([[0], np.cumsum([(n + 63) // 64 * 64 for n in sizes])]).astype(np.int64)
+        total = max(64, int(offs[-1]))
+        with self.lock:
+            if self.buf is None or self.buf.numel() < total:
+                self.buf = None
+                self.buf = torch.empty(total + total // 4, dtype=torch.float32, pin_memory=True)
+            for a, n, o in zip(arrays, sizes, offs):
+                if n:
+                    self.buf[o:o + n].view(a.shape).copy_(torch.from_numpy(a))
+            dev = self.buf[:total].to(device)  # synchronous: the arena is free again on return
+        return [dev[o:o + n].view(a.shape) for a, n, o in zip(arrays, sizes, offs)]
+
+    def download64(self, t: torch.Tensor) -> np.ndarray:
+        """float64 host copy of a device float32 tensor: one pinned D2H copy,
+        then a multithreaded widening into the new array."""
+        n = t.numel()
+        with self.lock:
+            if self.buf is None or self.buf.numel() < n:
+                self.buf = None
+                self.buf = torch.empty(n + n // 4, dtype=torch.float32, pin_memory=True)
+            h = self.buf[:n].view(t.shape)
+            h.copy_(t)
+            out = np.empty(tuple(t.shape), dtype=np.float64)
+            torch.from_numpy(out).copy_(h)
+        return out
+
+
+_UPLOAD = _PinnedArena()
+_DOWNLOAD = _PinnedArena()
+
+
+def host_to_device_f32(arrays, device) -> list:
+    """float32 device copies of host arrays (see _PinnedArena)."""
+    device = torch.device(device)
+    if device.type != "cuda" or not torch.cuda.is_available():
+        return [_dev_f32(a, device) for a in arrays]
+    return _UPLOAD.upload(arrays, device)
+
+
+def device_to_host_f64(t: torch.Tensor) -> np.ndarray:
+    """float64 numpy copy of a tensor (the drop-in API returns float64)."""
+    t = t.detach()
+    if t.is_cuda and t.dtype == torch.float32 and t.is_contiguous() and t.numel() >= (1 << 16):
+        return _DOWNLOAD.download64(t)
+    return t.to(torch.float64).cpu().numpy()
 
 
 class GaussianTensors:
@@ -96,11 +160,16 @@ class GaussianTensors:
         reference's f64 SceneParams, this package's SceneArrays, ...).  A bool
         lobe_mask becomes 0/1 floats; ``prim_mask`` falls back to
         ``p.prim_mask`` when present."""
-        kw = {f: _dev_f32(getattr(p, f), device) for f in GRAD_FIELDS}
         lm = getattr(p, "lobe_mask", None)
-        kw["lobe_mask"] = None if lm is None else _dev_f32(lm, device)
         pm = prim_mask if prim_mask is not None else getattr(p, "prim_mask", None)
-        kw["prim_mask"] = None if pm is None else _dev_f32(pm, device)
+        src = {f: getattr(p, f) for f in GRAD_FIELDS}
+        src["lobe_mask"], src["prim_mask"] = lm, pm
+        names = [f for f, a in src.items() if a is not None]
+        if any(isinstance(src[f], torch.Tensor) for f in names):
+            kw = {f: (None if src[f] is None else _dev_f32(src[f], device)) for f in src}
+        else:  # host arrays: one staged copy (host_to_device_f32)
+            kw = dict.fromkeys(src)
+            kw.update(zip(names, host_to_device_f32([src[f] for f in names], device)))
         return cls(**kw)
 
     def c_params(self) -> _ffi.SgsParams:

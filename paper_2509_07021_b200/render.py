@@ -32,7 +32,7 @@ import torch
 from . import _ffi
 from .camera import Camera, to_sgs
 from .loss import image_loss
-from .rasterizer import GRAD_FIELDS, GaussianTensors, Rasterizer
+from .rasterizer import GRAD_FIELDS, GaussianTensors, Rasterizer, device_to_host_f64
 
 ALPHA_MAX = 0.99
 T_CUTOFF = 1e-4
@@ -206,7 +206,7 @@ def _upload(p) -> GaussianTensors:
 
 
 def _to_np64(t: torch.Tensor) -> np.ndarray:
-    return t.detach().to(torch.float64).cpu().numpy()
+    return device_to_host_f64(t)
 
 
 # ------------------------------------------------------------------ forward

@@ -45,6 +45,7 @@ def test_our_arm_line():
     assert 0 < d["roofline"]["frac"] < 2
     assert {"value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"} <= d["e2e"].keys()
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    assert d["e2e_dropin"]["value"] > 0 and d["e2e_dropin"]["views"] >= 1  # render._render_params path
     assert d["gpu_launches"] > 0
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= d["clocks"].keys()
     assert "workload" in d["config"]

@@ -140,3 +140,22 @@ def test_graph_cache_is_bounded():
     assert len(rast._graphs) == 4
     for v, o in zip(views, outs):
         assert torch.equal(o[0], rast.forward(g, v, track=False).img)
+
+
+def test_staged_upload_matches_numpy_conversion_and_alignment():
+    """GaussianTensors.from_arrays narrows host float64 arrays through one
+    pinned arena (rasterizer._PinnedArena): the same float32 values as
+    numpy's astype, every field 256-byte aligned (the kernels' float4 loads),
+    and the float64 download is exact."""
+    from paper_2509_07021_b200 import render as R
+    from paper_2509_07021_b200.rasterizer import GRAD_FIELDS, device_to_host_f64
+    scene, _ = scenes.config0(n=1001)   # odd sizes: offsets must be padded
+    p = R.SceneParams(**{f: getattr(scene, f).astype(np.float64) + 1e-9 for f in scenes.FIELDS},
+                      lobe_mask=scene.lobe_mask)
+    g = GaussianTensors.from_arrays(p)
+    for f in GRAD_FIELDS + ("lobe_mask",):
+        t = getattr(g, f)
+        assert t.data_ptr() % 256 == 0, f
+        assert np.array_equal(t.cpu().numpy(), np.asarray(getattr(p, f), dtype=np.float32)), f
+    x = torch.rand((300, 400, 3), device="cuda")
+    assert np.array_equal(device_to_host_f64(x), x.cpu().numpy().astype(np.float64))
