@@ -118,16 +118,35 @@ __device__ __forceinline__ int length_class(uint32_t len) {
   return c < kOrderClasses ? c : kOrderClasses - 1;
 }
 
-__global__ void __launch_bounds__(1024) cell_order_kernel(const uint2* __restrict__ ranges, int base, int n,
-                                                          uint32_t* __restrict__ order) {
+// Length of item i: the cell's list length (forward), or with `cand_end` the
+// candidates tile i of the window kept in the forward (backward raster: its
+// work is the kept part of the list, walked back to front).
+struct OrderSrc {
+  const uint2* ranges;
+  int base;
+  const uint32_t* cand_end;  // null: cell list lengths
+  int tiles_x, tile0, super_x;
+  bool filt;
+};
+
+__device__ __forceinline__ uint32_t order_len(const OrderSrc& o, int i) {
+  if (!o.cand_end) {
+    const uint2 r = o.ranges[o.base + i];
+    return r.y > r.x ? r.y - r.x : 0u;
+  }
+  const int tile = i + o.tile0, tx = tile % o.tiles_x, ty = tile / o.tiles_x;
+  const uint32_t s = o.ranges[list_cell(o.filt, tx, ty, tile, o.super_x)].x, e = o.cand_end[tile];
+  return e > s ? e - s : 0u;
+}
+
+__global__ void __launch_bounds__(1024) cell_order_kernel(OrderSrc src, int n, uint32_t* __restrict__ order) {
   __shared__ uint32_t hist[kOrderClasses];
   __shared__ uint32_t cursor[kOrderClasses];
   const int t = threadIdx.x;
   if (t < kOrderClasses) hist[t] = 0;
   __syncthreads();
   for (int i = t; i < n; i += blockDim.x) {
-    const uint2 r = ranges[base + i];
-    atomicAdd(&hist[length_class(r.y > r.x ? r.y - r.x : 0u)], 1u);
+    atomicAdd(&hist[length_class(order_len(src, i))], 1u);
   }
   __syncthreads();
   if (t < 32) {  // exclusive scan over classes, longest class first
@@ -144,8 +163,7 @@ __global__ void __launch_bounds__(1024) cell_order_kernel(const uint2* __restric
   }
   __syncthreads();
   for (int i = t; i < n; i += blockDim.x) {
-    const uint2 r = ranges[base + i];
-    order[atomicAdd(&cursor[length_class(r.y > r.x ? r.y - r.x : 0u)], 1u)] = (uint32_t)i;
+    order[atomicAdd(&cursor[length_class(order_len(src, i))], 1u)] = (uint32_t)i;
   }
 }
 
@@ -652,7 +670,9 @@ __global__ void __launch_bounds__(kBwdThreads, SGS_BWD_MIN_BLOCKS) raster_bwd_ke
   __shared__ float s_part[kBwdThreads / 32][kBwdChunk][kGrad];
   __shared__ uint32_t s_max_nc;
 
-  const int tile = blockIdx.x + cam.tile_y0 * cam.tiles_x;
+  // tiles in kept-work order, heaviest first (launch_raster_bwd): the long
+  // tiles start in the first wave instead of forming the tail
+  const int tile = (int)la.order[blockIdx.x] + cam.tile_y0 * cam.tiles_x;
   const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
   const int t = threadIdx.x, lane = t & 31;
   const int wq = t >> 5, lq = t & 31;  // 8x8 quadrants per warp, as in the forward
@@ -904,7 +924,8 @@ int launch_raster_fwd(const SgsCam& cam, float3 bg, const sgs_workspace* ws, con
     grid = n_cells;
   }
   {
-    cell_order_kernel<<<1, 1024, 0, st>>>(a.ranges, a.cell_base, n_cells, at<uint32_t>(ws, lo.cell_order));
+    const OrderSrc src{a.ranges, a.cell_base, nullptr, cam.tiles_x, 0, lo.super_x, filt};
+    cell_order_kernel<<<1, 1024, 0, st>>>(src, n_cells, at<uint32_t>(ws, lo.cell_order));
     SGS_LAUNCH_CHECK("cell_order_kernel");
   }
 #define SGS_FWD(I, C, F, K) \
@@ -951,6 +972,11 @@ int launch_raster_bwd(const SgsCam& cam, float3 bg, const sgs_workspace* ws, con
     SGS_CUDA(cudaFuncSetAttribute(raster_bwd_kernel<true, 0>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     SGS_CUDA(cudaFuncSetAttribute(raster_bwd_kernel<false, 0>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     carve = true;
+  }
+  {
+    const OrderSrc src{a.ranges, 0, a.cand_end, cam.tiles_x, cam.tile_y0 * cam.tiles_x, lo.super_x, filt};
+    cell_order_kernel<<<1, 1024, 0, st>>>(src, grid, at<uint32_t>(ws, lo.cell_order));
+    SGS_LAUNCH_CHECK("cell_order_kernel (backward)");
   }
   if (!det_scratch) {
     SGS_CUDA(cudaMemsetAsync(grad2d, 0, nv * sizeof(float), st));
