@@ -285,10 +285,19 @@ class Ctx:
         import torch.distributed as dist
         self.args = args
         self.rank, self.world, self.local = dist_env()
+        # SGS_BENCH_SHARED_GPU=1: functional check of the multi-rank control
+        # flow on a one-GPU box (every rank on cuda:0, gloo collectives); its
+        # numbers are not measurements and the line says so
+        self.shared = os.environ.get("SGS_BENCH_SHARED_GPU") == "1" and self.world > 1
+        if self.shared:
+            self.local = 0
         torch.cuda.set_device(self.local)
         self.dev = torch.device("cuda", self.local)
         if self.world > 1 and not dist.is_initialized():
-            dist.init_process_group("nccl", device_id=self.dev)
+            if self.shared:
+                dist.init_process_group("gloo")
+            else:
+                dist.init_process_group("nccl", device_id=self.dev)
         self.peaks, self.peak_src = measured_peaks()
         self.n_sm = torch.cuda.get_device_properties(self.dev).multi_processor_count
         self.sm_mhz = float(self.peaks.get("sm_max_mhz", 1965.0))
@@ -947,6 +956,8 @@ def run_ours(args):
             "stages": h["stages"], "super_tile_entries_per_view": h["super_tile_entries_per_view"],
             "gpu_launches": h["gpu_launches"], "clocks": h["clocks"],
         }
+        if ctx.shared:
+            line["functional_check_only"] = "SGS_BENCH_SHARED_GPU: all ranks shared one GPU over gloo; not a measurement"
         if workloads:
             line["workloads"] = workloads
             line["gpu_launches"] += sum(int(w.get("gpu_launches", 0)) for w in workloads.values())
