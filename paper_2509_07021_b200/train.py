@@ -50,7 +50,7 @@ class SoftPruneTrainer:
     data-parallel training step over this rank's share of the views."""
 
     def __init__(self, arrays, prim_logit, lobe_logit, cfg: TrainConfig = TrainConfig(),
-                 device="cuda", group=None, grad_fn=None, streams: int = 4, comm_chunks: int = 4,
+                 device="cuda", group=None, grad_fn=None, streams: int = 8, comm_chunks: int = 4,
                  chunk_single_rank: bool = False):
         """``streams``: views of a step in flight at once on this many CUDA
         streams (each with its own workspace); their parameter backwards
