@@ -318,7 +318,7 @@ __device__ __forceinline__ uint32_t tile_local_bit(int tx, int ty) {
 }
 
 // Forward raster: 128 threads per 16x16 tile, each thread owns two
-// vertically adjacent pixels (a warp covers a 16x4 block, which keeps its
+// vertically adjacent pixels (a warp covers an 8x8 quadrant, which keeps its
 // lanes' supports and termination coherent).  Per staged record the two
 // pixels share the record loads, dx and A dx; the per-pixel blend is
 // predicated, and a warp skips a record outright when none of its 64 pixels
@@ -636,7 +636,7 @@ __device__ __forceinline__ int reduce9_index(int lane) {
 }
 
 // Backward raster: 128 threads per tile, two vertically adjacent pixels per
-// thread (a warp covers 16x4 pixels, as in the forward), walking the tile's
+// thread (a warp covers an 8x8 quadrant, as in the forward), walking the tile's
 // list back to front from the last entry any pixel kept.  Per record each
 // thread sums its two pixels' nine partials, the warp reduces them with
 // warp_reduce9, and nine lanes store the totals into the warp's slot of the
