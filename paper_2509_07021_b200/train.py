@@ -223,8 +223,12 @@ class SoftPruneTrainer:
     def _graph_key(self, cams, targets, mine, tail=None):
         from .camera import to_sgs
         cfg = (tuple(sorted(self.cfg.lr.items())), self.cfg.lambda_mask, self.cfg.lambda_ssim)
+        # the graph reads the parameters and targets through these pointers:
+        # replaced (not updated in place) tensors need a new capture
+        ptrs = tuple(t.data_ptr() for t in self.params.values()) + (self.prim_logit.data_ptr(),
+                                                                     self.lobe_logit.data_ptr())
         return (tuple(mine), tuple(bytes(to_sgs(cams[v], grad_floor=GRAD_OPACITY_FLOOR)) for v in mine),
-                tuple(targets[v].data_ptr() for v in mine), tail, cfg)
+                tuple(targets[v].data_ptr() for v in mine), tail, cfg, ptrs)
 
     def step(self, cams, targets, rank: int = 0, world: int = 1, apply: bool = True, sync: bool = True,
              graph: bool = False):
