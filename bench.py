@@ -708,6 +708,9 @@ def run_cfg3(ctx) -> dict:
     torch.cuda.synchronize(dev)
     for v, cam in enumerate(cams):
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+        # the GPU sleeps while the host enqueues the view's four phases, so
+        # host-side call overhead never shows up inside an event interval
+        torch.cuda._sleep(20_000_000)
         ev[0].record(stream)
         fr = rast.forward(g, cam, check=False)
         ev[1].record(stream)
@@ -916,8 +919,20 @@ def e2e_roofline(h, h2d, d2h, steps) -> dict:
             "frac": bound * 1e3 / achieved_ms}
 
 
+def torch_sync(ctx):
+    import torch
+    torch.cuda.synchronize(ctx.dev)
+
+
 def run_ours(args):
     """Our arm: the configs[2] headline (+ the sub-workloads with --workload all)."""
+    import gc
+    # No automatic garbage collection inside the timed regions: a full
+    # collection pauses the host for milliseconds, longer than the GPU's
+    # queued work, and showed up as gaps of up to 8 ms inside the per-phase
+    # event intervals.  Collections run explicitly between workloads.
+    gc.collect()
+    gc.disable()
     ctx = Ctx(args)
     if args.workload in ("train", "stress", "cfg1"):
         fn = {"train": run_cfg3, "stress": run_cfg4, "cfg1": lambda c: run_cfg1(c)}[args.workload]
@@ -932,10 +947,11 @@ def run_ours(args):
     h = run_headline(ctx)
     workloads = {}
     if args.workload == "all":
-        workloads["cfg1"] = run_cfg1(ctx)
-        workloads["cfg3"] = run_cfg3(ctx)
-        workloads["cfg4"] = run_cfg4(ctx)
-        workloads["cfg2_key64"] = run_key64(ctx, h["scene"], h["cams"])
+        for name, fn in (("cfg1", run_cfg1), ("cfg3", run_cfg3), ("cfg4", run_cfg4),
+                         ("cfg2_key64", lambda c: run_key64(c, h["scene"], h["cams"]))):
+            gc.collect()
+            torch_sync(ctx)
+            workloads[name] = fn(ctx)
     if ctx.rank == 0:
         h2d, d2h = h["e2e_bytes"]
         line = {

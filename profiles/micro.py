@@ -70,6 +70,7 @@ if what in ("all", "train"):
         _, dimg, _ = image_loss(fr.img, targets[v], LossConfig())
         for rep in range(3):  # the first launch of a view is not timed
             e0, e1 = ev(), ev()
+            torch.cuda._sleep(2_000_000)  # the host enqueues while the GPU is busy
             e0.record(); rast.backward_raster(g, fr, dimg); e1.record()
             torch.cuda.synchronize()
             if rep:
