@@ -9,6 +9,7 @@ B200 exactly as that rank would run it, the slowest rank sets the step time.
 
   python profiles/predict_scaling.py > profiles/r02_predicted_scaling.json
 """
+import gc
 import json
 import sys
 from pathlib import Path
@@ -23,6 +24,8 @@ from paper_2509_07021_b200.train import SoftPruneTrainer  # noqa: E402
 
 NVLINK_BUSBW_GBS = 360.0  # conservative NCCL all-reduce bus bandwidth for a 78 MB bucket on NVLink 5 (assumed)
 ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+gc.collect()
+gc.disable()  # no collection pauses inside the event-timed shares
 out = {"assumptions": {"allreduce_busbw_GBs": NVLINK_BUSBW_GBS}}
 
 # ---- configs[2]
