@@ -159,8 +159,8 @@ int sgs_preprocess(const sgs_params* params, const sgs_camera* cam, const sgs_wo
   if (rc) return rc;
   cudaStream_t st = as_stream(stream);
   SGS_CUDA(cudaMemsetAsync(at<Counters>(ws, lo.counters), 0, sizeof(Counters), st));
-  if (lo.sort_mode == SGS_SORT_DEPTH_FIRST)  // digit histograms the preprocess / emission accumulate
-    SGS_CUDA(cudaMemsetAsync(at<uint32_t>(ws, lo.hist), 0, (size_t)(kSuperHistOff + 512) * 4, st));
+  // the depth-digit histograms the preprocess accumulates (both sort modes)
+  SGS_CUDA(cudaMemsetAsync(at<uint32_t>(ws, lo.hist) + kDepthHistOff, 0, (size_t)4 * 256 * 4, st));
   if (lo.n == 0) return SGS_OK;
   return launch_preprocess(*params, c, ws, lo, st);
 }

@@ -435,8 +435,7 @@ __global__ void __launch_bounds__(256) emit_entries(const uint32_t* __restrict__
 
 // Final location of the sorted values (which ping-pong buffer).
 bool final_in_alt(const Layout& lo) {
-  int passes = lo.sort_mode == SGS_SORT_KEY64 ? (32 + tile_sort_bits(lo.n_tiles) + 7) / 8
-                                              : super_sort_passes(lo.n_super);
+  int passes = lo.sort_mode == SGS_SORT_KEY64 ? tile_sort_passes(lo.n_tiles) : super_sort_passes(lo.n_super);
   return (passes & 1) != 0;
 }
 
@@ -454,6 +453,9 @@ static int bin_entries(const SgsCam& cam, const sgs_workspace* ws, const Layout&
   uint32_t* v1 = at<uint32_t>(ws, lo.ent_val_alt);
   uint2* ranges = at<uint2>(ws, lo.ranges);
   const int n_cells = kSuper ? lo.n_super : lo.n_tiles;
+  // the emission accumulates the cell digit counts (fused_hist): from zero on
+  // every sgs_bin, which may be repeated after one sgs_preprocess
+  if (fused_hist) SGS_CUDA(cudaMemsetAsync(at<uint32_t>(ws, lo.hist) + kSuperHistOff, 0, 512 * 4, st));
   emit_entries<KT, kSuper><<<persistent_grid(n, 256, SGS_EMIT_CTAS), 256, 0, st>>>(
       perm, n, n_ptr, at<uint32_t>(ws, kSuper ? lo.super_touched : lo.tiles_touched), at<uint2>(ws, lo.rect),
       at<float4>(ws, lo.rec_geo), at<float4>(ws, lo.rec_con), at<float4>(ws, lo.rec_span),
@@ -464,19 +466,17 @@ static int bin_entries(const SgsCam& cam, const sgs_workspace* ws, const Layout&
       ranges, n_cells);
   SGS_LAUNCH_CHECK("emit_entries");
   bool alt = false;
-  uint32_t* hist = at<uint32_t>(ws, lo.hist) + (fused_hist ? kSuperHistOff : 0);
+  // the cell sort's digit counts live apart from the preprocess's depth
+  // histograms (kDepthHistOff), which a repeated sgs_bin reads again
+  uint32_t* hist = at<uint32_t>(ws, lo.hist) + kSuperHistOff;
   int rc = radix_sort_pairs<KT, IPT, RBITS>(k0, v0, k1, v1, &ctr->n_sort, cap, key_bits, hist,
                                      at<uint32_t>(ws, lo.status), &ctr->part_counter[8], &alt, st, false,
-                                     RsRangeOut{ranges, tile_shift}, kSuper ? 16 : 0, true, fused_hist);
+                                     RsRangeOut{ranges, tile_shift}, tile_shift, true, fused_hist);
   if (rc) return rc;
-  if (!kSuper) {
-    // 64-bit keys: entries were emitted in primitive-index order, so equal
-    // (tile, depth) keys need the float64 residual order too
-    depth_tie_fixup<KT><<<persistent_grid(cap, 256, 8), 256, 0, st>>>(alt ? k1 : k0, alt ? v1 : v0,
-                                                                    at<float>(ws, lo.depth_res), &ctr->n_sort, cap,
-                                                                    ~KT(0));
-    SGS_LAUNCH_CHECK("depth_tie_fixup");
-  }
+  // both key forms were emitted in the float64 depth order (ties fixed up
+  // before the emission), so the stable sort over the cell digits alone
+  // gives (cell, depth, residual, index) order: for 64-bit keys the LSD
+  // passes over the already-ordered low 32 depth bits are skipped
   // cells without entries keep (0xffffffff, 0): every consumer reads a range
   // as [start, max(start, end)), i.e. empty
   return rc;
@@ -488,40 +488,39 @@ int launch_bin(const SgsCam& cam, const sgs_workspace* ws, const Layout& lo, cud
   const uint32_t cap = (uint32_t)lo.cap;
   unsigned long long* offsets = at<unsigned long long>(ws, lo.offsets);
   unsigned long long* status64 = at<unsigned long long>(ws, lo.scan_blocks);  // scan look-back status
+  uint32_t* ka = at<uint32_t>(ws, lo.dkey_alt);
+  uint32_t* kb = at<uint32_t>(ws, lo.dkey_tmp);
+  uint32_t* ia = at<uint32_t>(ws, lo.didx);
+  uint32_t* ib = at<uint32_t>(ws, lo.didx_alt);
+  bool alt = false;
+  // Both modes first sort the primitives by depth: 31-bit keys
+  // (0x7fffffff = not emitting), 4 passes, the four digit histograms
+  // accumulated by the preprocess.  Full frames sort all N primitives
+  // (n_depth = N), the first pass reading the preprocess's keys in place;
+  // strip renders sort only the emitting ones, compacted first.  Either input
+  // is left intact, so sgs_bin may be repeated after one sgs_preprocess.
+  const bool window = cam.tile_y0 > 0 || cam.tile_y1 < cam.tiles_y;
+  const uint32_t* k_first = at<uint32_t>(ws, lo.depth_key);
+  const uint32_t* v_first = nullptr;
+  if (window) {
+    SGS_CUDA(cudaMemsetAsync(&ctr->n_depth, 0, sizeof(uint32_t), st));
+    compact_depth_keys<<<persistent_grid(n, 256, 8), 256, 0, st>>>(at<uint32_t>(ws, lo.depth_key), n,
+                                                                 at<uint32_t>(ws, lo.dkey_c),
+                                                                 at<uint32_t>(ws, lo.didx_c), &ctr->n_depth);
+    SGS_LAUNCH_CHECK("compact_depth_keys");
+    k_first = at<uint32_t>(ws, lo.dkey_c);
+    v_first = at<uint32_t>(ws, lo.didx_c);
+  }
+  int rc = radix_sort_pairs<uint32_t, kDepthSortIPT, 8, kDepthSortThreads>(
+      ka, ia, kb, ib, &ctr->n_depth, n, 31, at<uint32_t>(ws, lo.hist) + kDepthHistOff,
+      at<uint32_t>(ws, lo.status), &ctr->part_counter[0], &alt, st, !window, RsRangeOut{nullptr, 0}, 0, false,
+      true, k_first, v_first);
+  if (rc) return rc;
+  uint32_t* perm = alt ? ib : ia;
+  depth_tie_fixup<uint32_t><<<persistent_grid(n, 256, 8), 256, 0, st>>>(
+      alt ? kb : ka, perm, at<float>(ws, lo.depth_res), &ctr->n_depth, n, 0x7fffffffu);
+  SGS_LAUNCH_CHECK("depth_tie_fixup");
   if (lo.sort_mode == SGS_SORT_DEPTH_FIRST) {
-    uint32_t* ka = at<uint32_t>(ws, lo.dkey_alt);
-    uint32_t* kb = at<uint32_t>(ws, lo.dkey_tmp);
-    uint32_t* ia = at<uint32_t>(ws, lo.didx);
-    uint32_t* ib = at<uint32_t>(ws, lo.didx_alt);
-    bool alt = false;
-    // depth keys are 31-bit (0x7fffffff = not emitting): 4 passes over N; the
-    // depth keys are 31-bit (0x7fffffff = not emitting): 4 passes; the
-    // preprocess accumulated the four depth-digit histograms.  Full frames
-    // sort all N primitives (n_depth = N), the first pass reading the
-    // preprocess's keys in place; strip renders sort only the emitting ones,
-    // compacted first.  Either input is left intact, so sgs_bin may be
-    // repeated after one sgs_preprocess.
-    const bool window = cam.tile_y0 > 0 || cam.tile_y1 < cam.tiles_y;
-    const uint32_t* k_first = at<uint32_t>(ws, lo.depth_key);
-    const uint32_t* v_first = nullptr;
-    if (window) {
-      SGS_CUDA(cudaMemsetAsync(&ctr->n_depth, 0, sizeof(uint32_t), st));
-      compact_depth_keys<<<persistent_grid(n, 256, 8), 256, 0, st>>>(at<uint32_t>(ws, lo.depth_key), n,
-                                                                   at<uint32_t>(ws, lo.dkey_c),
-                                                                   at<uint32_t>(ws, lo.didx_c), &ctr->n_depth);
-      SGS_LAUNCH_CHECK("compact_depth_keys");
-      k_first = at<uint32_t>(ws, lo.dkey_c);
-      v_first = at<uint32_t>(ws, lo.didx_c);
-    }
-    int rc = radix_sort_pairs<uint32_t, kDepthSortIPT, 8, kDepthSortThreads>(
-        ka, ia, kb, ib, &ctr->n_depth, n, 31, at<uint32_t>(ws, lo.hist) + kDepthHistOff,
-        at<uint32_t>(ws, lo.status), &ctr->part_counter[0], &alt, st, !window, RsRangeOut{nullptr, 0}, 0, false,
-        true, k_first, v_first);
-    if (rc) return rc;
-    uint32_t* perm = alt ? ib : ia;
-    depth_tie_fixup<uint32_t><<<persistent_grid(n, 256, 8), 256, 0, st>>>(
-        alt ? kb : ka, perm, at<float>(ws, lo.depth_res), &ctr->n_depth, n, 0x7fffffffu);
-    SGS_LAUNCH_CHECK("depth_tie_fixup");
     rc = launch_scan(at<uint32_t>(ws, lo.super_touched), perm, n, &ctr->n_depth, cap, status64, offsets, ctr, st);
     if (rc) return rc;
     // keys (super_id << 16 | 16-bit tile mask), sorted on the super id bits only
@@ -530,10 +529,12 @@ int launch_bin(const SgsCam& cam, const sgs_workspace* ws, const Layout& lo, cud
       return bin_entries<uint32_t, kTileSortIPT, 9, true>(cam, ws, lo, perm, &ctr->n_depth, sbits, 16, st);
     return bin_entries<uint32_t, kTileSortIPT, 8, true>(cam, ws, lo, perm, &ctr->n_depth, sbits, 16, st);
   }
-  int rc = launch_scan(at<uint32_t>(ws, lo.tiles_touched), nullptr, n, nullptr, cap, status64, offsets, ctr, st);
+  // SGS_SORT_KEY64: (tile << 32 | depth bits) keys emitted in depth order,
+  // sorted on the tile bits
+  rc = launch_scan(at<uint32_t>(ws, lo.tiles_touched), perm, n, &ctr->n_depth, cap, status64, offsets, ctr, st);
   if (rc) return rc;
-  return bin_entries<unsigned long long, kKey64SortIPT, 8, false>(cam, ws, lo, nullptr, nullptr,
-                                                                  32 + tile_sort_bits(lo.n_tiles), 32, st);
+  return bin_entries<unsigned long long, kKey64SortIPT, 8, false>(cam, ws, lo, perm, &ctr->n_depth,
+                                                                  tile_sort_bits(lo.n_tiles), 32, st);
 }
 
 // Generic 64-bit pair sort exported through the ABI (for tests / tools).

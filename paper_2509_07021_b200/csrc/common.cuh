@@ -159,10 +159,10 @@ inline int make_layout(const sgs_workspace* ws, Layout* lo) {
   lo->dkey_tmp = take(n * 4);
   lo->didx = take(n * 4);
   lo->didx_alt = take(n * 4);
-  // depth-first mode: the emitting primitives' (depth key, index), compacted
-  // by the preprocess (the depth sort's read-only first-pass input)
-  lo->dkey_c = take(ws->sort_mode == SGS_SORT_DEPTH_FIRST ? n * 4 : 0);
-  lo->didx_c = take(ws->sort_mode == SGS_SORT_DEPTH_FIRST ? n * 4 : 0);
+  // strip renders: the emitting primitives' (depth key, index), compacted
+  // (the depth sort's read-only first-pass input); both sort modes
+  lo->dkey_c = take(n * 4);
+  lo->didx_c = take(n * 4);
   lo->offsets = take(n * 8);
   lo->scan_blocks = take(((n + 2047) / 2048 + 1) * 8);
   const uint64_t key_bytes = k64 ? 8 : 4;  // depth-first: (super_id << 16 | tile mask)
@@ -173,13 +173,15 @@ inline int make_layout(const sgs_workspace* ws, Layout* lo) {
   lo->ranges = take((uint64_t)lo->n_tiles * 8);
   lo->hist = take(16 * 512 * 4);
   // onesweep look-back status: per pass, per partition, 256 digits of u32
-  int tile_passes = k64 ? (32 + tile_sort_bits(lo->n_tiles) + 7) / 8 : super_sort_passes(lo->n_super);
+  // both modes sort the primitives by depth first; the entry sort then runs
+  // over the cell id digits only (64-bit keys: the tile bits above bit 32)
+  int tile_passes = k64 ? tile_sort_passes(lo->n_tiles) : super_sort_passes(lo->n_super);
   int ipt = k64 ? kKey64SortIPT : kTileSortIPT;
   uint64_t parts_tile = (cap + (uint64_t)kRadixThreads * ipt - 1) / ((uint64_t)kRadixThreads * ipt);
   uint64_t parts_depth =
       (n + (uint64_t)kDepthSortThreads * kDepthSortIPT - 1) / ((uint64_t)kDepthSortThreads * kDepthSortIPT);
   uint64_t st_tile = parts_tile * 512 * 4 * (uint64_t)tile_passes;
-  uint64_t st_depth = k64 ? 0 : parts_depth * 256 * 4 * 4;
+  uint64_t st_depth = parts_depth * 256 * 4 * 4;
   lo->status_bytes = st_tile > st_depth ? st_tile : st_depth;
   lo->status = take(lo->status_bytes);
   lo->total = off;

@@ -412,8 +412,7 @@ int launch_preprocess(const sgs_params& P, const SgsCam& cam, const sgs_workspac
                                               at<float>(ws, lo.depth_res),                                        \
                                               at<uint2>(ws, lo.rect), at<uint32_t>(ws, lo.tiles_touched),        \
                                               at<uint32_t>(ws, lo.super_touched),                                 \
-                                              lo.sort_mode == SGS_SORT_DEPTH_FIRST                                 \
-                                                  ? at<uint32_t>(ws, lo.hist) + kDepthHistOff : nullptr,   \
+                                              at<uint32_t>(ws, lo.hist) + kDepthHistOff,                         \
                                               lo.row_cap ? at<uint32_t>(ws, lo.row_off) : nullptr,                 \
                                               lo.row_cap ? at<uint16_t>(ws, lo.row_spans) : nullptr,               \
                                               (uint32_t)lo.row_cap, ctr)
