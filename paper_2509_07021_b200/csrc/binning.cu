@@ -7,18 +7,19 @@
 // contract is the list of 64-bit keys (tile << 32 | depth_bits) with
 // primitive-index values, stably sorted, plus per-tile [start, end) ranges.
 //
-// Two bit-identical ways to produce it:
-//   SGS_SORT_KEY64       emit entries in primitive-index order with the full
-//                        64-bit key and radix-sort 32 + ceil(log2 T) bits
-//                        (6 onesweep passes at 1080p, 24 B/entry/pass);
-//   SGS_SORT_DEPTH_FIRST radix-sort the N primitives once on their 31-bit
-//                        depth keys (4 passes over N, not E), emit entries in
-//                        that (depth, index) order carrying only the tile id,
-//                        then stably radix-sort on the tile id alone
-//                        (ceil(log2 T / 8) passes: 2 at 1080p and 4K, 16 B per
-//                        entry per pass).  A stable sort on tile of a list
-//                        already ordered by (depth, index) yields exactly the
-//                        (tile, depth, index) order of the 64-bit sort.
+// Both modes first radix-sort the N primitives on their 31-bit depth keys
+// (4 passes over N, not E) and order runs of equal keys by the float64
+// residual and index (depth_tie_fixup), then emit entries in that order; a
+// stable radix sort on the cell id of a list already in (depth, index) order
+// yields exactly the (tile, depth, index) order of the full 64-bit sort.
+//   SGS_SORT_KEY64       the entries carry the literal 64-bit key
+//                        (tile << 32 | depth_bits); the LSD sort runs over the
+//                        tile digits only, the low 32 bits arriving ordered
+//                        (2 onesweep passes at 1080p, 24 B/entry/pass);
+//   SGS_SORT_DEPTH_FIRST the entries are (super-tile id << 16 | 16-bit tile
+//                        mask), about a sixth as many, sorted on the
+//                        super-tile id (one 9-bit pass at 1080p); the raster
+//                        filters each super-tile list by its tile's mask bit.
 #include <algorithm>
 #include <utility>
 
