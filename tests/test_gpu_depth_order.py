@@ -60,9 +60,10 @@ def test_configs_lists_follow_reference_float64_order(cfg):
     _check_lists(scene, cams[0])
 
 
-def test_config4_strip_lists_follow_reference_float64_order():
+@pytest.mark.parametrize("mode", [_ffi.SORT_DEPTH_FIRST, _ffi.SORT_KEY64])
+def test_config4_strip_lists_follow_reference_float64_order(mode):
     scene, (cam,) = scenes.config4()
-    _check_lists(scene, cam, tile_rows=(60, 64))
+    _check_lists(scene, cam, mode, tile_rows=(60, 64))
 
 
 def test_exact_ties_keep_lower_index():

@@ -97,10 +97,13 @@ def test_background_and_importance():
     np.testing.assert_allclose(ws.cpu().numpy(), ref.weight_sums, rtol=1e-4, atol=1e-4)
 
 
-def test_strips_equal_full_frame():
+@pytest.mark.parametrize("mode", MODES)
+def test_strips_equal_full_frame(mode):
+    """Tile-row windows (the strip path: emitting depth keys compacted before
+    the depth sort) in both sort modes: bins bit-exact, strips tile the frame."""
     scene, cams = scenes.config0()
     cam = cams[0]
-    rast = Rasterizer()
+    rast = Rasterizer(sort_mode=mode)
     g = GaussianTensors.from_arrays(scene)
     full = rast.forward(g, cam).img.clone()
     parts = torch.zeros_like(full)
