@@ -55,8 +55,15 @@ class _PinnedArena:
         self.buf = None
         self.lock = threading.Lock()
 
+    @staticmethod
+    def _host(a) -> np.ndarray:
+        a = np.ascontiguousarray(np.asarray(a))
+        if not a.dtype.isnative or a.dtype.kind not in "fbiu":  # torch.from_numpy needs native numbers
+            a = np.ascontiguousarray(a, dtype=np.float32)
+        return a
+
     def upload(self, arrays, device) -> list:
-        arrays = [np.ascontiguousarray(np.asarray(a)) for a in arrays]
+        arrays = [self._host(a) for a in arrays]
         sizes = [a.size for a in arrays]
         # each array starts on a 256-byte boundary (the kernels' float4 loads
         # need 16, coalescing likes 256)
