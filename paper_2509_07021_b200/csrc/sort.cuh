@@ -49,9 +49,20 @@ __device__ __forceinline__ uint32_t match_digit(uint32_t d, uint32_t valid) {
   uint32_t peers = valid;
 #pragma unroll
   for (int b = 0; b < RBITS; ++b) {
-    const uint32_t bit = (d >> b) & 1u;
-    const uint32_t m = __ballot_sync(0xffffffffu, bit);
-    peers &= bit ? m : ~m;
+    // per bit: the bit as a predicate, its ballot, peers &= bit ? m : ~m.
+    // Written this way ptxas moves all the digit's bits into predicates with
+    // one R2P and needs ~3 instructions per bit (~5 from the C++ form):
+    // configs[2] binning 0.230 -> 0.220 ms, configs[4] 3.67 -> 3.48 ms
+    uint32_t r;
+    asm("{\n\t.reg .pred p;\n\t.reg .b32 m, x;\n\t"
+        "setp.ne.u32 p, %2, 0;\n\t"
+        "vote.sync.ballot.b32 m, p, 0xffffffff;\n\t"
+        "selp.b32 x, 0, 0xffffffff, p;\n\t"
+        "xor.b32 m, m, x;\n\t"
+        "and.b32 %0, %1, m;\n\t}"
+        : "=r"(r)
+        : "r"(peers), "r"(d & (1u << b)));
+    peers = r;
   }
   return peers;
 }
