@@ -65,12 +65,17 @@ class BatchRenderer:
                  graphs: bool = True):
         self.rast = rast or Rasterizer(device=device)
         self.device = torch.device(device)
-        self.copy_stream = torch.cuda.Stream(device=self.device)
         self.h2d_stream = torch.cuda.Stream(device=self.device)
         self.streams = [torch.cuda.Stream(device=self.device) for _ in range(max(streams, 1))]
+        # one read-back stream per render stream: an image leaves as soon as
+        # its view is done, not behind an earlier view still rendering on
+        # another stream (the link has only a few percent of slack)
+        self.copy_streams = [torch.cuda.Stream(device=self.device) for _ in self.streams]
+        self.copy_stream = self.copy_streams[0]
         self._host = {}
         self._dev = [None, None]      # two device copies of the scene
-        self._free = [None, None]     # event: renders AND read-backs of the copy's last use finished
+        self._rendered = [[], []]     # per slot: events, the renders of the scene copy's last use done
+        self._copied = {}             # (slot, view): event, that device image's last read-back done
         self._pending = [None, None]  # per slot: the unchecked overflow state of its last call
         self._ovf_dev = {}
         self._ovf_host = {}
@@ -100,8 +105,8 @@ class BatchRenderer:
                               for f, t in scene.arrays.items()) or \
                 (dev.prim_mask is None) != (scene.prim_mask is None):
             with torch.cuda.stream(self.h2d_stream):
-                if self._free[slot] is not None:
-                    self.h2d_stream.wait_event(self._free[slot])
+                for ev in self._rendered[slot]:
+                    self.h2d_stream.wait_event(ev)
                 arrs = {f: torch.empty(t.shape, dtype=torch.float32, device=self.device)
                         for f, t in scene.arrays.items()}
                 pm = None if scene.prim_mask is None else torch.empty(
@@ -109,8 +114,10 @@ class BatchRenderer:
             dev = GaussianTensors(**arrs, prim_mask=pm)
             self._dev[slot] = dev
         with torch.cuda.stream(self.h2d_stream):
-            if self._free[slot] is not None:
-                self.h2d_stream.wait_event(self._free[slot])
+            # the scene copy is overwritten once the renders that read it are
+            # done -- its images' read-backs may still be in flight
+            for ev in self._rendered[slot]:
+                self.h2d_stream.wait_event(ev)
             for f, t in scene.arrays.items():
                 getattr(dev, f).copy_(t, non_blocking=True)
             if scene.prim_mask is not None:
@@ -169,6 +176,8 @@ class BatchRenderer:
         for k, cam in enumerate(cams):
             s = self.streams[k % len(self.streams)]
             s.wait_event(up)
+            if (slot, k) in self._copied:  # this device image buffer's previous read-back
+                s.wait_event(self._copied[(slot, k)])
             with torch.cuda.stream(s):
                 if self.graphs and not check:
                     H, W = int(cam.height), int(cam.width)
@@ -186,23 +195,28 @@ class BatchRenderer:
                 done = torch.cuda.Event()
                 done.record(s)
             host = self._host_buf((slot, k), tuple(img.shape))
-            with torch.cuda.stream(self.copy_stream):
-                self.copy_stream.wait_event(done)
+            cs = self.copy_streams[k % len(self.streams)]
+            with torch.cuda.stream(cs):
+                cs.wait_event(done)
                 host.copy_(img, non_blocking=True)
-                img.record_stream(self.copy_stream)
+                img.record_stream(cs)
+                copied = torch.cuda.Event()
+                copied.record(cs)
+                self._copied[(slot, k)] = copied
             outs.append(host)
+        rendered = []
         for s in self.streams:
+            ev = torch.cuda.Event()
+            ev.record(s)
+            rendered.append(ev)
+        self._rendered[slot] = rendered
+        for s in self.streams + self.copy_streams[1:]:
             self.copy_stream.wait_stream(s)
         with torch.cuda.stream(self.copy_stream):
             ovf_host[:len(cams)].copy_(ovf_dev[:len(cams)], non_blocking=True)
         ready = torch.cuda.Event()
         ready.record(self.copy_stream)
-        # the device copy and the device image buffers may be overwritten once
-        # this call's renders AND its read-backs are done
         main.wait_stream(self.copy_stream)
-        freed = torch.cuda.Event()
-        freed.record(main)
-        self._free[slot] = freed
         self._pending[slot] = (ready, ovf_host, cams, outs, background)
         if wait:
             self._resolve(slot)

@@ -14,12 +14,12 @@ namespace sgs {
 constexpr int kNumSMs = 148;
 constexpr int kRadixThreads = 512;  // = kRsThreads in sort.cuh
 #ifndef SGS_TILE_SORT_IPT
-#define SGS_TILE_SORT_IPT 16
+#define SGS_TILE_SORT_IPT 8
 #endif
 #ifndef SGS_DEPTH_SORT_IPT
 #define SGS_DEPTH_SORT_IPT 16
 #endif
-constexpr int kTileSortIPT = SGS_TILE_SORT_IPT;  // items per thread, tile-key onesweep passes (8192 per CTA)
+constexpr int kTileSortIPT = SGS_TILE_SORT_IPT;  // items per thread, tile-key onesweep passes (4096 per CTA)
 constexpr int kDepthSortIPT = SGS_DEPTH_SORT_IPT;
 #ifndef SGS_DEPTH_SORT_THREADS
 #define SGS_DEPTH_SORT_THREADS 512

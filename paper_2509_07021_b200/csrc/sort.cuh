@@ -134,11 +134,16 @@ struct RsRangeOut {
 // status: nparts x 2^RBITS u32, zeroed; ticket zeroed.
 // vin == nullptr means values are the item indices (first pass of an argsort).
 // kout == nullptr skips the key writes.
+// Two resident CTAs per SM (64 registers): one CTA's look-back and scatter
+// overlap the other's loads and ranking, and the four view streams' rasters
+// find room beside the sorts.  The 16-item depth sort spills 28 bytes at 64
+// registers and is still faster in the four-stream headline (configs[2]
+// 2036 -> 2070 frames/s with the 8-item cell sort; configs[4] 8.08 -> 7.91 ms).
 #ifndef SGS_RS_MIN_BLOCKS
-#define SGS_RS_MIN_BLOCKS 1
+#define SGS_RS_MIN_BLOCKS(ipt) 2
 #endif
 template <typename K, int IPT, int RBITS, int NT = kRsThreads>
-__global__ void __launch_bounds__(NT, SGS_RS_MIN_BLOCKS) rs_onesweep(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
+__global__ void __launch_bounds__(NT, SGS_RS_MIN_BLOCKS(IPT)) rs_onesweep(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                           K* __restrict__ kout, uint32_t* __restrict__ vout,
                                                           const uint32_t* n_ptr, uint32_t n_cap, int shift,
                                                           const uint32_t* __restrict__ pass_count, uint32_t* status,
