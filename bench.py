@@ -60,7 +60,7 @@ def parse():
     ap.add_argument("--cams", type=int, default=N_CAMS, help="configs[2] cameras per step (the batch)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sort-mode", type=int, default=0)
-    ap.add_argument("--streams", type=int, default=4,
+    ap.add_argument("--streams", type=int, default=8,
                     help="concurrent CUDA streams the views of a step are spread over")
     ap.add_argument("--no-graphs", action="store_true",
                     help="launch every kernel from the host instead of replaying per-view CUDA graphs")

@@ -61,7 +61,7 @@ class BatchRenderer:
     ``wait=False``, when the call's slot is next used (the call after next)
     or at ``finish()``."""
 
-    def __init__(self, rast: Rasterizer | None = None, device="cuda", streams: int = 4,
+    def __init__(self, rast: Rasterizer | None = None, device="cuda", streams: int = 8,
                  graphs: bool = True):
         self.rast = rast or Rasterizer(device=device)
         self.device = torch.device(device)

@@ -2,7 +2,7 @@
 is available to this build): each rank's share of the work is timed on one
 B200 exactly as that rank would run it, the slowest rank sets the step time.
 
-  configs[2]  64 views, rank r renders 64/N of them (4 streams, graphs)
+  configs[2]  64 views, rank r renders 64/N of them (8 streams, graphs)
   configs[3]  8-view training step, rank r runs 8/N views + the bucket
               all-reduce (modelled: 2 (N-1)/N x bucket bytes / busbw)
   configs[4]  profiles/strips (per-strip stage times, measured-cost strips)
@@ -32,7 +32,8 @@ out = {"assumptions": {"allreduce_busbw_GBs": NVLINK_BUSBW_GBS}}
 scene, cams = scenes.config2()
 rast = Rasterizer()
 g = GaussianTensors.from_arrays(scene)
-streams = [torch.cuda.current_stream()] + [torch.cuda.Stream() for _ in range(3)]
+NSTREAMS = 8
+streams = [torch.cuda.current_stream()] + [torch.cuda.Stream() for _ in range(NSTREAMS - 1)]
 for k, c in enumerate(cams):
     rast.forward(g, c, check=True, track=False)
 bufs = [(torch.empty((c.height, c.width, 3), device="cuda"), torch.empty((c.height, c.width), device="cuda"))
@@ -44,7 +45,7 @@ def render(views, reps=5):
 
     def step():
         for j, v in enumerate(views):
-            with torch.cuda.stream(streams[j % 4]):
+            with torch.cuda.stream(streams[j % NSTREAMS]):
                 rast.graph_forward(g, cams[v], bufs[v])
     for s in streams[1:]:
         s.wait_stream(main)
