@@ -20,16 +20,17 @@ if what in ("all", "render"):
     cams = cams[:16]
     rast = Rasterizer()
     g = GaussianTensors.from_arrays(scene)
-    streams = [torch.cuda.current_stream()] + [torch.cuda.Stream() for _ in range(3)]
+    S = int(os.environ.get("MICRO_STREAMS", "8"))  # as bench.py
+    streams = [torch.cuda.current_stream()] + [torch.cuda.Stream() for _ in range(S - 1)]
     for _ in range(3):
         for k, c in enumerate(cams):
-            with torch.cuda.stream(streams[k % 4]):
+            with torch.cuda.stream(streams[k % S]):
                 rast.forward(g, c, check=True, track=False)
     torch.cuda.synchronize()
     bufs = [(torch.empty((c.height, c.width, 3), device=dev), torch.empty((c.height, c.width), device=dev)) for c in cams]
     def step():
         for k, c in enumerate(cams):
-            with torch.cuda.stream(streams[k % 4]):
+            with torch.cuda.stream(streams[k % S]):
                 rast.graph_forward(g, c, bufs[k])
     main = streams[0]
     for s in streams[1:]: s.wait_stream(main)
