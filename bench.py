@@ -40,6 +40,7 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "frames/s & Mpix/s at 1080p, 1M Gaussians, 3 SG lobes (1/2/4/8 B200); peak render VRAM"
 UNIT = "frames/s"
+SHARED_NOTE = "SGS_BENCH_SHARED_GPU: all ranks shared one GPU over gloo; not a measurement"
 WORKLOAD = "configs[2]: 1,000,000 Gaussians (64 clusters), 3 SG lobes, 64 cameras 1920x1080, FoV 60"
 N_CAMS = 64
 # libsgs kernels per forward frame (depth-first mode, 1080p): preprocess (also
@@ -56,7 +57,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=None, help="override the workload's Gaussian count")
+    ap.add_argument("--n", "--gaussians", dest="n", type=int, default=None, help="override the workload's Gaussian count")
     ap.add_argument("--cams", type=int, default=N_CAMS, help="configs[2] cameras per step (the batch)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sort-mode", type=int, default=0)
@@ -951,6 +952,8 @@ def run_ours(args):
             line = dict(res)
             line.update({"n_gpus": ctx.world, "warmup": args.warmup, "higher_is_better": True,
                          "vs_baseline": None, "data": "synthetic (seeded BASELINE configs distributions)"})
+            if ctx.shared:
+                line["functional_check_only"] = SHARED_NOTE
             print(json.dumps(line), flush=True)
         ctx.close()
         return
@@ -983,7 +986,7 @@ def run_ours(args):
             "gpu_launches": h["gpu_launches"], "clocks": h["clocks"],
         }
         if ctx.shared:
-            line["functional_check_only"] = "SGS_BENCH_SHARED_GPU: all ranks shared one GPU over gloo; not a measurement"
+            line["functional_check_only"] = SHARED_NOTE
         if workloads:
             line["workloads"] = workloads
             line["gpu_launches"] += sum(int(w.get("gpu_launches", 0)) for w in workloads.values())

@@ -54,3 +54,30 @@ def test_our_arm_line():
     assert all(w[k]["value"] > 0 for k in w)
     assert w["cfg1"]["vram"]["measured_peak_dynamic_bytes"] > 0
     assert 0 < w["cfg3"]["roofline_backward"]["frac"] < 2
+
+
+def _run_two_ranks(args, timeout, env_extra):
+    import os
+    env = dict(os.environ, **env_extra)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29533", str(ROOT / "bench.py"), "--gpus", "2", *args]
+    out = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=timeout, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]   # rank 0 alone prints
+    return json.loads(lines[0])
+
+
+@pytest.mark.gpu
+def test_two_rank_control_flow_on_one_gpu():
+    """The torchrun path of our arm (view shards, barriers, max-over-ranks
+    timing, the trainer's bucketed all-reduce) with both ranks sharing the
+    one GPU over gloo (SGS_BENCH_SHARED_GPU): a functional check, marked as
+    such in the line -- the driver's multi-GPU runs use NCCL, one GPU each."""
+    d = _run_two_ranks(["--steps", "1", "--warmup", "3", "--cams", "4", "--gaussians", "100000", "--workload", "render",
+                        "--no-cpu-baseline"], timeout=900, env_extra={"SGS_BENCH_SHARED_GPU": "1"})
+    assert d["n_gpus"] == 2 and d["value"] > 0 and "functional_check_only" in d
+    assert d["e2e"]["value"] > 0
+    t = _run_two_ranks(["--steps", "1", "--warmup", "3", "--gaussians", "50000", "--workload", "train"], timeout=900,
+                       env_extra={"SGS_BENCH_SHARED_GPU": "1"})
+    assert t["n_gpus"] == 2 and t["value"] > 0 and "functional_check_only" in t
