@@ -246,6 +246,14 @@ int sgs_raster_backward_det(const sgs_camera* cam, const float background[3],
 int sgs_preprocess_backward(const sgs_params* params, const sgs_camera* cam, const float* grad2d,
                             sgs_grads* grads, void* stream);
 
+/* K7 for several views of one primitive set (a training step): the same
+ * rows as one sgs_preprocess_backward per view in view order (bit-identical),
+ * with each primitive's parameters read, its view-independent terms formed and
+ * its gradient rows written once per 8 views.  cams[v] / grad2d[v]: host
+ * arrays of n_views cameras and device partial buffers (K6 outputs). */
+int sgs_preprocess_backward_views(const sgs_params* params, const sgs_camera* cams, int n_views,
+                                  const float* const* grad2d, sgs_grads* grads, void* stream);
+
 /* Per-primitive projection (all N primitives, 16 floats each):
  * [visible, depth, mean2d x/y, cov2d 00/01/11, conic 00/01/11, color_pre rgb,
  * color rgb] -- the per-primitive outputs of _prepare (render.py:259-317) and

@@ -108,6 +108,8 @@ SIGNATURES = {
     "sgs_fixed_to_float": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p]),
     "sgs_preprocess_backward": (C.c_int, [_P(SgsParams), _P(SgsCamera), C.c_void_p, _P(SgsGrads),
                                           C.c_void_p]),
+    "sgs_preprocess_backward_views": (C.c_int, [_P(SgsParams), _P(SgsCamera), C.c_int, _P(C.c_void_p),
+                                                _P(SgsGrads), C.c_void_p]),
     "sgs_project_records": (C.c_int, [_P(SgsParams), _P(SgsCamera), C.c_void_p, C.c_void_p]),
     "sgs_get_stats": (C.c_int, [_P(SgsWorkspace), _P(SgsStats), C.c_void_p]),
     "sgs_vram_model": (C.c_int, [_P(SgsParams), _P(SgsCamera), C.c_int32, _P(SgsWorkspace),

@@ -53,6 +53,8 @@ int launch_raster_bwd(const SgsCam& cam, float3 bg, const sgs_workspace* ws, con
                       cudaStream_t st);
 uint64_t raster_bwd_det_scratch_bytes(int64_t n);
 int launch_fixed_to_float(const unsigned long long* fx, int64_t n, int frac_bits, float* out, int acc, cudaStream_t st);
+int launch_preprocess_bwd_views(const sgs_params& P, const SgsCam* cams, const float* const* grad2d, int n_views,
+                                const sgs_grads& g, cudaStream_t st);
 int launch_preprocess_bwd(const sgs_params& P, const SgsCam& cam, const float* grad2d, const sgs_grads& g,
                           cudaStream_t st);
 int launch_export_lists(const SgsCam& cam, const sgs_workspace* ws, const Layout& lo, const uint32_t* vals,
@@ -255,6 +257,29 @@ int sgs_fixed_to_float(const uint64_t* fx, int64_t n, int32_t frac_bits, float* 
                                as_stream(stream));
 }
 
+static int sgs_preprocess_backward_check(const sgs_params* params, const sgs_camera* cam, const float* grad2d,
+                                         sgs_grads* grads) {
+  int rc = check_params(params, nullptr);
+  if (rc) return rc;
+  if (!grads || !grad2d || (params->n > 0 && (!grads->position || !grads->quat || !grads->log_scale ||
+                                              !grads->opacity || !grads->diffuse ||
+                                              (params->n_lobes > 0 &&
+                                               (!grads->axis_raw || !grads->sharpness || !grads->amplitude))))) {
+    set_error("null gradient buffer");
+    return SGS_E_ARG;
+  }
+  if ((grads->flags & ~(SGS_GRADS_ACCUMULATE | SGS_GRADS_MASK_LOGIT)) != 0 ||
+      (reinterpret_cast<uintptr_t>(grads->quat) & 15u) != 0) {
+    set_error("invalid gradient flags or unaligned quaternion gradient (16-byte rows)");
+    return SGS_E_ARG;
+  }
+  if (!cam) {
+    set_error("null camera");
+    return SGS_E_ARG;
+  }
+  return SGS_OK;
+}
+
 int sgs_preprocess_backward(const sgs_params* params, const sgs_camera* cam, const float* grad2d, sgs_grads* grads,
                             void* stream) {
   int rc = check_params(params, nullptr);
@@ -281,6 +306,42 @@ int sgs_preprocess_backward(const sgs_params* params, const sgs_camera* cam, con
   if (rc) return rc;
   if (params->n == 0) return SGS_OK;
   return launch_preprocess_bwd(*params, c, grad2d, *grads, as_stream(stream));
+}
+
+
+int sgs_preprocess_backward_views(const sgs_params* params, const sgs_camera* cams, int n_views,
+                                  const float* const* grad2d, sgs_grads* grads, void* stream) {
+  if (n_views < 1 || !cams || !grad2d) {
+    set_error("need at least one view with its camera and partials");
+    return SGS_E_ARG;
+  }
+  for (int v = 0; v < n_views; ++v)
+    if (!grad2d[v]) {
+      set_error("null partials for view %d", v);
+      return SGS_E_ARG;
+    }
+  // validate like sgs_preprocess_backward (view 0), then convert every camera
+  int rc = sgs_preprocess_backward_check(params, &cams[0], grad2d[0], grads);
+  if (rc) return rc;
+  if (params->n == 0) return SGS_OK;
+  SgsCam c[64];
+  for (int v0 = 0; v0 < n_views; v0 += 64) {
+    const int nv = n_views - v0 < 64 ? n_views - v0 : 64;
+    for (int k = 0; k < nv; ++k) {
+      Layout lo{};
+      lo.W = cams[v0 + k].width;
+      lo.H = cams[v0 + k].height;
+      lo.tiles_x = (lo.W + SGS_TILE - 1) / SGS_TILE;
+      lo.tiles_y = (lo.H + SGS_TILE - 1) / SGS_TILE;
+      rc = make_cam(&cams[v0 + k], lo, &c[k]);
+      if (rc) return rc;
+    }
+    sgs_grads g = *grads;
+    if (v0 > 0) g.flags |= SGS_GRADS_ACCUMULATE;
+    rc = launch_preprocess_bwd_views(*params, c, grad2d + v0, nv, g, as_stream(stream));
+    if (rc) return rc;
+  }
+  return SGS_OK;
 }
 
 int sgs_project_records(const sgs_params* params, const sgs_camera* cam, float* out, void* stream) {

@@ -549,6 +549,20 @@ class Rasterizer:
                         mask_logit: bool = False) -> dict:
         """K7 alone: parameter (and mask) gradients from K6's partials, on the
         current stream (``c_cam`` = the frame's sgs_camera)."""
+        return self.backward_params_views(g, [c_cam], [grad2d], mask_grads, out, accumulate, mask_logit)
+
+    def backward_params_views(self, g: GaussianTensors, c_cams, grad2ds, mask_grads: bool = True,
+                              out: dict | None = None, accumulate: bool = False,
+                              mask_logit: bool = False) -> dict:
+        """K7 over several views (``c_cams`` / ``grad2ds``: their sgs_cameras and
+        K6 partials): the sum of the per-view gradients in view order, with
+        the parameters read and the gradient rows written once per 8 views
+        (sgs_preprocess_backward_views)."""
+        if len(c_cams) != len(grad2ds) or not c_cams:
+            raise ValueError("one K6 partial buffer per camera, at least one view")
+        for t in grad2ds:
+            if t.dtype != torch.float32 or not t.is_contiguous() or t.numel() != g.n * 9:
+                raise ValueError("K6 partials must be contiguous float32 (N, 9) tensors")
         if out is None:
             if accumulate:
                 raise ValueError("accumulate=True needs the output tensors")
@@ -571,8 +585,14 @@ class Rasterizer:
         cg.lobe_mask = _ptr(out.get("lobe_mask")) if mask_grads else None
         cg.prim_mask = _ptr(out.get("prim_mask")) if mask_grads else None
         params = g.c_params()
-        _ffi.call("sgs_preprocess_backward", C.byref(params), C.byref(c_cam), _ptr(grad2d),
-                  C.byref(cg), C.c_void_p(_stream_ptr()))
+        if len(c_cams) == 1:
+            _ffi.call("sgs_preprocess_backward", C.byref(params), C.byref(c_cams[0]), _ptr(grad2ds[0]),
+                      C.byref(cg), C.c_void_p(_stream_ptr()))
+            return out
+        cams = (_ffi.SgsCamera * len(c_cams))(*c_cams)
+        ptrs = (C.c_void_p * len(grad2ds))(*[t.data_ptr() for t in grad2ds])
+        _ffi.call("sgs_preprocess_backward_views", C.byref(params), cams, len(c_cams), ptrs, C.byref(cg),
+                  C.c_void_p(_stream_ptr()))
         return out
 
     # ----------------------------------------------------------------- exports

@@ -137,12 +137,12 @@ class SoftPruneTrainer:
 
     def _views_pipelined(self, g: GaussianTensors, cams, targets, mine, ovf, capture: bool = False):
         """The step's views on ``n_streams`` streams: forward, loss and raster
-        backward of view j on stream j mod S, then its K7 into the bucket on
-        the accumulation stream in view order, chunk by chunk (one writer:
-        the bucket update is a plain read-modify-write).  Returns the summed
-        loss (device) and one event per chunk, recorded on the accumulation
-        stream when the last view's K7 has added that chunk's rows.  The
-        current stream waits for the views' streams only, not for K7
+        backward of view j on stream j mod S; then, on the accumulation stream
+        once every view's partials are in, one K7 over all the views per
+        primitive chunk (sgs_preprocess_backward_views: one writer, the views
+        summed in order).  Returns the summed loss (device) and one event per
+        chunk, recorded on the accumulation stream when that chunk's rows are
+        complete.  The current stream waits for the views' streams only, not for K7
         (``capture``: inside a CUDA-graph capture -- no chunk events, every
         stream joined back, see _capture_views)."""
         from .loss import image_loss
@@ -157,6 +157,7 @@ class SoftPruneTrainer:
         chunk_done = [torch.cuda.Event() for _ in range(self.chunks)]
         gc = [self._chunk_gaussians(g, c) for c in range(self.chunks)]
         outs = [self._bucket_out(c) for c in range(self.chunks)]
+        c_cams, g2ds = [], []
         for j, v in enumerate(mine):
             st = views[j % len(views)]
             st.wait_event(start)
@@ -169,15 +170,22 @@ class SoftPruneTrainer:
                 done.record(st)
             acc.wait_event(done)
             grad2d.record_stream(acc)
-            with torch.cuda.stream(acc):
-                for c in range(self.chunks):
-                    self.rast.backward_params(gc[c], frame.cam, grad2d[self._rows(c)], mask_grads=True,
-                                              out=outs[c], accumulate=True, mask_logit=True)
-                    if j == len(mine) - 1 and not capture:
-                        chunk_done[c].record(acc)
+            c_cams.append(frame.cam)
+            g2ds.append(grad2d)
             if not capture:
                 lo.record_stream(main)
             losses.append(lo[0])
+        # K7 once for all the views (they finish their raster backwards
+        # together anyway): each primitive's parameters read and its bucket
+        # rows written once per 8 views, the views summed in order
+        if mine:
+            with torch.cuda.stream(acc):
+                for c in range(self.chunks):
+                    r = self._rows(c)
+                    self.rast.backward_params_views(gc[c], c_cams, [t[r] for t in g2ds], mask_grads=True,
+                                                    out=outs[c], accumulate=True, mask_logit=True)
+                    if not capture:
+                        chunk_done[c].record(acc)
         if not mine and not capture:
             for c in range(self.chunks):
                 chunk_done[c].record(acc)

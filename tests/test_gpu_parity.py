@@ -311,3 +311,27 @@ def test_autograd_function_matches_explicit_backward():
         assert torch.allclose(leaves[f].grad, want[f], rtol=1e-5, atol=1e-7 * float(want[f].abs().max())), f
     assert torch.allclose(lm.grad, want["lobe_mask"], rtol=1e-5, atol=1e-7 * float(want["lobe_mask"].abs().max()))
     assert torch.allclose(pm.grad, want["prim_mask"], rtol=1e-5, atol=1e-7 * float(want["prim_mask"].abs().max()))
+
+
+def test_multi_view_parameter_backward_equals_sequential():
+    """sgs_preprocess_backward_views (K7 over several views, rows written
+    once) is bit-identical to one sgs_preprocess_backward per view in view
+    order, accumulating -- including more views than one launch takes."""
+    scene, cams = scenes.config3(n=20000, n_views=10)
+    rast = Rasterizer()
+    g = GaussianTensors.from_arrays(scene)
+    c_cams, g2ds = [], []
+    for v, cam in enumerate(cams):
+        f = rast.forward(g, cam, grad_floor=0.001)
+        tgt = torch.from_numpy(scenes.target_image(0, cam.height, cam.width, v)).cuda()
+        dimg = (f.img - tgt) * 1e-3
+        g2ds.append(rast.backward_raster(g, f, dimg).clone())
+        c_cams.append(f.cam)
+    seq = None
+    for c, t in zip(c_cams, g2ds):
+        seq = rast.backward_params(g, c, t, mask_grads=True, out=seq, accumulate=seq is not None, mask_logit=True)
+    multi = rast.backward_params_views(g, c_cams, g2ds, mask_grads=True, mask_logit=True)
+    torch.cuda.synchronize()
+    for k in seq:
+        assert torch.equal(seq[k], multi[k]), k
+    assert float(multi["position"].abs().sum()) > 0
