@@ -480,7 +480,7 @@ def run_headline(ctx, timed_clocks: bool = True) -> dict:
     # ---- e2e through the host-buffer batch API
     pinned = PinnedScene(scene)
     br = BatchRenderer(rast, device=dev, streams=args.streams)
-    for _ in range(2):
+    for _ in range(br.slots):  # every slot's buffers allocated before the timed calls
         br.render_views(pinned, my_cams, wait=False)
     br.finish()
     ctx.barrier()

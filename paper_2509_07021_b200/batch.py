@@ -62,7 +62,7 @@ class BatchRenderer:
     or at ``finish()``."""
 
     def __init__(self, rast: Rasterizer | None = None, device="cuda", streams: int = 8,
-                 graphs: bool = True):
+                 graphs: bool = True, slots: int = 2):
         self.rast = rast or Rasterizer(device=device)
         self.device = torch.device(device)
         self.h2d_stream = torch.cuda.Stream(device=self.device)
@@ -73,10 +73,11 @@ class BatchRenderer:
         self.copy_streams = [torch.cuda.Stream(device=self.device) for _ in self.streams]
         self.copy_stream = self.copy_streams[0]
         self._host = {}
-        self._dev = [None, None]      # two device copies of the scene
-        self._rendered = [[], []]     # per slot: events, the renders of the scene copy's last use done
+        self.slots = max(2, int(slots))  # calls in flight: device scene copies / image buffer sets
+        self._dev = [None] * self.slots
+        self._rendered = [[] for _ in range(self.slots)]  # per slot: the renders of its last use done
         self._copied = {}             # (slot, view): event, that device image's last read-back done
-        self._pending = [None, None]  # per slot: the unchecked overflow state of its last call
+        self._pending = [None] * self.slots  # per slot: the unchecked overflow state of its last call
         self._ovf_dev = {}
         self._ovf_host = {}
         self._calls = 0
@@ -152,7 +153,7 @@ class BatchRenderer:
         """Wait for every call in flight and resolve its overflow checks:
         after this, every image a ``wait=False`` call returned is final."""
         torch.cuda.synchronize(self.device)
-        for slot in (0, 1):
+        for slot in range(self.slots):
             self._resolve(slot)
 
     def render_views(self, scene: PinnedScene, cams, background=(0.0, 0.0, 0.0), check=False,
@@ -164,7 +165,7 @@ class BatchRenderer:
         images are complete after ``finish()`` or once the call after next
         returns (the host buffers are then reused by the call after that)."""
         cams = list(cams)
-        slot = self._calls % 2
+        slot = self._calls % self.slots
         self._calls += 1
         self._resolve(slot)  # the slot's last call: overflow checked before its copy is reused
         main = torch.cuda.current_stream(self.device)
